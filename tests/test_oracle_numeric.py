@@ -1,0 +1,146 @@
+"""Pins of the numerical oracle (oracle/oracle.c) against things other than itself: brute-force
+definitions on tiny inputs, exact integer products (numpy int64 matmul, a library primitive),
+the flop-count closed forms of Sec. 2.1, and exactness under quantised inputs.  No GPU."""
+import glob
+import math
+import os
+
+import numpy as np
+import pytest
+
+import fmm_inputs as I
+from conftest import ALGS, GOLDEN
+from oracle import oracle as O
+
+ALG_FILES = sorted(glob.glob(os.path.join(ALGS, "*.txt")))
+ALGS_BY_NAME = {os.path.basename(p)[:-4]: O.load_alg(p) for p in ALG_FILES}
+
+
+def _exact(A, B):
+    """Exact product of integer-valued float matrices via int64 (library primitive)."""
+    return (A.astype(np.int64) @ B.astype(np.int64)).astype(np.float64)
+
+
+def test_classical_matches_brute_force_loops():
+    A, B = I.problem(5, 7, 3, seed=1)
+    C = O.classical(A, B)
+    ref = np.zeros((5, 3))
+    for i in range(5):
+        for j in range(3):
+            s = 0.0
+            for q in range(7):
+                s = s + A[i, q] * B[q, j]
+            ref[i, j] = s
+    assert np.array_equal(C, ref)  # same order, same rounding
+
+
+@pytest.mark.parametrize("layout", ["row", "col"])
+def test_classical_integer_exact_both_layouts(layout):
+    A, B = I.problem(33, 29, 31, seed=2, kind="integers", layout=layout)
+    assert np.array_equal(O.classical(A, B), _exact(A, B))
+
+
+def test_classical_degenerate_dims():
+    A = np.zeros((3, 0)); B = np.zeros((0, 4))
+    assert np.array_equal(O.classical(A, B), np.zeros((3, 4)))
+
+
+# ---- check (c): fast == classical bitwise on integer inputs ----------------------------------
+def _cases():
+    out = []
+    for name, a in ALGS_BY_NAME.items():
+        for L in (1, 2):
+            out.append((name, L, a.M ** L, a.K ** L, a.N ** L))          # exact base-case powers
+            out.append((name, L, 3 * a.M ** L + 1, 2 * a.K ** L + 1, 2 * a.N ** L + 2))  # peeled
+    out += [("strassen_222_7", 1, 4, 4, 4), ("strassen_222_7", 2, 4, 4, 4),   # BJ config 1 4x4
+            ("strassen_222_7", 1, 5, 5, 5), ("strassen_222_7", 3, 37, 41, 43),
+            ("hk_class_323_15", 1, 7, 5, 7), ("hk_class_323_15", 2, 101, 67, 89),
+            ("hk_class_323_15", 2, 7, 11, 13), ("laderman_class_333_23", 2, 29, 31, 28)]
+    return out
+
+
+@pytest.mark.parametrize("name,L,P,Q,N", _cases())
+def test_fast_equals_classical_bitwise_on_integers(name, L, P, Q, N):
+    a = ALGS_BY_NAME[name]
+    A, B = I.problem(P, Q, N, seed=L, kind="integers")
+    C = O.fast(A, B, a, L)
+    assert np.array_equal(C, _exact(A, B))
+    assert np.array_equal(C, O.classical(A, B))
+
+
+def test_fast_col_major_input_equals_row_major():
+    a = ALGS_BY_NAME["winograd_class_222_7"]
+    Ar, Br = I.problem(36, 20, 28, seed=4)
+    Ac, Bc = I.problem(36, 20, 28, seed=4, layout="col")
+    assert np.array_equal(O.fast(Ar, Br, a, 2), O.fast(Ac, Bc, a, 2))
+
+
+def test_fast_degenerate_and_sub_base_case_dims_fall_back_to_classical():
+    a = ALGS_BY_NAME["laderman_class_333_23"]
+    for (P, Q, N) in [(2, 9, 9), (9, 2, 9), (9, 9, 2), (1, 1, 1)]:
+        A, B = I.problem(P, Q, N, seed=3)
+        assert np.array_equal(O.fast(A, B, a, 2), O.classical(A, B))
+
+
+# ---- exactness trick: quantised inputs make every partial sum exact ---------------------------
+@pytest.mark.parametrize("name,L,P,Q,N", [
+    ("winograd_class_222_7", 2, 256, 256, 256),
+    ("hk_class_323_15", 2, 181, 70, 183),
+    ("alg_424_26", 2, 160, 40, 163),
+    ("laderman_class_333_23", 2, 91, 90, 92),
+    ("alg_433_29", 2, 161, 45, 46),
+])
+def test_fast_exact_on_quantized_inputs(name, L, P, Q, N):
+    a = ALGS_BY_NAME[name]
+    A, B = I.problem(P, Q, N, seed=5, kind="quantized")
+    s = 2.0 ** 11
+    exact = _exact(A * s, B * s) / (s * s)
+    assert np.array_equal(O.fast(A, B, a, L), exact)
+
+
+# ---- check (d): error growth within the fixed tolerance (reading R16: parity of the growth
+# itself is unpinned by the paper; the gate is BASELINE's 1e-10*|A|_F|B|_F for L <= 3) --------
+@pytest.mark.parametrize("name", list(ALGS_BY_NAME))
+def test_fast_float_error_within_fixed_tolerance(name):
+    a = ALGS_BY_NAME[name]
+    P, Q, N = (a.M ** 3 * 3, a.K ** 3 * 3, a.N ** 3 * 3) if a.M * a.K * a.N <= 12 else (a.M ** 2 * 7, a.K ** 2 * 7, a.N ** 2 * 7)
+    A, B = I.problem(P, Q, N, seed=6)
+    Cc = O.classical(A, B)
+    nrm = np.linalg.norm(A) * np.linalg.norm(B)
+    errs = []
+    for L in (1, 2, 3) if a.M * a.K * a.N <= 12 else (1, 2):
+        e = np.max(np.abs(O.fast(A, B, a, L) - Cc)) / nrm
+        errs.append(e)
+        assert e <= 1e-10
+    assert errs[0] < 1e-15  # rounding-level, far below the gate
+
+
+# ---- the sampled-entry oracle is bit-identical to the full oracle ------------------------------
+@pytest.mark.parametrize("name,L,P,Q,N", [
+    ("strassen_222_7", 3, 37, 41, 43), ("winograd_class_222_7", 2, 64, 64, 64),
+    ("hk_class_323_15", 2, 101, 67, 89), ("alg_424_26", 2, 70, 9, 66),
+    ("laderman_class_333_23", 2, 29, 31, 28), ("alg_433_29", 2, 50, 29, 31)])
+def test_fast_entries_bit_identical_to_fast(name, L, P, Q, N):
+    a = ALGS_BY_NAME[name]
+    A, B = I.problem(P, Q, N, seed=8)
+    C = O.fast(A, B, a, L)
+    rows, cols = np.meshgrid(np.arange(P), np.arange(N), indexing="ij")
+    e = O.fast_entries(A, B, a, L, rows.reshape(-1), cols.reshape(-1))
+    assert np.array_equal(e.reshape(P, N), C)
+    ce = O.classical_entries(A, B, [0, P - 1, P // 2], [N - 1, 0, N // 3])
+    Cc = O.classical(A, B)
+    assert np.array_equal(ce, np.array([Cc[0, N - 1], Cc[P - 1, 0], Cc[P // 2, N // 3]]))
+
+
+# ---- flop counts: Sec. 2.1 closed forms ----------------------------------------
+def test_flop_count_closed_forms():
+    rows = [ln.split() for ln in open(os.path.join(GOLDEN, "flop_counts.txt")) if ln.strip() and ln[0] != "#"]
+    s = ALGS_BY_NAME["strassen_222_7"]
+    for kind, n, val in rows:
+        n, val = int(n), int(val)
+        L = 0 if kind == "classical" else int(math.log2(n))
+        assert O.flops(n, n, n, s, L) == val
+    for k in range(0, 7):
+        n = 2 ** k
+        assert O.flops(n, n, n, s, 0) == 2 * n ** 3 - n ** 2
+        assert O.flops(n, n, n, s, k) == round(7 * n ** math.log2(7) - 6 * n ** 2)
