@@ -1,0 +1,181 @@
+/*
+ * fmm.h — C ABI of the B200-native recursive fast matrix multiplication library (libfmm.so).
+ *
+ * The method (arXiv 1409.2908, Benson & Ballard; PAPER.md cited as P:<line>): C = A*B computed by
+ * a bilinear <M,K,N;R> base-case algorithm given as coefficient matrices (U,V,W) (Sec. 2.2,
+ * P:295-331, Eq. lowrank), applied for L recursive steps (Sec. 2.1; Sec. 3.1):
+ *   S_r = sum_i u_ir A_i,  T_r = sum_j v_jr B_j,  M_r = S_r * T_r (recursively),  C_k = sum_r w_kr M_r
+ * with dynamic peeling of non-divisible dimensions at every level (Sec. 3.5).
+ *
+ * Conventions shared by every entry point
+ *  - Every function returns fmm_status_t; no C++ exception crosses the ABI.  On failure a
+ *    human-readable message is available from fmm_last_error() (thread-local, valid until the
+ *    next fmm_* call on the same thread).
+ *  - Block numbering follows the paper's row-major vectorisation: A-block (a,b) of the
+ *    M x K block grid is row a*K+b of U; B-block (b,c) is row b*N+c of V; C-block (a,c) is row
+ *    a*N+c of W.  Matrices U (MK x R), V (KN x R), W (MN x R) are passed row-major.
+ *  - All matrix data is IEEE binary64.  Leading dimensions are in elements.
+ *  - Device pointers passed to fmm_execute are owned by the caller and must live on the plan's
+ *    device; the library never allocates or frees caller buffers.  A plan owns its workspace.
+ *  - Arguments are validated before any device work; invalid ones return FMM_E_INVALID_ARG or
+ *    FMM_E_SHAPE and leave device state untouched.
+ *  - There is no CPU fallback: every arithmetic step of fmm_execute runs in this library's
+ *    sm_100a kernels.
+ */
+#ifndef FMM_H
+#define FMM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FMM_OK = 0,
+  FMM_E_INVALID_ARG = 1,   /* null pointer, negative size, bad option value */
+  FMM_E_NOT_EXACT = 2,     /* (U,V,W) fails the Brent equations */
+  FMM_E_SHAPE = 3,         /* non-conformable dimensions or too-small leading dimensions */
+  FMM_E_NO_MEMORY = 4,     /* workspace allocation failed or exceeds workspace_limit_bytes */
+  FMM_E_CUDA = 5,          /* a CUDA runtime / NVRTC error; message has the CUDA string */
+  FMM_E_NCCL = 6,          /* reserved for communicator errors */
+  FMM_E_UNSUPPORTED = 7,   /* e.g. APA (lambda) algorithms, too many recursion levels */
+  FMM_E_PARSE = 8          /* algorithm file syntax error; message names the line */
+} fmm_status_t;
+
+typedef struct fmm_alg_s fmm_alg;   /* immutable after creation; safe to share between threads */
+typedef struct fmm_plan_s fmm_plan_t; /* owns its workspace; one fmm_execute in flight per plan */
+
+typedef enum { FMM_ROW_MAJOR = 0, FMM_COL_MAJOR = 1 } fmm_layout;
+
+/* Addition-chain implementations (Sec. 3.2).  STREAMING: one kernel per phase reads
+   every input block once and writes every formed S_r / T_r (or C_k) once.
+   WRITE_ONCE: one output stream per S_r / T_r / C_k, each reading the blocks of its chain
+   (P:628-632).  (Pairwise daxpy chains, are not offered.) */
+typedef enum { FMM_ADD_STREAMING = 0, FMM_ADD_WRITE_ONCE = 1 } fmm_add_strategy;
+
+typedef struct {
+  int layout;               /* fmm_layout of A, B and C (all three share it) */
+  int strategy;             /* fmm_add_strategy */
+  int cse;                  /* 1: greedy length-two common-subexpression elimination in the
+                               streaming kernels (Sec. 3.3); temporaries live in
+                               registers.  0: every chain is summed in ascending index order
+                               (bit-identical to the oracle's order). */
+  int shard_rank;           /* multi-GPU leaf sharding (Sec. 4.3 HYBRID arithmetic, P:823-829,
+                               with GPUs in place of threads): this plan computes the partial
+                               product of its share of the R^L leaves; summing the C of all
+                               shard_count plans gives A*B.  0 / 1 for a single GPU. */
+  int shard_count;
+  size_t workspace_limit_bytes; /* 0 = no limit */
+} fmm_plan_options;
+
+/* Fill *opt with the defaults: row-major, streaming, cse = 1, shard 0 of 1, no limit. */
+void fmm_plan_options_default(fmm_plan_options* opt);
+
+/* ---- algorithms ------------------------------------------------------------------------- */
+
+/* Create an algorithm for base case <M,K,N> of rank R from exact rational coefficients
+   num/den (den > 0).  U_num/U_den are MK x R row-major, V_* KN x R, W_* MN x R.
+   The Brent equations sum_r u_ir v_jr w_kr = T_ijk, with T the matmul tensor of
+   P:412-421, are verified EXACTLY in 128-bit rational arithmetic over all (MK)(KN)(MN)
+   triples; any violation returns FMM_E_NOT_EXACT and *out is left NULL.
+   Limits: 1 <= M,K,N <= 16, 1 <= R <= 4096.  Host only; no device work. */
+fmm_status_t fmm_alg_create(int M, int K, int N, int R,
+                            const int64_t* U_num, const int64_t* U_den,
+                            const int64_t* V_num, const int64_t* V_den,
+                            const int64_t* W_num, const int64_t* W_den, fmm_alg** out);
+
+/* Load the text format of SPEC S:190: '#' comments; a header line "M K N R exact"; MK rows of
+   R entries (U), a blank line, KN rows (V), a blank line, MN rows (W).  Entries are integers or
+   rationals p/q.  Syntax errors return FMM_E_PARSE with the 1-based line number in the
+   message; APA files ("apa") return FMM_E_UNSUPPORTED; then validates as fmm_alg_create. */
+fmm_status_t fmm_alg_load(const char* path, fmm_alg** out);
+
+/* Query shape and sparsity: dims[0..3] = M,K,N,R; nnz[0..2] = nnz(U), nnz(V), nnz(W). */
+fmm_status_t fmm_alg_info(const fmm_alg* alg, int dims[4], int nnz[3]);
+void fmm_alg_destroy(fmm_alg* alg);
+
+/* ---- plans ------------------------------------------------------------------------------ */
+
+/* Plan C (P x Nc) = A (P x Q) * B (Q x Nc) with `levels` recursive steps (0 = one classical
+   DMMA GEMM).  The recursion stops early at a level whose sub-problem is smaller than the base
+   case (reading R10/R18 of DESIGN.md).  Column-major problems are planned through the
+   transposed algorithm of Prop. 1: a column-major P x Q array is the row-major
+   Q x P array of its transpose, so C^T = B^T A^T runs with <N,K,M> and no data moves.
+   Allocates the workspace on `device` with cudaMalloc; returns FMM_E_NO_MEMORY if that fails
+   or exceeds opt->workspace_limit_bytes (the message states the bytes needed: BFS execution
+   keeps every level's S_r, T_r and M_r resident, R/(MN) times the output per step).
+   Compiles the plan's addition kernels (NVRTC, sm_100a) on first use of an algorithm/variant.
+   opt may be NULL (defaults). */
+fmm_status_t fmm_plan_create(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels,
+                             const fmm_plan_options* opt, int device, fmm_plan_t** out);
+
+/* Workspace bytes held by the plan. */
+fmm_status_t fmm_plan_workspace_bytes(const fmm_plan_t* plan, size_t* bytes);
+
+/* Predicted work of one fmm_execute, per phase, from the plan's own chain/kernel structure:
+   [0] leaf GEMM flops (2 m n k per leaf product and peel strip)
+   [1] addition flops (one per add/sub in the emitted chains)
+   [2] addition-kernel algorithmic HBM bytes (8 B per element read or written by the
+       formation and assembly kernels, Sec. 3.2 counts P:638-653 in bytes)
+   [3] leaf GEMM operand/result bytes at one read of S, T and one write of M per leaf
+   [4] number of kernel launches per execute
+   [5] effective levels used
+   [6] number of leaf products computed by this plan (its shard)
+   [7] the paper's effective-GFLOPS numerator 2PQN - PN  */
+fmm_status_t fmm_plan_stats(const fmm_plan_t* plan, double out[8]);
+
+/* Execute C <- A*B (beta = 0: C is overwritten).  A, B, C are device pointers on the plan's
+   device laid out per opt->layout; C must not alias A or B.  Leading dimensions in elements:
+   row-major lda >= Q, ldb >= Nc, ldc >= Nc; column-major lda >= P, ldb >= Q, ldc >= P.
+   `stream` is a cudaStream_t (NULL = legacy default stream).  Stream-ordered and
+   asynchronous: returns after enqueueing; launch errors return FMM_E_CUDA, and asynchronous
+   kernel faults surface at the next fmm_* call on that plan or at fmm_sync.
+   With shard_count > 1 the result is this shard's partial product (sum over shards = A*B). */
+fmm_status_t fmm_execute(fmm_plan_t* plan, const double* A, int64_t lda, const double* B, int64_t ldb,
+                         double* C, int64_t ldc, void* stream);
+
+/* Same, timing the phases with CUDA events on `stream` (blocking: synchronises the stream).
+   ms[0] = formation kernels, ms[1] = leaf GEMM kernels, ms[2] = assembly kernels,
+   ms[3] = peel-strip GEMMs, ms[4] = total. */
+fmm_status_t fmm_execute_timed(fmm_plan_t* plan, const double* A, int64_t lda, const double* B,
+                               int64_t ldb, double* C, int64_t ldc, void* stream, float ms[5]);
+
+/* Host-memory execution (the end-to-end path): copies A and B (host, pinned or pageable) to
+   device staging buffers owned by the plan, executes, and copies C back to host, all on
+   `stream`; synchronises before returning. */
+fmm_status_t fmm_execute_host(fmm_plan_t* plan, const double* A, int64_t lda, const double* B,
+                              int64_t ldb, double* C, int64_t ldc, void* stream);
+
+/* Block until every fmm_execute on the plan has finished; reports asynchronous faults. */
+fmm_status_t fmm_sync(fmm_plan_t* plan);
+void fmm_plan_destroy(fmm_plan_t* plan);
+
+/* Short spellings of the north-star API: fmm_plan(alg U/V/W, M,K,N, levels) and
+   fmm_execute(A,B,C) (BASELINE.json).  fmm_plan == fmm_plan_create with default options on
+   the current device; fmm_exec == fmm_execute with tight leading dimensions on the default
+   stream. */
+fmm_status_t fmm_plan(const fmm_alg* alg, int64_t M, int64_t K, int64_t N, int levels, fmm_plan_t** out);
+fmm_status_t fmm_exec(fmm_plan_t* plan, const double* A, const double* B, double* C);
+
+/* ---- leaf sharding arithmetic (host only, Sec. 4.3) --------------------------- */
+
+/* For R^L leaves over G workers: *bfs = R^L - (R^L mod G) leaves split evenly (contiguous,
+   r_1-major), *dfs = R^L mod G leaves split by rows over all G. */
+fmm_status_t fmm_hybrid_split(int64_t R, int L, int64_t G, int64_t* bfs, int64_t* dfs);
+
+/* ---- kernels usable on their own (device pointers, stream-ordered) ---------------------- */
+
+/* Classical product C = alpha*A*B + beta*C with the library's DMMA GEMM kernel (row-major,
+   mma.sync f64 on the FP64 tensor pipe).  The L = 0 path of a plan. */
+fmm_status_t fmm_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda,
+                       const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* stream);
+
+const char* fmm_last_error(void);
+const char* fmm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FMM_H */

@@ -1,0 +1,118 @@
+// Internal declarations of libfmm (not part of the C ABI).  Shares nothing with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/fmm.h"
+
+namespace fmm {
+
+// ---- errors --------------------------------------------------------------------------------
+struct Error : std::runtime_error {
+  fmm_status_t code;
+  Error(fmm_status_t c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+void set_last_error(const std::string& msg);
+
+// Every extern "C" entry point wraps its body in these: no C++ exception crosses the ABI.
+#define FMM_API_BEGIN try {
+#define FMM_API_END                              \
+  }                                              \
+  catch (const ::fmm::Error& e) {                \
+    ::fmm::set_last_error(e.what());             \
+    return e.code;                               \
+  }                                              \
+  catch (const std::bad_alloc&) {                \
+    ::fmm::set_last_error("host out of memory"); \
+    return FMM_E_NO_MEMORY;                      \
+  }                                              \
+  catch (const std::exception& e) {              \
+    ::fmm::set_last_error(e.what());             \
+    return FMM_E_INVALID_ARG;                    \
+  }
+#define FMM_CUDA(x)                                                                              \
+  do {                                                                                           \
+    cudaError_t e_ = (x);                                                                        \
+    if (e_ != cudaSuccess)                                                                       \
+      throw ::fmm::Error(FMM_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_) + " (" + \
+                                         __FILE__ + ":" + std::to_string(__LINE__) + ")");      \
+  } while (0)
+
+// ---- exact rationals (coefficient storage, Brent check) ------------------------------------
+struct Rat {
+  __int128 n = 0, d = 1;  // d > 0, gcd(n, d) = 1
+};
+Rat rat_make(__int128 n, __int128 d);
+Rat rat_add(Rat a, Rat b);
+Rat rat_mul(Rat a, Rat b);
+inline bool rat_is_zero(const Rat& a) { return a.n == 0; }
+inline double rat_to_double(const Rat& a) { return (double)a.n / (double)a.d; }
+
+}  // namespace fmm
+
+// The algorithm object behind the opaque ABI handle.
+struct fmm_alg_s {
+  int M, K, N, R;
+  std::vector<fmm::Rat> U, V, W;   // row-major MK x R, KN x R, MN x R
+  std::vector<double> Ud, Vd, Wd;  // the same as doubles
+};
+
+namespace fmm {
+
+fmm_alg* alg_transpose_prop1(const fmm_alg& a);  // Prop. 1: <N,K,M>
+void alg_validate_exact(const fmm_alg& a);        // throws FMM_E_NOT_EXACT
+
+// ---- grouped DMMA GEMM (K2 / K4 / K5) -------------------------------------------------------
+struct GemmTask {
+  const double* A;
+  const double* B;
+  double* C;
+  long long lda, ldb, ldc;
+  int m, n, k;
+  int tiles_m, tiles_n;
+  int tile_begin;  // prefix sum of tiles over the task list
+  double alpha, beta;
+};
+// Fill tiles_m/tiles_n/tile_begin; returns the total number of CTA tiles.
+long long gemm_prepare(std::vector<GemmTask>& tasks);
+bool gemm_tasks_aligned16(const std::vector<GemmTask>& tasks);
+// Launch over a device copy of the prepared task list.
+void gemm_launch(const GemmTask* d_tasks, int ntasks, long long total_tiles, bool aligned16,
+                 cudaStream_t stream);
+int gemm_tile_m();
+int gemm_tile_n();
+
+// ---- linear-combination (addition chain) kernels, generated and compiled with NVRTC --------
+// One kernel computes, for every element position of a block, out_o = sum_i coef[o][i] * in_i.
+struct LincombSpec {
+  int nin = 0, nout = 0;
+  std::vector<double> coef;  // nout x nin, row-major; chain order = ascending input index
+  int strategy = FMM_ADD_STREAMING;
+  int cse = 0;
+  int vec = 2;  // doubles per thread access (2 = 16-byte vectors)
+};
+struct LincombKernel;  // compiled function handle
+// Per-node pointer table entry layout used by every generated kernel:
+//   const double* in[nin]; double* out[nout]; long long ld_in; long long ld_out;
+size_t lincomb_node_bytes(int nin, int nout);
+std::shared_ptr<LincombKernel> lincomb_get(const LincombSpec& spec);
+// Launch over `nodes` node entries (device table) for blocks of rows x cols elements.
+void lincomb_launch(const LincombKernel& k, const void* d_nodes, int nnodes, long long rows, long long cols,
+                    cudaStream_t stream);
+// Statistics of the generated code (for fmm_plan_stats): additions per element, and per-element
+// reads/writes of the kernel as launched.
+struct LincombCost {
+  double adds_per_elem;
+  double reads_per_elem;   // elements read (inputs) per element position
+  double writes_per_elem;  // elements written per element position
+};
+LincombCost lincomb_cost(const LincombKernel& k);
+int lincomb_cse_temps(const LincombKernel& k);
+std::string lincomb_source(const LincombKernel& k);
+
+}  // namespace fmm

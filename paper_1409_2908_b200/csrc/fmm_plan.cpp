@@ -1,0 +1,842 @@
+// L2: the plan compiler and executor.
+//
+// A plan turns (algorithm, P x Q x N problem, L steps, options) into a fixed sequence of kernel
+// launches over a breadth-first recursion tree (the paper's BFS scheme, Sec. 4.2, P:804-821,
+// with every node of a level processed by ONE batched launch instead of one OpenMP task each):
+//
+//   for l = 1..L:   K1 formation, A side: S of every level-l node from its parent's blocks
+//                   K1 formation, B side: T likewise                       (Sec. 3.2)
+//   level L:        K2 grouped DMMA GEMM over all leaves: M = alpha * S * T
+//   for l = L..1:   K3 assembly: parent C_k = sum_r w_kr M_r
+//                   K4 peel strips of the level-(l-1) nodes (grouped GEMM)
+//
+// Views: every operand is (pointer, leading dimension, scalar sigma).  A column of U or V with a
+// single nonzero is not formed: the child view aliases the parent block and its coefficient is
+// piped into sigma, which reaches the leaf GEMM as alpha.
+// Peeling: core P' = M floor(P/M) etc. at every level; strips per SPEC S:287-295 (R7).
+// Column-major: Prop. 1 transpose, the problem becomes N x Q x P with A and B swapped.
+// Sharding: HYBRID arithmetic over GPUs: the first R^L - (R^L mod G) leaves are split
+// evenly and contiguously, the remaining R^L mod G leaves are split by rows over all G.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "fmm_internal.h"
+
+using namespace fmm;
+
+namespace {
+
+struct View {
+  double* ptr = nullptr;
+  long long ld = 0;
+  double sigma = 1.0;
+};
+
+struct Dims {
+  long long P, Q, N;     // node problem at this level: (P x Q) * (Q x N)
+  long long P1, Q1, N1;  // divisible core (only meaningful below the last level)
+};
+
+struct Launch {
+  enum Kind { FORM_A, FORM_B, GEMM, ASSEMBLE, STRIPS } kind;
+  int level = 0;
+  size_t table_off = 0;  // byte offset in the device table buffer
+  int count = 0;         // nodes / tasks
+  long long rows = 0, cols = 0;
+  std::shared_ptr<LincombKernel> kern;
+  long long tiles = 0;
+  bool aligned16 = true;
+  double elem_reads = 0, elem_writes = 0, elem_adds = 0;  // totals over the launch (elements)
+  double flops = 0, gemm_bytes = 0;
+};
+
+long long round_up(long long x, long long m) { return (x + m - 1) / m * m; }
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+}  // namespace
+
+struct fmm_plan_s {
+  int device = 0;
+  fmm_plan_options opt{};
+  bool colmajor = false;
+  std::unique_ptr<fmm_alg> alg_t;  // Prop. 1 transpose (column-major plans)
+  const fmm_alg* alg = nullptr;     // the algorithm run (row-major orientation)
+  long long P = 0, Q = 0, N = 0;    // row-major problem dims after the transpose
+  long long userP = 0, userQ = 0, userN = 0;
+  int L = 0;
+  int R = 0;
+  std::vector<Dims> dims;  // levels 0..L
+  std::vector<long long> nodes_at;  // R^l
+
+  // columns of U / V: formed (nnz != 1) or singleton (block index, coefficient)
+  std::vector<int> formU, formV;             // formed column list (order = kernel output order)
+  std::vector<int> idxU, idxV;               // for each r: output slot if formed, else -1
+  std::vector<int> singU, singV;             // for each r: block index if singleton
+  std::vector<double> coefU, coefV;          // for each r: singleton coefficient
+
+  // sharding
+  long long leaves = 1;
+  std::vector<long long> leaf_r0, leaf_r1;   // active row range of each leaf (r0 == r1: inactive)
+  std::vector<std::vector<char>> needed;     // [level][node]
+  std::vector<std::vector<char>> strip_owner;// [level][node]
+
+  // workspace
+  double* ws = nullptr;
+  size_t ws_bytes = 0;
+  std::vector<long long> ldS, ldT, ldM;
+  std::vector<std::vector<long long>> offS, offT, offM;  // element offsets in ws, -1 = none
+  std::vector<long long> offZero;                        // per level: zero M block (shared)
+
+  // kernels (vec 2 / vec 1 variants created lazily)
+  std::shared_ptr<LincombKernel> kU[3], kV[3], kW[3];
+
+  // launch tables
+  std::vector<Launch> launches;
+  std::vector<char> h_tab;
+  char* h_pinned = nullptr;
+  char* d_tab = nullptr;
+  size_t tab_bytes = 0;
+  bool tab_valid = false;
+  const double* cA = nullptr;
+  const double* cB = nullptr;
+  double* cC = nullptr;
+  long long clda = -1, cldb = -1, cldc = -1;
+  cudaEvent_t upload_done = nullptr;
+  cudaEvent_t ev[8] = {};
+
+  // host-execute staging
+  double *sA = nullptr, *sB = nullptr, *sC = nullptr;
+
+  ~fmm_plan_s() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    if (upload_done) cudaEventSynchronize(upload_done);
+    cudaDeviceSynchronize();
+    if (ws) cudaFree(ws);
+    if (d_tab) cudaFree(d_tab);
+    if (h_pinned) cudaFreeHost(h_pinned);
+    if (sA) cudaFree(sA);
+    if (sB) cudaFree(sB);
+    if (sC) cudaFree(sC);
+    if (upload_done) cudaEventDestroy(upload_done);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    cudaSetDevice(cur);
+  }
+
+  std::shared_ptr<LincombKernel> kernel(int side, int vec) {
+    auto* slot = side == 0 ? kU : side == 1 ? kV : kW;
+    if (slot[vec]) return slot[vec];
+    LincombSpec s;
+    s.strategy = opt.strategy;
+    s.cse = opt.cse;
+    s.vec = vec;
+    const int M = alg->M, K = alg->K, Nb = alg->N;
+    if (side == 0 || side == 1) {
+      const int rows = side == 0 ? M * K : K * Nb;
+      const auto& X = side == 0 ? alg->Ud : alg->Vd;
+      const auto& form = side == 0 ? formU : formV;
+      s.nin = rows;
+      s.nout = (int)form.size();
+      s.coef.assign((size_t)s.nin * s.nout, 0.0);
+      for (int o = 0; o < s.nout; ++o)
+        for (int i = 0; i < rows; ++i) s.coef[(size_t)o * rows + i] = X[(size_t)i * R + form[o]];
+    } else {
+      s.nin = R;
+      s.nout = M * Nb;
+      s.coef.assign((size_t)s.nin * s.nout, 0.0);
+      for (int k = 0; k < M * Nb; ++k)
+        for (int r = 0; r < R; ++r) s.coef[(size_t)k * R + r] = alg->Wd[(size_t)k * R + r];
+    }
+    slot[vec] = lincomb_get(s);
+    return slot[vec];
+  }
+
+  long long node_first_leaf(int l, long long z) const {
+    long long f = z;
+    for (int q = l; q < L; ++q) f *= R;
+    return f;
+  }
+  long long node_leaf_span(int l) const {
+    long long f = 1;
+    for (int q = l; q < L; ++q) f *= R;
+    return f;
+  }
+
+  void setup_sharding() {
+    const long long G = std::max(1, opt.shard_count), g = opt.shard_rank;
+    leaves = nodes_at[L];
+    const long long dfs = leaves % G, bfs = leaves - dfs;
+    leaf_r0.assign(leaves, 0);
+    leaf_r1.assign(leaves, 0);
+    const long long pL = dims[L].P;
+    const long long per = bfs / G;
+    for (long long z = 0; z < leaves; ++z) {
+      if (z < bfs) {
+        if (z >= g * per && z < (g + 1) * per) leaf_r0[z] = 0, leaf_r1[z] = pL;
+      } else {
+        leaf_r0[z] = pL * g / G;
+        leaf_r1[z] = pL * (g + 1) / G;
+      }
+    }
+    needed.assign(L + 1, {});
+    strip_owner.assign(L + 1, {});
+    for (int l = 0; l <= L; ++l) {
+      needed[l].assign(nodes_at[l], 0);
+      strip_owner[l].assign(nodes_at[l], 0);
+    }
+    for (long long z = 0; z < leaves; ++z)
+      if (leaf_r1[z] > leaf_r0[z]) needed[L][z] = 1;
+    // strips of a node: computed by the rank owning its first leaf (rank 0 for remainder leaves)
+    for (int l = 0; l < L; ++l) {
+      const bool has_strips = dims[l].P1 < dims[l].P || dims[l].Q1 < dims[l].Q || dims[l].N1 < dims[l].N;
+      if (!has_strips) continue;
+      for (long long z = 0; z < nodes_at[l]; ++z) {
+        const long long f = node_first_leaf(l, z);
+        const long long owner = f < bfs ? (per > 0 ? f / per : 0) : 0;
+        if (owner == g) strip_owner[l][z] = 1, needed[l][z] = 1;
+      }
+    }
+    for (int l = L; l >= 1; --l)
+      for (long long z = 0; z < nodes_at[l]; ++z)
+        if (needed[l][z]) needed[l - 1][z / R] = 1;
+    needed[0][0] = 1;  // the root always writes C (zeros if this shard owns nothing)
+  }
+
+  void setup_workspace() {
+    ldS.assign(L + 1, 0);
+    ldT.assign(L + 1, 0);
+    ldM.assign(L + 1, 0);
+    offS.assign(L + 1, {});
+    offT.assign(L + 1, {});
+    offM.assign(L + 1, {});
+    offZero.assign(L + 1, -1);
+    long long total = 0;
+    auto take = [&](long long elems) {
+      const long long o = total;
+      total += round_up(elems, 32);  // 256-byte aligned blocks
+      return o;
+    };
+    for (int l = 1; l <= L; ++l) {
+      const Dims& d = dims[l];
+      ldS[l] = round_up(d.Q, 16);
+      ldT[l] = round_up(d.N, 16);
+      ldM[l] = round_up(d.N, 16);
+      offS[l].assign(nodes_at[l], -1);
+      offT[l].assign(nodes_at[l], -1);
+      offM[l].assign(nodes_at[l], -1);
+      bool any_unneeded = false;
+      for (long long z = 0; z < nodes_at[l]; ++z) {
+        const int r = (int)(z % R);
+        if (!needed[l][z]) {
+          any_unneeded = true;
+          continue;
+        }
+        if (idxU[r] >= 0) offS[l][z] = take(d.P * ldS[l]);
+        if (idxV[r] >= 0) offT[l][z] = take(d.Q * ldT[l]);
+        offM[l][z] = take(d.P * ldM[l]);
+      }
+      if (any_unneeded) offZero[l] = take(d.P * ldM[l]);
+    }
+    ws_bytes = (size_t)total * sizeof(double);
+    if (opt.workspace_limit_bytes && ws_bytes > opt.workspace_limit_bytes)
+      throw Error(FMM_E_NO_MEMORY, "plan needs " + std::to_string(ws_bytes) + " workspace bytes (all S_r, T_r, M_r of " +
+                                       std::to_string(L) + " BFS levels resident, R/(MN) x the output per step, P:820) > limit " +
+                                       std::to_string(opt.workspace_limit_bytes));
+    if (ws_bytes) {
+      cudaError_t e = cudaMalloc(&ws, ws_bytes);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        ws = nullptr;
+        throw Error(FMM_E_NO_MEMORY, "cudaMalloc of " + std::to_string(ws_bytes) + " workspace bytes failed");
+      }
+      // zero blocks of partially-owned leaves and shared zero blocks must read as zeros
+      FMM_CUDA(cudaMemset(ws, 0, ws_bytes));
+    }
+  }
+
+  View opA(int l, long long z, const View& root) const;
+  View opB(int l, long long z, const View& root) const;
+
+  // Build every launch and its table for the given execute arguments (row-major orientation).
+  void build(const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc, bool lazy_kernels);
+};
+
+View fmm_plan_s::opA(int l, long long z, const View& root) const {
+  if (l == 0) return root;
+  const int r = (int)(z % R);
+  const View par = opA(l - 1, z / R, root);
+  if (idxU[r] >= 0) return View{offS[l][z] >= 0 ? ws + offS[l][z] : nullptr, ldS[l], par.sigma};
+  const int i = singU[r];
+  const Dims& d = dims[l];
+  return View{par.ptr ? par.ptr + (i / alg->K) * d.P * par.ld + (i % alg->K) * d.Q : nullptr, par.ld,
+              par.sigma * coefU[r]};
+}
+
+View fmm_plan_s::opB(int l, long long z, const View& root) const {
+  if (l == 0) return root;
+  const int r = (int)(z % R);
+  const View par = opB(l - 1, z / R, root);
+  if (idxV[r] >= 0) return View{offT[l][z] >= 0 ? ws + offT[l][z] : nullptr, ldT[l], par.sigma};
+  const int j = singV[r];
+  const Dims& d = dims[l];
+  return View{par.ptr ? par.ptr + (j / alg->N) * d.Q * par.ld + (j % alg->N) * d.N : nullptr, par.ld,
+              par.sigma * coefV[r]};
+}
+
+static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+void fmm_plan_s::build(const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc,
+                       bool lazy_kernels) {
+  launches.clear();
+  h_tab.clear();
+  const View rootA{const_cast<double*>(A), lda, 1.0}, rootB{const_cast<double*>(B), ldb, 1.0};
+  const View rootC{C, ldc, 1.0};
+  const int M = alg->M, K = alg->K, Nb = alg->N;
+  auto push = [&](const void* p, size_t n) {
+    size_t off = h_tab.size();
+    h_tab.resize(align256(off + n));
+    std::memcpy(h_tab.data() + off, p, n);
+    return off;
+  };
+  auto outView = [&](int l, long long z) -> View {
+    if (l == 0) return rootC;
+    if (offM[l][z] >= 0) return View{ws + offM[l][z], ldM[l], 1.0};
+    return View{offZero[l] >= 0 ? ws + offZero[l] : nullptr, ldM[l], 1.0};
+  };
+
+  // ---- formation, levels 1..L ----
+  for (int l = 1; l <= L; ++l) {
+    const Dims& d = dims[l];
+    for (int side = 0; side < 2; ++side) {
+      const auto& form = side == 0 ? formU : formV;
+      if (form.empty()) continue;
+      const int nin = side == 0 ? M * K : K * Nb;
+      const int nout = (int)form.size();
+      const long long rows = side == 0 ? d.P : d.Q, cols = side == 0 ? d.Q : d.N;
+      if (rows <= 0 || cols <= 0) continue;
+      std::vector<char> tab;
+      const size_t nb = lincomb_node_bytes(nin, nout);
+      bool aligned = (cols % 2) == 0;
+      int count = 0;
+      double writes = 0;
+      for (long long zp = 0; zp < nodes_at[l - 1]; ++zp) {
+        if (!needed[l - 1][zp]) continue;
+        bool any = false;
+        for (int o = 0; o < nout; ++o) any |= needed[l][zp * R + form[o]] != 0;
+        if (!any) continue;
+        const View par = side == 0 ? opA(l - 1, zp, rootA) : opB(l - 1, zp, rootB);
+        std::vector<char> e(nb, 0);
+        auto** in = reinterpret_cast<const double**>(e.data());
+        auto** out = reinterpret_cast<double**>(e.data() + sizeof(void*) * nin);
+        auto* lds = reinterpret_cast<long long*>(e.data() + sizeof(void*) * (nin + nout));
+        for (int i = 0; i < nin; ++i) {
+          const long long off = side == 0 ? (i / K) * d.P * par.ld + (i % K) * d.Q : (i / Nb) * d.Q * par.ld + (i % Nb) * d.N;
+          in[i] = par.ptr + off;
+          aligned &= al16(in[i]);
+        }
+        for (int o = 0; o < nout; ++o) {
+          const long long z = zp * R + form[o];
+          const long long offv = side == 0 ? offS[l][z] : offT[l][z];
+          out[o] = needed[l][z] && offv >= 0 ? ws + offv : nullptr;
+          if (out[o]) writes += 1;
+        }
+        lds[0] = par.ld;
+        lds[1] = side == 0 ? ldS[l] : ldT[l];
+        aligned &= (lds[0] % 2 == 0) && (lds[1] % 2 == 0);
+        tab.insert(tab.end(), e.begin(), e.end());
+        ++count;
+      }
+      if (!count) continue;
+      Launch ln;
+      ln.kind = side == 0 ? Launch::FORM_A : Launch::FORM_B;
+      ln.level = l;
+      ln.count = count;
+      ln.rows = rows;
+      ln.cols = cols;
+      ln.aligned16 = aligned;
+      if (!lazy_kernels) ln.kern = kernel(side, aligned ? 2 : 1);
+      const auto k = kernel(side, 2);  // cost model is vec-independent
+      const LincombCost c = lincomb_cost(*k);
+      const double elems = (double)rows * cols;
+      ln.elem_adds = c.adds_per_elem * elems * count;
+      if (opt.strategy == FMM_ADD_STREAMING) {
+        ln.elem_reads = c.reads_per_elem * elems * count;
+        ln.elem_writes = writes * elems;
+      } else {
+        ln.elem_reads = c.reads_per_elem * elems * count;  // sum of chain lengths per node
+        ln.elem_writes = writes * elems;
+      }
+      ln.table_off = push(tab.data(), tab.size());
+      launches.push_back(ln);
+    }
+  }
+
+  // ---- leaf GEMMs ----
+  {
+    std::vector<GemmTask> tasks;
+    const Dims& d = dims[L];
+    for (long long z = 0; z < nodes_at[L]; ++z) {
+      const long long r0 = leaf_r0[z], r1 = leaf_r1[z];
+      if (r1 <= r0) continue;
+      const View a = opA(L, z, rootA), b = opB(L, z, rootB), c = outView(L, z);
+      GemmTask t{};
+      t.A = a.ptr + r0 * a.ld;
+      t.B = b.ptr;
+      t.C = c.ptr + r0 * c.ld;
+      t.lda = a.ld;
+      t.ldb = b.ld;
+      t.ldc = c.ld;
+      t.m = (int)(r1 - r0);
+      t.n = (int)d.N;
+      t.k = (int)d.Q;
+      t.alpha = a.sigma * b.sigma;
+      t.beta = 0.0;
+      if (t.m > 0 && t.n > 0) tasks.push_back(t);
+    }
+    if (!tasks.empty()) {
+      Launch ln;
+      ln.kind = Launch::GEMM;
+      ln.level = L;
+      ln.tiles = gemm_prepare(tasks);
+      ln.count = (int)tasks.size();
+      ln.aligned16 = gemm_tasks_aligned16(tasks);
+      for (auto& t : tasks) {
+        ln.flops += 2.0 * t.m * t.n * (double)t.k;
+        ln.gemm_bytes += 8.0 * ((double)t.m * t.k + (double)t.k * t.n + (double)t.m * t.n);
+      }
+      ln.table_off = push(tasks.data(), tasks.size() * sizeof(GemmTask));
+      launches.push_back(ln);
+    }
+  }
+
+  // ---- assembly and peel strips, levels L..1 ----
+  for (int l = L; l >= 1; --l) {
+    const Dims& d = dims[l];
+    const Dims& dp = dims[l - 1];
+    if (d.P > 0 && d.N > 0) {
+      std::vector<char> tab;
+      const int nin = R, nout = M * Nb;
+      const size_t nb = lincomb_node_bytes(nin, nout);
+      bool aligned = (d.N % 2) == 0;
+      int count = 0;
+      for (long long zp = 0; zp < nodes_at[l - 1]; ++zp) {
+        if (!needed[l - 1][zp]) continue;
+        const View par = outView(l - 1, zp);
+        std::vector<char> e(nb, 0);
+        auto** in = reinterpret_cast<const double**>(e.data());
+        auto** out = reinterpret_cast<double**>(e.data() + sizeof(void*) * nin);
+        auto* lds = reinterpret_cast<long long*>(e.data() + sizeof(void*) * (nin + nout));
+        for (int r = 0; r < R; ++r) {
+          in[r] = outView(l, zp * R + r).ptr;
+          aligned &= al16(in[r]);
+        }
+        for (int k = 0; k < nout; ++k) {
+          out[k] = par.ptr + (k / Nb) * d.P * par.ld + (k % Nb) * d.N;
+          aligned &= al16(out[k]);
+        }
+        lds[0] = ldM[l];
+        lds[1] = par.ld;
+        aligned &= (lds[0] % 2 == 0) && (lds[1] % 2 == 0);
+        tab.insert(tab.end(), e.begin(), e.end());
+        ++count;
+      }
+      if (count) {
+        Launch ln;
+        ln.kind = Launch::ASSEMBLE;
+        ln.level = l;
+        ln.count = count;
+        ln.rows = d.P;
+        ln.cols = d.N;
+        ln.aligned16 = aligned;
+        if (!lazy_kernels) ln.kern = kernel(2, aligned ? 2 : 1);
+        const LincombCost c = lincomb_cost(*kernel(2, 2));
+        const double elems = (double)d.P * d.N;
+        ln.elem_adds = c.adds_per_elem * elems * count;
+        ln.elem_reads = c.reads_per_elem * elems * count;
+        ln.elem_writes = c.writes_per_elem * elems * count;
+        ln.table_off = push(tab.data(), tab.size());
+        launches.push_back(ln);
+      }
+    }
+    // peel strips of the level-(l-1) nodes: (a) C'[0:P',0:N'] += A[:,Q':Q] B[Q':Q,0:N'],
+    // (b) C[P':P,:] = A[P':P,:] B, (c) C[0:P',N':N] = A[0:P',:] B[:,N':N]
+    std::vector<GemmTask> tasks;
+    for (long long zp = 0; zp < nodes_at[l - 1]; ++zp) {
+      if (!strip_owner[l - 1][zp]) continue;
+      const View a = opA(l - 1, zp, rootA), b = opB(l - 1, zp, rootB), c = outView(l - 1, zp);
+      const double alpha = a.sigma * b.sigma;
+      auto add = [&](const double* pa, const double* pb, double* pc, long long m, long long n, long long k, double beta) {
+        if (m <= 0 || n <= 0) return;
+        GemmTask t{};
+        t.A = pa;
+        t.B = pb;
+        t.C = pc;
+        t.lda = a.ld;
+        t.ldb = b.ld;
+        t.ldc = c.ld;
+        t.m = (int)m;
+        t.n = (int)n;
+        t.k = (int)k;
+        t.alpha = alpha;
+        t.beta = beta;
+        tasks.push_back(t);
+      };
+      if (dp.Q1 < dp.Q) add(a.ptr + dp.Q1, b.ptr + dp.Q1 * b.ld, c.ptr, dp.P1, dp.N1, dp.Q - dp.Q1, 1.0);
+      if (dp.P1 < dp.P) add(a.ptr + dp.P1 * a.ld, b.ptr, c.ptr + dp.P1 * c.ld, dp.P - dp.P1, dp.N, dp.Q, 0.0);
+      if (dp.N1 < dp.N) add(a.ptr, b.ptr + dp.N1, c.ptr + dp.N1, dp.P1, dp.N - dp.N1, dp.Q, 0.0);
+    }
+    if (!tasks.empty()) {
+      Launch ln;
+      ln.kind = Launch::STRIPS;
+      ln.level = l - 1;
+      ln.tiles = gemm_prepare(tasks);
+      ln.count = (int)tasks.size();
+      ln.aligned16 = gemm_tasks_aligned16(tasks);
+      for (auto& t : tasks) {
+        ln.flops += 2.0 * t.m * t.n * (double)t.k;
+        ln.gemm_bytes += 8.0 * ((double)t.m * t.k + (double)t.k * t.n + (1.0 + (t.beta != 0.0)) * t.m * t.n);
+      }
+      ln.table_off = push(tasks.data(), tasks.size() * sizeof(GemmTask));
+      launches.push_back(ln);
+    }
+  }
+}
+
+namespace {
+
+void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long long Nc, int levels,
+               const fmm_plan_options* opt, int device) {
+  if (!alg) throw Error(FMM_E_INVALID_ARG, "null algorithm");
+  if (P < 0 || Q < 0 || Nc < 0) throw Error(FMM_E_SHAPE, "negative dimension");
+  if (P > INT32_MAX || Q > INT32_MAX || Nc > INT32_MAX) throw Error(FMM_E_UNSUPPORTED, "dimension above 2^31-1");
+  if (levels < 0 || levels > 8) throw Error(FMM_E_UNSUPPORTED, "levels must be in [0, 8]");
+  if (opt) p->opt = *opt;
+  else fmm_plan_options_default(&p->opt);
+  if (p->opt.shard_count < 1) p->opt.shard_count = 1;
+  if (p->opt.shard_rank < 0 || p->opt.shard_rank >= p->opt.shard_count) throw Error(FMM_E_INVALID_ARG, "bad shard_rank");
+  if (p->opt.layout != FMM_ROW_MAJOR && p->opt.layout != FMM_COL_MAJOR) throw Error(FMM_E_INVALID_ARG, "bad layout");
+  if (p->opt.strategy != FMM_ADD_STREAMING && p->opt.strategy != FMM_ADD_WRITE_ONCE)
+    throw Error(FMM_E_INVALID_ARG, "bad strategy");
+  p->device = device;
+  FMM_CUDA(cudaSetDevice(device));
+  p->userP = P;
+  p->userQ = Q;
+  p->userN = Nc;
+  p->colmajor = p->opt.layout == FMM_COL_MAJOR;
+  if (p->colmajor) {
+    p->alg_t.reset(alg_transpose_prop1(*alg));
+    p->alg = p->alg_t.get();
+    p->P = Nc;
+    p->Q = Q;
+    p->N = P;
+  } else {
+    p->alg = alg;
+    p->P = P;
+    p->Q = Q;
+    p->N = Nc;
+  }
+  const fmm_alg* a = p->alg;
+  p->R = a->R;
+  const int M = a->M, K = a->K, Nb = a->N, R = a->R;
+  // effective levels (R10/R18): stop at a level whose problem is smaller than the base case
+  p->dims.clear();
+  Dims d{p->P, p->Q, p->N, 0, 0, 0};
+  int L = 0;
+  while (true) {
+    d.P1 = M * (d.P / M);
+    d.Q1 = K * (d.Q / K);
+    d.N1 = Nb * (d.N / Nb);
+    p->dims.push_back(d);
+    if (L == levels || d.P < M || d.Q < K || d.N < Nb) break;
+    d = Dims{d.P1 / M, d.Q1 / K, d.N1 / Nb, 0, 0, 0};
+    ++L;
+  }
+  p->L = L;
+  p->nodes_at.assign(L + 1, 1);
+  for (int l = 1; l <= L; ++l) {
+    if (p->nodes_at[l - 1] > (1LL << 40) / R) throw Error(FMM_E_UNSUPPORTED, "too many recursion nodes");
+    p->nodes_at[l] = p->nodes_at[l - 1] * R;
+  }
+  if (p->nodes_at[L] > 65535 * 16) throw Error(FMM_E_UNSUPPORTED, "too many leaves");
+  // formed / singleton columns
+  auto cols = [&](const std::vector<double>& X, int rows, std::vector<int>& form, std::vector<int>& idx,
+                  std::vector<int>& sing, std::vector<double>& coef) {
+    idx.assign(R, -1);
+    sing.assign(R, -1);
+    coef.assign(R, 0.0);
+    for (int r = 0; r < R; ++r) {
+      int nz = 0, last = -1;
+      for (int i = 0; i < rows; ++i)
+        if (X[(size_t)i * R + r] != 0.0) ++nz, last = i;
+      if (nz == 1) {
+        sing[r] = last;
+        coef[r] = X[(size_t)last * R + r];
+      } else {
+        idx[r] = (int)form.size();
+        form.push_back(r);
+      }
+    }
+  };
+  cols(a->Ud, M * K, p->formU, p->idxU, p->singU, p->coefU);
+  cols(a->Vd, K * Nb, p->formV, p->idxV, p->singV, p->coefV);
+  p->setup_sharding();
+  p->setup_workspace();
+  // compile the streaming/write-once kernels for the 16-byte variant now (NVRTC)
+  if (p->L > 0) {
+    if (!p->formU.empty()) p->kernel(0, 2);
+    if (!p->formV.empty()) p->kernel(1, 2);
+    p->kernel(2, 2);
+  }
+  // size the tables with a dry build (pointer values do not change the table sizes)
+  p->build(reinterpret_cast<const double*>(0x100000), std::max<long long>(p->Q, 1), reinterpret_cast<const double*>(0x200000),
+           std::max<long long>(p->N, 1), reinterpret_cast<double*>(0x300000), std::max<long long>(p->N, 1), true);
+  p->tab_bytes = std::max<size_t>(p->h_tab.size(), 256);
+  FMM_CUDA(cudaMalloc(&p->d_tab, p->tab_bytes));
+  FMM_CUDA(cudaMallocHost(&p->h_pinned, p->tab_bytes));
+  FMM_CUDA(cudaEventCreateWithFlags(&p->upload_done, cudaEventDisableTiming));
+  for (auto& e : p->ev) FMM_CUDA(cudaEventCreate(&e));
+  p->tab_valid = false;
+}
+
+void check_ld(const fmm_plan_t* p, long long lda, long long ldb, long long ldc) {
+  // user-orientation requirements (fmm.h)
+  if (!p->colmajor) {
+    if (lda < std::max<long long>(p->userQ, 1) || ldb < std::max<long long>(p->userN, 1) || ldc < std::max<long long>(p->userN, 1))
+      throw Error(FMM_E_SHAPE, "row-major requires lda >= Q, ldb >= Nc, ldc >= Nc");
+  } else {
+    if (lda < std::max<long long>(p->userP, 1) || ldb < std::max<long long>(p->userQ, 1) || ldc < std::max<long long>(p->userP, 1))
+      throw Error(FMM_E_SHAPE, "column-major requires lda >= P, ldb >= Q, ldc >= P");
+  }
+}
+
+// Enqueue the plan on `stream`; if ev_phase is non-null, record events between phases.
+void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc,
+         cudaStream_t stream, bool timed) {
+  // a pointer may be null only when its matrix is empty
+  if ((!A && p->userP * p->userQ > 0) || (!B && p->userQ * p->userN > 0) || (!C && p->userP * p->userN > 0))
+    throw Error(FMM_E_INVALID_ARG, "null matrix pointer");
+  check_ld(p, lda, ldb, ldc);
+  FMM_CUDA(cudaSetDevice(p->device));
+  // row-major orientation: for column-major, C^T = B^T A^T (Prop. 1)
+  const double* a = p->colmajor ? B : A;
+  const double* b = p->colmajor ? A : B;
+  const long long la = p->colmajor ? ldb : lda, lb = p->colmajor ? lda : ldb;
+  if (!p->tab_valid || a != p->cA || b != p->cB || C != p->cC || la != p->clda || lb != p->cldb || ldc != p->cldc) {
+    p->build(a, la, b, lb, C, ldc, false);
+    if (p->h_tab.size() > p->tab_bytes) throw Error(FMM_E_INVALID_ARG, "internal: table size grew");
+    FMM_CUDA(cudaEventSynchronize(p->upload_done));  // the previous upload has consumed h_pinned
+    std::memcpy(p->h_pinned, p->h_tab.data(), p->h_tab.size());
+    FMM_CUDA(cudaMemcpyAsync(p->d_tab, p->h_pinned, p->h_tab.size(), cudaMemcpyHostToDevice, stream));
+    FMM_CUDA(cudaEventRecord(p->upload_done, stream));
+    p->cA = a;
+    p->cB = b;
+    p->cC = C;
+    p->clda = la;
+    p->cldb = lb;
+    p->cldc = ldc;
+    p->tab_valid = true;
+  }
+  if (timed) FMM_CUDA(cudaEventRecord(p->ev[0], stream));
+  int phase = 0;  // 0 formation, 1 gemm, 2 assembly/strips
+  for (const Launch& ln : p->launches) {
+    const int ph = (ln.kind == Launch::FORM_A || ln.kind == Launch::FORM_B) ? 0 : ln.kind == Launch::GEMM ? 1 : 2;
+    if (timed && ph != phase) {
+      for (int q = phase + 1; q <= ph; ++q) FMM_CUDA(cudaEventRecord(p->ev[q], stream));
+      phase = ph;
+    }
+    const void* tab = p->d_tab + ln.table_off;
+    switch (ln.kind) {
+      case Launch::FORM_A:
+      case Launch::FORM_B:
+      case Launch::ASSEMBLE:
+        lincomb_launch(*ln.kern, tab, ln.count, ln.rows, ln.cols, stream);
+        break;
+      case Launch::GEMM:
+      case Launch::STRIPS:
+        gemm_launch(reinterpret_cast<const GemmTask*>(tab), ln.count, ln.tiles, ln.aligned16, stream);
+        break;
+    }
+  }
+  if (timed) {
+    for (int q = phase + 1; q <= 3; ++q) FMM_CUDA(cudaEventRecord(p->ev[q], stream));
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+void fmm_plan_options_default(fmm_plan_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->layout = FMM_ROW_MAJOR;
+  o->strategy = FMM_ADD_STREAMING;
+  o->cse = 1;
+  o->shard_rank = 0;
+  o->shard_count = 1;
+  o->workspace_limit_bytes = 0;
+}
+
+fmm_status_t fmm_plan_create(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels,
+                             const fmm_plan_options* opt, int device, fmm_plan_t** out) {
+  FMM_API_BEGIN
+  if (!out) throw Error(FMM_E_INVALID_ARG, "null out");
+  *out = nullptr;
+  std::unique_ptr<fmm_plan_t> p(new fmm_plan_t);
+  plan_init(p.get(), alg, P, Q, Nc, levels, opt, device);
+  *out = p.release();
+  return FMM_OK;
+  FMM_API_END
+}
+
+fmm_status_t fmm_plan(const fmm_alg* alg, int64_t M, int64_t K, int64_t N, int levels, fmm_plan_t** out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return fmm_plan_create(alg, M, K, N, levels, nullptr, dev, out);
+}
+
+fmm_status_t fmm_plan_workspace_bytes(const fmm_plan_t* p, size_t* bytes) {
+  FMM_API_BEGIN
+  if (!p || !bytes) throw Error(FMM_E_INVALID_ARG, "null argument");
+  *bytes = p->ws_bytes;
+  return FMM_OK;
+  FMM_API_END
+}
+
+fmm_status_t fmm_plan_stats(const fmm_plan_t* p, double out[8]) {
+  FMM_API_BEGIN
+  if (!p || !out) throw Error(FMM_E_INVALID_ARG, "null argument");
+  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (const Launch& ln : p->launches) {
+    s[0] += ln.flops;
+    s[1] += ln.elem_adds;
+    s[2] += 8.0 * (ln.elem_reads + ln.elem_writes);
+    s[3] += ln.gemm_bytes;
+    s[4] += 1;
+    if (ln.kind == Launch::GEMM) s[6] += ln.count;
+  }
+  s[5] = p->L;
+  s[7] = 2.0 * p->userP * p->userQ * (double)p->userN - (double)p->userP * p->userN;
+  std::memcpy(out, s, sizeof(s));
+  return FMM_OK;
+  FMM_API_END
+}
+
+fmm_status_t fmm_execute(fmm_plan_t* p, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                         int64_t ldc, void* stream) {
+  FMM_API_BEGIN
+  if (!p) throw Error(FMM_E_INVALID_ARG, "null plan");
+  run(p, A, lda, B, ldb, C, ldc, (cudaStream_t)stream, false);
+  return FMM_OK;
+  FMM_API_END
+}
+
+fmm_status_t fmm_exec(fmm_plan_t* p, const double* A, const double* B, double* C) {
+  if (!p) return FMM_E_INVALID_ARG;
+  if (!p->colmajor)
+    return fmm_execute(p, A, std::max<int64_t>(p->userQ, 1), B, std::max<int64_t>(p->userN, 1), C,
+                       std::max<int64_t>(p->userN, 1), nullptr);
+  return fmm_execute(p, A, std::max<int64_t>(p->userP, 1), B, std::max<int64_t>(p->userQ, 1), C,
+                     std::max<int64_t>(p->userP, 1), nullptr);
+}
+
+fmm_status_t fmm_execute_timed(fmm_plan_t* p, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                               int64_t ldc, void* stream, float ms[5]) {
+  FMM_API_BEGIN
+  if (!p || !ms) throw Error(FMM_E_INVALID_ARG, "null argument");
+  run(p, A, lda, B, ldb, C, ldc, (cudaStream_t)stream, true);
+  FMM_CUDA(cudaEventSynchronize(p->ev[3]));
+  float t01 = 0, t12 = 0, t23 = 0;
+  FMM_CUDA(cudaEventElapsedTime(&t01, p->ev[0], p->ev[1]));
+  FMM_CUDA(cudaEventElapsedTime(&t12, p->ev[1], p->ev[2]));
+  FMM_CUDA(cudaEventElapsedTime(&t23, p->ev[2], p->ev[3]));
+  ms[0] = t01;
+  ms[1] = t12;
+  ms[2] = t23;
+  ms[3] = 0.0f;
+  ms[4] = t01 + t12 + t23;
+  return FMM_OK;
+  FMM_API_END
+}
+
+fmm_status_t fmm_execute_host(fmm_plan_t* p, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                              int64_t ldc, void* stream) {
+  FMM_API_BEGIN
+  if (!p || !A || !B || !C) throw Error(FMM_E_INVALID_ARG, "null argument");
+  check_ld(p, lda, ldb, ldc);
+  FMM_CUDA(cudaSetDevice(p->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  // device staging with tight leading dimensions, in the caller's layout
+  const long long P = p->userP, Q = p->userQ, N = p->userN;
+  const bool cm = p->colmajor;
+  // (rows, cols) of the storage: row-major P x Q is P rows of Q; column-major is Q "rows" of P
+  const long long aR = cm ? Q : P, aC = cm ? P : Q, bR = cm ? N : Q, bC = cm ? Q : N, cR = cm ? N : P, cC = cm ? P : N;
+  if (!p->sA) {
+    FMM_CUDA(cudaMalloc(&p->sA, std::max<size_t>(8, (size_t)aR * aC * 8)));
+    FMM_CUDA(cudaMalloc(&p->sB, std::max<size_t>(8, (size_t)bR * bC * 8)));
+    FMM_CUDA(cudaMalloc(&p->sC, std::max<size_t>(8, (size_t)cR * cC * 8)));
+  }
+  if (aR && aC) FMM_CUDA(cudaMemcpy2DAsync(p->sA, aC * 8, A, lda * 8, aC * 8, aR, cudaMemcpyHostToDevice, s));
+  if (bR && bC) FMM_CUDA(cudaMemcpy2DAsync(p->sB, bC * 8, B, ldb * 8, bC * 8, bR, cudaMemcpyHostToDevice, s));
+  run(p, p->sA, std::max<long long>(aC, 1), p->sB, std::max<long long>(bC, 1), p->sC, std::max<long long>(cC, 1), s, false);
+  if (cR && cC) FMM_CUDA(cudaMemcpy2DAsync(C, ldc * 8, p->sC, cC * 8, cC * 8, cR, cudaMemcpyDeviceToHost, s));
+  FMM_CUDA(cudaStreamSynchronize(s));
+  return FMM_OK;
+  FMM_API_END
+}
+
+fmm_status_t fmm_sync(fmm_plan_t* p) {
+  FMM_API_BEGIN
+  if (!p) throw Error(FMM_E_INVALID_ARG, "null plan");
+  FMM_CUDA(cudaSetDevice(p->device));
+  FMM_CUDA(cudaDeviceSynchronize());
+  FMM_CUDA(cudaGetLastError());
+  return FMM_OK;
+  FMM_API_END
+}
+
+void fmm_plan_destroy(fmm_plan_t* p) { delete p; }
+
+fmm_status_t fmm_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda, const double* B,
+                       int64_t ldb, double beta, double* C, int64_t ldc, void* stream) {
+  FMM_API_BEGIN
+  if (m < 0 || n < 0 || k < 0) throw Error(FMM_E_SHAPE, "negative dimension");
+  if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) throw Error(FMM_E_UNSUPPORTED, "dimension above 2^31-1");
+  if (m == 0 || n == 0) return FMM_OK;
+  if (!A || !B || !C) throw Error(FMM_E_INVALID_ARG, "null matrix pointer");
+  if (lda < std::max<int64_t>(k, 1) || ldb < n || ldc < n) throw Error(FMM_E_SHAPE, "leading dimension too small");
+  thread_local GemmTask* d_task = nullptr;
+  thread_local int d_task_dev = -1;
+  int dev = 0;
+  FMM_CUDA(cudaGetDevice(&dev));
+  if (!d_task || d_task_dev != dev) {
+    FMM_CUDA(cudaMalloc(&d_task, sizeof(GemmTask) * 64));
+    d_task_dev = dev;
+  }
+  std::vector<GemmTask> t(1);
+  t[0].A = A;
+  t[0].B = B;
+  t[0].C = C;
+  t[0].lda = lda;
+  t[0].ldb = ldb;
+  t[0].ldc = ldc;
+  t[0].m = (int)m;
+  t[0].n = (int)n;
+  t[0].k = (int)k;
+  t[0].alpha = alpha;
+  t[0].beta = beta;
+  const long long tiles = gemm_prepare(t);
+  cudaStream_t s = (cudaStream_t)stream;
+  // the task descriptor is passed by value through a stream-ordered upload
+  FMM_CUDA(cudaMemcpyAsync(d_task, t.data(), sizeof(GemmTask), cudaMemcpyHostToDevice, s));
+  gemm_launch(d_task, 1, tiles, gemm_tasks_aligned16(t), s);
+  return FMM_OK;
+  FMM_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,271 @@
+"""Thin ctypes binding of libfmm.so (include/fmm.h).  Argument marshalling only: every step of
+the multiplication runs in the library's sm_100a kernels.  PyTorch is used for device memory and
+streams; there is no CPU fallback, and a missing library raises at import time.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from fractions import Fraction
+from typing import Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfmm.so")
+
+FMM_OK = 0
+_STATUS = {1: "FMM_E_INVALID_ARG", 2: "FMM_E_NOT_EXACT", 3: "FMM_E_SHAPE", 4: "FMM_E_NO_MEMORY",
+           5: "FMM_E_CUDA", 6: "FMM_E_NCCL", 7: "FMM_E_UNSUPPORTED", 8: "FMM_E_PARSE"}
+ROW_MAJOR, COL_MAJOR = 0, 1
+STREAMING, WRITE_ONCE = 0, 1
+
+
+class FmmError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.status = _STATUS.get(code, str(code))
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("layout", ctypes.c_int), ("strategy", ctypes.c_int), ("cse", ctypes.c_int),
+                ("shard_rank", ctypes.c_int), ("shard_count", ctypes.c_int),
+                ("workspace_limit_bytes", ctypes.c_size_t)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(the CUDA library is required; there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    i64, i32, vp, dp = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_double
+    p64 = ctypes.POINTER(ctypes.c_int64)
+    sig = {
+        "fmm_alg_create": [i32, i32, i32, i32, p64, p64, p64, p64, p64, p64, ctypes.POINTER(vp)],
+        "fmm_alg_load": [ctypes.c_char_p, ctypes.POINTER(vp)],
+        "fmm_alg_info": [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)],
+        "fmm_plan_create": [vp, i64, i64, i64, i32, ctypes.POINTER(_Options), i32, ctypes.POINTER(vp)],
+        "fmm_plan": [vp, i64, i64, i64, i32, ctypes.POINTER(vp)],
+        "fmm_plan_workspace_bytes": [vp, ctypes.POINTER(ctypes.c_size_t)],
+        "fmm_plan_stats": [vp, ctypes.POINTER(dp)],
+        "fmm_execute": [vp, vp, i64, vp, i64, vp, i64, vp],
+        "fmm_exec": [vp, vp, vp, vp],
+        "fmm_execute_timed": [vp, vp, i64, vp, i64, vp, i64, vp, ctypes.POINTER(ctypes.c_float)],
+        "fmm_execute_host": [vp, vp, i64, vp, i64, vp, i64, vp],
+        "fmm_sync": [vp],
+        "fmm_hybrid_split": [i64, i32, i64, p64, p64],
+        "fmm_dgemm": [i64, i64, i64, dp, vp, i64, vp, i64, dp, vp, i64, vp],
+    }
+    for name, args in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    lib.fmm_alg_destroy.argtypes = [vp]
+    lib.fmm_alg_destroy.restype = None
+    lib.fmm_plan_destroy.argtypes = [vp]
+    lib.fmm_plan_destroy.restype = None
+    lib.fmm_plan_options_default.argtypes = [ctypes.POINTER(_Options)]
+    lib.fmm_plan_options_default.restype = None
+    lib.fmm_last_error.restype = ctypes.c_char_p
+    lib.fmm_version.restype = ctypes.c_char_p
+    return lib
+
+
+_lib = _load()
+
+
+def _check(code: int):
+    if code != FMM_OK:
+        raise FmmError(code, _lib.fmm_last_error().decode())
+
+
+def version() -> str:
+    return _lib.fmm_version().decode()
+
+
+# ---- algorithms -----------------------------------------------------------------------------
+class Algorithm:
+    """An exact bilinear <M,K,N;R> algorithm (validated by the library's exact Brent check)."""
+
+    def __init__(self, handle, name: str = ""):
+        self._h = handle
+        self.name = name
+        dims = (ctypes.c_int * 4)()
+        nnz = (ctypes.c_int * 3)()
+        _check(_lib.fmm_alg_info(self._h, dims, nnz))
+        self.M, self.K, self.N, self.R = list(dims)
+        self.nnz = tuple(nnz)
+
+    @classmethod
+    def load(cls, path: str) -> "Algorithm":
+        h = ctypes.c_void_p()
+        _check(_lib.fmm_alg_load(path.encode(), ctypes.byref(h)))
+        return cls(h, name=os.path.splitext(os.path.basename(path))[0])
+
+    @classmethod
+    def create(cls, M: int, K: int, N: int, R: int, U: Sequence, V: Sequence, W: Sequence, name: str = "") -> "Algorithm":
+        """U (MK x R), V (KN x R), W (MN x R) as nested sequences of ints / Fractions."""
+        def arr(X, rows):
+            vals = [Fraction(v) for row in X for v in row]
+            if len(vals) != rows * R:
+                raise ValueError("coefficient matrix has the wrong shape")
+            num = (ctypes.c_int64 * len(vals))(*[v.numerator for v in vals])
+            den = (ctypes.c_int64 * len(vals))(*[v.denominator for v in vals])
+            return num, den
+        un, ud = arr(U, M * K)
+        vn, vd = arr(V, K * N)
+        wn, wd = arr(W, M * N)
+        h = ctypes.c_void_p()
+        _check(_lib.fmm_alg_create(M, K, N, R, un, ud, vn, vd, wn, wd, ctypes.byref(h)))
+        return cls(h, name=name)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.fmm_alg_destroy(self._h)
+            self._h = None
+
+
+# ---- tensors --------------------------------------------------------------------------------
+def _mat(t, layout: int, rows: int, cols: int, what: str):
+    import torch
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_cuda or t.dim() != 2:
+        raise TypeError(f"{what} must be a 2-D float64 CUDA tensor")
+    if tuple(t.shape) != (rows, cols):
+        raise ValueError(f"{what} has shape {tuple(t.shape)}, expected {(rows, cols)}")
+    s0, s1 = t.stride()
+    if layout == ROW_MAJOR:
+        if s1 != 1 and cols > 1:
+            raise ValueError(f"{what} must be row-major (unit column stride)")
+        ld = s0 if rows > 1 else max(cols, 1)
+    else:
+        if s0 != 1 and rows > 1:
+            raise ValueError(f"{what} must be column-major (unit row stride)")
+        ld = s1 if cols > 1 else max(rows, 1)
+    return ctypes.c_void_p(t.data_ptr()), int(max(ld, 1))
+
+
+def _stream_ptr(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+# ---- plans ----------------------------------------------------------------------------------
+class Plan:
+    """C (P x N) = A (P x Q) @ B (Q x N) with `levels` recursive steps of `alg` (fmm_plan_create)."""
+
+    def __init__(self, alg: Algorithm, P: int, Q: int, N: int, levels: int, layout: str = "row",
+                 strategy: str = "streaming", cse: bool = True, shard_rank: int = 0, shard_count: int = 1,
+                 device: Optional[int] = None, workspace_limit_bytes: int = 0):
+        import torch
+        self.alg, self.P, self.Q, self.N, self.levels = alg, P, Q, N, levels
+        self.layout = ROW_MAJOR if layout == "row" else COL_MAJOR
+        o = _Options()
+        _lib.fmm_plan_options_default(ctypes.byref(o))
+        o.layout = self.layout
+        o.strategy = STREAMING if strategy == "streaming" else WRITE_ONCE
+        o.cse = int(bool(cse))
+        o.shard_rank, o.shard_count = shard_rank, shard_count
+        o.workspace_limit_bytes = workspace_limit_bytes
+        self.device = torch.cuda.current_device() if device is None else device
+        h = ctypes.c_void_p()
+        _check(_lib.fmm_plan_create(alg._h, P, Q, N, levels, ctypes.byref(o), self.device, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.fmm_plan_destroy(self._h)
+            self._h = None
+
+    @property
+    def workspace_bytes(self) -> int:
+        b = ctypes.c_size_t()
+        _check(_lib.fmm_plan_workspace_bytes(self._h, ctypes.byref(b)))
+        return b.value
+
+    def stats(self) -> dict:
+        s = (ctypes.c_double * 8)()
+        _check(_lib.fmm_plan_stats(self._h, s))
+        keys = ["gemm_flops", "add_flops", "add_bytes", "gemm_bytes", "launches", "levels", "leaves", "paper_flops"]
+        return dict(zip(keys, list(s)))
+
+    def new_output(self):
+        import torch
+        if self.layout == ROW_MAJOR:
+            return torch.empty(self.P, self.N, dtype=torch.float64, device=f"cuda:{self.device}")
+        return torch.empty(self.N, self.P, dtype=torch.float64, device=f"cuda:{self.device}").t()
+
+    def _args(self, A, B, C):
+        a, lda = _mat(A, self.layout, self.P, self.Q, "A")
+        b, ldb = _mat(B, self.layout, self.Q, self.N, "B")
+        c, ldc = _mat(C, self.layout, self.P, self.N, "C")
+        return a, lda, b, ldb, c, ldc
+
+    def execute(self, A, B, C=None, stream=None):
+        """C <- A @ B on the stream (asynchronous). Returns C."""
+        if C is None:
+            C = self.new_output()
+        _check(_lib.fmm_execute(self._h, *self._args(A, B, C), _stream_ptr(stream)))
+        return C
+
+    def execute_timed(self, A, B, C=None, stream=None):
+        """Blocking; returns (C, {formation, gemm, assembly, total} ms)."""
+        if C is None:
+            C = self.new_output()
+        ms = (ctypes.c_float * 5)()
+        _check(_lib.fmm_execute_timed(self._h, *self._args(A, B, C), _stream_ptr(stream), ms))
+        return C, {"formation_ms": ms[0], "gemm_ms": ms[1], "assembly_ms": ms[2], "total_ms": ms[4]}
+
+    def execute_host(self, A, B, C, stream=None):
+        """Host (CPU) tensors / arrays in, host result out: H2D, execute, D2H (blocking)."""
+        import numpy as np
+        import torch
+
+        def hp(x, rows, cols, what, writable=False):
+            if isinstance(x, torch.Tensor):
+                if x.is_cuda or x.dtype != torch.float64:
+                    raise TypeError(f"{what} must be a float64 CPU tensor")
+                s0, s1 = x.stride()
+                ptr = x.data_ptr()
+            else:
+                if x.dtype != np.float64:
+                    raise TypeError(f"{what} must be float64")
+                s0, s1 = x.strides[0] // 8, x.strides[1] // 8
+                ptr = x.ctypes.data
+            if tuple(x.shape) != (rows, cols):
+                raise ValueError(f"{what} has shape {tuple(x.shape)}, expected {(rows, cols)}")
+            ld = s0 if self.layout == ROW_MAJOR else s1
+            return ctypes.c_void_p(ptr), int(max(ld, 1))
+        a, lda = hp(A, self.P, self.Q, "A")
+        b, ldb = hp(B, self.Q, self.N, "B")
+        c, ldc = hp(C, self.P, self.N, "C", True)
+        _check(_lib.fmm_execute_host(self._h, a, lda, b, ldb, c, ldc, _stream_ptr(stream)))
+        return C
+
+    def sync(self):
+        _check(_lib.fmm_sync(self._h))
+
+
+def plan(alg: Algorithm, M: int, K: int, N: int, levels: int) -> Plan:
+    """The north-star spelling fmm_plan(alg, M, K, N, levels): default options, row-major."""
+    return Plan(alg, M, K, N, levels)
+
+
+def dgemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, stream=None):
+    """C = alpha A B + beta C with the library's DMMA GEMM kernel (row-major CUDA tensors)."""
+    import torch
+    m, k = A.shape
+    n = B.shape[1]
+    if C is None:
+        C = torch.empty(m, n, dtype=torch.float64, device=A.device)
+    a, lda = _mat(A, ROW_MAJOR, m, k, "A")
+    b, ldb = _mat(B, ROW_MAJOR, k, n, "B")
+    c, ldc = _mat(C, ROW_MAJOR, m, n, "C")
+    _check(_lib.fmm_dgemm(m, n, k, alpha, a, lda, b, ldb, beta, c, ldc, _stream_ptr(stream)))
+    return C
+
+
+def hybrid_split(R: int, L: int, G: int):
+    bfs, dfs = ctypes.c_int64(), ctypes.c_int64()
+    _check(_lib.fmm_hybrid_split(R, L, G, ctypes.byref(bfs), ctypes.byref(dfs)))
+    return bfs.value, dfs.value

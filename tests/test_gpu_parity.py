@@ -1,0 +1,218 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Tolerances (BASELINE.json north star):
+  max|C_gpu - C_oracle_fast| <= 1e-12 |A|_F |B|_F
+  max|C_gpu - C_classical|   <= 1e-10 |A|_F |B|_F          (L <= 3)
+Integer and quantised inputs make every rounding exact, so there the results must be bit-exact.
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+import fmm_inputs as I
+from conftest import ALGS
+from oracle import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_1409_2908_b200 as F
+
+NAMES = [os.path.basename(p)[:-4] for p in sorted(glob.glob(os.path.join(ALGS, "*.txt")))]
+_ORA = {}
+
+
+def oalg(name):
+    if name not in _ORA:
+        _ORA[name] = O.load_alg(os.path.join(ALGS, name + ".txt"))
+    return _ORA[name]
+
+
+_FA = {}
+
+
+def falg(name):
+    if name not in _FA:
+        _FA[name] = F.load_alg(name)
+    return _FA[name]
+
+
+def dev(x, layout="row"):
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    if layout == "col":
+        t = torch.from_numpy(np.ascontiguousarray(x.T)).cuda().t()
+    return t
+
+
+def run(name, A, B, L, layout="row", **kw):
+    P, Q = A.shape
+    N = B.shape[1]
+    p = F.Plan(falg(name), P, Q, N, L, layout=layout, **kw)
+    C = p.execute(dev(A, layout), dev(B, layout))
+    torch.cuda.synchronize()
+    return C.cpu().numpy(), p
+
+
+def bound(A, B, c):
+    return c * np.linalg.norm(A) * np.linalg.norm(B)
+
+
+# ---- the DMMA GEMM kernel on its own ----------------------------------------------------------
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (128, 128, 16), (256, 384, 512), (129, 257, 33), (300, 17, 1000),
+                                   (7, 513, 64), (1000, 1000, 3)])
+def test_dgemm_matches_classical(m, n, k):
+    A, B = I.problem(m, k, n, seed=m + n + k)
+    C = F.dgemm(dev(A), dev(B)).cpu().numpy()
+    assert np.max(np.abs(C - O.classical(A, B))) <= bound(A, B, 1e-13)
+    Ai, Bi = I.problem(m, k, n, seed=3, kind="integers")
+    assert np.array_equal(F.dgemm(dev(Ai), dev(Bi)).cpu().numpy(), O.classical(Ai, Bi))
+
+
+def test_dgemm_alpha_beta_and_unaligned_views():
+    A, B = I.problem(200, 150, 170, seed=1, kind="integers")
+    Cin = I.integers(9, 200, 170)
+    # odd leading dimensions and odd offsets force the 8-byte copy path
+    Abig = torch.zeros(201, 153, dtype=torch.float64, device="cuda")
+    Abig[1:, 3:] = dev(A)
+    Bbig = torch.zeros(151, 175, dtype=torch.float64, device="cuda")
+    Bbig[1:, 5:] = dev(B)
+    C = dev(Cin).clone()
+    F.dgemm(Abig[1:, 3:], Bbig[1:, 5:], C, alpha=-2.0, beta=1.0)
+    assert np.array_equal(C.cpu().numpy(), Cin - 2.0 * O.classical(A, B))
+
+
+# ---- check (c) on the GPU: integer inputs are bit-exact ---------------------------------------
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("L", [1, 2])
+def test_fast_integer_bit_exact(name, L):
+    a = oalg(name)
+    P, Q, N = 3 * a.M ** L + 1, 2 * a.K ** L + 1, 2 * a.N ** L + 2  # peeled at every level
+    A, B = I.problem(P, Q, N, seed=L, kind="integers")
+    C, _ = run(name, A, B, L)
+    assert np.array_equal(C, O.classical(A, B))
+
+
+def test_config1_4x4_integers():
+    A, B = I.problem(4, 4, 4, seed=0, kind="integers")
+    for L in (1, 2):
+        C, _ = run("strassen_222_7", A, B, L)
+        assert np.array_equal(C, A @ B)
+
+
+# ---- float parity against oracle_fast at sizes spanning several tiles and a ragged tail -------
+CASES = [
+    ("strassen_222_7", 1, 256, 256, 256),                 # BASELINE config 1
+    ("strassen_222_7", 3, 1000, 999, 1001),
+    ("winograd_class_222_7", 2, 1024, 1024, 1024),
+    ("winograd_class_222_7", 2, 777, 529, 901),
+    ("hk_class_323_15", 2, 600, 90, 600),                  # config 3 shape family, peeled at level 2
+    ("hk_class_323_15", 1, 451, 301, 452),
+    ("alg_424_26", 2, 800, 120, 800),                      # config 4 family
+    ("laderman_class_333_23", 2, 450, 450, 450),           # config 5 family
+    ("laderman_class_333_23", 1, 331, 332, 333),
+    ("alg_433_29", 2, 720, 144, 144),                      # config 5t family
+    ("alg_433_29", 1, 401, 302, 299),
+]
+
+
+@pytest.mark.parametrize("name,L,P,Q,N", CASES)
+@pytest.mark.parametrize("layout", ["row", "col"])
+def test_fast_float_parity(name, L, P, Q, N, layout):
+    A, B = I.problem(P, Q, N, seed=L + P)
+    C, _ = run(name, A, B, L, layout=layout)
+    ref = O.fast(A, B, oalg(name), L)
+    assert np.max(np.abs(C - ref)) <= bound(A, B, 1e-12)
+    assert np.max(np.abs(C - O.classical(A, B))) <= bound(A, B, 1e-10)
+
+
+@pytest.mark.parametrize("strategy", ["streaming", "write_once"])
+@pytest.mark.parametrize("cse", [False, True])
+def test_strategies_and_cse(strategy, cse):
+    for name, L, P, Q, N in [("alg_424_26", 2, 320, 64, 320), ("winograd_class_222_7", 2, 512, 512, 512)]:
+        A, B = I.problem(P, Q, N, seed=5)
+        C, _ = run(name, A, B, L, strategy=strategy, cse=cse)
+        assert np.max(np.abs(C - O.fast(A, B, oalg(name), L))) <= bound(A, B, 1e-12)
+        Ai, Bi = I.problem(P, Q, N, seed=6, kind="integers")
+        Ci, _ = run(name, Ai, Bi, L, strategy=strategy, cse=cse)
+        assert np.array_equal(Ci, Ai @ Bi)
+
+
+def test_quantized_inputs_exact_at_scale():
+    # g = 11 grid: every partial sum of classical and fast algorithms is exact
+    for name, L, P, Q, N in [("winograd_class_222_7", 2, 2048, 2048, 2048), ("alg_433_29", 2, 1800, 360, 360)]:
+        A, B = I.problem(P, Q, N, seed=7, kind="quantized")
+        C, _ = run(name, A, B, L)
+        s = 2.0 ** 11
+        exact = ((A * s).astype(np.int64) @ (B * s).astype(np.int64)).astype(np.float64) / (s * s)
+        assert np.array_equal(C, exact)
+
+
+# ---- sharding (HYBRID arithmetic): shards sum to the product ----------------------
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_shards_sum_to_product(G):
+    name, L, P, Q, N = "winograd_class_222_7", 2, 300, 200, 250
+    Ai, Bi = I.problem(P, Q, N, seed=8, kind="integers")
+    total = np.zeros((P, N))
+    for g in range(G):
+        C, _ = run(name, Ai, Bi, L, shard_rank=g, shard_count=G)
+        total += C
+    assert np.array_equal(total, Ai @ Bi)
+
+
+# ---- edge cases -------------------------------------------------------------------------------
+def test_degenerate_dims():
+    a = falg("strassen_222_7")
+    for (P, Q, N) in [(0, 5, 5), (5, 0, 5), (5, 5, 0), (1, 1, 1), (1, 7, 1), (3, 3, 3)]:
+        A, B = I.problem(P, Q, N, seed=1, kind="integers")
+        p = F.Plan(a, P, Q, N, 2)
+        C = torch.full((P, N), 7.0, dtype=torch.float64, device="cuda")
+        p.execute(dev(A) if A.size else torch.zeros(P, Q, dtype=torch.float64, device="cuda"),
+                  dev(B) if B.size else torch.zeros(Q, N, dtype=torch.float64, device="cuda"), C)
+        assert np.array_equal(C.cpu().numpy(), A @ B)
+
+
+def test_levels_beyond_base_case_stop_early():
+    A, B = I.problem(20, 20, 20, seed=2, kind="integers")
+    C, p = run("laderman_class_333_23", A, B, 8)
+    assert np.array_equal(C, A @ B)
+    assert p.stats()["levels"] == 2  # 20 -> 6 -> 2 < 3
+
+
+def test_strided_inputs_and_output():
+    A, B = I.problem(130, 66, 98, seed=4)
+    Ab = torch.zeros(130, 80, dtype=torch.float64, device="cuda"); Ab[:, :66] = dev(A)
+    Bb = torch.zeros(66, 111, dtype=torch.float64, device="cuda"); Bb[:, 5:103] = dev(B)
+    Cb = torch.zeros(130, 200, dtype=torch.float64, device="cuda")
+    p = F.Plan(falg("strassen_222_7"), 130, 66, 98, 2)
+    p.execute(Ab[:, :66], Bb[:, 5:103], Cb[:, 1:99])
+    ref = O.fast(A, B, oalg("strassen_222_7"), 2)
+    assert np.max(np.abs(Cb[:, 1:99].cpu().numpy() - ref)) <= bound(A, B, 1e-12)
+    assert not Cb[:, 0].any() and not Cb[:, 99:].any()  # nothing written outside C
+
+
+def test_deterministic():
+    A, B = I.problem(513, 257, 515, seed=9)
+    p = F.Plan(falg("alg_424_26"), 513, 257, 515, 2)
+    C1 = p.execute(dev(A), dev(B)).clone()
+    C2 = p.execute(dev(A), dev(B))
+    assert torch.equal(C1, C2)
+
+
+def test_errors_are_reported():
+    p = F.Plan(falg("strassen_222_7"), 8, 8, 8, 1)
+    with pytest.raises(ValueError):
+        p.execute(torch.zeros(8, 9, dtype=torch.float64, device="cuda"), torch.zeros(8, 8, dtype=torch.float64, device="cuda"))
+    with pytest.raises(F.FmmError) as e:
+        F.Plan(falg("strassen_222_7"), -1, 8, 8, 1)
+    assert e.value.status == "FMM_E_SHAPE"
+
+
+def test_execute_host_end_to_end():
+    A, B = I.problem(300, 200, 310, seed=10)
+    p = F.Plan(falg("hk_class_323_15"), 300, 200, 310, 2)
+    C = np.zeros((300, 310))
+    p.execute_host(A, B, C)
+    assert np.max(np.abs(C - O.fast(A, B, oalg("hk_class_323_15"), 2))) <= bound(A, B, 1e-12)

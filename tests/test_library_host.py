@@ -1,0 +1,102 @@
+"""Host-side checks of the C-ABI library (no GPU): it loads, exports every symbol include/fmm.h
+declares, and its host logic (exact Brent validation, file parser, HYBRID split arithmetic)
+behaves as the paper fixes.  No compute call is made here."""
+import ctypes
+import glob
+import os
+import re
+import subprocess
+
+import pytest
+
+from conftest import ALGS, GOLDEN, ROOT
+from oracle import oracle as O
+
+HEADER = os.path.join(ROOT, "include", "fmm.h")
+
+
+@pytest.fixture(scope="module")
+def F():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1409_2908_b200 as F
+    return F
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(fmm_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol(F):
+    names = declared_functions()
+    assert len(names) >= 15
+    lib = ctypes.CDLL(F.LIB_PATH)
+    for n in names:
+        assert hasattr(lib, n), n
+    out = subprocess.run(["nm", "-D", "--defined-only", F.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (fmm_[a-z0-9_]+)", out))
+    assert set(names) <= exported
+
+
+def test_library_is_sm100a_only(F):
+    out = subprocess.run(["cuobjdump", "--list-elf", F.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out)
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(ALGS, "*.txt"))), ids=os.path.basename)
+def test_library_accepts_every_algorithm_file(F, path):
+    a = F.Algorithm.load(path)
+    o = O.load_alg(path)
+    assert (a.M, a.K, a.N, a.R) == (o.M, o.K, o.N, o.R)
+    assert a.nnz == o.nnz()
+
+
+def test_library_rejects_printed_strassen_W(F, tmp_path):
+    # P:396-401's W fails the Brent equations (reading R1); the library must say so exactly
+    f = tmp_path / "printed.txt"
+    f.write_text(open(os.path.join(GOLDEN, "strassen_printed.txt")).read())
+    with pytest.raises(F.FmmError) as e:
+        F.Algorithm.load(str(f))
+    assert e.value.status == "FMM_E_NOT_EXACT"
+
+
+def test_library_create_exact_and_mutated(F):
+    s = O.load_alg(os.path.join(ALGS, "laderman_class_333_23.txt"))
+    a = F.Algorithm.create(3, 3, 3, 23, s.U, s.V, s.W)
+    assert a.R == 23
+    W = [list(r) for r in s.W]
+    W[4][7] = W[4][7] + 1
+    with pytest.raises(F.FmmError) as e:
+        F.Algorithm.create(3, 3, 3, 23, s.U, s.V, W)
+    assert e.value.status == "FMM_E_NOT_EXACT"
+    # rational coefficients are accepted exactly: scale column 0 by (2, 1/4, 2)
+    from fractions import Fraction as Fr
+    U = [[v * (2 if r == 0 else 1) for r, v in enumerate(row)] for row in s.U]
+    V = [[v * (Fr(1, 4) if r == 0 else 1) for r, v in enumerate(row)] for row in s.V]
+    W = [[v * (2 if r == 0 else 1) for r, v in enumerate(row)] for row in s.W]
+    F.Algorithm.create(3, 3, 3, 23, U, V, W)
+
+
+def test_parser_errors_name_the_line(F, tmp_path):
+    f = tmp_path / "bad.txt"
+    f.write_text("# comment\n2 2 2 7 exact\n1 0 1 0 1 -1 0\n0 0 0 x 1 0 1\n")
+    with pytest.raises(F.FmmError) as e:
+        F.Algorithm.load(str(f))
+    assert e.value.status == "FMM_E_PARSE" and "line 4" in str(e.value)
+    f.write_text("2 2 2 7 apa\n")
+    with pytest.raises(F.FmmError) as e:
+        F.Algorithm.load(str(f))
+    assert e.value.status == "FMM_E_UNSUPPORTED"
+
+
+def test_hybrid_split_matches_paper(F):
+    rows = [list(map(int, l.split())) for l in open(os.path.join(GOLDEN, "hybrid_split.txt")) if l.strip() and l[0] != "#"]
+    for R, L, P, bfs, dfs in rows:
+        assert F.hybrid_split(R, L, P) == (bfs, dfs)
+    for R in (7, 15, 23, 26, 29):
+        for G in (1, 2, 4, 8):
+            b, d = F.hybrid_split(R, 2, G)
+            assert b + d == R * R and b % G == 0 and d < G
