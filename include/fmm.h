@@ -142,6 +142,13 @@ fmm_status_t fmm_execute(fmm_plan_t* plan, const double* A, int64_t lda, const d
 fmm_status_t fmm_execute_timed(fmm_plan_t* plan, const double* A, int64_t lda, const double* B,
                                int64_t ldb, double* C, int64_t ldc, void* stream, float ms[5]);
 
+/* Same as fmm_execute, additionally recording four caller-created cudaEvent_t on `stream`
+   (non-blocking): events[0] before the first kernel, [1] after the formation kernels, [2] after
+   the leaf GEMM, [3] after the assembly and peel-strip kernels.  Used to time the phases inside
+   a timed region without synchronising. */
+fmm_status_t fmm_execute_events(fmm_plan_t* plan, const double* A, int64_t lda, const double* B,
+                                int64_t ldb, double* C, int64_t ldc, void* stream, void* events[4]);
+
 /* Host-memory execution (the end-to-end path): copies A and B (host, pinned or pageable) to
    device staging buffers owned by the plan, executes, and copies C back to host, all on
    `stream`; synchronises before returning. */
@@ -171,6 +178,11 @@ fmm_status_t fmm_hybrid_split(int64_t R, int L, int64_t G, int64_t* bfs, int64_t
    mma.sync f64 on the FP64 tensor pipe).  The L = 0 path of a plan. */
 fmm_status_t fmm_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda,
                        const double* B, int64_t ldb, double beta, double* C, int64_t ldc, void* stream);
+
+/* Measure the FP64 ceilings of the current device with this library's microbenchmark kernels
+   (independent mma.sync.m8n8k4.f64 chains; independent DFMA chains), ~50 ms.  The roofline
+   denominator for the leaf GEMM (MEASURED_PEAKS.json carries no FP64 figure). */
+fmm_status_t fmm_probe_fp64_peak(double* dmma_tflops, double* dfma_tflops);
 
 const char* fmm_last_error(void);
 const char* fmm_version(void);

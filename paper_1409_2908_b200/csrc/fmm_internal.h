@@ -86,6 +86,12 @@ void gemm_launch(const GemmTask* d_tasks, int ntasks, long long total_tiles, boo
                  cudaStream_t stream);
 int gemm_tile_m();
 int gemm_tile_n();
+// TMA + warp-specialised variant (fmm_gemm_tma.cu): needs 16-byte aligned views, even lds.
+bool gemm_tma_eligible(const std::vector<GemmTask>& tasks);
+size_t gemm_tma_map_bytes();  // bytes of one tensor map (two per task: A then B)
+void gemm_tma_maps(const std::vector<GemmTask>& tasks, void* out);
+void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles,
+                     cudaStream_t stream);
 
 // ---- linear-combination (addition chain) kernels, generated and compiled with NVRTC --------
 // One kernel computes, for every element position of a block, out_o = sum_i coef[o][i] * in_i.

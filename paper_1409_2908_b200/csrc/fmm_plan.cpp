@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -49,6 +50,8 @@ struct Launch {
   std::shared_ptr<LincombKernel> kern;
   long long tiles = 0;
   bool aligned16 = true;
+  bool tma = false;          // GEMM launches: TMA warp-specialised kernel
+  size_t maps_off = 0;       // byte offset of the tensor maps (2 per task)
   double elem_reads = 0, elem_writes = 0, elem_adds = 0;  // totals over the launch (elements)
   double flops = 0, gemm_bytes = 0;
 };
@@ -90,6 +93,7 @@ struct fmm_plan_s {
   std::vector<std::vector<long long>> offS, offT, offM;  // element offsets in ws, -1 = none
   std::vector<long long> offZero;                        // per level: zero M block (shared)
 
+  bool use_tma = true;  // FMM_NO_TMA=1 forces the cp.async GEMM (diagnostics)
   // kernels (vec 2 / vec 1 variants created lazily)
   std::shared_ptr<LincombKernel> kU[3], kV[3], kW[3];
 
@@ -300,8 +304,18 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
   auto push = [&](const void* p, size_t n) {
     size_t off = h_tab.size();
     h_tab.resize(align256(off + n));
-    std::memcpy(h_tab.data() + off, p, n);
+    if (p) std::memcpy(h_tab.data() + off, p, n);
     return off;
+  };
+  auto push_maps = [&](Launch& ln, const std::vector<GemmTask>& tasks) {
+    ln.tma = !lazy_kernels && use_tma && gemm_tma_eligible(tasks);
+    if (lazy_kernels) {  // dry build: reserve the space the maps would need
+      ln.maps_off = push(nullptr, 2 * gemm_tma_map_bytes() * tasks.size());
+      return;
+    }
+    std::vector<char> maps(2 * gemm_tma_map_bytes() * tasks.size());
+    if (ln.tma) gemm_tma_maps(tasks, maps.data());
+    ln.maps_off = push(maps.data(), maps.size());
   };
   auto outView = [&](int l, long long z) -> View {
     if (l == 0) return rootC;
@@ -410,6 +424,7 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
         ln.gemm_bytes += 8.0 * ((double)t.m * t.k + (double)t.k * t.n + (double)t.m * t.n);
       }
       ln.table_off = push(tasks.data(), tasks.size() * sizeof(GemmTask));
+      push_maps(ln, tasks);
       launches.push_back(ln);
     }
   }
@@ -502,6 +517,7 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
         ln.gemm_bytes += 8.0 * ((double)t.m * t.k + (double)t.k * t.n + (1.0 + (t.beta != 0.0)) * t.m * t.n);
       }
       ln.table_off = push(tasks.data(), tasks.size() * sizeof(GemmTask));
+      push_maps(ln, tasks);
       launches.push_back(ln);
     }
   }
@@ -524,6 +540,7 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
     throw Error(FMM_E_INVALID_ARG, "bad strategy");
   p->device = device;
   FMM_CUDA(cudaSetDevice(device));
+  if (const char* e = getenv("FMM_NO_TMA")) p->use_tma = !(e[0] == '1');
   p->userP = P;
   p->userQ = Q;
   p->userN = Nc;
@@ -616,7 +633,8 @@ void check_ld(const fmm_plan_t* p, long long lda, long long ldb, long long ldc) 
 
 // Enqueue the plan on `stream`; if ev_phase is non-null, record events between phases.
 void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc,
-         cudaStream_t stream, bool timed) {
+         cudaStream_t stream, cudaEvent_t* evs) {
+  const bool timed = evs != nullptr;
   // a pointer may be null only when its matrix is empty
   if ((!A && p->userP * p->userQ > 0) || (!B && p->userQ * p->userN > 0) || (!C && p->userP * p->userN > 0))
     throw Error(FMM_E_INVALID_ARG, "null matrix pointer");
@@ -641,12 +659,12 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
     p->cldc = ldc;
     p->tab_valid = true;
   }
-  if (timed) FMM_CUDA(cudaEventRecord(p->ev[0], stream));
+  if (timed) FMM_CUDA(cudaEventRecord(evs[0], stream));
   int phase = 0;  // 0 formation, 1 gemm, 2 assembly/strips
   for (const Launch& ln : p->launches) {
     const int ph = (ln.kind == Launch::FORM_A || ln.kind == Launch::FORM_B) ? 0 : ln.kind == Launch::GEMM ? 1 : 2;
     if (timed && ph != phase) {
-      for (int q = phase + 1; q <= ph; ++q) FMM_CUDA(cudaEventRecord(p->ev[q], stream));
+      for (int q = phase + 1; q <= ph; ++q) FMM_CUDA(cudaEventRecord(evs[q], stream));
       phase = ph;
     }
     const void* tab = p->d_tab + ln.table_off;
@@ -658,12 +676,15 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
         break;
       case Launch::GEMM:
       case Launch::STRIPS:
-        gemm_launch(reinterpret_cast<const GemmTask*>(tab), ln.count, ln.tiles, ln.aligned16, stream);
+        if (ln.tma)
+          gemm_tma_launch(reinterpret_cast<const GemmTask*>(tab), p->d_tab + ln.maps_off, ln.count, ln.tiles, stream);
+        else
+          gemm_launch(reinterpret_cast<const GemmTask*>(tab), ln.count, ln.tiles, ln.aligned16, stream);
         break;
     }
   }
   if (timed) {
-    for (int q = phase + 1; q <= 3; ++q) FMM_CUDA(cudaEventRecord(p->ev[q], stream));
+    for (int q = phase + 1; q <= 3; ++q) FMM_CUDA(cudaEventRecord(evs[q], stream));
   }
 }
 
@@ -731,7 +752,7 @@ fmm_status_t fmm_execute(fmm_plan_t* p, const double* A, int64_t lda, const doub
                          int64_t ldc, void* stream) {
   FMM_API_BEGIN
   if (!p) throw Error(FMM_E_INVALID_ARG, "null plan");
-  run(p, A, lda, B, ldb, C, ldc, (cudaStream_t)stream, false);
+  run(p, A, lda, B, ldb, C, ldc, (cudaStream_t)stream, nullptr);
   return FMM_OK;
   FMM_API_END
 }
@@ -749,7 +770,7 @@ fmm_status_t fmm_execute_timed(fmm_plan_t* p, const double* A, int64_t lda, cons
                                int64_t ldc, void* stream, float ms[5]) {
   FMM_API_BEGIN
   if (!p || !ms) throw Error(FMM_E_INVALID_ARG, "null argument");
-  run(p, A, lda, B, ldb, C, ldc, (cudaStream_t)stream, true);
+  run(p, A, lda, B, ldb, C, ldc, (cudaStream_t)stream, p->ev);
   FMM_CUDA(cudaEventSynchronize(p->ev[3]));
   float t01 = 0, t12 = 0, t23 = 0;
   FMM_CUDA(cudaEventElapsedTime(&t01, p->ev[0], p->ev[1]));
@@ -760,6 +781,17 @@ fmm_status_t fmm_execute_timed(fmm_plan_t* p, const double* A, int64_t lda, cons
   ms[2] = t23;
   ms[3] = 0.0f;
   ms[4] = t01 + t12 + t23;
+  return FMM_OK;
+  FMM_API_END
+}
+
+fmm_status_t fmm_execute_events(fmm_plan_t* p, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                                int64_t ldc, void* stream, void* events[4]) {
+  FMM_API_BEGIN
+  if (!p || !events) throw Error(FMM_E_INVALID_ARG, "null argument");
+  for (int q = 0; q < 4; ++q)
+    if (!events[q]) throw Error(FMM_E_INVALID_ARG, "null event");
+  run(p, A, lda, B, ldb, C, ldc, (cudaStream_t)stream, reinterpret_cast<cudaEvent_t*>(events));
   return FMM_OK;
   FMM_API_END
 }
@@ -783,7 +815,7 @@ fmm_status_t fmm_execute_host(fmm_plan_t* p, const double* A, int64_t lda, const
   }
   if (aR && aC) FMM_CUDA(cudaMemcpy2DAsync(p->sA, aC * 8, A, lda * 8, aC * 8, aR, cudaMemcpyHostToDevice, s));
   if (bR && bC) FMM_CUDA(cudaMemcpy2DAsync(p->sB, bC * 8, B, ldb * 8, bC * 8, bR, cudaMemcpyHostToDevice, s));
-  run(p, p->sA, std::max<long long>(aC, 1), p->sB, std::max<long long>(bC, 1), p->sC, std::max<long long>(cC, 1), s, false);
+  run(p, p->sA, std::max<long long>(aC, 1), p->sB, std::max<long long>(bC, 1), p->sC, std::max<long long>(cC, 1), s, nullptr);
   if (cR && cC) FMM_CUDA(cudaMemcpy2DAsync(C, ldc * 8, p->sC, cC * 8, cC * 8, cR, cudaMemcpyDeviceToHost, s));
   FMM_CUDA(cudaStreamSynchronize(s));
   return FMM_OK;
@@ -815,7 +847,7 @@ fmm_status_t fmm_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const doub
   int dev = 0;
   FMM_CUDA(cudaGetDevice(&dev));
   if (!d_task || d_task_dev != dev) {
-    FMM_CUDA(cudaMalloc(&d_task, sizeof(GemmTask) * 64));
+    FMM_CUDA(cudaMalloc(&d_task, 4096));
     d_task_dev = dev;
   }
   std::vector<GemmTask> t(1);
@@ -832,9 +864,16 @@ fmm_status_t fmm_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const doub
   t[0].beta = beta;
   const long long tiles = gemm_prepare(t);
   cudaStream_t s = (cudaStream_t)stream;
-  // the task descriptor is passed by value through a stream-ordered upload
-  FMM_CUDA(cudaMemcpyAsync(d_task, t.data(), sizeof(GemmTask), cudaMemcpyHostToDevice, s));
-  gemm_launch(d_task, 1, tiles, gemm_tasks_aligned16(t), s);
+  // the task descriptor (and its tensor maps) go through a stream-ordered upload
+  const bool tma = gemm_tma_eligible(t) && !(getenv("FMM_NO_TMA") && getenv("FMM_NO_TMA")[0] == '1');
+  alignas(128) char buf[1024];
+  std::memcpy(buf, t.data(), sizeof(GemmTask));
+  if (tma) gemm_tma_maps(t, buf + 512);
+  FMM_CUDA(cudaMemcpyAsync(d_task, buf, sizeof(buf), cudaMemcpyHostToDevice, s));
+  if (tma)
+    gemm_tma_launch(d_task, reinterpret_cast<char*>(d_task) + 512, 1, tiles, s);
+  else
+    gemm_launch(d_task, 1, tiles, gemm_tasks_aligned16(t), s);
   return FMM_OK;
   FMM_API_END
 }

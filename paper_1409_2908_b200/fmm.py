@@ -51,6 +51,8 @@ def _load():
         "fmm_exec": [vp, vp, vp, vp],
         "fmm_execute_timed": [vp, vp, i64, vp, i64, vp, i64, vp, ctypes.POINTER(ctypes.c_float)],
         "fmm_execute_host": [vp, vp, i64, vp, i64, vp, i64, vp],
+        "fmm_execute_events": [vp, vp, i64, vp, i64, vp, i64, vp, ctypes.POINTER(vp)],
+        "fmm_probe_fp64_peak": [ctypes.POINTER(dp), ctypes.POINTER(dp)],
         "fmm_sync": [vp],
         "fmm_hybrid_split": [i64, i32, i64, p64, p64],
         "fmm_dgemm": [i64, i64, i64, dp, vp, i64, vp, i64, dp, vp, i64, vp],
@@ -216,6 +218,13 @@ class Plan:
         _check(_lib.fmm_execute_timed(self._h, *self._args(A, B, C), _stream_ptr(stream), ms))
         return C, {"formation_ms": ms[0], "gemm_ms": ms[1], "assembly_ms": ms[2], "total_ms": ms[4]}
 
+    def execute_events(self, A, B, C, events, stream=None):
+        """Asynchronous execute that records 4 torch.cuda.Event on the stream: before, after
+        formation, after the leaf GEMM, after assembly/strips."""
+        ev = (ctypes.c_void_p * 4)(*[e.cuda_event for e in events])
+        _check(_lib.fmm_execute_events(self._h, *self._args(A, B, C), _stream_ptr(stream), ev))
+        return C
+
     def execute_host(self, A, B, C, stream=None):
         """Host (CPU) tensors / arrays in, host result out: H2D, execute, D2H (blocking)."""
         import numpy as np
@@ -263,6 +272,13 @@ def dgemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, stream=None):
     c, ldc = _mat(C, ROW_MAJOR, m, n, "C")
     _check(_lib.fmm_dgemm(m, n, k, alpha, a, lda, b, ldb, beta, c, ldc, _stream_ptr(stream)))
     return C
+
+
+def probe_fp64_peak():
+    """(DMMA TFLOP/s, DFMA TFLOP/s) measured on the current device by the library's probes."""
+    a, b = ctypes.c_double(), ctypes.c_double()
+    _check(_lib.fmm_probe_fp64_peak(ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
 
 
 def hybrid_split(R: int, L: int, G: int):

@@ -216,3 +216,14 @@ def test_execute_host_end_to_end():
     C = np.zeros((300, 310))
     p.execute_host(A, B, C)
     assert np.max(np.abs(C - O.fast(A, B, oalg("hk_class_323_15"), 2))) <= bound(A, B, 1e-12)
+
+
+def test_cp_async_gemm_path_matches_tma_path(monkeypatch):
+    # FMM_NO_TMA=1 forces the cp.async grouped GEMM; both must give oracle parity
+    A, B = I.problem(700, 300, 650, seed=11)
+    ref = O.fast(A, B, oalg("alg_424_26"), 2)
+    C_tma, _ = run("alg_424_26", A, B, 2)
+    monkeypatch.setenv("FMM_NO_TMA", "1")
+    C_cp, _ = run("alg_424_26", A, B, 2)
+    for C in (C_tma, C_cp):
+        assert np.max(np.abs(C - ref)) <= bound(A, B, 1e-12)
