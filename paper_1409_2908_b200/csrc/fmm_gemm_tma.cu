@@ -3,14 +3,14 @@
 // Same contract as grouped_dgemm in fmm_gemm.cu (task table of C = alpha A B + beta C, row-major),
 // used whenever every operand view is 16-byte aligned with even leading dimensions (what TMA
 // requires).  Structure, per CTA (one per SM, looping over tiles):
-//   thread 0 (producer, inside warp 0): issues cp.async.bulk.tensor (TMA) loads of the A tile
+//   warpgroup 0 (producer): one thread issues cp.async.bulk.tensor (TMA) loads of the A tile
 //       (one 128x16 box) and the B tile (eight 16x16 boxes) per k-step into a 6-stage ring of
-//       shared-memory buffers, STAGES-1 steps ahead, signalling a "full" mbarrier with
-//       complete_tx; its cursor runs over the CTA's whole (tile, k-step) sequence, so loads for
-//       the next tile are in flight while the current tile's epilogue runs.  (A separate
-//       producer warp would make 9 warps, and the register file split over 4 sub-partitions
-//       would cap every thread at 168 registers; the 64x32 warp tile needs ~210.)
-//   warps 0-7 (consumers): 2 x 4 warps of 64 x 32 outputs; wait "full", read register fragments,
+//       shared-memory buffers as soon as a stage is released, signalling a "full" mbarrier with
+//       complete_tx; it runs over the CTA's whole (tile, k-step) sequence, so the next tile's
+//       loads are in flight while the current tile's epilogue runs.  It gives its registers
+//       away with setmaxnreg.dec (40), so the consumers can grow to 232 (setmaxnreg.inc) —
+//       the 64x32 warp tile needs ~210, above the 168 a flat 384-thread launch would allow.
+//   warpgroups 1-2 (consumers): 2 x 4 warps of 64 x 32 outputs; wait "full", read register fragments,
 //       issue mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4), arrive "empty"; epilogue straight from
 //       registers with 16-byte stores.  No CTA-wide barrier in the main loop.
 // TMA writes the tiles with the 128-byte swizzle (16-byte chunk index XOR row mod 8).  The DMMA
@@ -32,7 +32,7 @@ namespace fmm {
 
 namespace {
 constexpr int BM = 128, BN = 128, BK = 16, STAGES = 6;
-constexpr int CONSUMERS = 8, THREADS = CONSUMERS * 32;
+constexpr int CONSUMERS = 8, THREADS = 128 + CONSUMERS * 32;  // warpgroup 0 = producer, 1-2 = consumers
 constexpr int A_BYTES = BM * BK * 8;   // 16 KB
 constexpr int B_BYTES = BK * BN * 8;   // 16 KB (8 boxes of 16 x 16)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -120,45 +120,36 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   __syncthreads();
 
-  // ---- producer state (thread 0 only): a cursor over this CTA's (tile, k-step) sequence ----
-  int p_tile = blockIdx.x, p_kt = 0, p_KT = 0, p_stage = 0;
-  unsigned p_phase = 0;
-  TileCoord p_tc{0, 0, 0};
-  auto p_advance_tile = [&]() {
-    while (p_tile < total_tiles) {
-      p_tc = locate(tasks, ntasks, p_tile);
-      p_KT = (__ldg(&tasks[p_tc.task].k) + BK - 1) / BK;
-      if (p_KT > 0) return;
-      p_tile += gridDim.x;
-    }
-  };
-  // issue the next k-step's TMA loads (if any remain); waits until the stage is free
-  auto produce = [&]() {
-    if (p_tile >= total_tiles) return;
-    mbar_wait(empty_bar(p_stage), p_phase ^ 1u);
-    const unsigned sa = base + p_stage * STAGE_BYTES, sb = sa + A_BYTES;
-    const CUtensorMap* ma = maps + 2 * p_tc.task;
-    const CUtensorMap* mb = ma + 1;
-    mbar_expect_tx(full_bar(p_stage), STAGE_BYTES);
-    tma_load_2d(sa, ma, p_kt * BK, p_tc.m0, full_bar(p_stage));
+  if (warp < 4) {
+    // ------------------------------ producer warpgroup ------------------------------
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    if (warp == 0 && lane == 0) {
+      int stage = 0;
+      unsigned phase = 0;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        const TileCoord tc = locate(tasks, ntasks, tile);
+        const CUtensorMap* ma = maps + 2 * tc.task;
+        const CUtensorMap* mb = ma + 1;
+        const int KT = (__ldg(&tasks[tc.task].k) + BK - 1) / BK;
+        for (int kt = 0; kt < KT; ++kt) {
+          mbar_wait(empty_bar(stage), phase ^ 1u);
+          const unsigned sa = base + stage * STAGE_BYTES, sb = sa + A_BYTES;
+          mbar_expect_tx(full_bar(stage), STAGE_BYTES);
+          tma_load_2d(sa, ma, kt * BK, tc.m0, full_bar(stage));
 #pragma unroll
-    for (int b = 0; b < BN / 16; ++b) tma_load_2d(sb + b * 2048, mb, p_tc.n0 + 16 * b, p_kt * BK, full_bar(p_stage));
-    if (++p_stage == STAGES) p_stage = 0, p_phase ^= 1u;
-    if (++p_kt == p_KT) {
-      p_kt = 0;
-      p_tile += gridDim.x;
-      p_advance_tile();
+          for (int b = 0; b < BN / 16; ++b) tma_load_2d(sb + b * 2048, mb, tc.n0 + 16 * b, kt * BK, full_bar(stage));
+          if (++stage == STAGES) stage = 0, phase ^= 1u;
+        }
+      }
     }
-  };
-  const bool producer = threadIdx.x == 0;
-  if (producer) {
-    p_advance_tile();
-    for (int q = 0; q < STAGES - 1; ++q) produce();
+    return;
   }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
 
   // ------------------------------ consumers ------------------------------
+  const int cw = warp - 4;  // consumer warp 0..7
   const int r = lane >> 2, c = lane & 3;
-  const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;
+  const int wm = (cw >> 2) * 64, wn = (cw & 3) * 32;
   // A fragment byte offsets within a stage (without the k-step chunk XOR): subtile i row
   //   R = wm + 16*(i/2) + 2r + (i%2); chunk = (2s + (c>>1)) ^ (R & 7); half = c & 1
   const unsigned a_row0 = (unsigned)(wm + 2 * r) * 128u;  // i = 0
@@ -208,7 +199,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(empty_bar(stage));
       if (++stage == STAGES) stage = 0, phase ^= 1u;
-      if (producer) produce();  // refill the stage released one step ago, STAGES-1 ahead
     }
 
     // ---- epilogue: C = alpha * acc (+ beta * C) ----
