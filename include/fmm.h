@@ -172,6 +172,12 @@ fmm_status_t fmm_exec(fmm_plan_t* plan, const double* A, const double* B, double
    r_1-major), *dfs = R^L mod G leaves split by rows over all G. */
 fmm_status_t fmm_hybrid_split(int64_t R, int L, int64_t G, int64_t* bfs, int64_t* dfs);
 
+/* The leaf share of worker g of G (the partition every sharded plan uses): for each of the
+   `leaves` leaves (index r_1-major), rows [r0[z], r1[z]) of its product belong to worker g
+   (r0 == r1: none).  The first leaves - (leaves mod G) leaves go whole to one worker each in
+   contiguous equal ranges; each remaining leaf is split by rows over all G.  Host only. */
+fmm_status_t fmm_shard_leaf_rows(int64_t leaves, int64_t rows, int64_t G, int64_t g, int64_t* r0, int64_t* r1);
+
 /* ---- kernels usable on their own (device pointers, stream-ordered) ---------------------- */
 
 /* Classical product C = alpha*A*B + beta*C with the library's DMMA GEMM kernel (row-major,

@@ -281,4 +281,26 @@ fmm_status_t fmm_hybrid_split(int64_t R, int L, int64_t G, int64_t* bfs, int64_t
   FMM_API_END
 }
 
+fmm_status_t fmm_shard_leaf_rows(int64_t leaves, int64_t rows, int64_t G, int64_t g, int64_t* r0, int64_t* r1) {
+  FMM_API_BEGIN
+  if (leaves < 1 || rows < 0 || G < 1 || g < 0 || g >= G || !r0 || !r1)
+    throw Error(FMM_E_INVALID_ARG, "bad shard arguments");
+  // HYBRID arithmetic with GPUs as the workers: the first leaves - (leaves mod G)
+  // leaves are dealt out in contiguous, equal ranges (BFS part); each of the remaining
+  // leaves mod G leaves is split by rows over all G workers (DFS part).
+  const int64_t dfs = leaves % G, bfs = leaves - dfs, per = bfs / G;
+  for (int64_t z = 0; z < leaves; ++z) {
+    if (z < bfs) {
+      const bool mine = z >= g * per && z < (g + 1) * per;
+      r0[z] = 0;
+      r1[z] = mine ? rows : 0;
+    } else {
+      r0[z] = rows * g / G;
+      r1[z] = rows * (g + 1) / G;
+    }
+  }
+  return FMM_OK;
+  FMM_API_END
+}
+
 }  // extern "C"

@@ -175,18 +175,12 @@ struct fmm_plan_s {
     const long long G = std::max(1, opt.shard_count), g = opt.shard_rank;
     leaves = nodes_at[L];
     const long long dfs = leaves % G, bfs = leaves - dfs;
-    leaf_r0.assign(leaves, 0);
-    leaf_r1.assign(leaves, 0);
-    const long long pL = dims[L].P;
     const long long per = bfs / G;
-    for (long long z = 0; z < leaves; ++z) {
-      if (z < bfs) {
-        if (z >= g * per && z < (g + 1) * per) leaf_r0[z] = 0, leaf_r1[z] = pL;
-      } else {
-        leaf_r0[z] = pL * g / G;
-        leaf_r1[z] = pL * (g + 1) / G;
-      }
-    }
+    std::vector<int64_t> r0(leaves), r1(leaves);
+    if (fmm_shard_leaf_rows(leaves, dims[L].P, G, g, r0.data(), r1.data()) != FMM_OK)
+      throw Error(FMM_E_INVALID_ARG, "bad shard arguments");
+    leaf_r0.assign(r0.begin(), r0.end());
+    leaf_r1.assign(r1.begin(), r1.end());
     needed.assign(L + 1, {});
     strip_owner.assign(L + 1, {});
     for (int l = 0; l <= L; ++l) {

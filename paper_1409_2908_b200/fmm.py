@@ -55,6 +55,7 @@ def _load():
         "fmm_probe_fp64_peak": [ctypes.POINTER(dp), ctypes.POINTER(dp)],
         "fmm_sync": [vp],
         "fmm_hybrid_split": [i64, i32, i64, p64, p64],
+        "fmm_shard_leaf_rows": [i64, i64, i64, i64, p64, p64],
         "fmm_dgemm": [i64, i64, i64, dp, vp, i64, vp, i64, dp, vp, i64, vp],
     }
     for name, args in sig.items():
@@ -279,6 +280,14 @@ def probe_fp64_peak():
     a, b = ctypes.c_double(), ctypes.c_double()
     _check(_lib.fmm_probe_fp64_peak(ctypes.byref(a), ctypes.byref(b)))
     return a.value, b.value
+
+
+def shard_leaf_rows(leaves: int, rows: int, G: int, g: int):
+    """[(r0, r1)] per leaf: the rows of each leaf product that worker g of G computes."""
+    r0 = (ctypes.c_int64 * leaves)()
+    r1 = (ctypes.c_int64 * leaves)()
+    _check(_lib.fmm_shard_leaf_rows(leaves, rows, G, g, r0, r1))
+    return list(zip(r0, r1))
 
 
 def hybrid_split(R: int, L: int, G: int):
