@@ -68,9 +68,15 @@ typedef struct {
                                shard_count plans gives A*B.  0 / 1 for a single GPU. */
   int shard_count;
   size_t workspace_limit_bytes; /* 0 = no limit */
+  int peel_align;           /* 1: when the paper's core N' = N floor(Nc/N) gives an odd column-block
+                               width, peel to N' = 2N floor(Nc/(2N)) instead (one extra column
+                               block in the classical strip), so every sub-block view is 16-byte
+                               aligned and TMA / 16-byte vector paths apply (R7b).
+                               0: the paper's minimal peeling everywhere. */
 } fmm_plan_options;
 
-/* Fill *opt with the defaults: row-major, streaming, cse = 1, shard 0 of 1, no limit. */
+/* Fill *opt with the defaults: row-major, streaming, cse = 1, shard 0 of 1, no limit,
+   peel_align = 1. */
 void fmm_plan_options_default(fmm_plan_options* opt);
 
 /* ---- algorithms ------------------------------------------------------------------------- */
@@ -149,11 +155,19 @@ fmm_status_t fmm_execute_timed(fmm_plan_t* plan, const double* A, int64_t lda, c
 fmm_status_t fmm_execute_events(fmm_plan_t* plan, const double* A, int64_t lda, const double* B,
                                 int64_t ldb, double* C, int64_t ldc, void* stream, void* events[4]);
 
-/* Host-memory execution (the end-to-end path): copies A and B (host, pinned or pageable) to
-   device staging buffers owned by the plan, executes, and copies C back to host, all on
-   `stream`; synchronises before returning. */
+/* Host-memory execution (the end-to-end path): copies A and B (host memory) to device staging
+   buffers owned by the plan, executes on `stream`, and copies C back to host; synchronises
+   before returning. */
 fmm_status_t fmm_execute_host(fmm_plan_t* plan, const double* A, int64_t lda, const double* B,
                               int64_t ldb, double* C, int64_t ldc, void* stream);
+
+/* Pipelined host-memory execution: enqueue the H2D copies (plan-owned copy-in stream), the
+   computation (`stream`) and the D2H copy (plan-owned copy-out stream) and return.  The plan
+   alternates two staging sets, so back-to-back calls overlap copy-in of one problem, compute of
+   another and copy-out of a third.  Host buffers must be pinned for overlap and must stay valid
+   and unmodified (C unread) until fmm_sync(plan) returns. */
+fmm_status_t fmm_execute_host_async(fmm_plan_t* plan, const double* A, int64_t lda, const double* B,
+                                    int64_t ldb, double* C, int64_t ldc, void* stream);
 
 /* Block until every fmm_execute on the plan has finished; reports asynchronous faults. */
 fmm_status_t fmm_sync(fmm_plan_t* plan);

@@ -189,11 +189,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 int gemm_tile_m() { return BM; }
 int gemm_tile_n() { return BN; }
 
-long long gemm_prepare(std::vector<GemmTask>& tasks) {
+long long gemm_prepare(std::vector<GemmTask>& tasks, int bm, int bn) {
   long long total = 0;
   for (auto& t : tasks) {
-    t.tiles_m = (t.m + BM - 1) / BM;
-    t.tiles_n = (t.n + BN - 1) / BN;
+    t.tiles_m = (t.m + bm - 1) / bm;
+    t.tiles_n = (t.n + bn - 1) / bn;
     t.tile_begin = (int)total;
     total += (long long)t.tiles_m * t.tiles_n;
   }

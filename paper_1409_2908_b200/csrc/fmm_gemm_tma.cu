@@ -24,6 +24,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 #include "fmm_internal.h"
@@ -31,12 +33,10 @@
 namespace fmm {
 
 namespace {
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 6;
+constexpr int BM = 128, BK = 16, STAGES = 6;
 constexpr int CONSUMERS = 8, THREADS = 128 + CONSUMERS * 32;  // warpgroup 0 = producer, 1-2 = consumers
 constexpr int A_BYTES = BM * BK * 8;   // 16 KB
-constexpr int B_BYTES = BK * BN * 8;   // 16 KB (8 boxes of 16 x 16)
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr size_t smem_bytes(int bn) { return (size_t)STAGES * (A_BYTES + BK * bn * 8) + 1024 /*align*/ + 256 /*barriers*/; }
 constexpr int GROUP_M = 8;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -83,6 +83,7 @@ __device__ __forceinline__ double lds64(unsigned addr) {
 struct TileCoord {
   int task, m0, n0;
 };
+template <int BN>
 __device__ __forceinline__ TileCoord locate(const GemmTask* __restrict__ tasks, int ntasks, int tile) {
   int lo = 0, hi = ntasks - 1;
   while (lo < hi) {
@@ -100,13 +101,22 @@ __device__ __forceinline__ TileCoord locate(const GemmTask* __restrict__ tasks, 
   return {lo, tm * BM, tn * BN};
 }
 
+// BN columns per CTA tile, consumer warps arranged WGM x WGN (WGM * WGN = 8); warp tile
+// (128 / WGM) x (BN / WGN), both multiples of 16 so the fragment permutations apply.
+template <int BN, int WGM, int WGN>
 __global__ void __launch_bounds__(THREADS, 1)
     grouped_dgemm_tma(const GemmTask* __restrict__ tasks, const CUtensorMap* __restrict__ maps, int ntasks,
                       int total_tiles) {
+  static_assert(WGM * WGN == CONSUMERS, "8 consumer warps");
+  constexpr int WTM = BM / WGM, WTN = BN / WGN;
+  static_assert(WTM % 16 == 0 && WTN % 16 == 0, "warp tile must be a multiple of 16");
+  constexpr int MI = WTM / 8, NI = WTN / 8;
+  constexpr int B_BYTES_T = BK * BN * 8;  // BN/16 boxes of 16 x 16
+  constexpr int STAGE_T = A_BYTES + B_BYTES_T;
   extern __shared__ unsigned char smem_raw[];
   const unsigned raw = smem_u32(smem_raw);
   const unsigned base = (raw + 1023u) & ~1023u;  // 1024-byte alignment for the 128B swizzle
-  const unsigned bars = base + STAGES * STAGE_BYTES;
+  const unsigned bars = base + STAGES * STAGE_T;
   auto full_bar = [&](int s) { return bars + 8u * s; };
   auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -127,14 +137,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       int stage = 0;
       unsigned phase = 0;
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-        const TileCoord tc = locate(tasks, ntasks, tile);
+        const TileCoord tc = locate<BN>(tasks, ntasks, tile);
         const CUtensorMap* ma = maps + 2 * tc.task;
         const CUtensorMap* mb = ma + 1;
         const int KT = (__ldg(&tasks[tc.task].k) + BK - 1) / BK;
         for (int kt = 0; kt < KT; ++kt) {
           mbar_wait(empty_bar(stage), phase ^ 1u);
-          const unsigned sa = base + stage * STAGE_BYTES, sb = sa + A_BYTES;
-          mbar_expect_tx(full_bar(stage), STAGE_BYTES);
+          const unsigned sa = base + stage * STAGE_T, sb = sa + A_BYTES;
+          mbar_expect_tx(full_bar(stage), STAGE_T);
           tma_load_2d(sa, ma, kt * BK, tc.m0, full_bar(stage));
 #pragma unroll
           for (int b = 0; b < BN / 16; ++b) tma_load_2d(sb + b * 2048, mb, tc.n0 + 16 * b, kt * BK, full_bar(stage));
@@ -149,71 +159,71 @@ __global__ void __launch_bounds__(THREADS, 1)
   // ------------------------------ consumers ------------------------------
   const int cw = warp - 4;  // consumer warp 0..7
   const int r = lane >> 2, c = lane & 3;
-  const int wm = (cw >> 2) * 64, wn = (cw & 3) * 32;
-  // A fragment byte offsets within a stage (without the k-step chunk XOR): subtile i row
-  //   R = wm + 16*(i/2) + 2r + (i%2); chunk = (2s + (c>>1)) ^ (R & 7); half = c & 1
-  const unsigned a_row0 = (unsigned)(wm + 2 * r) * 128u;  // i = 0
+  const int wm = (cw / WGN) * WTM, wn = (cw % WGN) * WTN;
+  // A fragment: subtile i, fragment row r -> tile row R = wm + 16*(i/2) + 2r + (i%2);
+  //   16-byte chunk = (2s + (c>>1)) ^ (R & 7); 8-byte half = c & 1
+  const unsigned a_row0 = (unsigned)(wm + 2 * r) * 128u;
   const unsigned xa0 = (unsigned)((2 * r) & 7), xa1 = (unsigned)((2 * r + 1) & 7);
   const unsigned ha = (unsigned)(c & 1) * 8u, ca = (unsigned)(c >> 1);
-  // B fragment: box b = wn/16 + jj/2; phys col = 4*(jj%2) + map0[r] ; k row = 4s + c
+  // B fragment: subtile jj, fragment col r -> box wn/16 + jj/2, box col 4*(jj%2) + map0[r];
+  //   k row = 4s + c; chunk = (box col >> 1) ^ (k row & 7)
   const unsigned map0 = (r == 0) ? 0u : (r == 1) ? 1u : (r == 2) ? 8u : (r == 3) ? 9u : (r == 4) ? 2u : (r == 5) ? 3u : (r == 6) ? 10u : 11u;
-  const unsigned hb = map0 & 1u, cb0 = map0 >> 1;  // chunk for jj%2 == 0; +2 for jj%2 == 1
+  const unsigned hb = map0 & 1u, cb0 = map0 >> 1;
   const unsigned b_box0 = (unsigned)(wn / 16) * 2048u;
 
   int stage = 0;
   unsigned phase = 0;
   for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-    const TileCoord tc = locate(tasks, ntasks, tile);
+    const TileCoord tc = locate<BN>(tasks, ntasks, tile);
     const GemmTask& t = tasks[tc.task];
-    const int k = __ldg(&t.k);
-    const int KT = (k + BK - 1) / BK;
-    double acc[8][4][2];
+    const int KT = (__ldg(&t.k) + BK - 1) / BK;
+    double acc[MI][NI][2];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < MI; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     for (int kt = 0; kt < KT; ++kt) {
       mbar_wait(full_bar(stage), phase);
-      const unsigned sa = base + stage * STAGE_BYTES, sb = sa + A_BYTES;
+      const unsigned sa = base + stage * STAGE_T, sb = sa + A_BYTES;
 #pragma unroll
       for (int s = 0; s < BK / 4; ++s) {
-        double a[8], b[4];
+        double a[MI], b[NI];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < MI; ++i) {
           const unsigned x = (i & 1) ? xa1 : xa0;
           const unsigned chunk = ((unsigned)(2 * s) + ca) ^ x;
           a[i] = lds64(sa + a_row0 + (unsigned)(16 * (i >> 1) + (i & 1)) * 128u + chunk * 16u + ha);
         }
         const unsigned krow = (unsigned)(4 * s + c);
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
+        for (int jj = 0; jj < NI; ++jj) {
           const unsigned chunk = (cb0 + 2u * (jj & 1)) ^ (krow & 7u);
           b[jj] = lds64(sb + b_box0 + (unsigned)(jj >> 1) * 2048u + krow * 128u + chunk * 16u + hb * 8u);
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < MI; ++i)
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) dmma(acc[i][jj], a[i], b[jj]);
+          for (int jj = 0; jj < NI; ++jj) dmma(acc[i][jj], a[i], b[jj]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty_bar(stage));
       if (++stage == STAGES) stage = 0, phase ^= 1u;
     }
 
-    // ---- epilogue: C = alpha * acc (+ beta * C) ----
+    // ---- epilogue: C = alpha * acc (+ beta * C), from registers ----
     const double alpha = __ldg(&t.alpha), beta = __ldg(&t.beta);
     const int m = __ldg(&t.m), n = __ldg(&t.n);
     const long long ldc = __ldg(&t.ldc);
     double* C = t.C;
     const int cofs = (c == 0) ? 0 : (c == 1) ? 8 : (c == 2) ? 2 : 10;  // map0[2c]
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < MI; ++i) {
       const int row = tc.m0 + wm + 16 * (i >> 1) + 2 * r + (i & 1);
       if (row >= m) continue;
       double* crow = C + (long long)row * ldc;
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
+      for (int jj = 0; jj < NI; ++jj) {
         const int col = tc.n0 + wn + 16 * (jj >> 1) + 4 * (jj & 1) + cofs;
         double v0 = alpha * acc[i][jj][0], v1 = alpha * acc[i][jj][1];
         if (col + 1 < n) {
@@ -284,22 +294,69 @@ void gemm_tma_maps(const std::vector<GemmTask>& tasks, void* out) {
   }
 }
 
-void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles,
-                     cudaStream_t stream) {
-  if (total_tiles <= 0 || ntasks <= 0) return;
-  static int sms = 0;
-  static bool configured = false;
+template <int BN, int WGM, int WGN>
+static void launch_cfg(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int sms,
+                       cudaStream_t stream) {
+  static bool configured = false;  // per process; one device per process (torchrun)
+  auto kern = grouped_dgemm_tma<BN, WGM, WGN>;
   if (!configured) {
-    int dev = 0;
-    FMM_CUDA(cudaGetDevice(&dev));
-    FMM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    FMM_CUDA(cudaFuncSetAttribute(grouped_dgemm_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(BN)));
     configured = true;
   }
   const int grid = (int)std::min<long long>(total_tiles, sms);
-  grouped_dgemm_tma<<<grid, THREADS, SMEM_BYTES, stream>>>(d_tasks, reinterpret_cast<const CUtensorMap*>(d_maps), ntasks,
-                                                          (int)total_tiles);
+  kern<<<grid, THREADS, smem_bytes(BN), stream>>>(d_tasks, reinterpret_cast<const CUtensorMap*>(d_maps), ntasks,
+                                                 (int)total_tiles);
   FMM_CUDA(cudaGetLastError());
+}
+
+int gemm_choose_bn(const std::vector<GemmTask>& tasks) {
+  if (const char* e = getenv("FMM_GEMM_BN")) return atoi(e);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
+    cudaGetLastError();
+  }
+  // relative DMMA efficiency of each tile width (narrow tiles read more operand bytes per flop)
+  static const int menu[] = {128, 112, 96, 80, 64};
+  static const double eff[] = {1.00, 0.985, 0.975, 0.965, 0.94};
+  int best = 128;
+  double best_t = 1e300;
+  for (int q = 0; q < 5; ++q) {
+    const int bn = menu[q];
+    double work = 0, tiles = 0;
+    for (const auto& t : tasks) {
+      const double tl = (double)((t.m + BM - 1) / BM) * ((t.n + bn - 1) / bn);
+      tiles += tl;
+      work += tl * BM * bn * (double)(((t.k + BK - 1) / BK) * BK + 32 /* epilogue, prologue */);
+    }
+    if (tiles <= 0) continue;
+    const double waves = std::ceil(tiles / sms);
+    const double tmax = std::max(work / tiles * waves, work / sms);  // per-SM time, unit work
+    const double t_est = tmax / eff[q];
+    if (t_est < best_t * 0.999) best_t = t_est, best = bn;
+  }
+  return best;
+}
+
+void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn,
+                     cudaStream_t stream) {
+  if (total_tiles <= 0 || ntasks <= 0) return;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    FMM_CUDA(cudaGetDevice(&dev));
+    FMM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  switch (bn) {
+    case 128: launch_cfg<128, 2, 4>(d_tasks, d_maps, ntasks, total_tiles, sms, stream); break;
+    case 112: launch_cfg<112, 8, 1>(d_tasks, d_maps, ntasks, total_tiles, sms, stream); break;
+    case 96: launch_cfg<96, 4, 2>(d_tasks, d_maps, ntasks, total_tiles, sms, stream); break;
+    case 80: launch_cfg<80, 8, 1>(d_tasks, d_maps, ntasks, total_tiles, sms, stream); break;
+    case 64: launch_cfg<64, 4, 2>(d_tasks, d_maps, ntasks, total_tiles, sms, stream); break;
+    default: throw Error(FMM_E_INVALID_ARG, "unsupported GEMM tile width " + std::to_string(bn));
+  }
 }
 
 }  // namespace fmm

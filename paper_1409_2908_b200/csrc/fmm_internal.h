@@ -79,7 +79,7 @@ struct GemmTask {
   double alpha, beta;
 };
 // Fill tiles_m/tiles_n/tile_begin; returns the total number of CTA tiles.
-long long gemm_prepare(std::vector<GemmTask>& tasks);
+long long gemm_prepare(std::vector<GemmTask>& tasks, int bm = 128, int bn = 128);
 bool gemm_tasks_aligned16(const std::vector<GemmTask>& tasks);
 // Launch over a device copy of the prepared task list.
 void gemm_launch(const GemmTask* d_tasks, int ntasks, long long total_tiles, bool aligned16,
@@ -90,8 +90,16 @@ int gemm_tile_n();
 bool gemm_tma_eligible(const std::vector<GemmTask>& tasks);
 size_t gemm_tma_map_bytes();  // bytes of one tensor map (two per task: A then B)
 void gemm_tma_maps(const std::vector<GemmTask>& tasks, void* out);
-void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles,
+void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn,
                      cudaStream_t stream);
+// Thin products (one dimension <= skinny_limit()) on the CUDA cores (fmm_skinny.cu): ids index
+// the task table; row tasks have m <= limit, column tasks n <= limit.
+int skinny_limit();
+void skinny_launch(const GemmTask* d_tasks, const int* d_row_ids, int nrow, int max_n, const int* d_col_ids, int ncol,
+                   int max_m, cudaStream_t stream);
+// Pick the TMA kernel's tile width (128 rows x bn columns) for a task list from a cost model of
+// padded work, measured per-width efficiency and wave quantisation; FMM_GEMM_BN overrides.
+int gemm_choose_bn(const std::vector<GemmTask>& tasks);
 
 // ---- linear-combination (addition chain) kernels, generated and compiled with NVRTC --------
 // One kernel computes, for every element position of a block, out_o = sum_i coef[o][i] * in_i.

@@ -42,7 +42,7 @@ struct Dims {
 };
 
 struct Launch {
-  enum Kind { FORM_A, FORM_B, GEMM, ASSEMBLE, STRIPS } kind;
+  enum Kind { FORM_A, FORM_B, GEMM, ASSEMBLE, STRIPS, SKINNY } kind;
   int level = 0;
   size_t table_off = 0;  // byte offset in the device table buffer
   int count = 0;         // nodes / tasks
@@ -51,6 +51,9 @@ struct Launch {
   long long tiles = 0;
   bool aligned16 = true;
   bool tma = false;          // GEMM launches: TMA warp-specialised kernel
+  int bn = 128;              // GEMM launches: CTA tile width
+  size_t ids_off = 0;        // SKINNY: int ids (row tasks then column tasks)
+  int nrow = 0, ncol = 0, max_n = 0, max_m = 0;
   size_t maps_off = 0;       // byte offset of the tensor maps (2 per task)
   double elem_reads = 0, elem_writes = 0, elem_adds = 0;  // totals over the launch (elements)
   double flops = 0, gemm_bytes = 0;
@@ -97,22 +100,32 @@ struct fmm_plan_s {
   // kernels (vec 2 / vec 1 variants created lazily)
   std::shared_ptr<LincombKernel> kU[3], kV[3], kW[3];
 
-  // launch tables
+  // launch tables: `launches`/`h_tab` are the scratch of the last build; two device slots cache
+  // the tables of the two most recent (A, B, C, ld) sets (the pipelined host path alternates two
+  // staging buffer sets)
   std::vector<Launch> launches;
   std::vector<char> h_tab;
   char* h_pinned = nullptr;
-  char* d_tab = nullptr;
   size_t tab_bytes = 0;
-  bool tab_valid = false;
-  const double* cA = nullptr;
-  const double* cB = nullptr;
-  double* cC = nullptr;
-  long long clda = -1, cldb = -1, cldc = -1;
+  struct Slot {
+    char* d_tab = nullptr;
+    bool valid = false;
+    const double* A = nullptr;
+    const double* B = nullptr;
+    double* C = nullptr;
+    long long lda = -1, ldb = -1, ldc = -1;
+    std::vector<Launch> launches;
+    unsigned long long used = 0;
+  } slot[2];
+  unsigned long long use_clock = 0;
   cudaEvent_t upload_done = nullptr;
   cudaEvent_t ev[8] = {};
 
-  // host-execute staging
-  double *sA = nullptr, *sB = nullptr, *sC = nullptr;
+  // host-execute staging: two buffer sets, copy-in / copy-out streams, ordering events
+  double *sA[2] = {nullptr, nullptr}, *sB[2] = {nullptr, nullptr}, *sC[2] = {nullptr, nullptr};
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_in[2] = {}, ev_comp[2] = {}, ev_out[2] = {};
+  unsigned long long host_iter = 0;
 
   ~fmm_plan_s() {
     int cur = 0;
@@ -121,11 +134,18 @@ struct fmm_plan_s {
     if (upload_done) cudaEventSynchronize(upload_done);
     cudaDeviceSynchronize();
     if (ws) cudaFree(ws);
-    if (d_tab) cudaFree(d_tab);
+    for (auto& sl : slot)
+      if (sl.d_tab) cudaFree(sl.d_tab);
     if (h_pinned) cudaFreeHost(h_pinned);
-    if (sA) cudaFree(sA);
-    if (sB) cudaFree(sB);
-    if (sC) cudaFree(sC);
+    for (int b = 0; b < 2; ++b) {
+      if (sA[b]) cudaFree(sA[b]);
+      if (sB[b]) cudaFree(sB[b]);
+      if (sC[b]) cudaFree(sC[b]);
+      for (cudaEvent_t e : {ev_in[b], ev_comp[b], ev_out[b]})
+        if (e) cudaEventDestroy(e);
+    }
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
     if (upload_done) cudaEventDestroy(upload_done);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -301,8 +321,12 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
     if (p) std::memcpy(h_tab.data() + off, p, n);
     return off;
   };
-  auto push_maps = [&](Launch& ln, const std::vector<GemmTask>& tasks) {
+  auto choose_tiles = [&](Launch& ln, std::vector<GemmTask>& tasks) {
     ln.tma = !lazy_kernels && use_tma && gemm_tma_eligible(tasks);
+    ln.bn = ln.tma ? gemm_choose_bn(tasks) : 128;
+    ln.tiles = gemm_prepare(tasks, 128, ln.bn);
+  };
+  auto push_maps = [&](Launch& ln, const std::vector<GemmTask>& tasks) {
     if (lazy_kernels) {  // dry build: reserve the space the maps would need
       ln.maps_off = push(nullptr, 2 * gemm_tma_map_bytes() * tasks.size());
       return;
@@ -310,6 +334,49 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
     std::vector<char> maps(2 * gemm_tma_map_bytes() * tasks.size());
     if (ln.tma) gemm_tma_maps(tasks, maps.data());
     ln.maps_off = push(maps.data(), maps.size());
+  };
+  // one grouped DMMA launch for the regular tasks, one CUDA-core launch for thin ones
+  auto emit_gemm = [&](Launch::Kind kind, int level, std::vector<GemmTask>& all) {
+    std::vector<GemmTask> reg, thin;
+    for (const auto& t : all) {
+      if (t.m <= 0 || t.n <= 0) continue;
+      (std::min(t.m, t.n) <= skinny_limit() ? thin : reg).push_back(t);
+    }
+    if (!reg.empty()) {
+      Launch ln;
+      ln.kind = kind;
+      ln.level = level;
+      choose_tiles(ln, reg);
+      ln.count = (int)reg.size();
+      ln.aligned16 = gemm_tasks_aligned16(reg);
+      for (auto& t : reg) {
+        ln.flops += 2.0 * t.m * t.n * (double)t.k;
+        ln.gemm_bytes += 8.0 * ((double)t.m * t.k + (double)t.k * t.n + (1.0 + (t.beta != 0.0)) * t.m * t.n);
+      }
+      ln.table_off = push(reg.data(), reg.size() * sizeof(GemmTask));
+      push_maps(ln, reg);
+      launches.push_back(ln);
+    }
+    if (!thin.empty()) {
+      Launch ln;
+      ln.kind = Launch::SKINNY;
+      ln.level = level;
+      ln.count = (int)thin.size();
+      std::vector<int> rows, cols;
+      for (int q = 0; q < (int)thin.size(); ++q) {
+        const auto& t = thin[q];
+        if (t.m <= skinny_limit()) rows.push_back(q), ln.max_n = std::max(ln.max_n, t.n);
+        else cols.push_back(q), ln.max_m = std::max(ln.max_m, t.m);
+        ln.flops += 2.0 * t.m * t.n * (double)t.k;
+        ln.gemm_bytes += 8.0 * ((double)t.m * t.k + (double)t.k * t.n + (1.0 + (t.beta != 0.0)) * t.m * t.n);
+      }
+      ln.nrow = (int)rows.size();
+      ln.ncol = (int)cols.size();
+      rows.insert(rows.end(), cols.begin(), cols.end());
+      ln.table_off = push(thin.data(), thin.size() * sizeof(GemmTask));
+      ln.ids_off = push(rows.data(), rows.size() * sizeof(int));
+      launches.push_back(ln);
+    }
   };
   auto outView = [&](int l, long long z) -> View {
     if (l == 0) return rootC;
@@ -406,21 +473,7 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
       t.beta = 0.0;
       if (t.m > 0 && t.n > 0) tasks.push_back(t);
     }
-    if (!tasks.empty()) {
-      Launch ln;
-      ln.kind = Launch::GEMM;
-      ln.level = L;
-      ln.tiles = gemm_prepare(tasks);
-      ln.count = (int)tasks.size();
-      ln.aligned16 = gemm_tasks_aligned16(tasks);
-      for (auto& t : tasks) {
-        ln.flops += 2.0 * t.m * t.n * (double)t.k;
-        ln.gemm_bytes += 8.0 * ((double)t.m * t.k + (double)t.k * t.n + (double)t.m * t.n);
-      }
-      ln.table_off = push(tasks.data(), tasks.size() * sizeof(GemmTask));
-      push_maps(ln, tasks);
-      launches.push_back(ln);
-    }
+    emit_gemm(Launch::GEMM, L, tasks);
   }
 
   // ---- assembly and peel strips, levels L..1 ----
@@ -476,6 +529,30 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
     // (b) C[P':P,:] = A[P':P,:] B, (c) C[0:P',N':N] = A[0:P',:] B[:,N':N]
     std::vector<GemmTask> tasks;
     for (long long zp = 0; zp < nodes_at[l - 1]; ++zp) {
+      if (l - 1 == 0 && !strip_owner[0][0] && opt.shard_count > 1) {
+        // a shard that does not own the root's strips still writes its partial C there: zeros
+        // (k = 0 tasks); deeper strip regions live in the zero-initialised workspace
+        const View c = outView(0, 0);
+        auto zero = [&](double* pc, long long m, long long n) {
+          if (m <= 0 || n <= 0) return;
+          GemmTask t{};
+          t.A = rootA.ptr;
+          t.B = rootB.ptr;
+          t.C = pc;
+          t.lda = rootA.ld;
+          t.ldb = rootB.ld;
+          t.ldc = c.ld;
+          t.m = (int)m;
+          t.n = (int)n;
+          t.k = 0;
+          t.alpha = 1.0;
+          t.beta = 0.0;
+          tasks.push_back(t);
+        };
+        if (dp.P1 < dp.P) zero(c.ptr + dp.P1 * c.ld, dp.P - dp.P1, dp.N);
+        if (dp.N1 < dp.N) zero(c.ptr + dp.N1, dp.P1, dp.N - dp.N1);
+        continue;
+      }
       if (!strip_owner[l - 1][zp]) continue;
       const View a = opA(l - 1, zp, rootA), b = opB(l - 1, zp, rootB), c = outView(l - 1, zp);
       const double alpha = a.sigma * b.sigma;
@@ -499,21 +576,7 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
       if (dp.P1 < dp.P) add(a.ptr + dp.P1 * a.ld, b.ptr, c.ptr + dp.P1 * c.ld, dp.P - dp.P1, dp.N, dp.Q, 0.0);
       if (dp.N1 < dp.N) add(a.ptr, b.ptr + dp.N1, c.ptr + dp.N1, dp.P1, dp.N - dp.N1, dp.Q, 0.0);
     }
-    if (!tasks.empty()) {
-      Launch ln;
-      ln.kind = Launch::STRIPS;
-      ln.level = l - 1;
-      ln.tiles = gemm_prepare(tasks);
-      ln.count = (int)tasks.size();
-      ln.aligned16 = gemm_tasks_aligned16(tasks);
-      for (auto& t : tasks) {
-        ln.flops += 2.0 * t.m * t.n * (double)t.k;
-        ln.gemm_bytes += 8.0 * ((double)t.m * t.k + (double)t.k * t.n + (1.0 + (t.beta != 0.0)) * t.m * t.n);
-      }
-      ln.table_off = push(tasks.data(), tasks.size() * sizeof(GemmTask));
-      push_maps(ln, tasks);
-      launches.push_back(ln);
-    }
+    emit_gemm(Launch::STRIPS, l - 1, tasks);
   }
 }
 
@@ -562,6 +625,8 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
     d.P1 = M * (d.P / M);
     d.Q1 = K * (d.Q / K);
     d.N1 = Nb * (d.N / Nb);
+    // R7b: keep column-block widths even so sub-block views stay 16-byte aligned (TMA)
+    if (p->opt.peel_align && L < levels && (d.N1 / Nb) % 2 == 1 && d.N / (2 * Nb) >= 1) d.N1 = 2 * Nb * (d.N / (2 * Nb));
     p->dims.push_back(d);
     if (L == levels || d.P < M || d.Q < K || d.N < Nb) break;
     d = Dims{d.P1 / M, d.Q1 / K, d.N1 / Nb, 0, 0, 0};
@@ -607,11 +672,10 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
   p->build(reinterpret_cast<const double*>(0x100000), std::max<long long>(p->Q, 1), reinterpret_cast<const double*>(0x200000),
            std::max<long long>(p->N, 1), reinterpret_cast<double*>(0x300000), std::max<long long>(p->N, 1), true);
   p->tab_bytes = std::max<size_t>(p->h_tab.size(), 256);
-  FMM_CUDA(cudaMalloc(&p->d_tab, p->tab_bytes));
+  for (auto& sl : p->slot) FMM_CUDA(cudaMalloc(&sl.d_tab, p->tab_bytes));
   FMM_CUDA(cudaMallocHost(&p->h_pinned, p->tab_bytes));
   FMM_CUDA(cudaEventCreateWithFlags(&p->upload_done, cudaEventDisableTiming));
   for (auto& e : p->ev) FMM_CUDA(cudaEventCreate(&e));
-  p->tab_valid = false;
 }
 
 void check_ld(const fmm_plan_t* p, long long lda, long long ldb, long long ldc) {
@@ -638,40 +702,63 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
   const double* a = p->colmajor ? B : A;
   const double* b = p->colmajor ? A : B;
   const long long la = p->colmajor ? ldb : lda, lb = p->colmajor ? lda : ldb;
-  if (!p->tab_valid || a != p->cA || b != p->cB || C != p->cC || la != p->clda || lb != p->cldb || ldc != p->cldc) {
+  fmm_plan_s::Slot* sl = nullptr;
+  for (auto& c : p->slot)
+    if (c.valid && c.A == a && c.B == b && c.C == C && c.lda == la && c.ldb == lb && c.ldc == ldc) sl = &c;
+  if (!sl) {
+    sl = p->slot[0].used <= p->slot[1].used ? &p->slot[0] : &p->slot[1];
     p->build(a, la, b, lb, C, ldc, false);
     if (p->h_tab.size() > p->tab_bytes) throw Error(FMM_E_INVALID_ARG, "internal: table size grew");
     FMM_CUDA(cudaEventSynchronize(p->upload_done));  // the previous upload has consumed h_pinned
     std::memcpy(p->h_pinned, p->h_tab.data(), p->h_tab.size());
-    FMM_CUDA(cudaMemcpyAsync(p->d_tab, p->h_pinned, p->h_tab.size(), cudaMemcpyHostToDevice, stream));
+    // stream-ordered: kernels of earlier executes on this stream that read the slot finish first
+    FMM_CUDA(cudaMemcpyAsync(sl->d_tab, p->h_pinned, p->h_tab.size(), cudaMemcpyHostToDevice, stream));
     FMM_CUDA(cudaEventRecord(p->upload_done, stream));
-    p->cA = a;
-    p->cB = b;
-    p->cC = C;
-    p->clda = la;
-    p->cldb = lb;
-    p->cldc = ldc;
-    p->tab_valid = true;
+    sl->valid = true;
+    sl->A = a;
+    sl->B = b;
+    sl->C = C;
+    sl->lda = la;
+    sl->ldb = lb;
+    sl->ldc = ldc;
+    sl->launches = p->launches;
   }
+  sl->used = ++p->use_clock;
+  char* d_tab = sl->d_tab;
   if (timed) FMM_CUDA(cudaEventRecord(evs[0], stream));
   int phase = 0;  // 0 formation, 1 gemm, 2 assembly/strips
-  for (const Launch& ln : p->launches) {
-    const int ph = (ln.kind == Launch::FORM_A || ln.kind == Launch::FORM_B) ? 0 : ln.kind == Launch::GEMM ? 1 : 2;
+  for (const Launch& ln : sl->launches) {
+    const int ph = (ln.kind == Launch::FORM_A || ln.kind == Launch::FORM_B)                      ? 0
+                   : (ln.kind == Launch::GEMM || (ln.kind == Launch::SKINNY && ln.level == p->L)) ? 1
+                                                                                                   : 2;
+    if (ln.kind == Launch::SKINNY) {
+      const int* ids = reinterpret_cast<const int*>(d_tab + ln.ids_off);
+      if (timed && ph != phase) {
+        for (int q = phase + 1; q <= ph; ++q) FMM_CUDA(cudaEventRecord(evs[q], stream));
+        phase = ph;
+      }
+      skinny_launch(reinterpret_cast<const GemmTask*>(d_tab + ln.table_off), ids, ln.nrow, ln.max_n, ids + ln.nrow,
+                    ln.ncol, ln.max_m, stream);
+      continue;
+    }
     if (timed && ph != phase) {
       for (int q = phase + 1; q <= ph; ++q) FMM_CUDA(cudaEventRecord(evs[q], stream));
       phase = ph;
     }
-    const void* tab = p->d_tab + ln.table_off;
+    const void* tab = d_tab + ln.table_off;
     switch (ln.kind) {
       case Launch::FORM_A:
       case Launch::FORM_B:
       case Launch::ASSEMBLE:
         lincomb_launch(*ln.kern, tab, ln.count, ln.rows, ln.cols, stream);
         break;
+      case Launch::SKINNY:
+        break;
       case Launch::GEMM:
       case Launch::STRIPS:
         if (ln.tma)
-          gemm_tma_launch(reinterpret_cast<const GemmTask*>(tab), p->d_tab + ln.maps_off, ln.count, ln.tiles, stream);
+          gemm_tma_launch(reinterpret_cast<const GemmTask*>(tab), d_tab + ln.maps_off, ln.count, ln.tiles, ln.bn,
+                          stream);
         else
           gemm_launch(reinterpret_cast<const GemmTask*>(tab), ln.count, ln.tiles, ln.aligned16, stream);
         break;
@@ -695,6 +782,7 @@ void fmm_plan_options_default(fmm_plan_options* o) {
   o->shard_rank = 0;
   o->shard_count = 1;
   o->workspace_limit_bytes = 0;
+  o->peel_align = 1;
 }
 
 fmm_status_t fmm_plan_create(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels,
@@ -733,7 +821,8 @@ fmm_status_t fmm_plan_stats(const fmm_plan_t* p, double out[8]) {
     s[2] += 8.0 * (ln.elem_reads + ln.elem_writes);
     s[3] += ln.gemm_bytes;
     s[4] += 1;
-    if (ln.kind == Launch::GEMM) s[6] += ln.count;
+    if (ln.kind == Launch::GEMM || (ln.kind == Launch::SKINNY && ln.level == p->L)) s[6] += ln.count;
+    if (ln.kind == Launch::SKINNY) s[4] += (ln.nrow > 0) + (ln.ncol > 0) - 1;
   }
   s[5] = p->L;
   s[7] = 2.0 * p->userP * p->userQ * (double)p->userN - (double)p->userP * p->userN;
@@ -790,28 +879,68 @@ fmm_status_t fmm_execute_events(fmm_plan_t* p, const double* A, int64_t lda, con
   FMM_API_END
 }
 
-fmm_status_t fmm_execute_host(fmm_plan_t* p, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
-                              int64_t ldc, void* stream) {
-  FMM_API_BEGIN
-  if (!p || !A || !B || !C) throw Error(FMM_E_INVALID_ARG, "null argument");
+// Host-buffer execution, pipelined: iteration i uses staging set b = i % 2.  The copy-in stream
+// waits until compute i-2 has finished reading set b; compute (on `stream`) waits for copy-in i
+// and for copy-out i-2 (which reads sC[b]); copy-out i waits for compute i.  Consecutive calls
+// therefore overlap H2D of the next problem, compute, and D2H of the previous one (PCIe is full
+// duplex).  Host buffers must stay valid (and, for overlap, be pinned) until fmm_sync.
+static void host_async(fmm_plan_t* p, const double* A, long long lda, const double* B, long long ldb, double* C,
+                       long long ldc, cudaStream_t s) {
+  if (!A || !B || !C) throw Error(FMM_E_INVALID_ARG, "null argument");
   check_ld(p, lda, ldb, ldc);
   FMM_CUDA(cudaSetDevice(p->device));
-  cudaStream_t s = (cudaStream_t)stream;
-  // device staging with tight leading dimensions, in the caller's layout
   const long long P = p->userP, Q = p->userQ, N = p->userN;
   const bool cm = p->colmajor;
   // (rows, cols) of the storage: row-major P x Q is P rows of Q; column-major is Q "rows" of P
   const long long aR = cm ? Q : P, aC = cm ? P : Q, bR = cm ? N : Q, bC = cm ? Q : N, cR = cm ? N : P, cC = cm ? P : N;
-  if (!p->sA) {
-    FMM_CUDA(cudaMalloc(&p->sA, std::max<size_t>(8, (size_t)aR * aC * 8)));
-    FMM_CUDA(cudaMalloc(&p->sB, std::max<size_t>(8, (size_t)bR * bC * 8)));
-    FMM_CUDA(cudaMalloc(&p->sC, std::max<size_t>(8, (size_t)cR * cC * 8)));
+  if (!p->s_in) {
+    FMM_CUDA(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
+    FMM_CUDA(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      FMM_CUDA(cudaEventCreateWithFlags(&p->ev_in[b], cudaEventDisableTiming));
+      FMM_CUDA(cudaEventCreateWithFlags(&p->ev_comp[b], cudaEventDisableTiming));
+      FMM_CUDA(cudaEventCreateWithFlags(&p->ev_out[b], cudaEventDisableTiming));
+    }
   }
-  if (aR && aC) FMM_CUDA(cudaMemcpy2DAsync(p->sA, aC * 8, A, lda * 8, aC * 8, aR, cudaMemcpyHostToDevice, s));
-  if (bR && bC) FMM_CUDA(cudaMemcpy2DAsync(p->sB, bC * 8, B, ldb * 8, bC * 8, bR, cudaMemcpyHostToDevice, s));
-  run(p, p->sA, std::max<long long>(aC, 1), p->sB, std::max<long long>(bC, 1), p->sC, std::max<long long>(cC, 1), s, nullptr);
-  if (cR && cC) FMM_CUDA(cudaMemcpy2DAsync(C, ldc * 8, p->sC, cC * 8, cC * 8, cR, cudaMemcpyDeviceToHost, s));
-  FMM_CUDA(cudaStreamSynchronize(s));
+  const int b = (int)(p->host_iter++ & 1);
+  if (!p->sA[b]) {
+    FMM_CUDA(cudaMalloc(&p->sA[b], std::max<size_t>(8, (size_t)aR * aC * 8)));
+    FMM_CUDA(cudaMalloc(&p->sB[b], std::max<size_t>(8, (size_t)bR * bC * 8)));
+    FMM_CUDA(cudaMalloc(&p->sC[b], std::max<size_t>(8, (size_t)cR * cC * 8)));
+  }
+  // copy in, once compute i-2 has released set b
+  FMM_CUDA(cudaStreamWaitEvent(p->s_in, p->ev_comp[b], 0));
+  if (aR && aC) FMM_CUDA(cudaMemcpy2DAsync(p->sA[b], aC * 8, A, lda * 8, aC * 8, aR, cudaMemcpyHostToDevice, p->s_in));
+  if (bR && bC) FMM_CUDA(cudaMemcpy2DAsync(p->sB[b], bC * 8, B, ldb * 8, bC * 8, bR, cudaMemcpyHostToDevice, p->s_in));
+  FMM_CUDA(cudaEventRecord(p->ev_in[b], p->s_in));
+  // compute
+  FMM_CUDA(cudaStreamWaitEvent(s, p->ev_in[b], 0));
+  FMM_CUDA(cudaStreamWaitEvent(s, p->ev_out[b], 0));
+  run(p, p->sA[b], std::max<long long>(aC, 1), p->sB[b], std::max<long long>(bC, 1), p->sC[b], std::max<long long>(cC, 1),
+      s, nullptr);
+  FMM_CUDA(cudaEventRecord(p->ev_comp[b], s));
+  // copy out
+  FMM_CUDA(cudaStreamWaitEvent(p->s_out, p->ev_comp[b], 0));
+  if (cR && cC) FMM_CUDA(cudaMemcpy2DAsync(C, ldc * 8, p->sC[b], cC * 8, cC * 8, cR, cudaMemcpyDeviceToHost, p->s_out));
+  FMM_CUDA(cudaEventRecord(p->ev_out[b], p->s_out));
+}
+
+fmm_status_t fmm_execute_host_async(fmm_plan_t* p, const double* A, int64_t lda, const double* B, int64_t ldb,
+                                    double* C, int64_t ldc, void* stream) {
+  FMM_API_BEGIN
+  if (!p) throw Error(FMM_E_INVALID_ARG, "null plan");
+  host_async(p, A, lda, B, ldb, C, ldc, (cudaStream_t)stream);
+  return FMM_OK;
+  FMM_API_END
+}
+
+fmm_status_t fmm_execute_host(fmm_plan_t* p, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                              int64_t ldc, void* stream) {
+  FMM_API_BEGIN
+  if (!p) throw Error(FMM_E_INVALID_ARG, "null plan");
+  host_async(p, A, lda, B, ldb, C, ldc, (cudaStream_t)stream);
+  FMM_CUDA(cudaStreamSynchronize(p->s_out));
+  FMM_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
   return FMM_OK;
   FMM_API_END
 }
@@ -856,16 +985,17 @@ fmm_status_t fmm_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const doub
   t[0].k = (int)k;
   t[0].alpha = alpha;
   t[0].beta = beta;
-  const long long tiles = gemm_prepare(t);
   cudaStream_t s = (cudaStream_t)stream;
   // the task descriptor (and its tensor maps) go through a stream-ordered upload
   const bool tma = gemm_tma_eligible(t) && !(getenv("FMM_NO_TMA") && getenv("FMM_NO_TMA")[0] == '1');
+  const int bn = tma ? gemm_choose_bn(t) : 128;
+  const long long tiles = gemm_prepare(t, 128, bn);
   alignas(128) char buf[1024];
   std::memcpy(buf, t.data(), sizeof(GemmTask));
   if (tma) gemm_tma_maps(t, buf + 512);
   FMM_CUDA(cudaMemcpyAsync(d_task, buf, sizeof(buf), cudaMemcpyHostToDevice, s));
   if (tma)
-    gemm_tma_launch(d_task, reinterpret_cast<char*>(d_task) + 512, 1, tiles, s);
+    gemm_tma_launch(d_task, reinterpret_cast<char*>(d_task) + 512, 1, tiles, bn, s);
   else
     gemm_launch(d_task, 1, tiles, gemm_tasks_aligned16(t), s);
   return FMM_OK;

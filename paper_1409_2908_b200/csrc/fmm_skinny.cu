@@ -1,0 +1,150 @@
+// K4: thin peel strips (SPEC S:290 (b) last P-P' rows, (c) last N-N' columns).
+//
+// A strip is a classical product with one tiny dimension (1 to 2N-1 rows or columns).  On the
+// 128-row DMMA tile it would waste up to 99 % of the tensor work, so thin tasks of a strip launch
+// run here instead, on the FP64 CUDA cores, HBM/L2-bound:
+//   row strips (m <= 8): a block covers 32 output columns x 8 k-slices; each thread keeps all
+//       m rows of its column in registers over its k-slice (B read once, coalesced; A[i][k] a
+//       warp-uniform broadcast), and the slices are reduced through shared memory.
+//   column strips (n <= 8): two output rows per warp; lanes split k (A rows read coalesced,
+//       4 loads in flight), the B strip is staged transposed in shared memory per k-chunk, each
+//       lane accumulates all n outputs, then a warp shuffle reduction.
+// C = alpha * A B + beta * C, same task table as the GEMM kernels.
+#include <cuda_runtime.h>
+
+#include "fmm_internal.h"
+
+namespace fmm {
+
+namespace {
+constexpr int THIN = 8;  // strips are < 2 x (base-case dim) wide
+
+// 32 columns x 8 k-slices per block: each thread sums k = ks, ks+8, ... for its column and all
+// m rows (independent loads in flight across slices), then the slices are reduced in smem.
+__global__ void __launch_bounds__(256) skinny_rows(const GemmTask* __restrict__ tasks, const int* __restrict__ ids,
+                                                   int count) {
+  __shared__ double red[8][THIN][33];
+  const GemmTask t = tasks[ids[blockIdx.y]];
+  const int tx = threadIdx.x & 31, ks = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + tx;
+  double acc[THIN];
+#pragma unroll
+  for (int i = 0; i < THIN; ++i) acc[i] = 0.0;
+  if (j < t.n) {
+    int k = ks;
+    for (; k + 24 < t.k; k += 32) {  // 4 independent B loads in flight per thread
+      double b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) b[u] = __ldg(t.B + (long long)(k + 8 * u) * t.ldb + j);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int i = 0; i < THIN; ++i)
+          if (i < t.m) acc[i] = fma(__ldg(t.A + (long long)i * t.lda + k + 8 * u), b[u], acc[i]);
+    }
+    for (; k < t.k; k += 8) {
+      const double b = __ldg(t.B + (long long)k * t.ldb + j);
+#pragma unroll
+      for (int i = 0; i < THIN; ++i)
+        if (i < t.m) acc[i] = fma(__ldg(t.A + (long long)i * t.lda + k), b, acc[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < THIN; ++i) red[ks][i][tx] = acc[i];
+  __syncthreads();
+  // thread (ks, tx) finalises row i = ks of column j
+  if (j < t.n) {
+#pragma unroll
+    for (int h = 0; h < 1; ++h) {
+      const int i = ks + 8 * h;
+      if (i < t.m) {
+        double v = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v += red[q][i][tx];
+        double* c = t.C + (long long)i * t.ldc + j;
+        *c = t.beta != 0.0 ? fma(t.beta, *c, t.alpha * v) : t.alpha * v;
+      }
+    }
+  }
+}
+
+// Column strips: 16 rows per block (2 per warp); the B strip (k x n, n <= 8) is staged
+// transposed through shared memory in k-chunks, so lane reads of B are conflict-free and A rows
+// are read coalesced with 4 loads in flight per lane.
+constexpr int KC = 256, ROWS_PER_WARP = 2;
+__global__ void __launch_bounds__(256) skinny_cols(const GemmTask* __restrict__ tasks, const int* __restrict__ ids,
+                                                   int count) {
+  __shared__ double bt[THIN][KC];
+  const GemmTask t = tasks[ids[blockIdx.y]];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row0 = (blockIdx.x * 8 + warp) * ROWS_PER_WARP;
+  double acc[ROWS_PER_WARP][THIN];
+#pragma unroll
+  for (int q = 0; q < ROWS_PER_WARP; ++q)
+#pragma unroll
+    for (int j = 0; j < THIN; ++j) acc[q][j] = 0.0;
+  for (int k0 = 0; k0 < t.k; k0 += KC) {
+    const int kc = min(KC, t.k - k0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kc * t.n; e += blockDim.x) {
+      const int kk = e / t.n, j = e % t.n;
+      bt[j][kk] = __ldg(t.B + (long long)(k0 + kk) * t.ldb + j);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < ROWS_PER_WARP; ++q) {
+      const int i = row0 + q;
+      if (i >= t.m) continue;
+      const double* arow = t.A + (long long)i * t.lda + k0;
+      for (int kk = lane; kk < kc; kk += 128) {
+        double a[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[u] = kk + 32 * u < kc ? __ldg(arow + kk + 32 * u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (kk + 32 * u < kc)
+#pragma unroll
+            for (int j = 0; j < THIN; ++j)
+              if (j < t.n) acc[q][j] = fma(a[u], bt[j][kk + 32 * u], acc[q][j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < ROWS_PER_WARP; ++q) {
+    const int i = row0 + q;
+#pragma unroll
+    for (int j = 0; j < THIN; ++j) {
+      double v = acc[q][j];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      acc[q][j] = v;
+    }
+    if (i < t.m && lane < t.n) {
+      double v = 0.0;
+#pragma unroll
+      for (int j = 0; j < THIN; ++j)
+        if (j == lane) v = acc[q][j];
+      double* c = t.C + (long long)i * t.ldc + lane;
+      *c = t.beta != 0.0 ? fma(t.beta, *c, t.alpha * v) : t.alpha * v;
+    }
+  }
+}
+}  // namespace
+
+int skinny_limit() { return THIN; }
+
+void skinny_launch(const GemmTask* d_tasks, const int* d_row_ids, int nrow, int max_n, const int* d_col_ids, int ncol,
+                   int max_m, cudaStream_t stream) {
+  if (nrow > 0 && max_n > 0) {
+    dim3 grid((unsigned)((max_n + 31) / 32), (unsigned)nrow);
+    skinny_rows<<<grid, 256, 0, stream>>>(d_tasks, d_row_ids, nrow);
+    FMM_CUDA(cudaGetLastError());
+  }
+  if (ncol > 0 && max_m > 0) {
+    dim3 grid((unsigned)((max_m + 8 * ROWS_PER_WARP - 1) / (8 * ROWS_PER_WARP)), (unsigned)ncol);
+    skinny_cols<<<grid, 256, 0, stream>>>(d_tasks, d_col_ids, ncol);
+    FMM_CUDA(cudaGetLastError());
+  }
+}
+
+}  // namespace fmm

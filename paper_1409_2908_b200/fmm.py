@@ -29,7 +29,7 @@ class FmmError(RuntimeError):
 class _Options(ctypes.Structure):
     _fields_ = [("layout", ctypes.c_int), ("strategy", ctypes.c_int), ("cse", ctypes.c_int),
                 ("shard_rank", ctypes.c_int), ("shard_count", ctypes.c_int),
-                ("workspace_limit_bytes", ctypes.c_size_t)]
+                ("workspace_limit_bytes", ctypes.c_size_t), ("peel_align", ctypes.c_int)]
 
 
 def _load():
@@ -52,6 +52,7 @@ def _load():
         "fmm_execute_timed": [vp, vp, i64, vp, i64, vp, i64, vp, ctypes.POINTER(ctypes.c_float)],
         "fmm_execute_host": [vp, vp, i64, vp, i64, vp, i64, vp],
         "fmm_execute_events": [vp, vp, i64, vp, i64, vp, i64, vp, ctypes.POINTER(vp)],
+        "fmm_execute_host_async": [vp, vp, i64, vp, i64, vp, i64, vp],
         "fmm_probe_fp64_peak": [ctypes.POINTER(dp), ctypes.POINTER(dp)],
         "fmm_sync": [vp],
         "fmm_hybrid_split": [i64, i32, i64, p64, p64],
@@ -159,7 +160,7 @@ class Plan:
 
     def __init__(self, alg: Algorithm, P: int, Q: int, N: int, levels: int, layout: str = "row",
                  strategy: str = "streaming", cse: bool = True, shard_rank: int = 0, shard_count: int = 1,
-                 device: Optional[int] = None, workspace_limit_bytes: int = 0):
+                 device: Optional[int] = None, workspace_limit_bytes: int = 0, peel_align: bool = True):
         import torch
         self.alg, self.P, self.Q, self.N, self.levels = alg, P, Q, N, levels
         self.layout = ROW_MAJOR if layout == "row" else COL_MAJOR
@@ -170,6 +171,7 @@ class Plan:
         o.cse = int(bool(cse))
         o.shard_rank, o.shard_count = shard_rank, shard_count
         o.workspace_limit_bytes = workspace_limit_bytes
+        o.peel_align = int(bool(peel_align))
         self.device = torch.cuda.current_device() if device is None else device
         h = ctypes.c_void_p()
         _check(_lib.fmm_plan_create(alg._h, P, Q, N, levels, ctypes.byref(o), self.device, ctypes.byref(h)))
@@ -226,8 +228,10 @@ class Plan:
         _check(_lib.fmm_execute_events(self._h, *self._args(A, B, C), _stream_ptr(stream), ev))
         return C
 
-    def execute_host(self, A, B, C, stream=None):
-        """Host (CPU) tensors / arrays in, host result out: H2D, execute, D2H (blocking)."""
+    def execute_host(self, A, B, C, stream=None, asynchronous=False):
+        """Host (CPU) tensors / arrays in, host result out: H2D, execute, D2H.  Blocking unless
+        asynchronous=True (fmm_execute_host_async: pipelined with neighbouring calls; the host
+        buffers must be pinned and stay untouched until sync())."""
         import numpy as np
         import torch
 
@@ -249,7 +253,8 @@ class Plan:
         a, lda = hp(A, self.P, self.Q, "A")
         b, ldb = hp(B, self.Q, self.N, "B")
         c, ldc = hp(C, self.P, self.N, "C", True)
-        _check(_lib.fmm_execute_host(self._h, a, lda, b, ldb, c, ldc, _stream_ptr(stream)))
+        fn = _lib.fmm_execute_host_async if asynchronous else _lib.fmm_execute_host
+        _check(fn(self._h, a, lda, b, ldb, c, ldc, _stream_ptr(stream)))
         return C
 
     def sync(self):

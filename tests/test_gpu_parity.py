@@ -227,3 +227,46 @@ def test_cp_async_gemm_path_matches_tma_path(monkeypatch):
     C_cp, _ = run("alg_424_26", A, B, 2)
     for C in (C_tma, C_cp):
         assert np.max(np.abs(C - ref)) <= bound(A, B, 1e-12)
+
+
+@pytest.mark.parametrize("peel_align", [False, True])
+def test_peel_modes_and_thin_strips(peel_align):
+    # c3's shape family at small scale: odd level-2 column blocks (paper peeling) vs aligned peeling;
+    # both give oracle parity, and integer inputs stay bit-exact (thin strips run on CUDA cores)
+    for name, L, P, Q, N in [("hk_class_323_15", 2, 400, 60, 400), ("strassen_222_7", 2, 203, 101, 207)]:
+        A, B = I.problem(P, Q, N, seed=12)
+        C, _ = run(name, A, B, L, peel_align=peel_align)
+        assert np.max(np.abs(C - O.fast(A, B, oalg(name), L))) <= bound(A, B, 1e-12)
+        Ai, Bi = I.problem(P, Q, N, seed=13, kind="integers")
+        Ci, _ = run(name, Ai, Bi, L, peel_align=peel_align)
+        assert np.array_equal(Ci, Ai @ Bi)
+
+
+@pytest.mark.parametrize("bn", ["128", "112", "96", "80", "64"])
+def test_every_tma_tile_width(bn, monkeypatch):
+    monkeypatch.setenv("FMM_GEMM_BN", bn)
+    A, B = I.problem(300, 200, 333, seed=14)
+    ref = O.classical(A, B)
+    C = F.dgemm(dev(A), dev(B)).cpu().numpy()
+    assert np.max(np.abs(C - ref)) <= bound(A, B, 1e-13)
+    Ai, Bi = I.problem(260, 72, 410, seed=15, kind="integers")
+    C, _ = run("alg_433_29", Ai, Bi, 1)
+    assert np.array_equal(C, Ai @ Bi)
+
+
+def test_execute_host_async_pipeline():
+    # three back-to-back pipelined host calls with different inputs and outputs
+    import torch as T
+    name, L, P, Q, N = "winograd_class_222_7", 2, 256, 192, 320
+    p = F.Plan(falg(name), P, Q, N, L)
+    outs, refs = [], []
+    for s in range(3):
+        A, B = I.problem(P, Q, N, seed=20 + s)
+        Ah, Bh = T.from_numpy(A).pin_memory(), T.from_numpy(B).pin_memory()
+        Ch = T.zeros(P, N, dtype=T.float64).pin_memory()
+        p.execute_host(Ah, Bh, Ch, asynchronous=True)
+        outs.append((Ah, Bh, Ch))
+        refs.append(O.fast(A, B, oalg(name), L))
+    p.sync()
+    for (Ah, Bh, Ch), ref in zip(outs, refs):
+        assert np.max(np.abs(Ch.numpy() - ref)) <= bound(Ah.numpy(), Bh.numpy(), 1e-12)
