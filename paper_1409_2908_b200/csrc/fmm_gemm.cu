@@ -201,6 +201,15 @@ long long gemm_prepare(std::vector<GemmTask>& tasks, int bm, int bn) {
   return total;
 }
 
+void gemm_uniform_grid(const std::vector<GemmTask>& tasks, int* tm, int* tn) {
+  *tm = *tn = 0;
+  if (tasks.empty()) return;
+  for (const auto& t : tasks)
+    if (t.tiles_m != tasks[0].tiles_m || t.tiles_n != tasks[0].tiles_n) return;
+  *tm = tasks[0].tiles_m;
+  *tn = tasks[0].tiles_n;
+}
+
 bool gemm_tasks_aligned16(const std::vector<GemmTask>& tasks) {
   for (const auto& t : tasks) {
     if ((reinterpret_cast<uintptr_t>(t.A) & 15) || (reinterpret_cast<uintptr_t>(t.B) & 15)) return false;

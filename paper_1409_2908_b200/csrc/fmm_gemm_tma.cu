@@ -83,15 +83,30 @@ __device__ __forceinline__ double lds64(unsigned addr) {
 struct TileCoord {
   int task, m0, n0;
 };
+// Uniform launches (every task has the same tile grid, e.g. all leaves of a level) map a tile to
+// its task by division; others binary-search the tile prefix sums in the task table.
+struct Uniform {
+  int tiles, tiles_m, tiles_n;  // tiles == 0: not uniform
+};
 template <int BN>
-__device__ __forceinline__ TileCoord locate(const GemmTask* __restrict__ tasks, int ntasks, int tile) {
-  int lo = 0, hi = ntasks - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(&tasks[mid].tile_begin) <= tile) lo = mid; else hi = mid - 1;
+__device__ __forceinline__ TileCoord locate(const GemmTask* __restrict__ tasks, int ntasks, int tile, Uniform u) {
+  int lo, tiles_m, tiles_n, local;
+  if (u.tiles) {
+    lo = tile / u.tiles;
+    local = tile - lo * u.tiles;
+    tiles_m = u.tiles_m;
+    tiles_n = u.tiles_n;
+  } else {
+    lo = 0;
+    int hi = ntasks - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (__ldg(&tasks[mid].tile_begin) <= tile) lo = mid; else hi = mid - 1;
+    }
+    tiles_m = __ldg(&tasks[lo].tiles_m);
+    tiles_n = __ldg(&tasks[lo].tiles_n);
+    local = tile - __ldg(&tasks[lo].tile_begin);
   }
-  const int tiles_m = __ldg(&tasks[lo].tiles_m), tiles_n = __ldg(&tasks[lo].tiles_n);
-  const int local = tile - __ldg(&tasks[lo].tile_begin);
   const int span = GROUP_M * tiles_n;
   const int group = local / span;
   const int first_m = group * GROUP_M;
@@ -106,7 +121,7 @@ __device__ __forceinline__ TileCoord locate(const GemmTask* __restrict__ tasks, 
 template <int BN, int WGM, int WGN>
 __global__ void __launch_bounds__(THREADS, 1)
     grouped_dgemm_tma(const GemmTask* __restrict__ tasks, const CUtensorMap* __restrict__ maps, int ntasks,
-                      int total_tiles) {
+                      int total_tiles, Uniform uni) {
   static_assert(WGM * WGN == CONSUMERS, "8 consumer warps");
   constexpr int WTM = BM / WGM, WTN = BN / WGN;
   static_assert(WTM % 16 == 0 && WTN % 16 == 0, "warp tile must be a multiple of 16");
@@ -137,7 +152,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       int stage = 0;
       unsigned phase = 0;
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-        const TileCoord tc = locate<BN>(tasks, ntasks, tile);
+        const TileCoord tc = locate<BN>(tasks, ntasks, tile, uni);
         const CUtensorMap* ma = maps + 2 * tc.task;
         const CUtensorMap* mb = ma + 1;
         const int KT = (__ldg(&tasks[tc.task].k) + BK - 1) / BK;
@@ -174,9 +189,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   int stage = 0;
   unsigned phase = 0;
   for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-    const TileCoord tc = locate<BN>(tasks, ntasks, tile);
+    const TileCoord tc = locate<BN>(tasks, ntasks, tile, uni);
     const GemmTask& t = tasks[tc.task];
     const int KT = (__ldg(&t.k) + BK - 1) / BK;
+    // epilogue parameters, fetched now so their latency hides behind the main loop
+    const double alpha = __ldg(&t.alpha), beta = __ldg(&t.beta);
+    const int m = __ldg(&t.m), n = __ldg(&t.n);
+    const long long ldc = __ldg(&t.ldc);
+    double* C = t.C;
     double acc[MI][NI][2];
 #pragma unroll
     for (int i = 0; i < MI; ++i)
@@ -212,10 +232,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 
     // ---- epilogue: C = alpha * acc (+ beta * C), from registers ----
-    const double alpha = __ldg(&t.alpha), beta = __ldg(&t.beta);
-    const int m = __ldg(&t.m), n = __ldg(&t.n);
-    const long long ldc = __ldg(&t.ldc);
-    double* C = t.C;
     const int cofs = (c == 0) ? 0 : (c == 1) ? 8 : (c == 2) ? 2 : 10;  // map0[2c]
 #pragma unroll
     for (int i = 0; i < MI; ++i) {
@@ -296,7 +312,7 @@ void gemm_tma_maps(const std::vector<GemmTask>& tasks, void* out) {
 
 template <int BN, int WGM, int WGN>
 static void launch_cfg(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int sms,
-                       cudaStream_t stream) {
+                       Uniform uni, cudaStream_t stream) {
   static bool configured = false;  // per process; one device per process (torchrun)
   auto kern = grouped_dgemm_tma<BN, WGM, WGN>;
   if (!configured) {
@@ -305,7 +321,7 @@ static void launch_cfg(const GemmTask* d_tasks, const void* d_maps, int ntasks, 
   }
   const int grid = (int)std::min<long long>(total_tiles, sms);
   kern<<<grid, THREADS, smem_bytes(BN), stream>>>(d_tasks, reinterpret_cast<const CUtensorMap*>(d_maps), ntasks,
-                                                 (int)total_tiles);
+                                                 (int)total_tiles, uni);
   FMM_CUDA(cudaGetLastError());
 }
 
@@ -341,7 +357,8 @@ int gemm_choose_bn(const std::vector<GemmTask>& tasks) {
 }
 
 void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn,
-                     cudaStream_t stream) {
+                     int uniform_tm, int uniform_tn, cudaStream_t stream) {
+  const Uniform uni{uniform_tm * uniform_tn, uniform_tm, uniform_tn};
   if (total_tiles <= 0 || ntasks <= 0) return;
   static int sms = 0;
   if (!sms) {
@@ -350,11 +367,11 @@ void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, lo
     FMM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   switch (bn) {
-    case 128: launch_cfg<128, 2, 4>(d_tasks, d_maps, ntasks, total_tiles, sms, stream); break;
-    case 112: launch_cfg<112, 8, 1>(d_tasks, d_maps, ntasks, total_tiles, sms, stream); break;
-    case 96: launch_cfg<96, 4, 2>(d_tasks, d_maps, ntasks, total_tiles, sms, stream); break;
-    case 80: launch_cfg<80, 8, 1>(d_tasks, d_maps, ntasks, total_tiles, sms, stream); break;
-    case 64: launch_cfg<64, 4, 2>(d_tasks, d_maps, ntasks, total_tiles, sms, stream); break;
+    case 128: launch_cfg<128, 2, 4>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
+    case 112: launch_cfg<112, 8, 1>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
+    case 96: launch_cfg<96, 4, 2>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
+    case 80: launch_cfg<80, 8, 1>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
+    case 64: launch_cfg<64, 4, 2>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
     default: throw Error(FMM_E_INVALID_ARG, "unsupported GEMM tile width " + std::to_string(bn));
   }
 }

@@ -90,8 +90,11 @@ int gemm_tile_n();
 bool gemm_tma_eligible(const std::vector<GemmTask>& tasks);
 size_t gemm_tma_map_bytes();  // bytes of one tensor map (two per task: A then B)
 void gemm_tma_maps(const std::vector<GemmTask>& tasks, void* out);
+// uniform_tm/tn: the common tile grid when every task has the same one (else 0, 0).
 void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn,
-                     cudaStream_t stream);
+                     int uniform_tm, int uniform_tn, cudaStream_t stream);
+// (tiles_m, tiles_n) shared by every task of a prepared list, or (0, 0).
+void gemm_uniform_grid(const std::vector<GemmTask>& tasks, int* tm, int* tn);
 // Thin products (one dimension <= skinny_limit()) on the CUDA cores (fmm_skinny.cu): ids index
 // the task table; row tasks have m <= limit, column tasks n <= limit.
 int skinny_limit();

@@ -52,6 +52,7 @@ struct Launch {
   bool aligned16 = true;
   bool tma = false;          // GEMM launches: TMA warp-specialised kernel
   int bn = 128;              // GEMM launches: CTA tile width
+  int uni_tm = 0, uni_tn = 0;  // GEMM launches: common tile grid of all tasks (0 = mixed)
   size_t ids_off = 0;        // SKINNY: int ids (row tasks then column tasks)
   int nrow = 0, ncol = 0, max_n = 0, max_m = 0;
   size_t maps_off = 0;       // byte offset of the tensor maps (2 per task)
@@ -325,6 +326,7 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
     ln.tma = !lazy_kernels && use_tma && gemm_tma_eligible(tasks);
     ln.bn = ln.tma ? gemm_choose_bn(tasks) : 128;
     ln.tiles = gemm_prepare(tasks, 128, ln.bn);
+    gemm_uniform_grid(tasks, &ln.uni_tm, &ln.uni_tn);
   };
   auto push_maps = [&](Launch& ln, const std::vector<GemmTask>& tasks) {
     if (lazy_kernels) {  // dry build: reserve the space the maps would need
@@ -758,7 +760,7 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
       case Launch::STRIPS:
         if (ln.tma)
           gemm_tma_launch(reinterpret_cast<const GemmTask*>(tab), d_tab + ln.maps_off, ln.count, ln.tiles, ln.bn,
-                          stream);
+                          ln.uni_tm, ln.uni_tn, stream);
         else
           gemm_launch(reinterpret_cast<const GemmTask*>(tab), ln.count, ln.tiles, ln.aligned16, stream);
         break;
@@ -995,7 +997,7 @@ fmm_status_t fmm_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const doub
   if (tma) gemm_tma_maps(t, buf + 512);
   FMM_CUDA(cudaMemcpyAsync(d_task, buf, sizeof(buf), cudaMemcpyHostToDevice, s));
   if (tma)
-    gemm_tma_launch(d_task, reinterpret_cast<char*>(d_task) + 512, 1, tiles, bn, s);
+    gemm_tma_launch(d_task, reinterpret_cast<char*>(d_task) + 512, 1, tiles, bn, t[0].tiles_m, t[0].tiles_n, s);
   else
     gemm_launch(d_task, 1, tiles, gemm_tasks_aligned16(t), s);
   return FMM_OK;
