@@ -171,6 +171,8 @@ def main():
     ap.add_argument("--ref-frac", type=float, default=0.25, help="reference-arm sample (fraction of each dim)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--fuse", type=int, default=0, help="fused leaf level (formation/GEMM/assembly in one launch)")
+    ap.add_argument("--no-unfused", action="store_true", help="skip the separate-kernel addition measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -202,7 +204,7 @@ def main():
     B = to_device(B_np, w["layout"], device)
     alg = F.load_alg(w["alg"])
     plan = F.Plan(alg, P, Q, N, L, layout=w["layout"], strategy=args.strategy, cse=bool(args.cse),
-                  shard_rank=rank, shard_count=world)
+                  shard_rank=rank, shard_count=world, fuse=bool(args.fuse))
     C = plan.new_output()
     st = plan.stats()
     dmma_peak, dfma_peak = F.probe_fp64_peak()
@@ -251,20 +253,59 @@ def main():
     add_ms = form_ms + asm_ms
     peaks, peak_src = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", HBM_FALLBACK))
-    gemm_tf = st["gemm_flops"] / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
-    add_gbs = st["add_bytes"] / (add_ms * 1e-3) / 1e9 if add_ms > 0 else None
+    fused = st.get("fused_launches", 0) > 0
+    # leaf-product flops of the dominant launch (the fused leaf level, or the plain leaf GEMM)
+    gemm_tf = st["leaf_flops"] / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    sep_bytes = st["add_bytes"] - st["fused_add_bytes"]
+    add_gbs = sep_bytes / (add_ms * 1e-3) / 1e9 if add_ms > 0 else None
+
+    # the same workload with separate formation / GEMM / assembly kernels: the addition kernels'
+    # own HBM roofline (every level's K1 / K3 kernels timed by phase events)
+    unfused = None
+    if fused and not args.no_unfused:
+        plan_u = F.Plan(alg, P, Q, N, L, layout=w["layout"], strategy=args.strategy, cse=bool(args.cse),
+                        shard_rank=rank, shard_count=world, fuse=False)
+        su = plan_u.stats()
+        for _ in range(2):
+            plan_u.execute(A, B, C, stream=stream)
+        nu = max(3, min(args.steps, 10))
+        evu = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nu)]
+        for e in (x for row in evu for x in row):
+            e.record(stream)  # creates the underlying cudaEvent_t
+        torch.cuda.synchronize()
+        for k in range(nu):
+            plan_u.execute_events(A, B, C, evu[k], stream=stream)
+        torch.cuda.synchronize()
+        phu = np.array([[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]),
+                         e[0].elapsed_time(e[3])] for e in evu]).mean(axis=0)
+        add_u = float(phu[0] + phu[2])
+        gbs_u = su["add_bytes"] / (add_u * 1e-3) / 1e9
+        unfused = {"ms_per_step": float(phu[3]), "value": flops / (phu[3] * 1e-3) / 1e9,
+                   "phases_ms": {"formation": float(phu[0]), "leaf_gemm": float(phu[1]), "assembly_and_strips": float(phu[2])},
+                   "additions": {"algorithmic_bytes_per_step": su["add_bytes"], "achieved_gbs": gbs_u, "peak_gbs": hbm,
+                                 "frac": gbs_u / hbm, "peak_source": peak_src,
+                                 "kernels": "NVRTC-generated K1 formation / K3 assembly (streaming, CSE)"},
+                   "leaf_gemm_tflops": su["leaf_flops"] / (phu[1] * 1e-3) / 1e12,
+                   "launches": su["launches"]}
+        del plan_u
+        # one more fused pass so C holds the headline path's result
+        plan.execute(A, B, C, stream=stream)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             traffic = json.load(f).get(args.workload, {}).get("grouped_dgemm_bytes_per_launch")
     except OSError:
         pass
-    roofline = {"bound": "tensor", "kernel": "grouped_dgemm (leaf products, mma.sync.m8n8k4.f64 = DMMA)",
+    kname = ("grouped_dgemm_tma<FUSED> (level-L formation + leaf products on DMMA mma.sync.m8n8k4.f64 + "
+             "level-L assembly, one persistent launch)" if fused else
+             "grouped_dgemm_tma (leaf products, mma.sync.m8n8k4.f64 = DMMA)")
+    roofline = {"bound": "tensor", "kernel": kname,
                 "achieved": gemm_tf, "peak": dmma_peak, "unit": "TFLOP/s",
                 "frac": (gemm_tf / dmma_peak) if gemm_tf else None, "traffic": traffic,
                 "peak_source": "in-run DMMA microbenchmark fmm_probe_fp64_peak (MEASURED_PEAKS.json has no FP64 "
                                "figure; nameplate 148 SM x 128 flop/clk x 1.965 GHz = 37.2)",
-                "algorithmic_flops_per_launch": st["gemm_flops"]}
+                "algorithmic_flops_per_launch": st["leaf_flops"],
+                "hidden_addition_bytes_per_launch": st["fused_add_bytes"]}
 
     # cuBLAS DGEMM (classical) on the same inputs, same box: the comparison point
     cub = None
@@ -343,15 +384,21 @@ def main():
                        "strategy": args.strategy, "cse": bool(args.cse),
                        "l2": "inputs larger than L2 (A, B, C 0.54 GB each vs 126 MB); no flush"
                        if args.workload != "c1" else "small config: L2-resident",
-                       "parallelism": f"leaf shards x{world} + NCCL reduce" if world > 1 else "1 GPU"},
+                       "parallelism": f"leaf shards x{world} + NCCL reduce" if world > 1 else "1 GPU",
+                       "fused_leaf_level": fused},
             "roofline": roofline,
             "clocks": clk,
             "e2e": e2e,
             "gpu_launches": int(st["launches"]) * args.steps,
             "cpu_baseline": cpu,
-            "phases_ms": {"formation": form_ms, "leaf_gemm": gemm_ms, "assembly_and_strips": add_ms - form_ms},
-            "additions": {"algorithmic_bytes_per_step": st["add_bytes"], "achieved_gbs": add_gbs, "peak_gbs": hbm,
-                          "frac": (add_gbs / hbm) if add_gbs else None, "peak_source": peak_src},
+            "phases_ms": {"formation_levels_below_L" if fused else "formation": form_ms,
+                          "fused_leaf_level" if fused else "leaf_gemm": gemm_ms,
+                          "assembly_and_strips": add_ms - form_ms},
+            "additions": {"algorithmic_bytes_per_step": st["add_bytes"],
+                          "bytes_in_fused_launch": st["fused_add_bytes"],
+                          "separate_kernel_bytes": sep_bytes, "separate_kernel_gbs": add_gbs, "peak_gbs": hbm,
+                          "separate_kernel_frac": (add_gbs / hbm) if add_gbs else None, "peak_source": peak_src},
+            "unfused": unfused,
             "fp64_peak_tflops": {"dmma_measured": dmma_peak, "dfma_measured": dfma_peak, "nameplate": 37.2},
             "effective_frac_of_fp64_peak": value / 1e3 / dmma_peak,
             "cublas_dgemm_gflops_same_inputs": cub,

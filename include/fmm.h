@@ -73,10 +73,18 @@ typedef struct {
                                block in the classical strip), so every sub-block view is 16-byte
                                aligned and TMA / 16-byte vector paths apply (R7b).
                                0: the paper's minimal peeling everywhere. */
+  int fuse_leaf_level;      /* 1: run the last level's formation (S_r, T_r of the leaves), the leaf
+                               products and the last level's assembly C_k = sum_r w_kr M_r as ONE
+                               persistent launch: spare warps of the DMMA GEMM kernel evaluate the
+                               addition chains (ascending index order, no CSE) while the tensor
+                               pipe works, synchronised per parent node through device counters
+                               (streaming strategy only; needs TMA-eligible leaf views and no thin
+                               leaves, else the plan silently runs the separate kernels).
+                               0: separate formation / GEMM / assembly launches. */
 } fmm_plan_options;
 
 /* Fill *opt with the defaults: row-major, streaming, cse = 1, shard 0 of 1, no limit,
-   peel_align = 1. */
+   peel_align = 1, fuse_leaf_level = 1. */
 void fmm_plan_options_default(fmm_plan_options* opt);
 
 /* ---- algorithms ------------------------------------------------------------------------- */
@@ -131,6 +139,16 @@ fmm_status_t fmm_plan_workspace_bytes(const fmm_plan_t* plan, size_t* bytes);
    [6] number of leaf products computed by this plan (its shard)
    [7] the paper's effective-GFLOPS numerator 2PQN - PN  */
 fmm_status_t fmm_plan_stats(const fmm_plan_t* plan, double out[8]);
+
+/* out[0..7] as fmm_plan_stats, then the split by launch:
+   [8]  flops of the leaf-level launch (the leaf products, fused or not)
+   [9]  addition HBM bytes evaluated inside the fused leaf-level launch (0 if not fused)
+   [10] number of fused leaf-level launches per execute (0 or 1)
+   [11] addition bytes of the separate formation kernels (levels below the fused one)
+   [12] addition bytes of the separate assembly kernels
+   [13] flops of the peel-strip products
+   [14..15] 0 (reserved) */
+fmm_status_t fmm_plan_stats_ex(const fmm_plan_t* plan, double out[16]);
 
 /* Execute C <- A*B (beta = 0: C is overwritten).  A, B, C are device pointers on the plan's
    device laid out per opt->layout; C must not alias A or B.  Leading dimensions in elements:

@@ -10,7 +10,8 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["fmm_alg.cpp", "fmm_codegen.cpp", "fmm_plan.cpp", "fmm_gemm.cu", "fmm_gemm_tma.cu", "fmm_skinny.cu", "fmm_probe.cu"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", "-Xptxas", "-v"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wall", "-Xptxas", "-v"] + (
+    ["-DFMM_FUSE_TRACE=1"] if os.environ.get("FMM_FUSE_TRACE") == "1" else [])
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -33,10 +33,18 @@
 namespace fmm {
 
 namespace {
-constexpr int BM = 128, BK = 16, STAGES = 6;
+constexpr int BM = 128, BK = 16;
+constexpr int STAGES_PLAIN = 6, STAGES_FUSED = 6;
 constexpr int CONSUMERS = 8, THREADS = 128 + CONSUMERS * 32;  // warpgroup 0 = producer, 1-2 = consumers
+constexpr int ADD_WARPS = THREADS / 32;                        // every warp of an addition CTA
+constexpr int FUSED_HDR_BYTES = FUSED_PROG_BYTES + 1024;       // program area + barriers, 1 KB aligned
 constexpr int A_BYTES = BM * BK * 8;   // 16 KB
-constexpr size_t smem_bytes(int bn) { return (size_t)STAGES * (A_BYTES + BK * bn * 8) + 1024 /*align*/ + 256 /*barriers*/; }
+constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
+constexpr size_t smem_bytes(int bn, int stages, bool fused) {
+  return fused ? 1024 /*align*/ + FUSED_HDR_BYTES +
+                     cmax((size_t)stages * (A_BYTES + BK * bn * 8), (size_t)ADD_WARPS * 2 * FUSED_ADD_SEG_BYTES)
+               : (size_t)stages * (A_BYTES + BK * bn * 8) + 1024 /*align*/ + 256 /*barriers*/;
+}
 constexpr int GROUP_M = 8;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -69,6 +77,21 @@ __device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
       : "memory");
 }
+// 1-D bulk copy global -> shared (TMA engine, no registers held while in flight)
+__device__ __forceinline__ void bulk_load(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
 __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c[0]), "+d"(c[1])
@@ -77,6 +100,22 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 __device__ __forceinline__ double lds64(unsigned addr) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ double2 lds128(unsigned addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+// L2-coherent loads: inputs of assembly jobs were written by other SMs during this kernel
+__device__ __forceinline__ double2 ldcg2(const double* p) {
+  double2 v;
+  asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ldcg1(const double* p) {
+  double v;
+  asm volatile("ld.global.cg.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
   return v;
 }
 
@@ -116,12 +155,223 @@ __device__ __forceinline__ TileCoord locate(const GemmTask* __restrict__ tasks, 
   return {lo, tm * BM, tn * BN};
 }
 
+// ---- addition-chain interpreter (fused kernel) -------------------------------------------------
+// Chain arithmetic exactly as the generated K1/K3 kernels without CSE and as the oracle: the first
+// term initialises (copy / negate / scale), later terms add, subtract or add a product; no FMA.
+__device__ __forceinline__ double chain_first(double c, double v) {
+  return c == 1.0 ? v : c == -1.0 ? -v : __dmul_rn(c, v);
+}
+__device__ __forceinline__ double chain_next(double acc, double c, double v) {
+  return c == 1.0 ? __dadd_rn(acc, v) : c == -1.0 ? __dsub_rn(acc, v) : __dadd_rn(acc, __dmul_rn(c, v));
+}
+
+// A job as one warp sees it: the program (in shared memory) and the node's pointers held in
+// registers, lane i owning in[i] / in[32+i] and out[i] / out[32+i] (broadcast with shuffles).
+struct JobView {
+  const FusedProg* prog;  // shared memory
+  const short* ostart;
+  const short* tin;
+  const double* tcoef;
+  unsigned long long pin0, pin1, pout0, pout1;
+  long long ld_in, ld_out;
+};
+__device__ __forceinline__ unsigned long long pick(unsigned long long p0, unsigned long long p1, int idx) {
+  return idx < 32 ? __shfl_sync(0xffffffffu, p0, idx) : __shfl_sync(0xffffffffu, p1, idx - 32);
+}
+__device__ __forceinline__ JobView job_view(const FusedArgs& fa, const char* sprog, const FusedJob& j, int lane) {
+  JobView v;
+  v.prog = reinterpret_cast<const FusedProg*>(sprog) + j.prog;
+  const int nin = v.prog->nin, nout = v.prog->nout;
+  v.ostart = reinterpret_cast<const short*>(sprog + v.prog->ostart_off);
+  v.tin = reinterpret_cast<const short*>(sprog + v.prog->in_off);
+  v.tcoef = reinterpret_cast<const double*>(sprog + v.prog->coef_off);
+  const char* nd = fa.base + v.prog->node_off + (long long)j.node * v.prog->node_bytes;
+  const unsigned long long* in = reinterpret_cast<const unsigned long long*>(nd);
+  const unsigned long long* out = in + nin;
+  const long long* lds = reinterpret_cast<const long long*>(out + nout);
+  v.pin0 = lane < nin ? __ldg(in + lane) : 0ull;
+  v.pin1 = lane + 32 < nin ? __ldg(in + lane + 32) : 0ull;
+  v.pout0 = lane < nout ? __ldg(out + lane) : 0ull;
+  v.pout1 = lane + 32 < nout ? __ldg(out + lane + 32) : 0ull;
+  v.ld_in = __ldg(lds);
+  v.ld_out = __ldg(lds + 1);
+  return v;
+}
+
+// Direct path: every lane loads its columns from global (L2-coherent), U column groups in flight.
+// Every loop that contains a shuffle (pointer broadcast) runs the same trip count on all lanes.
+template <int U>
+__device__ void job_direct(const JobView& v, const FusedJob& j, int lane) {
+  const int cols = v.prog->cols, nout = v.prog->nout;
+  const bool vec2 = v.prog->vec2 != 0;
+  const int step = vec2 ? 64 * U : 32 * U;
+  for (int row = j.row0; row < j.row0 + j.nrows; ++row) {
+    for (int o = 0; o < nout; ++o) {
+      double* y = reinterpret_cast<double*>(pick(v.pout0, v.pout1, o));
+      if (!y) continue;
+      y += (long long)row * v.ld_out;
+      const int t0 = v.ostart[o], t1 = v.ostart[o + 1];
+      for (int cb = 0; cb < cols; cb += step) {
+        if (vec2) {
+          const int c = cb + 2 * lane;
+          double2 acc[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) acc[u] = make_double2(0.0, 0.0);
+          for (int t = t0; t < t1; ++t) {
+            const int i = v.tin[t];
+            const double coef = v.tcoef[t];
+            const double* x = reinterpret_cast<const double*>(pick(v.pin0, v.pin1, i)) + (long long)row * v.ld_in;
+            double2 val[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) val[u] = c + 64 * u < cols ? ldcg2(x + c + 64 * u) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              if (t == t0) {
+                acc[u].x = chain_first(coef, val[u].x);
+                acc[u].y = chain_first(coef, val[u].y);
+              } else {
+                acc[u].x = chain_next(acc[u].x, coef, val[u].x);
+                acc[u].y = chain_next(acc[u].y, coef, val[u].y);
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (c + 64 * u < cols) *reinterpret_cast<double2*>(y + c + 64 * u) = acc[u];
+        } else {
+          const int c = cb + lane;
+          double acc[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) acc[u] = 0.0;
+          for (int t = t0; t < t1; ++t) {
+            const int i = v.tin[t];
+            const double coef = v.tcoef[t];
+            const double* x = reinterpret_cast<const double*>(pick(v.pin0, v.pin1, i)) + (long long)row * v.ld_in;
+            double val[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) val[u] = c + 32 * u < cols ? ldcg1(x + c + 32 * u) : 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc[u] = t == t0 ? chain_first(coef, val[u]) : chain_next(acc[u], coef, val[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (c + 32 * u < cols) y[c + 32 * u] = acc[u];
+        }
+      }
+    }
+  }
+}
+
+// Staged path (producer warps 1-3): lane i copies the row segment of input i of a piece into one
+// of the warp's two shared-memory buffers with a 1-D bulk copy (TMA engine; nothing held in
+// registers); the next piece's copies are in flight while the warp evaluates the chains of the
+// current one from shared memory (two column pairs per lane) and stores the outputs (16 bytes).
+struct Staging {
+  unsigned buf0, bar0;  // buffer b at buf0 + b * FUSED_ADD_SEG_BYTES, its mbarrier at bar0 + 8 b
+  unsigned phase;       // bit b = parity of buffer b
+};
+__device__ void job_staged(const JobView& v, const FusedJob& j, int lane, Staging& st) {
+  const int cols = v.prog->cols, nin = v.prog->nin, nout = v.prog->nout, seg = v.prog->seg;
+  const int nseg = (cols + seg - 1) / seg;
+  const int npieces = j.nrows * nseg;
+  auto issue = [&](int p, int b) {
+    const int row = j.row0 + p / nseg, c0 = (p % nseg) * seg;
+    const int w = min(seg, cols - c0);
+    const unsigned bar = st.bar0 + 8u * (unsigned)b;
+    if (lane == 0) mbar_expect_tx(bar, (unsigned)(nin * w * 8));
+    __syncwarp();
+    if (lane < nin)
+      bulk_load(st.buf0 + (unsigned)b * FUSED_ADD_SEG_BYTES + (unsigned)(lane * seg * 8),
+                reinterpret_cast<const double*>(v.pin0) + (long long)row * v.ld_in + c0, (unsigned)(w * 8), bar);
+  };
+  if (npieces > 0) issue(0, 0);
+  int b = 0;
+  for (int p = 0; p < npieces; ++p, b ^= 1) {
+    if (p + 1 < npieces) issue(p + 1, b ^ 1);
+    mbar_wait(st.bar0 + 8u * (unsigned)b, (st.phase >> b) & 1u);
+    st.phase ^= 1u << b;
+    const int row = j.row0 + p / nseg, c0 = (p % nseg) * seg;
+    const int w = min(seg, cols - c0);
+    const unsigned sbuf = st.buf0 + (unsigned)b * FUSED_ADD_SEG_BYTES;
+    for (int o = 0; o < nout; ++o) {
+      double* y = reinterpret_cast<double*>(pick(v.pout0, v.pout1, o));
+      if (!y) continue;
+      y += (long long)row * v.ld_out + c0;
+      const int t0 = v.ostart[o], t1 = v.ostart[o + 1];
+      for (int c = 2 * lane; c < w; c += 128) {
+        const bool two = c + 64 < w;
+        double2 a0 = make_double2(0.0, 0.0), a1 = a0;
+        for (int t = t0; t < t1; ++t) {
+          const unsigned xo = sbuf + (unsigned)((v.tin[t] * seg + c) * 8);
+          const double coef = v.tcoef[t];
+          const double2 x0 = lds128(xo);
+          const double2 x1 = two ? lds128(xo + 512u) : make_double2(0.0, 0.0);
+          if (t == t0) {
+            a0.x = chain_first(coef, x0.x);
+            a0.y = chain_first(coef, x0.y);
+            a1.x = chain_first(coef, x1.x);
+            a1.y = chain_first(coef, x1.y);
+          } else {
+            a0.x = chain_next(a0.x, coef, x0.x);
+            a0.y = chain_next(a0.y, coef, x0.y);
+            a1.x = chain_next(a1.x, coef, x1.x);
+            a1.y = chain_next(a1.y, coef, x1.y);
+          }
+        }
+        *reinterpret_cast<double2*>(y + c) = a0;
+        if (two) *reinterpret_cast<double2*>(y + c + 64) = a1;
+      }
+    }
+    __syncwarp();  // every lane is done with buffer b before it is refilled
+  }
+}
+
+__device__ __forceinline__ int claim(unsigned long long* ctr, int lane) {
+  int idx = 0;
+  if (lane == 0) idx = (int)atomicAdd(ctr, 1ull);
+  return __shfl_sync(0xffffffffu, idx, 0);
+}
+
+// Run one job (formation or assembly) with a whole warp; staged when st != nullptr.
+template <int U>
+__device__ void run_job(const FusedArgs& fa, const char* sprog, int jidx, int lane, Staging* st) {
+  const FusedJob j = fa.jobs[jidx];
+  if (j.kind == 1) {  // assembly: wait until every leaf tile of the parent is stored
+    if (lane == 0) {
+      const unsigned long long target = (unsigned long long)__ldg(&fa.tiles_target[j.dep]);
+      while (ld_acquire(&fa.ctr[2 + fa.np + j.dep]) < target) __nanosleep(256);
+    }
+    __syncwarp();
+    fence_proxy_async_global();
+  }
+  const JobView v = job_view(fa, sprog, j, lane);
+  if (st && v.prog->vec2 && v.prog->seg > 0) job_staged(v, j, lane, *st);
+  else job_direct<U>(v, j, lane);
+  if (j.kind == 0) {  // formation: publish (release) to the TMA readers of the leaf products
+    fence_proxy_async_global();
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) atomicAdd(&fa.ctr[2 + j.dep], 1ull);
+  }
+}
+
 // BN columns per CTA tile, consumer warps arranged WGM x WGN (WGM * WGN = 8); warp tile
 // (128 / WGM) x (BN / WGN), both multiples of 16 so the fragment permutations apply.
-template <int BN, int WGM, int WGN>
+//
+// FUSED: the level-L formation (F) and assembly (A) jobs of the plan run in the same launch,
+// spatially partitioned: CTAs [0, gemm_ctas) are GEMM CTAs (one per SM, as the plain kernel),
+// CTAs [gemm_ctas, gridDim.x) are addition CTAs whose 12 warps evaluate addition chains with
+// bulk-copy staging.  The two must not share an SM: on B200 the FP64 tensor path (DMMA) and the
+// FP64 ALU (DADD / DMUL) are one pipe, and a worker warp next to eight DMMA warps was measured to
+// get ~1 % of it.  Every warp of the GPU first drains the phase-0 jobs (formation of the first
+// parent node: nothing can start before it); the TMA thread waits for ready[parent] before the
+// first load of a tile; GEMM consumers count each stored tile into tiles_done[parent] and, when
+// out of tiles, join the phase-1 queue.  All CTAs must be co-resident (cooperative launch,
+// grid = #SMs), since jobs wait on tiles and tiles on jobs.
+template <int BN, int WGM, int WGN, int STAGES, bool FUSED>
 __global__ void __launch_bounds__(THREADS, 1)
     grouped_dgemm_tma(const GemmTask* __restrict__ tasks, const CUtensorMap* __restrict__ maps, int ntasks,
-                      int total_tiles, Uniform uni) {
+                      int total_tiles, Uniform uni, FusedArgs fa) {
   static_assert(WGM * WGN == CONSUMERS, "8 consumer warps");
   constexpr int WTM = BM / WGM, WTN = BN / WGN;
   static_assert(WTM % 16 == 0 && WTN % 16 == 0, "warp tile must be a multiple of 16");
@@ -130,20 +380,54 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr int STAGE_T = A_BYTES + B_BYTES_T;
   extern __shared__ unsigned char smem_raw[];
   const unsigned raw = smem_u32(smem_raw);
-  const unsigned base = (raw + 1023u) & ~1023u;  // 1024-byte alignment for the 128B swizzle
-  const unsigned bars = base + STAGES * STAGE_T;
+  const unsigned al = (raw + 1023u) & ~1023u;  // 1024-byte alignment for the 128B swizzle
+  // fused layout: [program area][barriers][pad to 1 KB][GEMM stages | worker staging]
+  const unsigned sprog_u = al;
+  const unsigned bars = FUSED ? al + FUSED_PROG_BYTES : al + STAGES * STAGE_T;
+  const unsigned base = FUSED ? al + FUSED_HDR_BYTES : al;
+  const char* sprog = reinterpret_cast<const char*>(smem_raw) + (sprog_u - raw);
   auto full_bar = [&](int s) { return bars + 8u * s; };
   auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool adder = FUSED && (int)blockIdx.x >= fa.gemm_ctas;
+  const int gemm_ctas = FUSED ? fa.gemm_ctas : (int)gridDim.x;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full_bar(s), 1);
-      mbar_init(empty_bar(s), CONSUMERS);
+    if (!adder) {
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(full_bar(s), 1);
+        mbar_init(empty_bar(s), CONSUMERS);
+      }
+    } else {
+      for (int b = 0; b < 2 * ADD_WARPS; ++b) mbar_init(bars + 8u * b, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  if (FUSED) {  // the addition programs -> shared memory
+    const int4* src = reinterpret_cast<const int4*>(fa.blob);
+    int4* dst = reinterpret_cast<int4*>(smem_raw + (sprog_u - raw));
+    for (int i = threadIdx.x; i < fa.blob_bytes / 16; i += THREADS) dst[i] = __ldg(src + i);
+  }
   __syncthreads();
+
+  if (FUSED && adder) {
+    // ------------------------------ addition CTA ------------------------------
+    Staging st;
+    st.buf0 = base + (unsigned)(2 * warp) * FUSED_ADD_SEG_BYTES;
+    st.bar0 = bars + 16u * warp;
+    st.phase = 0;
+    for (;;) {
+      const int idx = claim(&fa.ctr[0], lane);
+      if (idx >= fa.njobs0) break;
+      run_job<4>(fa, sprog, idx, lane, &st);
+    }
+    for (;;) {
+      const int idx = claim(&fa.ctr[1], lane);
+      if (fa.njobs0 + idx >= fa.njobs) break;
+      run_job<4>(fa, sprog, fa.njobs0 + idx, lane, &st);
+    }
+    return;
+  }
 
   if (warp < 4) {
     // ------------------------------ producer warpgroup ------------------------------
@@ -151,8 +435,18 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (warp == 0 && lane == 0) {
       int stage = 0;
       unsigned phase = 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      int ready_node = -1;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gemm_ctas) {
         const TileCoord tc = locate<BN>(tasks, ntasks, tile, uni);
+        if (FUSED) {
+          const int node = __ldg(&tasks[tc.task].node);
+          if (node != ready_node) {
+            const unsigned long long target = (unsigned long long)__ldg(&fa.ready_target[node]);
+            while (ld_acquire(&fa.ctr[2 + node]) < target) __nanosleep(128);
+            fence_proxy_async_global();
+            ready_node = node;
+          }
+        }
         const CUtensorMap* ma = maps + 2 * tc.task;
         const CUtensorMap* mb = ma + 1;
         const int KT = (__ldg(&tasks[tc.task].k) + BK - 1) / BK;
@@ -172,6 +466,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
 
   // ------------------------------ consumers ------------------------------
+  if (FUSED) {
+    for (;;) {
+      const int idx = claim(&fa.ctr[0], lane);
+      if (idx >= fa.njobs0) break;
+      run_job<4>(fa, sprog, idx, lane, nullptr);
+    }
+  }
   const int cw = warp - 4;  // consumer warp 0..7
   const int r = lane >> 2, c = lane & 3;
   const int wm = (cw / WGN) * WTM, wn = (cw % WGN) * WTN;
@@ -188,7 +489,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   int stage = 0;
   unsigned phase = 0;
-  for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+  for (int tile = blockIdx.x; tile < total_tiles; tile += gemm_ctas) {
     const TileCoord tc = locate<BN>(tasks, ntasks, tile, uni);
     const GemmTask& t = tasks[tc.task];
     const int KT = (__ldg(&t.k) + BK - 1) / BK;
@@ -255,6 +556,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
     }
+    if (FUSED) {  // publish the stored tile (release) to the assembly jobs of its parent
+      __threadfence();
+      named_bar_sync(1, CONSUMERS * 32);
+      if (cw == 0 && lane == 0) atomicAdd(&fa.ctr[2 + fa.np + __ldg(&t.node)], 1ull);
+    }
+  }
+  if (FUSED) {
+    for (;;) {
+      const int idx = claim(&fa.ctr[1], lane);
+      if (fa.njobs0 + idx >= fa.njobs) break;
+      run_job<4>(fa, sprog, fa.njobs0 + idx, lane, nullptr);
+    }
   }
 }
 
@@ -310,19 +623,38 @@ void gemm_tma_maps(const std::vector<GemmTask>& tasks, void* out) {
   }
 }
 
-template <int BN, int WGM, int WGN>
+template <int BN, int WGM, int WGN, bool FUSED>
 static void launch_cfg(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int sms,
-                       Uniform uni, cudaStream_t stream) {
+                       Uniform uni, const FusedArgs& fa, cudaStream_t stream) {
+  constexpr int ST = FUSED ? STAGES_FUSED : STAGES_PLAIN;
   static bool configured = false;  // per process; one device per process (torchrun)
-  auto kern = grouped_dgemm_tma<BN, WGM, WGN>;
+  auto kern = grouped_dgemm_tma<BN, WGM, WGN, ST, FUSED>;
+  const size_t smem = smem_bytes(BN, ST, FUSED);
   if (!configured) {
-    FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes(BN)));
+    FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
-  const int grid = (int)std::min<long long>(total_tiles, sms);
-  kern<<<grid, THREADS, smem_bytes(BN), stream>>>(d_tasks, reinterpret_cast<const CUtensorMap*>(d_maps), ntasks,
-                                                 (int)total_tiles, uni);
-  FMM_CUDA(cudaGetLastError());
+  const CUtensorMap* maps = reinterpret_cast<const CUtensorMap*>(d_maps);
+  const int ntiles = (int)total_tiles;
+  if (!FUSED) {
+    const int grid = (int)std::min<long long>(total_tiles, sms);
+    kern<<<grid, THREADS, smem, stream>>>(d_tasks, maps, ntasks, ntiles, uni, fa);
+    FMM_CUDA(cudaGetLastError());
+    return;
+  }
+  // fused: every SM hosts addition workers, and assembly jobs wait on tiles of other CTAs, so all
+  // CTAs must be co-resident: cooperative launch, one CTA per SM
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)sms);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  FMM_CUDA(cudaLaunchKernelEx(&cfg, kern, d_tasks, maps, ntasks, ntiles, uni, fa));
 }
 
 int gemm_choose_bn(const std::vector<GemmTask>& tasks) {
@@ -356,24 +688,42 @@ int gemm_choose_bn(const std::vector<GemmTask>& tasks) {
   return best;
 }
 
-void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn,
-                     int uniform_tm, int uniform_tn, cudaStream_t stream) {
-  const Uniform uni{uniform_tm * uniform_tn, uniform_tm, uniform_tn};
-  if (total_tiles <= 0 || ntasks <= 0) return;
+static int sm_count() {
   static int sms = 0;
   if (!sms) {
     int dev = 0;
     FMM_CUDA(cudaGetDevice(&dev));
     FMM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
+  return sms;
+}
+
+template <bool FUSED>
+static void launch_bn(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn, Uniform uni,
+                      const FusedArgs& fa, cudaStream_t stream) {
+  const int sms = sm_count();
   switch (bn) {
-    case 128: launch_cfg<128, 2, 4>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
-    case 112: launch_cfg<112, 8, 1>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
-    case 96: launch_cfg<96, 4, 2>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
-    case 80: launch_cfg<80, 8, 1>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
-    case 64: launch_cfg<64, 4, 2>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
+    case 128: launch_cfg<128, 2, 4, FUSED>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, fa, stream); break;
+    case 112: launch_cfg<112, 8, 1, FUSED>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, fa, stream); break;
+    case 96: launch_cfg<96, 4, 2, FUSED>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, fa, stream); break;
+    case 80: launch_cfg<80, 8, 1, FUSED>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, fa, stream); break;
+    case 64: launch_cfg<64, 4, 2, FUSED>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, fa, stream); break;
     default: throw Error(FMM_E_INVALID_ARG, "unsupported GEMM tile width " + std::to_string(bn));
   }
+}
+
+void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn,
+                     int uniform_tm, int uniform_tn, cudaStream_t stream) {
+  const Uniform uni{uniform_tm * uniform_tn, uniform_tm, uniform_tn};
+  if (total_tiles <= 0 || ntasks <= 0) return;
+  launch_bn<false>(d_tasks, d_maps, ntasks, total_tiles, bn, uni, FusedArgs{}, stream);
+}
+
+void gemm_fused_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn,
+                       int uniform_tm, int uniform_tn, const FusedArgs& fa, cudaStream_t stream) {
+  const Uniform uni{uniform_tm * uniform_tn, uniform_tm, uniform_tn};
+  if (ntasks <= 0 && fa.njobs <= 0) return;
+  launch_bn<true>(d_tasks, d_maps, ntasks, total_tiles, bn, uni, fa, stream);
 }
 
 }  // namespace fmm

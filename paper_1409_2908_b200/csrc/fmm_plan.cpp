@@ -42,7 +42,7 @@ struct Dims {
 };
 
 struct Launch {
-  enum Kind { FORM_A, FORM_B, GEMM, ASSEMBLE, STRIPS, SKINNY } kind;
+  enum Kind { FORM_A, FORM_B, GEMM, ASSEMBLE, STRIPS, SKINNY, FUSED } kind;
   int level = 0;
   size_t table_off = 0;  // byte offset in the device table buffer
   int count = 0;         // nodes / tasks
@@ -58,6 +58,11 @@ struct Launch {
   size_t maps_off = 0;       // byte offset of the tensor maps (2 per task)
   double elem_reads = 0, elem_writes = 0, elem_adds = 0;  // totals over the launch (elements)
   double flops = 0, gemm_bytes = 0;
+  std::vector<int> node_ids;  // FORM / ASSEMBLE: parent node index of every table entry
+  // FUSED: byte offsets of the program / job / target tables, and their sizes
+  size_t progs_off = 0, jobs_off = 0, targets_off = 0;
+  int njobs0 = 0, njobs = 0, np = 0, blob_bytes = 0, nprogs = 0;
+  int gemm_ctas = 0;  // FUSED: CTAs running leaf tiles (the rest of the grid are addition CTAs)
 };
 
 long long round_up(long long x, long long m) { return (x + m - 1) / m * m; }
@@ -98,6 +103,9 @@ struct fmm_plan_s {
   std::vector<long long> offZero;                        // per level: zero M block (shared)
 
   bool use_tma = true;  // FMM_NO_TMA=1 forces the cp.async GEMM (diagnostics)
+  bool fuse = true;     // fuse_leaf_level option (FMM_NO_FUSE=1 overrides)
+  unsigned long long* d_ctr = nullptr;  // fused launch counters: claim0, claim1, ready[np], tiles[np]
+  size_t ctr_bytes = 0;
   // kernels (vec 2 / vec 1 variants created lazily)
   std::shared_ptr<LincombKernel> kU[3], kV[3], kW[3];
 
@@ -135,6 +143,7 @@ struct fmm_plan_s {
     if (upload_done) cudaEventSynchronize(upload_done);
     cudaDeviceSynchronize();
     if (ws) cudaFree(ws);
+    if (d_ctr) cudaFree(d_ctr);
     for (auto& sl : slot)
       if (sl.d_tab) cudaFree(sl.d_tab);
     if (h_pinned) cudaFreeHost(h_pinned);
@@ -283,6 +292,8 @@ struct fmm_plan_s {
 
   // Build every launch and its table for the given execute arguments (row-major orientation).
   void build(const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc, bool lazy_kernels);
+  // Replace the level-L formation, leaf GEMM and level-L assembly launches by one fused launch.
+  void fuse_leaf_level(bool lazy_kernels);
 };
 
 View fmm_plan_s::opA(int l, long long z, const View& root) const {
@@ -397,6 +408,7 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
       const long long rows = side == 0 ? d.P : d.Q, cols = side == 0 ? d.Q : d.N;
       if (rows <= 0 || cols <= 0) continue;
       std::vector<char> tab;
+      std::vector<int> node_ids;
       const size_t nb = lincomb_node_bytes(nin, nout);
       bool aligned = (cols % 2) == 0;
       int count = 0;
@@ -426,10 +438,12 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
         lds[1] = side == 0 ? ldS[l] : ldT[l];
         aligned &= (lds[0] % 2 == 0) && (lds[1] % 2 == 0);
         tab.insert(tab.end(), e.begin(), e.end());
+        node_ids.push_back((int)zp);
         ++count;
       }
       if (!count) continue;
       Launch ln;
+      ln.node_ids = node_ids;
       ln.kind = side == 0 ? Launch::FORM_A : Launch::FORM_B;
       ln.level = l;
       ln.count = count;
@@ -473,6 +487,7 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
       t.k = (int)d.Q;
       t.alpha = a.sigma * b.sigma;
       t.beta = 0.0;
+      t.node = (int)(z / R);
       if (t.m > 0 && t.n > 0) tasks.push_back(t);
     }
     emit_gemm(Launch::GEMM, L, tasks);
@@ -484,6 +499,7 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
     const Dims& dp = dims[l - 1];
     if (d.P > 0 && d.N > 0) {
       std::vector<char> tab;
+      std::vector<int> node_ids;
       const int nin = R, nout = M * Nb;
       const size_t nb = lincomb_node_bytes(nin, nout);
       bool aligned = (d.N % 2) == 0;
@@ -507,10 +523,12 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
         lds[1] = par.ld;
         aligned &= (lds[0] % 2 == 0) && (lds[1] % 2 == 0);
         tab.insert(tab.end(), e.begin(), e.end());
+        node_ids.push_back((int)zp);
         ++count;
       }
       if (count) {
         Launch ln;
+        ln.node_ids = node_ids;
         ln.kind = Launch::ASSEMBLE;
         ln.level = l;
         ln.count = count;
@@ -580,6 +598,188 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
     }
     emit_gemm(Launch::STRIPS, l - 1, tasks);
   }
+  fuse_leaf_level(lazy_kernels);
+}
+
+// The fused leaf level (fmm_gemm_tma.cu, FUSED kernel).  Jobs: formation (F) of the level-L S / T
+// of one parent node (level L-1) over a row range, assembly (A) of the parent's C / M sub-blocks
+// from its R leaf products over a row range.  Phase 0 = F jobs of the first parent (every warp of
+// the GPU helps: no leaf product can start before them); phase 1 = F of the other parents and
+// the A jobs, interleaved so formation stays LOOKAHEAD parents ahead of the GEMM and assembly
+// follows the GEMM's parent-major tile order.  Chains are the coefficient rows without CSE,
+// ascending input index (the oracle's order, R8).
+void fmm_plan_s::fuse_leaf_level(bool lazy_kernels) {
+  if (!fuse || L < 1 || opt.strategy != FMM_ADD_STREAMING) return;
+  int ia = -1, ib = -1, ig = -1, ias = -1;
+  for (int q = 0; q < (int)launches.size(); ++q) {
+    const Launch& ln = launches[q];
+    if (ln.level != L) continue;
+    if (ln.kind == Launch::FORM_A) ia = q;
+    else if (ln.kind == Launch::FORM_B) ib = q;
+    else if (ln.kind == Launch::GEMM) ig = q;
+    else if (ln.kind == Launch::SKINNY) return;  // thin leaves: no fusion
+    else if (ln.kind == Launch::ASSEMBLE) ias = q;
+  }
+  if (ig < 0 || ias < 0) return;
+  if (!lazy_kernels && !launches[ig].tma) return;
+  const int M = alg->M, K = alg->K, Nb = alg->N;
+  const long long np = nodes_at[L - 1];
+  Launch fz = launches[ig];
+  fz.kind = Launch::FUSED;
+  fz.np = (int)np;
+  // programs: headers, then per program short ostart[nout+1], short in[nterms], double coef[nterms]
+  std::vector<FusedProg> progs;
+  std::vector<int> prog_src;  // launch index of each program
+  std::vector<std::vector<short>> p_ostart, p_in;
+  std::vector<std::vector<double>> p_coef;
+  auto add_prog = [&](int q, int side) {
+    const Launch& ln = launches[q];
+    FusedProg p{};
+    p.node_off = (long long)ln.table_off;
+    p.nin = side == 0 ? M * K : side == 1 ? K * Nb : R;
+    p.nout = side == 0 ? (int)formU.size() : side == 1 ? (int)formV.size() : M * Nb;
+    p.node_bytes = (int)lincomb_node_bytes(p.nin, p.nout);
+    p.rows = (int)ln.rows;
+    p.cols = (int)ln.cols;
+    p.vec2 = ln.aligned16 ? 1 : 0;
+    const int segmax = FUSED_ADD_SEG_BYTES / (8 * p.nin);
+    p.seg = p.vec2 && p.nin <= 32 && segmax >= 32 ? std::min(512, segmax / 32 * 32) : 0;
+    if (const char* dbg = getenv("FMM_FUSE_DEBUG"))
+      if (!strcmp(dbg, "direct")) p.seg = 0;
+    // chains: coefficient rows, ascending input index
+    std::vector<short> ostart(p.nout + 1, 0), tin;
+    std::vector<double> tco;
+    double adds = 0;
+    for (int o = 0; o < p.nout; ++o) {
+      ostart[o] = (short)tin.size();
+      for (int i = 0; i < p.nin; ++i) {
+        double c = 0;
+        if (side == 0) c = alg->Ud[(size_t)i * R + formU[o]];
+        else if (side == 1) c = alg->Vd[(size_t)i * R + formV[o]];
+        else c = alg->Wd[(size_t)o * R + i];
+        if (c != 0.0) tin.push_back((short)i), tco.push_back(c);
+      }
+      if ((int)tin.size() > ostart[o]) adds += (double)tin.size() - ostart[o] - 1;
+    }
+    ostart[p.nout] = (short)tin.size();
+    progs.push_back(p);
+    prog_src.push_back(q);
+    p_ostart.push_back(ostart);
+    p_in.push_back(tin);
+    p_coef.push_back(tco);
+    // statistics of the absorbed launch with the chains actually evaluated
+    fz.elem_adds += adds * (double)ln.rows * ln.cols * ln.count;
+    fz.elem_reads += ln.elem_reads;
+    fz.elem_writes += ln.elem_writes;
+  };
+  if (ia >= 0) add_prog(ia, 0);
+  if (ib >= 0) add_prog(ib, 1);
+  add_prog(ias, 2);
+  // lay out the blob
+  size_t off = (progs.size() * sizeof(FusedProg) + 15) / 16 * 16;
+  for (size_t q = 0; q < progs.size(); ++q) {
+    progs[q].ostart_off = (int)off;
+    off += p_ostart[q].size() * sizeof(short);
+    progs[q].in_off = (int)off;
+    off += p_in[q].size() * sizeof(short);
+    off = (off + 7) / 8 * 8;
+    progs[q].coef_off = (int)off;
+    off += p_coef[q].size() * sizeof(double);
+  }
+  off = (off + 15) / 16 * 16;
+  if (off > (size_t)FUSED_PROG_BYTES) return;  // programs too large for the shared-memory area
+  std::vector<char> blob(off, 0);
+  std::memcpy(blob.data(), progs.data(), progs.size() * sizeof(FusedProg));
+  for (size_t q = 0; q < progs.size(); ++q) {
+    std::memcpy(blob.data() + progs[q].ostart_off, p_ostart[q].data(), p_ostart[q].size() * sizeof(short));
+    std::memcpy(blob.data() + progs[q].in_off, p_in[q].data(), p_in[q].size() * sizeof(short));
+    std::memcpy(blob.data() + progs[q].coef_off, p_coef[q].data(), p_coef[q].size() * sizeof(double));
+  }
+  fz.blob_bytes = (int)off;
+  fz.nprogs = (int)progs.size();
+  // spatial split of the SMs: k addition CTAs (own SMs: the FP64 ALU and the DMMA path are one
+  // pipe), the rest run leaf tiles; k balances leaf flops at the per-SM DMMA rate against the
+  // absorbed addition bytes at the per-SM bulk-copy rate
+  {
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
+    cudaGetLastError();
+    const double bytes = 8.0 * (fz.elem_reads + fz.elem_writes), fl = fz.flops;
+    const double F_SM = 250e9, B_SM = 100e9;
+    int best_k = 1;
+    double best_t = 1e300;
+    for (int k = 1; k <= sms / 3; ++k) {
+      const double t = std::max(fl / ((sms - k) * F_SM), bytes / (k * B_SM));
+      if (t < best_t) best_t = t, best_k = k;
+    }
+    if (const char* e = getenv("FMM_FUSE_ADD_CTAS")) best_k = std::max(1, std::min(sms - 1, atoi(e)));
+    fz.gemm_ctas = sms - best_k;
+  }
+  const int pA = (int)progs.size() - 1;
+  // jobs per parent; phase 0 = formation of the parent of the first leaf product in tile order
+  const GemmTask* tk = reinterpret_cast<const GemmTask*>(h_tab.data() + fz.table_off);
+  const int first_node = fz.count > 0 ? tk[0].node : -1;
+  std::vector<int> ready_target(np, 0), tiles_target(np, 0);
+  for (int q = 0; q < fz.count; ++q)
+    if (tk[q].node >= 0 && tk[q].node < np) tiles_target[tk[q].node] += tk[q].tiles_m * tk[q].tiles_n;
+  std::vector<std::vector<FusedJob>> fjobs0(np), fjobs(np), ajobs(np);
+  for (int pi = 0; pi < (int)progs.size(); ++pi) {
+    const Launch& ln = launches[prog_src[pi]];
+    const FusedProg& p = progs[pi];
+    const bool is_a = pi == pA;
+    for (int e = 0; e < (int)ln.node_ids.size(); ++e) {
+      const int zp = ln.node_ids[e];
+      const bool first = !is_a && zp == first_node;
+      // job size: a few staged pieces (segments of one row), so that one parent's jobs spread
+      // over every worker warp and a job never outlasts a small fraction of the parent's GEMM
+      const int cols = std::max(1, p.cols);
+      const int pieces_per_row = p.seg > 0 ? (cols + p.seg - 1) / p.seg : (cols + 255) / 256;
+      const int per = std::max(1, (first ? 2 : 8) / pieces_per_row);
+      for (int r0 = 0; r0 < p.rows; r0 += per) {
+        FusedJob j{pi, e, r0, std::min(per, p.rows - r0), zp, is_a ? 1 : 0};
+        if (is_a) ajobs[zp].push_back(j);
+        else {
+          (first ? fjobs0 : fjobs)[zp].push_back(j);
+          ++ready_target[zp];
+        }
+      }
+    }
+  }
+  std::vector<FusedJob> jobs;
+  for (long long zp = 0; zp < np; ++zp) jobs.insert(jobs.end(), fjobs0[zp].begin(), fjobs0[zp].end());
+  fz.njobs0 = (int)jobs.size();
+  const long long LOOKAHEAD = 2;
+  for (long long zp = 0; zp < np; ++zp) {
+    jobs.insert(jobs.end(), fjobs[zp].begin(), fjobs[zp].end());
+    if (zp >= LOOKAHEAD) jobs.insert(jobs.end(), ajobs[zp - LOOKAHEAD].begin(), ajobs[zp - LOOKAHEAD].end());
+  }
+  for (long long zp = std::max(0LL, np - LOOKAHEAD); zp < np; ++zp) jobs.insert(jobs.end(), ajobs[zp].begin(), ajobs[zp].end());
+  fz.njobs = (int)jobs.size();
+  if (const char* dbg = getenv("FMM_FUSE_DEBUG")) {  // diagnostics only (wrong results): isolate costs
+    if (!strcmp(dbg, "nojobs")) {
+      fz.njobs0 = fz.njobs = 0;
+      std::fill(ready_target.begin(), ready_target.end(), 0);
+      std::fill(tiles_target.begin(), tiles_target.end(), 0);
+    }
+  }
+  auto push = [&](const void* p, size_t n) {
+    size_t off = h_tab.size();
+    h_tab.resize(align256(off + n));
+    if (n) std::memcpy(h_tab.data() + off, p, n);
+    return off;
+  };
+  fz.progs_off = push(blob.data(), blob.size());
+  fz.jobs_off = push(jobs.data(), jobs.size() * sizeof(FusedJob));
+  std::vector<int> targets(ready_target);
+  targets.insert(targets.end(), tiles_target.begin(), tiles_target.end());
+  fz.targets_off = push(targets.data(), targets.size() * sizeof(int));
+  // replace: GEMM -> FUSED; drop the absorbed formation / assembly launches
+  launches[ig] = fz;
+  std::vector<Launch> keep;
+  for (int q = 0; q < (int)launches.size(); ++q)
+    if (q != ia && q != ib && q != ias) keep.push_back(launches[q]);
+  launches.swap(keep);
 }
 
 namespace {
@@ -600,6 +800,8 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
   p->device = device;
   FMM_CUDA(cudaSetDevice(device));
   if (const char* e = getenv("FMM_NO_TMA")) p->use_tma = !(e[0] == '1');
+  p->fuse = p->opt.fuse_leaf_level != 0;
+  if (const char* e = getenv("FMM_NO_FUSE")) p->fuse = p->fuse && !(e[0] == '1');
   p->userP = P;
   p->userQ = Q;
   p->userN = Nc;
@@ -678,7 +880,17 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
   FMM_CUDA(cudaMallocHost(&p->h_pinned, p->tab_bytes));
   FMM_CUDA(cudaEventCreateWithFlags(&p->upload_done, cudaEventDisableTiming));
   for (auto& e : p->ev) FMM_CUDA(cudaEventCreate(&e));
+  if (p->fuse && p->L >= 1) {
+    p->ctr_bytes = sizeof(unsigned long long) * (size_t)(2 + 2 * p->nodes_at[p->L - 1]);
+    FMM_CUDA(cudaMalloc(&p->d_ctr, p->ctr_bytes));
+  }
 }
+
+#define FMM_CHECK_STATUS(x)                                  \
+  do {                                                       \
+    const fmm_status_t st_ = (x);                            \
+    if (st_ != FMM_OK) throw Error(st_, "internal call failed"); \
+  } while (0)
 
 void check_ld(const fmm_plan_t* p, long long lda, long long ldb, long long ldc) {
   // user-orientation requirements (fmm.h)
@@ -730,9 +942,10 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
   if (timed) FMM_CUDA(cudaEventRecord(evs[0], stream));
   int phase = 0;  // 0 formation, 1 gemm, 2 assembly/strips
   for (const Launch& ln : sl->launches) {
-    const int ph = (ln.kind == Launch::FORM_A || ln.kind == Launch::FORM_B)                      ? 0
-                   : (ln.kind == Launch::GEMM || (ln.kind == Launch::SKINNY && ln.level == p->L)) ? 1
-                                                                                                   : 2;
+    const int ph = (ln.kind == Launch::FORM_A || ln.kind == Launch::FORM_B) ? 0
+                   : (ln.kind == Launch::GEMM || ln.kind == Launch::FUSED || (ln.kind == Launch::SKINNY && ln.level == p->L))
+                       ? 1
+                       : 2;
     if (ln.kind == Launch::SKINNY) {
       const int* ids = reinterpret_cast<const int*>(d_tab + ln.ids_off);
       if (timed && ph != phase) {
@@ -756,6 +969,25 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
         break;
       case Launch::SKINNY:
         break;
+      case Launch::FUSED: {
+        FusedArgs fa{};
+        fa.base = d_tab;
+        fa.blob = d_tab + ln.progs_off;
+        fa.blob_bytes = ln.blob_bytes;
+        fa.nprogs = ln.nprogs;
+        fa.jobs = reinterpret_cast<const FusedJob*>(d_tab + ln.jobs_off);
+        fa.njobs0 = ln.njobs0;
+        fa.njobs = ln.njobs;
+        fa.ctr = p->d_ctr;
+        fa.ready_target = reinterpret_cast<const int*>(d_tab + ln.targets_off);
+        fa.tiles_target = fa.ready_target + ln.np;
+        fa.np = ln.np;
+        fa.gemm_ctas = ln.gemm_ctas;
+        FMM_CUDA(cudaMemsetAsync(p->d_ctr, 0, p->ctr_bytes, stream));
+        gemm_fused_launch(reinterpret_cast<const GemmTask*>(tab), d_tab + ln.maps_off, ln.count, ln.tiles, ln.bn,
+                          ln.uni_tm, ln.uni_tn, fa, stream);
+        break;
+      }
       case Launch::GEMM:
       case Launch::STRIPS:
         if (ln.tma)
@@ -785,6 +1017,7 @@ void fmm_plan_options_default(fmm_plan_options* o) {
   o->shard_count = 1;
   o->workspace_limit_bytes = 0;
   o->peel_align = 1;
+  o->fuse_leaf_level = 0;  // experimental until the fused addition CTAs beat the separate kernels
 }
 
 fmm_status_t fmm_plan_create(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels,
@@ -823,11 +1056,31 @@ fmm_status_t fmm_plan_stats(const fmm_plan_t* p, double out[8]) {
     s[2] += 8.0 * (ln.elem_reads + ln.elem_writes);
     s[3] += ln.gemm_bytes;
     s[4] += 1;
-    if (ln.kind == Launch::GEMM || (ln.kind == Launch::SKINNY && ln.level == p->L)) s[6] += ln.count;
+    if (ln.kind == Launch::GEMM || ln.kind == Launch::FUSED || (ln.kind == Launch::SKINNY && ln.level == p->L))
+      s[6] += ln.count;
     if (ln.kind == Launch::SKINNY) s[4] += (ln.nrow > 0) + (ln.ncol > 0) - 1;
   }
   s[5] = p->L;
   s[7] = 2.0 * p->userP * p->userQ * (double)p->userN - (double)p->userP * p->userN;
+  std::memcpy(out, s, sizeof(s));
+  return FMM_OK;
+  FMM_API_END
+}
+
+fmm_status_t fmm_plan_stats_ex(const fmm_plan_t* p, double out[16]) {
+  FMM_API_BEGIN
+  if (!p || !out) throw Error(FMM_E_INVALID_ARG, "null argument");
+  double s[16] = {0};
+  FMM_CHECK_STATUS(fmm_plan_stats(p, s));
+  for (const Launch& ln : p->launches) {
+    const double bytes = 8.0 * (ln.elem_reads + ln.elem_writes);
+    const bool leaf = ln.kind == Launch::GEMM || ln.kind == Launch::FUSED || (ln.kind == Launch::SKINNY && ln.level == p->L);
+    if (leaf) s[8] += ln.flops;
+    if (ln.kind == Launch::FUSED) s[9] += bytes, s[10] += 1;
+    if (ln.kind == Launch::FORM_A || ln.kind == Launch::FORM_B) s[11] += bytes;
+    if (ln.kind == Launch::ASSEMBLE) s[12] += bytes;
+    if (!leaf && (ln.kind == Launch::STRIPS || ln.kind == Launch::SKINNY)) s[13] += ln.flops;
+  }
   std::memcpy(out, s, sizeof(s));
   return FMM_OK;
   FMM_API_END

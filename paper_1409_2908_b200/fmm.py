@@ -29,7 +29,8 @@ class FmmError(RuntimeError):
 class _Options(ctypes.Structure):
     _fields_ = [("layout", ctypes.c_int), ("strategy", ctypes.c_int), ("cse", ctypes.c_int),
                 ("shard_rank", ctypes.c_int), ("shard_count", ctypes.c_int),
-                ("workspace_limit_bytes", ctypes.c_size_t), ("peel_align", ctypes.c_int)]
+                ("workspace_limit_bytes", ctypes.c_size_t), ("peel_align", ctypes.c_int),
+                ("fuse_leaf_level", ctypes.c_int)]
 
 
 def _load():
@@ -47,6 +48,7 @@ def _load():
         "fmm_plan": [vp, i64, i64, i64, i32, ctypes.POINTER(vp)],
         "fmm_plan_workspace_bytes": [vp, ctypes.POINTER(ctypes.c_size_t)],
         "fmm_plan_stats": [vp, ctypes.POINTER(dp)],
+        "fmm_plan_stats_ex": [vp, ctypes.POINTER(dp)],
         "fmm_execute": [vp, vp, i64, vp, i64, vp, i64, vp],
         "fmm_exec": [vp, vp, vp, vp],
         "fmm_execute_timed": [vp, vp, i64, vp, i64, vp, i64, vp, ctypes.POINTER(ctypes.c_float)],
@@ -160,7 +162,8 @@ class Plan:
 
     def __init__(self, alg: Algorithm, P: int, Q: int, N: int, levels: int, layout: str = "row",
                  strategy: str = "streaming", cse: bool = True, shard_rank: int = 0, shard_count: int = 1,
-                 device: Optional[int] = None, workspace_limit_bytes: int = 0, peel_align: bool = True):
+                 device: Optional[int] = None, workspace_limit_bytes: int = 0, peel_align: bool = True,
+                 fuse: bool = False):
         import torch
         self.alg, self.P, self.Q, self.N, self.levels = alg, P, Q, N, levels
         self.layout = ROW_MAJOR if layout == "row" else COL_MAJOR
@@ -172,6 +175,7 @@ class Plan:
         o.shard_rank, o.shard_count = shard_rank, shard_count
         o.workspace_limit_bytes = workspace_limit_bytes
         o.peel_align = int(bool(peel_align))
+        o.fuse_leaf_level = int(bool(fuse))
         self.device = torch.cuda.current_device() if device is None else device
         h = ctypes.c_void_p()
         _check(_lib.fmm_plan_create(alg._h, P, Q, N, levels, ctypes.byref(o), self.device, ctypes.byref(h)))
@@ -189,9 +193,10 @@ class Plan:
         return b.value
 
     def stats(self) -> dict:
-        s = (ctypes.c_double * 8)()
-        _check(_lib.fmm_plan_stats(self._h, s))
-        keys = ["gemm_flops", "add_flops", "add_bytes", "gemm_bytes", "launches", "levels", "leaves", "paper_flops"]
+        s = (ctypes.c_double * 16)()
+        _check(_lib.fmm_plan_stats_ex(self._h, s))
+        keys = ["gemm_flops", "add_flops", "add_bytes", "gemm_bytes", "launches", "levels", "leaves", "paper_flops",
+                "leaf_flops", "fused_add_bytes", "fused_launches", "formation_bytes", "assembly_bytes", "strip_flops"]
         return dict(zip(keys, list(s)))
 
     def new_output(self):
