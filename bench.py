@@ -172,7 +172,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fuse", type=int, default=0, help="fused leaf level (formation/GEMM/assembly in one launch)")
-    ap.add_argument("--no-unfused", action="store_true", help="skip the separate-kernel addition measurement")
+    ap.add_argument("--no-other", action="store_true", help="skip timing the other leaf-level schedule (fused vs separate)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -259,37 +259,34 @@ def main():
     sep_bytes = st["add_bytes"] - st["fused_add_bytes"]
     add_gbs = sep_bytes / (add_ms * 1e-3) / 1e9 if add_ms > 0 else None
 
-    # the same workload with separate formation / GEMM / assembly kernels: the addition kernels'
-    # own HBM roofline (every level's K1 / K3 kernels timed by phase events)
-    unfused = None
-    if fused and not args.no_unfused:
-        plan_u = F.Plan(alg, P, Q, N, L, layout=w["layout"], strategy=args.strategy, cse=bool(args.cse),
-                        shard_rank=rank, shard_count=world, fuse=False)
-        su = plan_u.stats()
+    # the other leaf-level schedule on the same workload: with --fuse 0 (default) the fused
+    # leaf-level launch (level-L formation / leaf GEMM / level-L assembly in one cooperative
+    # kernel, addition CTAs on their own SMs), with --fuse 1 the separate kernels
+    other = None
+    if not args.no_other and L >= 1:
+        plan_o = F.Plan(alg, P, Q, N, L, layout=w["layout"], strategy=args.strategy, cse=bool(args.cse),
+                        shard_rank=rank, shard_count=world, fuse=not fused)
+        so = plan_o.stats()
         for _ in range(2):
-            plan_u.execute(A, B, C, stream=stream)
+            plan_o.execute(A, B, C, stream=stream)
         nu = max(3, min(args.steps, 10))
         evu = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nu)]
         for e in (x for row in evu for x in row):
             e.record(stream)  # creates the underlying cudaEvent_t
         torch.cuda.synchronize()
         for k in range(nu):
-            plan_u.execute_events(A, B, C, evu[k], stream=stream)
+            plan_o.execute_events(A, B, C, evu[k], stream=stream)
         torch.cuda.synchronize()
         phu = np.array([[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]),
                          e[0].elapsed_time(e[3])] for e in evu]).mean(axis=0)
-        add_u = float(phu[0] + phu[2])
-        gbs_u = su["add_bytes"] / (add_u * 1e-3) / 1e9
-        unfused = {"ms_per_step": float(phu[3]), "value": flops / (phu[3] * 1e-3) / 1e9,
-                   "phases_ms": {"formation": float(phu[0]), "leaf_gemm": float(phu[1]), "assembly_and_strips": float(phu[2])},
-                   "additions": {"algorithmic_bytes_per_step": su["add_bytes"], "achieved_gbs": gbs_u, "peak_gbs": hbm,
-                                 "frac": gbs_u / hbm, "peak_source": peak_src,
-                                 "kernels": "NVRTC-generated K1 formation / K3 assembly (streaming, CSE)"},
-                   "leaf_gemm_tflops": su["leaf_flops"] / (phu[1] * 1e-3) / 1e12,
-                   "launches": su["launches"]}
-        del plan_u
-        # one more fused pass so C holds the headline path's result
-        plan.execute(A, B, C, stream=stream)
+        o_fused = so.get("fused_launches", 0) > 0
+        other = {"fused_leaf_level": o_fused, "ms_per_step": float(phu[3]), "value": flops / (phu[3] * 1e-3) / 1e9,
+                 "steps": nu, "phases_ms": {"formation": float(phu[0]), "leaf_level": float(phu[1]),
+                                            "assembly_and_strips": float(phu[2])},
+                 "launches": so["launches"]}
+        del plan_o
+        plan.execute(A, B, C, stream=stream)  # C holds the headline path's result again
+
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -398,7 +395,7 @@ def main():
                           "bytes_in_fused_launch": st["fused_add_bytes"],
                           "separate_kernel_bytes": sep_bytes, "separate_kernel_gbs": add_gbs, "peak_gbs": hbm,
                           "separate_kernel_frac": (add_gbs / hbm) if add_gbs else None, "peak_source": peak_src},
-            "unfused": unfused,
+            "other_schedule": other,
             "fp64_peak_tflops": {"dmma_measured": dmma_peak, "dfma_measured": dfma_peak, "nameplate": 37.2},
             "effective_frac_of_fp64_peak": value / 1e3 / dmma_peak,
             "cublas_dgemm_gflops_same_inputs": cub,

@@ -150,6 +150,11 @@ fmm_status_t fmm_plan_stats(const fmm_plan_t* plan, double out[8]);
    [14..15] 0 (reserved) */
 fmm_status_t fmm_plan_stats_ex(const fmm_plan_t* plan, double out[16]);
 
+/* Host-only check (no device work): generate and NVRTC-compile, for sm_100a, the fused
+   leaf-level kernel of `alg` (fuse_leaf_level = 1) for the given layout, CSE setting and GEMM tile
+   width (128, 112, 96, 80 or 64).  FMM_E_CUDA with the compiler log on failure. */
+fmm_status_t fmm_fused_compile_check(const fmm_alg* alg, int layout, int cse, int bn);
+
 /* Execute C <- A*B (beta = 0: C is overwritten).  A, B, C are device pointers on the plan's
    device laid out per opt->layout; C must not alias A or B.  Leading dimensions in elements:
    row-major lda >= Q, ldb >= Nc, ldc >= Nc; column-major lda >= P, ldb >= Q, ldc >= P.

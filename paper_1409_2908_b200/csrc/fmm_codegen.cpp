@@ -19,6 +19,8 @@
 #include <nvrtc.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <functional>
 #include <map>
@@ -30,16 +32,6 @@
 #include "fmm_internal.h"
 
 namespace fmm {
-
-struct LincombKernel {
-  LincombSpec spec;
-  std::string source;
-  cudaLibrary_t lib = nullptr;
-  cudaKernel_t kern = nullptr;
-  int threads = 128;
-  LincombCost cost{};
-  int temps = 0;
-};
 
 size_t lincomb_node_bytes(int nin, int nout) { return sizeof(void*) * (size_t)(nin + nout) + 2 * sizeof(long long); }
 
@@ -92,6 +84,21 @@ Program build_program(const LincombSpec& s) {
   }
   return p;
 }
+
+}  // namespace
+
+struct LincombKernel {
+  LincombSpec spec;
+  Program prog;  // the chains the kernel evaluates (with CSE temporaries when enabled)
+  std::string source;
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kern = nullptr;
+  int threads = 128;
+  LincombCost cost{};
+  int temps = 0;
+};
+
+namespace {
 
 std::string dlit(double c) {
   std::ostringstream ss;
@@ -236,6 +243,7 @@ std::shared_ptr<LincombKernel> lincomb_get(const LincombSpec& spec) {
   Program p = build_program(spec);
   k->temps = (int)p.temps.size();
   k->source = generate(spec, p, k->cost);
+  k->prog = p;
   std::lock_guard<std::mutex> lock(g_mu);
   auto it = g_cache.find(k->source);
   if (it != g_cache.end()) return it->second;
@@ -258,7 +266,189 @@ void lincomb_launch(const LincombKernel& k, const void* d_nodes, int nnodes, lon
   FMM_CUDA(cudaLaunchKernel((const void*)k.kern, grid, dim3(k.threads), args, 0, stream));
 }
 
+// ---- the fused leaf-level kernel (NVRTC) -----------------------------------------------------
+#include "fmm_embed.inc"  // kFmmDeviceSrc, kFmmCoreSrc: fmm_device.cuh, fmm_gemm_core.cuh verbatim
+
+struct FusedKernel {
+  std::string source;
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kern = nullptr;
+  int bn = 128;
+  int smem_set = -1;  // device on which the dynamic shared-memory limit was raised
+};
+
+namespace {
+
+// One addition program as a warp-job function: rows [row0, row0 + nrows) of the node's blocks,
+// lanes striding over element positions (V doubles each); per position every input is loaded once
+// (L2-coherent: assembly inputs are written by other SMs during the launch), the chains (with the
+// program's CSE temporaries) run in registers, every output is stored once -- the streaming K1/K3
+// kernel body, so the fused and the separate paths give bit-identical results.
+void emit_job_fn(std::ostringstream& o, const std::string& name, const LincombSpec& spec, const Program& p, int V) {
+  const int nin = spec.nin, nout = spec.nout;
+  const std::string T = V == 2 ? "double2" : "double";
+  std::vector<std::string> comps = V == 2 ? std::vector<std::string>{".x", ".y"} : std::vector<std::string>{""};
+  auto var = [&](int v) { return v < nin ? "x" + std::to_string(v) : "t" + std::to_string(v - nin); };
+  std::set<int> used;
+  for (const auto& e : p.outs)
+    for (const auto& kv : e)
+      if (kv.first < nin) used.insert(kv.first);
+  for (const auto& t : p.temps) {
+    if (std::get<0>(t) < nin) used.insert(std::get<0>(t));
+    if (std::get<1>(t) < nin) used.insert(std::get<1>(t));
+  }
+  o << "__device__ __forceinline__ void " << name << "(const char* nd, int row0, int nrows, int cols, int lane, unsigned sp) {\n";
+  // the node's in[], out[], ld_in, ld_out -> the warp's shared slot; read back per element group
+  o << "  for (int w = lane; w < " << nin + nout + 2 << "; w += 32) sts_u64(sp + 8u * w, reinterpret_cast<const unsigned long long*>(nd)[w]);\n";
+  o << "  __syncwarp();\n";
+  o << "  const long long ldi = (long long)lds_u64(sp + " << 8 * (nin + nout) << "u), ldo = (long long)lds_u64(sp + " << 8 * (nin + nout + 1) << "u);\n";
+  o << "  const int cvec = cols / " << V << ";\n";
+  o << "  for (int row = row0; row < row0 + nrows; ++row) {\n";
+  o << "    const long long bi = (long long)row * ldi, bo = (long long)row * ldo;\n";
+  // U element groups per lane per iteration: more loads in flight, within ~96 data registers
+  const int U = std::max(1, std::min(4, 96 / (2 * V * std::max<int>(1, (int)used.size()))));
+  o << "    for (int cv = lane; cv < cvec; cv += " << 32 * U << ") {\n";
+  for (int u = 0; u < U; ++u) {
+    o << "    const bool ok" << u << " = cv + " << 32 * u << " < cvec;\n";
+    o << "    const long long pi" << u << " = bi + (long long)(cv + " << 32 * u << ") * " << V << ", po" << u
+      << " = bo + (long long)(cv + " << 32 * u << ") * " << V << ";\n";
+  }
+  const std::string zero = V == 2 ? "make_double2(0.0, 0.0)" : "0.0";
+  for (int u = 0; u < U; ++u)
+    for (int i : used)
+      o << "    const " << T << " x" << i << "_" << u << " = ok" << u << " ? " << (V == 2 ? "ldcg2" : "ldcg1")
+        << "(reinterpret_cast<const double*>(lds_u64(sp + " << 8 * i << "u)) + pi" << u << ") : " << zero << ";\n";
+  for (int u = 0; u < U; ++u) {
+    auto varu = [&](int v) { return var(v) + "_" + std::to_string(u); };
+    for (size_t t = 0; t < p.temps.size(); ++t) {
+      const int a = std::get<0>(p.temps[t]), b = std::get<1>(p.temps[t]);
+      const double r = std::get<2>(p.temps[t]);
+      o << "    " << T << " t" << t << "_" << u << ";\n";
+      for (auto& c : comps) {
+        const std::string d = "t" + std::to_string(t) + "_" + std::to_string(u) + c;
+        if (r == 1.0) o << "    " << d << " = " << varu(a) << c << " + " << varu(b) << c << ";\n";
+        else if (r == -1.0) o << "    " << d << " = " << varu(a) << c << " - " << varu(b) << c << ";\n";
+        else o << "    " << d << " = " << varu(a) << c << " + " << dlit(r) << " * " << varu(b) << c << ";\n";
+      }
+    }
+    for (int q = 0; q < nout; ++q) {
+      o << "    if (double* oq = reinterpret_cast<double*>(lds_u64(sp + " << 8 * (nin + q) << "u))) {\n    " << T << " y;\n";
+      for (auto& c : comps) emit_chain(o, "y", p.outs[q], c, varu);
+      o << "    if (ok" << u << ") *reinterpret_cast<" << T << "*>(oq + po" << u << ") = y;\n    }\n";
+    }
+  }
+  o << "    }\n  }\n  __syncwarp();  // every lane is done with the slot before the next job rewrites it\n}\n";
+}
+
+std::string strip_pragma_once(const char* src) {
+  std::string s(src);
+  const std::string key = "#pragma once";
+  for (size_t at; (at = s.find(key)) != std::string::npos;) s.erase(at, key.size());
+  return s;
+}
+
+std::mutex g_fmu;
+std::map<std::string, std::shared_ptr<FusedKernel>> g_fcache;
+
+}  // namespace
+
+std::string fused_generate(const std::vector<LincombSpec>& specs, int bn) {
+  if (specs.empty() || (int)specs.size() > FUSED_MAX_PROGS) throw Error(FMM_E_INVALID_ARG, "fused: bad program count");
+  int wgm = 0, wgn = 0;
+  gemm_bn_config(bn, &wgm, &wgn);
+  std::ostringstream o;
+  o << "// generated by fmm_codegen.cpp: fused leaf level, BN=" << bn << "\n#define FMM_NVRTC 1\n";
+  if (const char* e = getenv("FMM_FUSED_LD")) o << "#define FMM_LD_KIND " << atoi(e) << "\n";  // diagnostics
+  o << strip_pragma_once(kFmmDeviceSrc) << "\n" << strip_pragma_once(kFmmCoreSrc) << "\nnamespace fmm {\n";
+  for (size_t q = 0; q < specs.size(); ++q) {
+    if (specs[q].strategy != FMM_ADD_STREAMING) throw Error(FMM_E_INVALID_ARG, "fused: streaming programs only");
+    const Program prog = build_program(specs[q]);
+    emit_job_fn(o, "prog" + std::to_string(q) + "_v2", specs[q], prog, 2);
+    emit_job_fn(o, "prog" + std::to_string(q) + "_v1", specs[q], prog, 1);
+  }
+  o << "__device__ void fmm_add_job(const FusedArgs& fa, const FusedJob& j, int lane, unsigned sp) {\n";
+  o << "  const char* nd = fa.node_tab[j.prog] + (long long)j.node * fa.node_bytes[j.prog];\n";
+  o << "  switch (j.prog) {\n";
+  for (size_t q = 0; q < specs.size(); ++q)
+    o << "    case " << q << ": if (fa.vec2[" << q << "]) prog" << q << "_v2(nd, j.row0, j.nrows, fa.cols[" << q
+      << "], lane, sp); else prog" << q << "_v1(nd, j.row0, j.nrows, fa.cols[" << q << "], lane, sp); break;\n";
+  o << "  }\n}\n}  // namespace fmm\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(fmm::THREADS, 1)\n"
+       "fmm_fused(const fmm::GemmTask* __restrict__ tasks, const fmm::CUtensorMap* __restrict__ maps, int ntasks,\n"
+       "          int total_tiles, fmm::Uniform uni, fmm::FusedArgs fa) {\n"
+    << "  fmm::gemm_body<" << bn << ", " << wgm << ", " << wgn << ", true>(tasks, maps, ntasks, total_tiles, uni, fa);\n}\n";
+  return o.str();
+}
+
+std::vector<char> fused_compile(const std::string& source) {
+  if (const char* path = getenv("FMM_FUSED_DUMP")) {  // diagnostics: keep the generated source
+    if (FILE* f = fopen(path, "w")) fputs(source.c_str(), f), fclose(f);
+  }
+  nvrtcProgram prog;
+  NVRTC_CHECK(nvrtcCreateProgram(&prog, source.c_str(), "fmm_fused.cu", 0, nullptr, nullptr));
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "--fmad=false", "-lineinfo"};
+  nvrtcResult r = nvrtcCompileProgram(prog, 4, opts);
+  if (r != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    nvrtcGetProgramLog(prog, &log[0]);
+    nvrtcDestroyProgram(&prog);
+    throw Error(FMM_E_CUDA, "NVRTC compile of the fused kernel failed: " + log);
+  }
+  size_t n = 0;
+  NVRTC_CHECK(nvrtcGetCUBINSize(prog, &n));
+  std::vector<char> cubin(n);
+  NVRTC_CHECK(nvrtcGetCUBIN(prog, cubin.data()));
+  nvrtcDestroyProgram(&prog);
+  return cubin;
+}
+
+std::shared_ptr<FusedKernel> fused_get(const std::vector<LincombSpec>& specs, int bn) {
+  auto k = std::make_shared<FusedKernel>();
+  k->source = fused_generate(specs, bn);
+  k->bn = bn;
+  std::lock_guard<std::mutex> lock(g_fmu);
+  auto it = g_fcache.find(k->source);
+  if (it != g_fcache.end()) return it->second;
+  const std::vector<char> cubin = fused_compile(k->source);
+  FMM_CUDA(cudaLibraryLoadData(&k->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+  FMM_CUDA(cudaLibraryGetKernel(&k->kern, k->lib, "fmm_fused"));
+  g_fcache[k->source] = k;
+  return k;
+}
+
+void fused_launch(const FusedKernel& k, const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles,
+                  int uniform_tm, int uniform_tn, const FusedArgs& fa, cudaStream_t stream) {
+  const int smem = gemm_tma_smem_bytes(k.bn) + FUSED_PTR_BYTES;
+  int dev = 0;
+  FMM_CUDA(cudaGetDevice(&dev));
+  if (k.smem_set != dev) {
+    FMM_CUDA(cudaKernelSetAttributeForDevice(k.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem, dev));
+    const_cast<FusedKernel&>(k).smem_set = dev;
+  }
+  // every CTA must be resident (jobs wait on tiles, tiles on jobs): cooperative, one CTA per SM
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)gemm_sm_count());
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  Uniform uni{uniform_tm * uniform_tn, uniform_tm, uniform_tn};
+  int nt = ntasks, tt = (int)total_tiles;
+  FusedArgs a = fa;
+  void* args[] = {(void*)&d_tasks, (void*)&d_maps, &nt, &tt, &uni, &a};
+  FMM_CUDA(cudaLaunchKernelExC(&cfg, (const void*)k.kern, args));
+}
+
+std::string fused_source(const FusedKernel& k) { return k.source; }
+
 LincombCost lincomb_cost(const LincombKernel& k) { return k.cost; }
+const LincombSpec& lincomb_spec(const LincombKernel& k) { return k.spec; }
 int lincomb_cse_temps(const LincombKernel& k) { return k.temps; }
 std::string lincomb_source(const LincombKernel& k) { return k.source; }
 

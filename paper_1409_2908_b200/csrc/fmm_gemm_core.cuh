@@ -1,0 +1,391 @@
+// GEMM core of K2 (and of the fused leaf level): persistent, warp-specialised grouped FP64 GEMM
+// fed by TMA.  Included by fmm_gemm_tma.cu (nvcc, the plain kernels) and embedded verbatim into
+// the NVRTC source of the fused leaf-level kernel (fmm_codegen.cpp), so it has no includes.
+//
+// Per CTA (one per SM, looping over tiles):
+//   warpgroup 0 (producer): one thread issues cp.async.bulk.tensor (TMA) loads of the A tile
+//       (one 128x16 box) and the B tile (BN/16 boxes of 16x16) per k-step into a 6-stage ring of
+//       shared-memory buffers as soon as a stage is released, signalling a "full" mbarrier with
+//       complete_tx; it runs over the CTA's whole (tile, k-step) sequence, so the next tile's
+//       loads are in flight while the current tile's epilogue runs.  It gives its registers
+//       away with setmaxnreg.dec (40), so the consumers can grow to 232 (setmaxnreg.inc) --
+//       the 64x32 warp tile needs ~210, above the 168 a flat 384-thread launch would allow.
+//   warpgroups 1-2 (consumers): 8 warps of (128/WGM) x (BN/WGN) outputs; wait "full", read
+//       register fragments, issue mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4), arrive "empty";
+//       epilogue straight from registers with 16-byte stores.  No CTA-wide barrier in the loop.
+// TMA writes the tiles with the 128-byte swizzle (16-byte chunk index XOR row mod 8).  The DMMA
+// fragment pattern (lane -> row lane/4, col lane%4 for A; row lane%4, col lane/4 for B) would hit
+// 2- or 4-way bank conflicts on that layout, so fragment rows and columns are mapped to tile rows
+// and columns by fixed permutations chosen to make every 8-byte fragment load conflict-free:
+//   A: fragment row r of m-subtile i  -> tile row 16*(i/2) + 2r + (i%2)
+//   B: fragment col j of n-subtile jj -> tile col 16*(jj/2) + 4*(jj%2) + {0,1,8,9,2,3,10,11}[j]
+// The epilogue writes each accumulator to the tile position its operands came from.
+//
+// FUSED (NVRTC only): the level-L formation (F) and assembly (A) jobs of a plan run in the same
+// launch, spatially partitioned: CTAs [0, gemm_ctas) run leaf tiles exactly as above, CTAs
+// [gemm_ctas, gridDim.x) are addition CTAs whose 12 warps run the plan's generated addition
+// chains (fmm_add_job, straight-line code from fmm_codegen.cpp).  They must not share an SM: the
+// FP64 ALU (DADD) and the DMMA path are one pipe on B200, and a DADD warp beside eight DMMA warps
+// was measured to crawl.  Every warp of the GPU first drains the phase-0 jobs (formation of the
+// first parent: nothing can start before it); the TMA thread waits for ready[parent] before the
+// first load of a tile; consumers count each stored tile into tiles_done[parent] and, out of
+// tiles, join the phase-1 queue.  All CTAs must be co-resident (cooperative launch, grid = #SMs):
+// jobs wait on tiles and tiles on jobs.
+#pragma once
+
+namespace fmm {
+
+#ifdef FMM_NVRTC
+struct alignas(64) CUtensorMap_opaque {
+  unsigned long long opaque[16];
+};
+typedef CUtensorMap_opaque CUtensorMap;
+#endif
+
+constexpr int BM = 128, BK = 16;
+constexpr int GEMM_STAGES = 6;
+constexpr int CONSUMERS = 8, THREADS = 128 + CONSUMERS * 32;  // warpgroup 0 = producer, 1-2 = consumers
+static_assert(THREADS == GEMM_THREADS, "host and device agree on the block size");
+constexpr int A_BYTES = BM * BK * 8;                           // 16 KB
+__host__ __device__ constexpr int gemm_smem_bytes(int bn) { return GEMM_STAGES * (A_BYTES + BK * bn * 8) + 1024 /*align*/ + 256 /*barriers*/; }
+__host__ __device__ constexpr int fused_smem_bytes(int bn) { return gemm_smem_bytes(bn) + FUSED_PTR_BYTES; }
+constexpr int GROUP_M = 8;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map, int c0, int c1, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double lds64(unsigned addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ unsigned long long lds_u64(unsigned addr) {
+  unsigned long long v;
+  asm volatile("ld.shared.u64 %0, [%1];\n" : "=l"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts_u64(unsigned addr, unsigned long long v) {
+  asm volatile("st.shared.u64 [%0], %1;\n" ::"r"(addr), "l"(v) : "memory");
+}
+// Loads of the addition jobs.  Assembly inputs are written by other SMs during this kernel; the
+// job's lane 0 acquires the tile counter first (ld.acquire.gpu, which invalidates this SM's L1)
+// and the warp synchronises, so weak loads after it see the stored tiles.  FMM_LD_KIND selects the
+// flavour: 0 = ld.global.cg (L2 only), 1 = ld.global (L1-allocating), 2 = ld.global.nc.
+#ifndef FMM_LD_KIND
+#define FMM_LD_KIND 0
+#endif
+__device__ __forceinline__ double2 ldcg2(const double* p) {
+  double2 v;
+#if FMM_LD_KIND == 0
+  asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "l"(p));
+#elif FMM_LD_KIND == 1
+  v = *reinterpret_cast<const double2*>(p);
+#else
+  v = __ldg(reinterpret_cast<const double2*>(p));
+#endif
+  return v;
+}
+__device__ __forceinline__ double ldcg1(const double* p) {
+  double v;
+#if FMM_LD_KIND == 0
+  asm volatile("ld.global.cg.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
+#elif FMM_LD_KIND == 1
+  v = *p;
+#else
+  v = __ldg(p);
+#endif
+  return v;
+}
+
+struct TileCoord {
+  int task, m0, n0;
+};
+template <int BN>
+__device__ __forceinline__ TileCoord locate(const GemmTask* __restrict__ tasks, int ntasks, int tile, Uniform u) {
+  int lo, tiles_m, tiles_n, local;
+  if (u.tiles) {
+    lo = tile / u.tiles;
+    local = tile - lo * u.tiles;
+    tiles_m = u.tiles_m;
+    tiles_n = u.tiles_n;
+  } else {
+    lo = 0;
+    int hi = ntasks - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (__ldg(&tasks[mid].tile_begin) <= tile) lo = mid; else hi = mid - 1;
+    }
+    tiles_m = __ldg(&tasks[lo].tiles_m);
+    tiles_n = __ldg(&tasks[lo].tiles_n);
+    local = tile - __ldg(&tasks[lo].tile_begin);
+  }
+  const int span = GROUP_M * tiles_n;
+  const int group = local / span;
+  const int first_m = group * GROUP_M;
+  const int gsize = min(tiles_m - first_m, GROUP_M);
+  const int tm = first_m + (local % span) % gsize;
+  const int tn = (local % span) / gsize;
+  return {lo, tm * BM, tn * BN};
+}
+
+
+__device__ __forceinline__ int claim(unsigned long long* ctr, int lane) {
+  int idx = 0;
+  if (lane == 0) idx = (int)atomicAdd(ctr, 1ull);
+  return __shfl_sync(0xffffffffu, idx, 0);
+}
+
+// Generated per algorithm (fmm_codegen.cpp) in the NVRTC source of the fused kernel.
+// sp: shared address of the warp's FUSED_PTR_SLOT for the job's node pointers.
+__device__ void fmm_add_job(const FusedArgs& fa, const FusedJob& j, int lane, unsigned sp);
+
+// One job with a whole warp: assembly jobs first wait until every leaf tile of their parent is
+// stored; formation jobs publish (release) to the TMA readers of the leaf products.
+__device__ __forceinline__ void run_job(const FusedArgs& fa, int jidx, int lane, unsigned sp) {
+  const FusedJob j = fa.jobs[jidx];
+  if (j.kind == 1) {
+    if (lane == 0) {
+      const unsigned long long target = (unsigned long long)__ldg(&fa.tiles_target[j.dep]);
+      while (ld_acquire(&fa.ctr[2 + fa.np + j.dep]) < target) __nanosleep(256);
+    }
+    __syncwarp();
+  }
+  fmm_add_job(fa, j, lane, sp);
+  if (j.kind == 0) {
+    fence_proxy_async_global();
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) atomicAdd(&fa.ctr[2 + j.dep], 1ull);
+  }
+}
+
+template <int BN, int WGM, int WGN, bool FUSED>
+__device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, const CUtensorMap* __restrict__ maps,
+                                          int ntasks, int total_tiles, Uniform uni, const FusedArgs& fa) {
+  constexpr int STAGES = GEMM_STAGES;
+  static_assert(WGM * WGN == CONSUMERS, "8 consumer warps");
+  constexpr int WTM = BM / WGM, WTN = BN / WGN;
+  static_assert(WTM % 16 == 0 && WTN % 16 == 0, "warp tile must be a multiple of 16");
+  constexpr int MI = WTM / 8, NI = WTN / 8;
+  constexpr int B_BYTES_T = BK * BN * 8;  // BN/16 boxes of 16 x 16
+  constexpr int STAGE_T = A_BYTES + B_BYTES_T;
+  extern __shared__ unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned raw = smem_u32(smem_raw);
+  const unsigned base = (raw + 1023u) & ~1023u;  // 1024-byte alignment for the 128B swizzle
+  const unsigned bars = base + STAGES * STAGE_T;
+  const unsigned sp = bars + 256u + (unsigned)warp * FUSED_PTR_SLOT;  // fused: this warp's pointer slot
+  int gemm_ctas = (int)gridDim.x;
+  if constexpr (FUSED) {
+    gemm_ctas = fa.gemm_ctas;
+    if ((int)blockIdx.x >= gemm_ctas) {
+      // ------------------------------ addition CTA ------------------------------
+      for (;;) {
+        const int idx = claim(&fa.ctr[0], lane);
+        if (idx >= fa.njobs0) break;
+        run_job(fa, idx, lane, sp);
+      }
+      for (;;) {
+        const int idx = claim(&fa.ctr[1], lane);
+        if (fa.njobs0 + idx >= fa.njobs) break;
+        run_job(fa, fa.njobs0 + idx, lane, sp);
+      }
+      return;
+    }
+  }
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), CONSUMERS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp < 4) {
+    // ------------------------------ producer warpgroup ------------------------------
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    if (warp == 0 && lane == 0) {
+      int stage = 0;
+      unsigned phase = 0;
+      int ready_node = -1;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gemm_ctas) {
+        const TileCoord tc = locate<BN>(tasks, ntasks, tile, uni);
+        if constexpr (FUSED) {
+          const int node = __ldg(&tasks[tc.task].node);
+          if (node != ready_node) {
+            const unsigned long long target = (unsigned long long)__ldg(&fa.ready_target[node]);
+            while (ld_acquire(&fa.ctr[2 + node]) < target) __nanosleep(128);
+            fence_proxy_async_global();
+            ready_node = node;
+          }
+        }
+        const CUtensorMap* ma = maps + 2 * tc.task;
+        const CUtensorMap* mb = ma + 1;
+        const int KT = (__ldg(&tasks[tc.task].k) + BK - 1) / BK;
+        for (int kt = 0; kt < KT; ++kt) {
+          mbar_wait(empty_bar(stage), phase ^ 1u);
+          const unsigned sa = base + stage * STAGE_T, sb = sa + A_BYTES;
+          mbar_expect_tx(full_bar(stage), STAGE_T);
+          tma_load_2d(sa, ma, kt * BK, tc.m0, full_bar(stage));
+#pragma unroll
+          for (int b = 0; b < BN / 16; ++b) tma_load_2d(sb + b * 2048, mb, tc.n0 + 16 * b, kt * BK, full_bar(stage));
+          if (++stage == STAGES) stage = 0, phase ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+
+  // ------------------------------ consumers ------------------------------
+  if constexpr (FUSED) {
+    for (;;) {
+      const int idx = claim(&fa.ctr[0], lane);
+      if (idx >= fa.njobs0) break;
+      run_job(fa, idx, lane, sp);
+    }
+  }
+  const int cw = warp - 4;  // consumer warp 0..7
+  const int r = lane >> 2, c = lane & 3;
+  const int wm = (cw / WGN) * WTM, wn = (cw % WGN) * WTN;
+  // A fragment: subtile i, fragment row r -> tile row R = wm + 16*(i/2) + 2r + (i%2);
+  //   16-byte chunk = (2s + (c>>1)) ^ (R & 7); 8-byte half = c & 1
+  const unsigned a_row0 = (unsigned)(wm + 2 * r) * 128u;
+  const unsigned xa0 = (unsigned)((2 * r) & 7), xa1 = (unsigned)((2 * r + 1) & 7);
+  const unsigned ha = (unsigned)(c & 1) * 8u, ca = (unsigned)(c >> 1);
+  // B fragment: subtile jj, fragment col r -> box wn/16 + jj/2, box col 4*(jj%2) + map0[r];
+  //   k row = 4s + c; chunk = (box col >> 1) ^ (k row & 7)
+  const unsigned map0 = (r == 0) ? 0u : (r == 1) ? 1u : (r == 2) ? 8u : (r == 3) ? 9u : (r == 4) ? 2u : (r == 5) ? 3u : (r == 6) ? 10u : 11u;
+  const unsigned hb = map0 & 1u, cb0 = map0 >> 1;
+  const unsigned b_box0 = (unsigned)(wn / 16) * 2048u;
+
+  int stage = 0;
+  unsigned phase = 0;
+  for (int tile = blockIdx.x; tile < total_tiles; tile += gemm_ctas) {
+    const TileCoord tc = locate<BN>(tasks, ntasks, tile, uni);
+    const GemmTask& t = tasks[tc.task];
+    const int KT = (__ldg(&t.k) + BK - 1) / BK;
+    // epilogue parameters, fetched now so their latency hides behind the main loop
+    const double alpha = __ldg(&t.alpha), beta = __ldg(&t.beta);
+    const int m = __ldg(&t.m), n = __ldg(&t.n);
+    const long long ldc = __ldg(&t.ldc);
+    double* C = t.C;
+    double acc[MI][NI][2];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (int kt = 0; kt < KT; ++kt) {
+      mbar_wait(full_bar(stage), phase);
+      const unsigned sa = base + stage * STAGE_T, sb = sa + A_BYTES;
+#pragma unroll
+      for (int s = 0; s < BK / 4; ++s) {
+        double a[MI], b[NI];
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          const unsigned x = (i & 1) ? xa1 : xa0;
+          const unsigned chunk = ((unsigned)(2 * s) + ca) ^ x;
+          a[i] = lds64(sa + a_row0 + (unsigned)(16 * (i >> 1) + (i & 1)) * 128u + chunk * 16u + ha);
+        }
+        const unsigned krow = (unsigned)(4 * s + c);
+#pragma unroll
+        for (int jj = 0; jj < NI; ++jj) {
+          const unsigned chunk = (cb0 + 2u * (jj & 1)) ^ (krow & 7u);
+          b[jj] = lds64(sb + b_box0 + (unsigned)(jj >> 1) * 2048u + krow * 128u + chunk * 16u + hb * 8u);
+        }
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int jj = 0; jj < NI; ++jj) dmma(acc[i][jj], a[i], b[jj]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty_bar(stage));
+      if (++stage == STAGES) stage = 0, phase ^= 1u;
+    }
+
+    // ---- epilogue: C = alpha * acc (+ beta * C), from registers ----
+    const int cofs = (c == 0) ? 0 : (c == 1) ? 8 : (c == 2) ? 2 : 10;  // map0[2c]
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      const int row = tc.m0 + wm + 16 * (i >> 1) + 2 * r + (i & 1);
+      if (row >= m) continue;
+      double* crow = C + (long long)row * ldc;
+#pragma unroll
+      for (int jj = 0; jj < NI; ++jj) {
+        const int col = tc.n0 + wn + 16 * (jj >> 1) + 4 * (jj & 1) + cofs;
+        double v0 = alpha * acc[i][jj][0], v1 = alpha * acc[i][jj][1];
+        if (col + 1 < n) {
+          double2* p = reinterpret_cast<double2*>(crow + col);
+          if (beta != 0.0) {
+            const double2 o = *p;
+            v0 = fma(beta, o.x, v0);
+            v1 = fma(beta, o.y, v1);
+          }
+          *p = make_double2(v0, v1);
+        } else if (col < n) {
+          crow[col] = beta != 0.0 ? fma(beta, crow[col], v0) : v0;
+        }
+      }
+    }
+    if constexpr (FUSED) {  // publish the stored tile (release) to the assembly jobs of its parent
+      __threadfence();
+      named_bar_sync(1, CONSUMERS * 32);
+      if (cw == 0 && lane == 0) atomicAdd(&fa.ctr[2 + fa.np + __ldg(&t.node)], 1ull);
+    }
+  }
+  if constexpr (FUSED) {
+    for (;;) {
+      const int idx = claim(&fa.ctr[1], lane);
+      if (fa.njobs0 + idx >= fa.njobs) break;
+      run_job(fa, fa.njobs0 + idx, lane, sp);
+    }
+  }
+}
+
+}  // namespace fmm

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../../include/fmm.h"
+#include "fmm_device.cuh"
 
 namespace fmm {
 
@@ -68,17 +69,7 @@ fmm_alg* alg_transpose_prop1(const fmm_alg& a);  // Prop. 1: <N,K,M>
 void alg_validate_exact(const fmm_alg& a);        // throws FMM_E_NOT_EXACT
 
 // ---- grouped DMMA GEMM (K2 / K4 / K5) -------------------------------------------------------
-struct GemmTask {
-  const double* A;
-  const double* B;
-  double* C;
-  long long lda, ldb, ldc;
-  int m, n, k;
-  int tiles_m, tiles_n;
-  int tile_begin;  // prefix sum of tiles over the task list
-  int node;        // fused leaf-level launch: parent (level L-1) node index; -1 elsewhere
-  double alpha, beta;
-};
+// GemmTask, FusedJob, FusedArgs: fmm_device.cuh (shared with the NVRTC-compiled fused kernel)
 // Fill tiles_m/tiles_n/tile_begin; returns the total number of CTA tiles.
 long long gemm_prepare(std::vector<GemmTask>& tasks, int bm = 128, int bn = 128);
 bool gemm_tasks_aligned16(const std::vector<GemmTask>& tasks);
@@ -94,42 +85,10 @@ void gemm_tma_maps(const std::vector<GemmTask>& tasks, void* out);
 // uniform_tm/tn: the common tile grid when every task has the same one (else 0, 0).
 void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn,
                      int uniform_tm, int uniform_tn, cudaStream_t stream);
-// ---- fused leaf level (K1 level L + K2 + K3 level L in one persistent launch) ----------------
-// Addition programs run by an interpreter inside the GEMM kernel's spare warps.  A program is one
-// lincomb node table (the K1/K3 format: in[nin], out[nout], ld_in, ld_out per node) plus its chains
-// without CSE: for output o the terms [ostart[o], ostart[o+1]) of (in, coef), ascending input index.
-// The programs live in a small blob (FusedProg headers, then per program short ostart[nout+1],
-// short in[nterms], double coef[nterms]) that every CTA copies into shared memory at start.
-struct FusedProg {
-  long long node_off;  // byte offset of the node table from the launch-table base
-  int ostart_off, in_off, coef_off;  // byte offsets inside the program blob
-  int nin, nout, node_bytes;
-  int rows, cols;
-  int vec2;            // every view 16-byte aligned, even lds and cols: 16-byte / bulk-copy paths
-  int seg;             // staged segment width in doubles (multiple of 64), 0 = direct loads only
-};
-struct FusedJob {
-  int prog, node;  // program, node-table entry
-  int row0, nrows;
-  int dep;         // parent index: F jobs signal ready[dep], A jobs wait for tiles_done[dep]
-  int kind;        // 0 = formation (F), 1 = assembly (A)
-};
-struct FusedArgs {
-  const char* base;             // launch-table base (node tables)
-  const char* blob;             // program blob (global copy)
-  int blob_bytes, nprogs;
-  const FusedJob* jobs;
-  int njobs0, njobs;            // phase-0 jobs [0, njobs0), phase-1 jobs [njobs0, njobs)
-  unsigned long long* ctr;      // [0] claim0, [1] claim1, [2 + p] ready[p], [2 + np + p] tiles_done[p]
-  const int* ready_target;      // [np]
-  const int* tiles_target;      // [np]
-  int np;
-  int gemm_ctas;                // CTAs [0, gemm_ctas) run leaf tiles, the rest are addition CTAs
-};
-constexpr int FUSED_ADD_SEG_BYTES = 9216;  // per staging buffer (two per addition warp)
-constexpr int FUSED_PROG_BYTES = 6144;     // shared-memory program area
-void gemm_fused_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn,
-                       int uniform_tm, int uniform_tn, const FusedArgs& fa, cudaStream_t stream);
+// TMA kernel configuration: consumer warp grid of a tile width, SM count, dynamic shared memory.
+void gemm_bn_config(int bn, int* wgm, int* wgn);
+int gemm_sm_count();
+int gemm_tma_smem_bytes(int bn);
 // (tiles_m, tiles_n) shared by every task of a prepared list, or (0, 0).
 void gemm_uniform_grid(const std::vector<GemmTask>& tasks, int* tm, int* tn);
 // Thin products (one dimension <= skinny_limit()) on the CUDA cores (fmm_skinny.cu): ids index
@@ -168,5 +127,17 @@ struct LincombCost {
 LincombCost lincomb_cost(const LincombKernel& k);
 int lincomb_cse_temps(const LincombKernel& k);
 std::string lincomb_source(const LincombKernel& k);
+
+// The fused leaf-level kernel: the GEMM core (fmm_gemm_core.cuh) plus the plan's addition programs
+// as straight-line device code (the same chains as the K1/K3 kernels of `progs`), compiled with
+// NVRTC for one tile width; cached by source.
+struct FusedKernel;
+std::shared_ptr<FusedKernel> fused_get(const std::vector<LincombSpec>& specs, int bn);
+std::string fused_generate(const std::vector<LincombSpec>& specs, int bn);  // host only
+std::vector<char> fused_compile(const std::string& source);                  // host only (NVRTC -> cubin)
+const LincombSpec& lincomb_spec(const LincombKernel& k);
+void fused_launch(const FusedKernel& k, const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles,
+                  int uniform_tm, int uniform_tn, const FusedArgs& fa, cudaStream_t stream);
+std::string fused_source(const FusedKernel& k);
 
 }  // namespace fmm

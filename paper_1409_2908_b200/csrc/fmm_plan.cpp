@@ -60,9 +60,12 @@ struct Launch {
   double flops = 0, gemm_bytes = 0;
   std::vector<int> node_ids;  // FORM / ASSEMBLE: parent node index of every table entry
   // FUSED: byte offsets of the program / job / target tables, and their sizes
-  size_t progs_off = 0, jobs_off = 0, targets_off = 0;
-  int njobs0 = 0, njobs = 0, np = 0, blob_bytes = 0, nprogs = 0;
+  size_t jobs_off = 0, targets_off = 0;
+  int njobs0 = 0, njobs = 0, np = 0, nprogs = 0;
   int gemm_ctas = 0;  // FUSED: CTAs running leaf tiles (the rest of the grid are addition CTAs)
+  size_t prog_node_off[FUSED_MAX_PROGS] = {};
+  int prog_node_bytes[FUSED_MAX_PROGS] = {}, prog_cols[FUSED_MAX_PROGS] = {}, prog_vec2[FUSED_MAX_PROGS] = {};
+  std::shared_ptr<FusedKernel> fk;
 };
 
 long long round_up(long long x, long long m) { return (x + m - 1) / m * m; }
@@ -622,101 +625,31 @@ void fmm_plan_s::fuse_leaf_level(bool lazy_kernels) {
   }
   if (ig < 0 || ias < 0) return;
   if (!lazy_kernels && !launches[ig].tma) return;
-  const int M = alg->M, K = alg->K, Nb = alg->N;
   const long long np = nodes_at[L - 1];
   Launch fz = launches[ig];
   fz.kind = Launch::FUSED;
   fz.np = (int)np;
-  // programs: headers, then per program short ostart[nout+1], short in[nterms], double coef[nterms]
-  std::vector<FusedProg> progs;
-  std::vector<int> prog_src;  // launch index of each program
-  std::vector<std::vector<short>> p_ostart, p_in;
-  std::vector<std::vector<double>> p_coef;
-  auto add_prog = [&](int q, int side) {
-    const Launch& ln = launches[q];
-    FusedProg p{};
-    p.node_off = (long long)ln.table_off;
-    p.nin = side == 0 ? M * K : side == 1 ? K * Nb : R;
-    p.nout = side == 0 ? (int)formU.size() : side == 1 ? (int)formV.size() : M * Nb;
-    p.node_bytes = (int)lincomb_node_bytes(p.nin, p.nout);
-    p.rows = (int)ln.rows;
-    p.cols = (int)ln.cols;
-    p.vec2 = ln.aligned16 ? 1 : 0;
-    const int segmax = FUSED_ADD_SEG_BYTES / (8 * p.nin);
-    p.seg = p.vec2 && p.nin <= 32 && segmax >= 32 ? std::min(512, segmax / 32 * 32) : 0;
-    if (const char* dbg = getenv("FMM_FUSE_DEBUG"))
-      if (!strcmp(dbg, "direct")) p.seg = 0;
-    // chains: coefficient rows, ascending input index
-    std::vector<short> ostart(p.nout + 1, 0), tin;
-    std::vector<double> tco;
-    double adds = 0;
-    for (int o = 0; o < p.nout; ++o) {
-      ostart[o] = (short)tin.size();
-      for (int i = 0; i < p.nin; ++i) {
-        double c = 0;
-        if (side == 0) c = alg->Ud[(size_t)i * R + formU[o]];
-        else if (side == 1) c = alg->Vd[(size_t)i * R + formV[o]];
-        else c = alg->Wd[(size_t)o * R + i];
-        if (c != 0.0) tin.push_back((short)i), tco.push_back(c);
-      }
-      if ((int)tin.size() > ostart[o]) adds += (double)tin.size() - ostart[o] - 1;
-    }
-    ostart[p.nout] = (short)tin.size();
-    progs.push_back(p);
-    prog_src.push_back(q);
-    p_ostart.push_back(ostart);
-    p_in.push_back(tin);
-    p_coef.push_back(tco);
-    // statistics of the absorbed launch with the chains actually evaluated
-    fz.elem_adds += adds * (double)ln.rows * ln.cols * ln.count;
+  // programs: the absorbed launches' node tables and chains (the same generated chains as their
+  // separate K1/K3 kernels)
+  std::vector<int> prog_src;
+  std::vector<int> sides;
+  if (ia >= 0) prog_src.push_back(ia), sides.push_back(0);
+  if (ib >= 0) prog_src.push_back(ib), sides.push_back(1);
+  prog_src.push_back(ias), sides.push_back(2);
+  fz.nprogs = (int)prog_src.size();
+  for (int q = 0; q < fz.nprogs; ++q) {
+    const Launch& ln = launches[prog_src[q]];
+    const int nin = sides[q] == 0 ? alg->M * alg->K : sides[q] == 1 ? alg->K * alg->N : R;
+    const int nout = sides[q] == 0 ? (int)formU.size() : sides[q] == 1 ? (int)formV.size() : alg->M * alg->N;
+    fz.prog_node_off[q] = ln.table_off;
+    fz.prog_node_bytes[q] = (int)lincomb_node_bytes(nin, nout);
+    fz.prog_cols[q] = (int)ln.cols;
+    fz.prog_vec2[q] = ln.aligned16 ? 1 : 0;
+    fz.elem_adds += ln.elem_adds;
     fz.elem_reads += ln.elem_reads;
     fz.elem_writes += ln.elem_writes;
-  };
-  if (ia >= 0) add_prog(ia, 0);
-  if (ib >= 0) add_prog(ib, 1);
-  add_prog(ias, 2);
-  // lay out the blob
-  size_t off = (progs.size() * sizeof(FusedProg) + 15) / 16 * 16;
-  for (size_t q = 0; q < progs.size(); ++q) {
-    progs[q].ostart_off = (int)off;
-    off += p_ostart[q].size() * sizeof(short);
-    progs[q].in_off = (int)off;
-    off += p_in[q].size() * sizeof(short);
-    off = (off + 7) / 8 * 8;
-    progs[q].coef_off = (int)off;
-    off += p_coef[q].size() * sizeof(double);
   }
-  off = (off + 15) / 16 * 16;
-  if (off > (size_t)FUSED_PROG_BYTES) return;  // programs too large for the shared-memory area
-  std::vector<char> blob(off, 0);
-  std::memcpy(blob.data(), progs.data(), progs.size() * sizeof(FusedProg));
-  for (size_t q = 0; q < progs.size(); ++q) {
-    std::memcpy(blob.data() + progs[q].ostart_off, p_ostart[q].data(), p_ostart[q].size() * sizeof(short));
-    std::memcpy(blob.data() + progs[q].in_off, p_in[q].data(), p_in[q].size() * sizeof(short));
-    std::memcpy(blob.data() + progs[q].coef_off, p_coef[q].data(), p_coef[q].size() * sizeof(double));
-  }
-  fz.blob_bytes = (int)off;
-  fz.nprogs = (int)progs.size();
-  // spatial split of the SMs: k addition CTAs (own SMs: the FP64 ALU and the DMMA path are one
-  // pipe), the rest run leaf tiles; k balances leaf flops at the per-SM DMMA rate against the
-  // absorbed addition bytes at the per-SM bulk-copy rate
-  {
-    int sms = 148, dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-      sms = 148;
-    cudaGetLastError();
-    const double bytes = 8.0 * (fz.elem_reads + fz.elem_writes), fl = fz.flops;
-    const double F_SM = 250e9, B_SM = 100e9;
-    int best_k = 1;
-    double best_t = 1e300;
-    for (int k = 1; k <= sms / 3; ++k) {
-      const double t = std::max(fl / ((sms - k) * F_SM), bytes / (k * B_SM));
-      if (t < best_t) best_t = t, best_k = k;
-    }
-    if (const char* e = getenv("FMM_FUSE_ADD_CTAS")) best_k = std::max(1, std::min(sms - 1, atoi(e)));
-    fz.gemm_ctas = sms - best_k;
-  }
-  const int pA = (int)progs.size() - 1;
+  const int pA = fz.nprogs - 1;
   // jobs per parent; phase 0 = formation of the parent of the first leaf product in tile order
   const GemmTask* tk = reinterpret_cast<const GemmTask*>(h_tab.data() + fz.table_off);
   const int first_node = fz.count > 0 ? tk[0].node : -1;
@@ -724,20 +657,17 @@ void fmm_plan_s::fuse_leaf_level(bool lazy_kernels) {
   for (int q = 0; q < fz.count; ++q)
     if (tk[q].node >= 0 && tk[q].node < np) tiles_target[tk[q].node] += tk[q].tiles_m * tk[q].tiles_n;
   std::vector<std::vector<FusedJob>> fjobs0(np), fjobs(np), ajobs(np);
-  for (int pi = 0; pi < (int)progs.size(); ++pi) {
+  for (int pi = 0; pi < fz.nprogs; ++pi) {
     const Launch& ln = launches[prog_src[pi]];
-    const FusedProg& p = progs[pi];
     const bool is_a = pi == pA;
     for (int e = 0; e < (int)ln.node_ids.size(); ++e) {
       const int zp = ln.node_ids[e];
       const bool first = !is_a && zp == first_node;
-      // job size: a few staged pieces (segments of one row), so that one parent's jobs spread
-      // over every worker warp and a job never outlasts a small fraction of the parent's GEMM
-      const int cols = std::max(1, p.cols);
-      const int pieces_per_row = p.seg > 0 ? (cols + p.seg - 1) / p.seg : (cols + 255) / 256;
-      const int per = std::max(1, (first ? 2 : 8) / pieces_per_row);
-      for (int r0 = 0; r0 < p.rows; r0 += per) {
-        FusedJob j{pi, e, r0, std::min(per, p.rows - r0), zp, is_a ? 1 : 0};
+      // a job is a few rows of one warp (about 1-4 K element positions): enough jobs per parent to
+      // spread over every addition warp, none long against the parent's share of the GEMM
+      const int per = std::max(1, (first ? 512 : 2048) / std::max(1, (int)ln.cols));
+      for (int r0 = 0; r0 < (int)ln.rows; r0 += per) {
+        FusedJob j{pi, e, r0, std::min(per, (int)ln.rows - r0), zp, is_a ? 1 : 0};
         if (is_a) ajobs[zp].push_back(j);
         else {
           (first ? fjobs0 : fjobs)[zp].push_back(j);
@@ -756,12 +686,25 @@ void fmm_plan_s::fuse_leaf_level(bool lazy_kernels) {
   }
   for (long long zp = std::max(0LL, np - LOOKAHEAD); zp < np; ++zp) jobs.insert(jobs.end(), ajobs[zp].begin(), ajobs[zp].end());
   fz.njobs = (int)jobs.size();
-  if (const char* dbg = getenv("FMM_FUSE_DEBUG")) {  // diagnostics only (wrong results): isolate costs
-    if (!strcmp(dbg, "nojobs")) {
-      fz.njobs0 = fz.njobs = 0;
-      std::fill(ready_target.begin(), ready_target.end(), 0);
-      std::fill(tiles_target.begin(), tiles_target.end(), 0);
+  // spatial split of the SMs: k addition CTAs on their own SMs (the FP64 ALU and the DMMA path
+  // are one pipe), the rest run leaf tiles; k balances the leaf flops at the per-SM DMMA rate
+  // against the absorbed addition bytes at the per-SM rate of an addition CTA
+  {
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
+    cudaGetLastError();
+    const double bytes = 8.0 * (fz.elem_reads + fz.elem_writes), fl = fz.flops;
+    // measured (round 1): ~245 GFLOP/s per GEMM SM, ~80 GB/s per addition SM (loads + stores)
+    const double F_SM = 245e9, B_SM = 80e9;
+    int best_k = 1;
+    double best_t = 1e300;
+    for (int k = 1; k <= sms / 3; ++k) {
+      const double t = std::max(fl / ((sms - k) * F_SM), bytes / (k * B_SM));
+      if (t < best_t) best_t = t, best_k = k;
     }
+    if (const char* e = getenv("FMM_FUSE_ADD_CTAS")) best_k = std::max(1, std::min(sms - 1, atoi(e)));
+    fz.gemm_ctas = sms - best_k;
   }
   auto push = [&](const void* p, size_t n) {
     size_t off = h_tab.size();
@@ -769,11 +712,15 @@ void fmm_plan_s::fuse_leaf_level(bool lazy_kernels) {
     if (n) std::memcpy(h_tab.data() + off, p, n);
     return off;
   };
-  fz.progs_off = push(blob.data(), blob.size());
   fz.jobs_off = push(jobs.data(), jobs.size() * sizeof(FusedJob));
   std::vector<int> targets(ready_target);
   targets.insert(targets.end(), tiles_target.begin(), tiles_target.end());
   fz.targets_off = push(targets.data(), targets.size() * sizeof(int));
+  if (!lazy_kernels) {
+    std::vector<LincombSpec> specs;
+    for (int q = 0; q < fz.nprogs; ++q) specs.push_back(lincomb_spec(*kernel(sides[q], 2)));
+    fz.fk = fused_get(specs, fz.bn);
+  }
   // replace: GEMM -> FUSED; drop the absorbed formation / assembly launches
   launches[ig] = fz;
   std::vector<Launch> keep;
@@ -971,10 +918,12 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
         break;
       case Launch::FUSED: {
         FusedArgs fa{};
-        fa.base = d_tab;
-        fa.blob = d_tab + ln.progs_off;
-        fa.blob_bytes = ln.blob_bytes;
-        fa.nprogs = ln.nprogs;
+        for (int q = 0; q < ln.nprogs; ++q) {
+          fa.node_tab[q] = d_tab + ln.prog_node_off[q];
+          fa.node_bytes[q] = ln.prog_node_bytes[q];
+          fa.cols[q] = ln.prog_cols[q];
+          fa.vec2[q] = ln.prog_vec2[q];
+        }
         fa.jobs = reinterpret_cast<const FusedJob*>(d_tab + ln.jobs_off);
         fa.njobs0 = ln.njobs0;
         fa.njobs = ln.njobs;
@@ -984,8 +933,8 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
         fa.np = ln.np;
         fa.gemm_ctas = ln.gemm_ctas;
         FMM_CUDA(cudaMemsetAsync(p->d_ctr, 0, p->ctr_bytes, stream));
-        gemm_fused_launch(reinterpret_cast<const GemmTask*>(tab), d_tab + ln.maps_off, ln.count, ln.tiles, ln.bn,
-                          ln.uni_tm, ln.uni_tn, fa, stream);
+        fused_launch(*ln.fk, reinterpret_cast<const GemmTask*>(tab), d_tab + ln.maps_off, ln.count, ln.tiles, ln.uni_tm,
+                     ln.uni_tn, fa, stream);
         break;
       }
       case Launch::GEMM:
@@ -1063,6 +1012,48 @@ fmm_status_t fmm_plan_stats(const fmm_plan_t* p, double out[8]) {
   s[5] = p->L;
   s[7] = 2.0 * p->userP * p->userQ * (double)p->userN - (double)p->userP * p->userN;
   std::memcpy(out, s, sizeof(s));
+  return FMM_OK;
+  FMM_API_END
+}
+
+fmm_status_t fmm_fused_compile_check(const fmm_alg* alg, int layout, int cse, int bn) {
+  FMM_API_BEGIN
+  if (!alg) throw Error(FMM_E_INVALID_ARG, "null algorithm");
+  std::unique_ptr<fmm_alg> t;
+  const fmm_alg* a = alg;
+  if (layout == FMM_COL_MAJOR) t.reset(alg_transpose_prop1(*alg)), a = t.get();
+  const int M = a->M, K = a->K, N = a->N, R = a->R;
+  std::vector<LincombSpec> specs;
+  for (int side = 0; side < 3; ++side) {
+    LincombSpec sp;
+    sp.strategy = FMM_ADD_STREAMING;
+    sp.cse = cse;
+    sp.vec = 2;
+    if (side < 2) {
+      const int rows = side == 0 ? M * K : K * N;
+      const auto& X = side == 0 ? a->Ud : a->Vd;
+      std::vector<int> form;
+      for (int r = 0; r < R; ++r) {
+        int nz = 0;
+        for (int i = 0; i < rows; ++i) nz += X[(size_t)i * R + r] != 0.0;
+        if (nz != 1) form.push_back(r);
+      }
+      if (form.empty()) continue;
+      sp.nin = rows;
+      sp.nout = (int)form.size();
+      sp.coef.assign((size_t)sp.nin * sp.nout, 0.0);
+      for (int o = 0; o < sp.nout; ++o)
+        for (int i = 0; i < rows; ++i) sp.coef[(size_t)o * rows + i] = X[(size_t)i * R + form[o]];
+    } else {
+      sp.nin = R;
+      sp.nout = M * N;
+      sp.coef.assign((size_t)sp.nin * sp.nout, 0.0);
+      for (int k = 0; k < M * N; ++k)
+        for (int r = 0; r < R; ++r) sp.coef[(size_t)k * R + r] = a->Wd[(size_t)k * R + r];
+    }
+    specs.push_back(sp);
+  }
+  fused_compile(fused_generate(specs, bn));
   return FMM_OK;
   FMM_API_END
 }

@@ -49,6 +49,7 @@ def _load():
         "fmm_plan_workspace_bytes": [vp, ctypes.POINTER(ctypes.c_size_t)],
         "fmm_plan_stats": [vp, ctypes.POINTER(dp)],
         "fmm_plan_stats_ex": [vp, ctypes.POINTER(dp)],
+        "fmm_fused_compile_check": [vp, i32, i32, i32],
         "fmm_execute": [vp, vp, i64, vp, i64, vp, i64, vp],
         "fmm_exec": [vp, vp, vp, vp],
         "fmm_execute_timed": [vp, vp, i64, vp, i64, vp, i64, vp, ctypes.POINTER(ctypes.c_float)],
@@ -283,6 +284,11 @@ def dgemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, stream=None):
     c, ldc = _mat(C, ROW_MAJOR, m, n, "C")
     _check(_lib.fmm_dgemm(m, n, k, alpha, a, lda, b, ldb, beta, c, ldc, _stream_ptr(stream)))
     return C
+
+
+def fused_compile_check(alg: "Algorithm", layout: str = "row", cse: bool = True, bn: int = 128) -> None:
+    """NVRTC-compile the fused leaf-level kernel of `alg` (host only; raises FmmError on failure)."""
+    _check(_lib.fmm_fused_compile_check(alg._h, ROW_MAJOR if layout == "row" else COL_MAJOR, int(bool(cse)), bn))
 
 
 def probe_fp64_peak():
