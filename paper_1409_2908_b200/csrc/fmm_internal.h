@@ -85,10 +85,15 @@ void gemm_tma_maps(const std::vector<GemmTask>& tasks, void* out);
 // uniform_tm/tn: the common tile grid when every task has the same one (else 0, 0).
 void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn,
                      int uniform_tm, int uniform_tn, cudaStream_t stream);
+// A rank-`rank` FP64 tensor map (no swizzle, zero OOB fill): dims/box innermost first, strides in
+// bytes for dims 1..rank-1.  false if TMA cannot describe the view (alignment, limits).
+bool tensor_map_nd(void* out, const double* ptr, int rank, const long long* dims, const long long* strides_bytes,
+                   const int* box);
 // TMA kernel configuration: consumer warp grid of a tile width, SM count, dynamic shared memory.
 void gemm_bn_config(int bn, int* wgm, int* wgn);
 int gemm_sm_count();
 int gemm_tma_smem_bytes(int bn);
+int gemm_fused_smem_bytes(int bn);
 // (tiles_m, tiles_n) shared by every task of a prepared list, or (0, 0).
 void gemm_uniform_grid(const std::vector<GemmTask>& tasks, int* tm, int* tn);
 // Thin products (one dimension <= skinny_limit()) on the CUDA cores (fmm_skinny.cu): ids index
