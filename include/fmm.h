@@ -106,6 +106,12 @@ fmm_status_t fmm_alg_create(int M, int K, int N, int R,
    message; APA files ("apa") return FMM_E_UNSUPPORTED; then validates as fmm_alg_create. */
 fmm_status_t fmm_alg_load(const char* path, fmm_alg** out);
 
+/* Equivalent algorithm for a permuted base case (Props. 1-2, exact; re-validated):
+   perm 0 <M,K,N> (copy), 1 <N,K,M> (Prop. 1), 2 <N,M,K> (Prop. 2), 3 <K,N,M> (Prop. 2 twice),
+   4 <K,M,N> (Prop. 1 after Prop. 2), 5 <M,N,K> (Prop. 1 after Prop. 2 twice).  Host only; the
+   caller owns *out (fmm_alg_destroy). */
+fmm_status_t fmm_alg_permute(const fmm_alg* alg, int perm, fmm_alg** out);
+
 /* Query shape and sparsity: dims[0..3] = M,K,N,R; nnz[0..2] = nnz(U), nnz(V), nnz(W). */
 fmm_status_t fmm_alg_info(const fmm_alg* alg, int dims[4], int nnz[3]);
 void fmm_alg_destroy(fmm_alg* alg);
@@ -149,6 +155,20 @@ fmm_status_t fmm_plan_stats(const fmm_plan_t* plan, double out[8]);
    [13] flops of the peel-strip products
    [14..15] 0 (reserved) */
 fmm_status_t fmm_plan_stats_ex(const fmm_plan_t* plan, double out[16]);
+
+/* Cost model (host only, no allocation): predicted milliseconds of a plan of `alg` for the problem
+   on one B200 -- leaf DMMA GEMM tile schedule (wave quantisation, tile widths), streaming addition
+   traffic at the measured HBM rate, peel strips, launch costs; the recursion stops where
+   plan_create stops (*used_levels, may be NULL).  The paper's cutoff question (Sec. 3.4,
+   P:741-759): compare levels = 0, 1, 2, ... */
+fmm_status_t fmm_plan_predict(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels, int layout, double* ms,
+                              int* used_levels);
+
+/* Shape matching: over the candidate algorithms, their six Prop. 1/2
+   permutations and levels 1..max_levels, the predicted-fastest plan, or the classical GEMM
+   (*alg_index = -1, *levels = 0) when nothing beats it.  *perm is for fmm_alg_permute. */
+fmm_status_t fmm_select(const fmm_alg* const* algs, int nalgs, int64_t P, int64_t Q, int64_t Nc, int max_levels, int layout,
+                        int* alg_index, int* perm, int* levels, double* ms);
 
 /* Host-only check (no device work): generate and NVRTC-compile, for sm_100a, the fused
    leaf-level kernel of `alg` (fuse_leaf_level = 1) for the given layout, CSE setting and GEMM tile

@@ -111,6 +111,20 @@ fmm_alg* alg_transpose_prop1(const fmm_alg& a) {
   return t;
 }
 
+fmm_alg* alg_cycle_prop2(const fmm_alg& a) {
+  // Prop. 2: <P_{MxN} W, U, P_{KxN} V> is an algorithm for <N,M,K>.
+  auto* t = new fmm_alg;
+  t->M = a.N;
+  t->K = a.M;
+  t->N = a.K;
+  t->R = a.R;
+  t->U = perm_rows(a.W, a.M, a.N, a.R);
+  t->V = a.U;
+  t->W = perm_rows(a.V, a.K, a.N, a.R);
+  fill_doubles(*t);
+  return t;
+}
+
 static fmm_alg* alg_from_rats(int M, int K, int N, int R, std::vector<Rat> U, std::vector<Rat> V,
                               std::vector<Rat> W) {
   if (M < 1 || K < 1 || N < 1 || M > 16 || K > 16 || N > 16 || R < 1 || R > 4096)
@@ -238,6 +252,22 @@ fmm_status_t fmm_alg_load(const char* path, fmm_alg** out) {
   if (!path || !out) throw Error(FMM_E_INVALID_ARG, "null argument");
   *out = nullptr;
   *out = alg_parse_file(path);
+  return FMM_OK;
+  FMM_API_END
+}
+
+fmm_status_t fmm_alg_permute(const fmm_alg* a, int perm, fmm_alg** out) {
+  FMM_API_BEGIN
+  if (!a || !out) throw Error(FMM_E_INVALID_ARG, "null argument");
+  if (perm < 0 || perm > 5) throw Error(FMM_E_INVALID_ARG, "perm must be in [0, 5]");
+  *out = nullptr;
+  // 0 <M,K,N>, 1 P1 <N,K,M>, 2 P2 <N,M,K>, 3 P2 P2 <K,N,M>, 4 P1 P2 <K,M,N>, 5 P1 P2 P2 <M,N,K>
+  std::unique_ptr<fmm_alg> t(new fmm_alg(*a));
+  const int cycles = perm == 2 || perm == 4 ? 1 : perm == 3 || perm == 5 ? 2 : 0;
+  for (int c = 0; c < cycles; ++c) t.reset(alg_cycle_prop2(*t));
+  if (perm == 1 || perm == 4 || perm == 5) t.reset(alg_transpose_prop1(*t));
+  alg_validate_exact(*t);  // the propositions are exact; re-checked anyway
+  *out = t.release();
   return FMM_OK;
   FMM_API_END
 }

@@ -66,6 +66,7 @@ struct fmm_alg_s {
 namespace fmm {
 
 fmm_alg* alg_transpose_prop1(const fmm_alg& a);  // Prop. 1: <N,K,M>
+fmm_alg* alg_cycle_prop2(const fmm_alg& a);      // Prop. 2: <N,M,K>
 void alg_validate_exact(const fmm_alg& a);        // throws FMM_E_NOT_EXACT
 
 // ---- grouped DMMA GEMM (K2 / K4 / K5) -------------------------------------------------------

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -1057,6 +1058,136 @@ fmm_status_t fmm_plan_stats(const fmm_plan_t* p, double out[8]) {
   s[5] = p->L;
   s[7] = 2.0 * p->userP * p->userQ * (double)p->userN - (double)p->userP * p->userN;
   std::memcpy(out, s, sizeof(s));
+  return FMM_OK;
+  FMM_API_END
+}
+
+}  // extern "C"
+
+// ---- cost model: predicted time of a plan (the paper's cutoff question, Sec. 3.4) -----
+// Leaf products: the persistent DMMA kernel's tile schedule (128 x BN tiles from the same width menu,
+// wave quantisation over the SMs, a fixed per-tile prologue/epilogue); thin products on the CUDA
+// cores; additions: streaming traffic (P:634-636 in bytes) at the addition kernels' measured HBM
+// rate; a fixed cost per launch.  Rates are the round-1 B200 measurements.
+namespace {
+struct CostModel {
+  int sms = 148;
+  double f_sm = 245e9;          // DMMA flop/s per SM on large tiles (0.97 x 37 TF / 148)
+  double add_bw = 6.0e12;       // K1 / K3 streaming kernels, bytes/s
+  double thin = 25e9;           // CUDA-core thin-strip flop/s per SM
+  double launch = 4e-6;         // seconds per kernel launch
+};
+
+double gemm_time(double count, long long m, long long n, long long k, const CostModel& cm) {
+  if (count <= 0 || m <= 0 || n <= 0) return 0.0;
+  if (k <= 0) return cm.launch;
+  if (std::min(m, n) <= 8) return 2.0 * count * m * n * (double)k / (cm.sms * cm.thin) + cm.launch;
+  static const int menu[] = {128, 112, 96, 80, 64};
+  static const double eff[] = {1.00, 0.985, 0.975, 0.965, 0.94};
+  double best = 1e300;
+  for (int q = 0; q < 5; ++q) {
+    const double tiles = count * (double)((m + 127) / 128) * (double)((n + menu[q] - 1) / menu[q]);
+    const double t_tile = 2.0 * 128 * menu[q] * (double)(((k + 15) / 16) * 16 + 32) / (cm.f_sm * eff[q]);
+    best = std::min(best, std::ceil(tiles / cm.sms) * t_tile);
+  }
+  return best + cm.launch;
+}
+
+int formed_columns(const std::vector<double>& X, int rows, int R) {
+  int f = 0;
+  for (int r = 0; r < R; ++r) {
+    int nz = 0;
+    for (int i = 0; i < rows; ++i) nz += X[(size_t)i * R + r] != 0.0;
+    f += nz != 1;
+  }
+  return f;
+}
+
+// seconds; levels beyond the base case are not taken (R10), as in plan_init
+double predict_seconds(const fmm_alg& a, long long P, long long Q, long long N, int levels, int* used_levels) {
+  const CostModel cm;
+  const int M = a.M, K = a.K, Nb = a.N, R = a.R;
+  const int fu = formed_columns(a.Ud, M * K, R), fv = formed_columns(a.Vd, K * Nb, R);
+  struct D { long long P, Q, N, P1, Q1, N1; };
+  std::vector<D> dims;
+  D d{P, Q, N, 0, 0, 0};
+  int L = 0;
+  while (true) {
+    d.P1 = M * (d.P / M);
+    d.Q1 = K * (d.Q / K);
+    d.N1 = Nb * (d.N / Nb);
+    dims.push_back(d);
+    if (L == levels || d.P < M || d.Q < K || d.N < Nb) break;
+    d = D{d.P1 / M, d.Q1 / K, d.N1 / Nb, 0, 0, 0};
+    ++L;
+  }
+  if (used_levels) *used_levels = L;
+  double nodes = 1, t = 0;
+  for (int l = 1; l <= L; ++l) {
+    const D& c = dims[l];
+    const D& pd = dims[l - 1];
+    // formation and assembly of level l (streaming bytes)
+    const double bytes = 8.0 * nodes *
+                         ((double)(M * K + fu) * c.P * c.Q * (fu > 0) + (double)(K * Nb + fv) * c.Q * c.N * (fv > 0) +
+                          (double)(R + M * Nb) * c.P * c.N);
+    t += bytes / cm.add_bw + cm.launch * (1 + (fu > 0) + (fv > 0));
+    // peel strips of the level-(l-1) nodes
+    t += gemm_time(nodes, pd.P1, pd.N1, pd.Q - pd.Q1, cm);
+    t += gemm_time(nodes, pd.P - pd.P1, pd.N, pd.Q, cm);
+    t += gemm_time(nodes, pd.P1, pd.N - pd.N1, pd.Q, cm);
+    nodes *= R;
+  }
+  t += gemm_time(nodes, dims[L].P, dims[L].N, dims[L].Q, cm);
+  return t;
+}
+}  // namespace
+
+extern "C" {
+
+fmm_status_t fmm_plan_predict(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels, int layout, double* ms,
+                              int* used_levels) {
+  FMM_API_BEGIN
+  if (!alg || !ms) throw Error(FMM_E_INVALID_ARG, "null argument");
+  if (P < 0 || Q < 0 || Nc < 0) throw Error(FMM_E_SHAPE, "negative dimension");
+  if (levels < 0 || levels > 8) throw Error(FMM_E_UNSUPPORTED, "levels must be in [0, 8]");
+  std::unique_ptr<fmm_alg> t;
+  const fmm_alg* a = alg;
+  long long p = P, n = Nc;
+  if (layout == FMM_COL_MAJOR) t.reset(alg_transpose_prop1(*alg)), a = t.get(), p = Nc, n = P;
+  *ms = 1e3 * predict_seconds(*a, p, Q, n, levels, used_levels);
+  return FMM_OK;
+  FMM_API_END
+}
+
+fmm_status_t fmm_select(const fmm_alg* const* algs, int nalgs, int64_t P, int64_t Q, int64_t Nc, int max_levels, int layout,
+                        int* alg_index, int* perm, int* levels, double* ms) {
+  FMM_API_BEGIN
+  if ((nalgs > 0 && !algs) || !alg_index || !perm || !levels || !ms) throw Error(FMM_E_INVALID_ARG, "null argument");
+  if (P < 0 || Q < 0 || Nc < 0) throw Error(FMM_E_SHAPE, "negative dimension");
+  if (max_levels < 0 || max_levels > 8) throw Error(FMM_E_UNSUPPORTED, "max_levels must be in [0, 8]");
+  // classical: one DMMA GEMM (levels = 0 of any algorithm)
+  const long long p = layout == FMM_COL_MAJOR ? Nc : P, n = layout == FMM_COL_MAJOR ? P : Nc;
+  double best = gemm_time(1, p, n, Q, CostModel());
+  *alg_index = -1, *perm = 0, *levels = 0;
+  for (int i = 0; i < nalgs; ++i) {
+    if (!algs[i]) throw Error(FMM_E_INVALID_ARG, "null algorithm in the candidate list");
+    for (int q = 0; q < 6; ++q) {
+      fmm_alg* pa = nullptr;
+      const fmm_status_t st = fmm_alg_permute(algs[i], q, &pa);
+      if (st != FMM_OK) return st;
+      std::unique_ptr<fmm_alg> own(pa);
+      std::unique_ptr<fmm_alg> tr;
+      const fmm_alg* a = pa;
+      if (layout == FMM_COL_MAJOR) tr.reset(alg_transpose_prop1(*pa)), a = tr.get();
+      for (int L = 1; L <= max_levels; ++L) {
+        int used = 0;
+        const double tt = predict_seconds(*a, p, Q, n, L, &used);
+        if (used < L) break;  // deeper levels are not taken
+        if (tt < best * (1 - 1e-9)) best = tt, *alg_index = i, *perm = q, *levels = L;
+      }
+    }
+  }
+  *ms = 1e3 * best;
   return FMM_OK;
   FMM_API_END
 }

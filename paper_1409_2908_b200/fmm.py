@@ -50,6 +50,10 @@ def _load():
         "fmm_plan_stats": [vp, ctypes.POINTER(dp)],
         "fmm_plan_stats_ex": [vp, ctypes.POINTER(dp)],
         "fmm_fused_compile_check": [vp, i32, i32, i32],
+        "fmm_alg_permute": [vp, i32, ctypes.POINTER(vp)],
+        "fmm_plan_predict": [vp, i64, i64, i64, i32, i32, ctypes.POINTER(dp), ctypes.POINTER(i32)],
+        "fmm_select": [vp, i32, i64, i64, i64, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32),
+                       ctypes.POINTER(dp)],
         "fmm_execute": [vp, vp, i64, vp, i64, vp, i64, vp],
         "fmm_exec": [vp, vp, vp, vp],
         "fmm_execute_timed": [vp, vp, i64, vp, i64, vp, i64, vp, ctypes.POINTER(ctypes.c_float)],
@@ -125,10 +129,37 @@ class Algorithm:
         _check(_lib.fmm_alg_create(M, K, N, R, un, ud, vn, vd, wn, wd, ctypes.byref(h)))
         return cls(h, name=name)
 
+    PERMS = ["MKN", "NKM", "NMK", "KNM", "KMN", "MNK"]  # fmm_alg_permute's perm index -> base case
+
+    def permute(self, perm: int) -> "Algorithm":
+        """The equivalent algorithm for a permuted base case (Props. 1-2, fmm_alg_permute)."""
+        h = ctypes.c_void_p()
+        _check(_lib.fmm_alg_permute(self._h, perm, ctypes.byref(h)))
+        return Algorithm(h, name=f"{self.name}^{self.PERMS[perm]}")
+
+    def predict_ms(self, P: int, Q: int, N: int, levels: int, layout: str = "row") -> float:
+        """The library's cost model (fmm_plan_predict): predicted ms of the plan on one B200."""
+        ms, used = ctypes.c_double(), ctypes.c_int()
+        _check(_lib.fmm_plan_predict(self._h, P, Q, N, levels, ROW_MAJOR if layout == "row" else COL_MAJOR,
+                                     ctypes.byref(ms), ctypes.byref(used)))
+        return ms.value
+
     def __del__(self):
         if getattr(self, "_h", None):
             _lib.fmm_alg_destroy(self._h)
             self._h = None
+
+
+def select(algs: Sequence[Algorithm], P: int, Q: int, N: int, max_levels: int = 3, layout: str = "row"):
+    """Shape matching (fmm_select): (algorithm or None for classical, levels, predicted ms) with the
+    algorithm already permuted to the chosen base case."""
+    arr = (ctypes.c_void_p * max(1, len(algs)))(*[a._h for a in algs])
+    ai, pm, lv, ms = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
+    _check(_lib.fmm_select(arr, len(algs), P, Q, N, max_levels, ROW_MAJOR if layout == "row" else COL_MAJOR,
+                           ctypes.byref(ai), ctypes.byref(pm), ctypes.byref(lv), ctypes.byref(ms)))
+    if ai.value < 0:
+        return None, 0, ms.value
+    return algs[ai.value].permute(pm.value), lv.value, ms.value
 
 
 # ---- tensors --------------------------------------------------------------------------------
