@@ -172,6 +172,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fuse", type=int, default=0, help="fused leaf level (formation/GEMM/assembly in one launch)")
+    ap.add_argument("--collapse", type=int, default=1, help="last two levels' formation / assembly in one pass each")
     ap.add_argument("--no-other", action="store_true", help="skip timing the other leaf-level schedule (fused vs separate)")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -204,7 +205,7 @@ def main():
     B = to_device(B_np, w["layout"], device)
     alg = F.load_alg(w["alg"])
     plan = F.Plan(alg, P, Q, N, L, layout=w["layout"], strategy=args.strategy, cse=bool(args.cse),
-                  shard_rank=rank, shard_count=world, fuse=bool(args.fuse))
+                  shard_rank=rank, shard_count=world, fuse=bool(args.fuse), collapse=bool(args.collapse))
     C = plan.new_output()
     st = plan.stats()
     dmma_peak, dfma_peak = F.probe_fp64_peak()
@@ -265,7 +266,7 @@ def main():
     other = None
     if not args.no_other and L >= 1:
         plan_o = F.Plan(alg, P, Q, N, L, layout=w["layout"], strategy=args.strategy, cse=bool(args.cse),
-                        shard_rank=rank, shard_count=world, fuse=not fused)
+                        shard_rank=rank, shard_count=world, fuse=not fused, collapse=False)
         so = plan_o.stats()
         for _ in range(2):
             plan_o.execute(A, B, C, stream=stream)
@@ -280,7 +281,7 @@ def main():
         phu = np.array([[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]),
                          e[0].elapsed_time(e[3])] for e in evu]).mean(axis=0)
         o_fused = so.get("fused_launches", 0) > 0
-        other = {"fused_leaf_level": o_fused, "ms_per_step": float(phu[3]), "value": flops / (phu[3] * 1e-3) / 1e9,
+        other = {"fused_leaf_level": o_fused, "collapsed_levels": bool(so.get("collapsed", 0)), "ms_per_step": float(phu[3]), "value": flops / (phu[3] * 1e-3) / 1e9,
                  "steps": nu, "phases_ms": {"formation": float(phu[0]), "leaf_level": float(phu[1]),
                                             "assembly_and_strips": float(phu[2])},
                  "launches": so["launches"]}
@@ -410,7 +411,7 @@ def main():
                        "l2": "inputs larger than L2 (A, B, C 0.54 GB each vs 126 MB); no flush"
                        if args.workload != "c1" else "small config: L2-resident",
                        "parallelism": f"leaf shards x{world} + NCCL reduce" if world > 1 else "1 GPU",
-                       "fused_leaf_level": fused},
+                       "fused_leaf_level": fused, "collapsed_levels": bool(st.get("collapsed", 0))},
             "roofline": roofline,
             "clocks": clk,
             "e2e": e2e,

@@ -81,10 +81,16 @@ typedef struct {
                                (streaming strategy only; needs TMA-eligible leaf views and no thin
                                leaves, else the plan silently runs the separate kernels).
                                0: separate formation / GEMM / assembly launches. */
+  int collapse_levels;      /* 1: evaluate the last two recursion levels' formation and assembly in
+                               one streaming pass each (the level-(L-1) S_r, T_r and M_r are never
+                               written to HBM: DESIGN.md sec. 6c), where it applies: streaming,
+                               L >= 2, a base case with MK, KN, MN <= 4, no peeling at level L-1.
+                               The chains are the oracle's two levels exactly (CSE is not used
+                               there).  0: one level per launch. */
 } fmm_plan_options;
 
 /* Fill *opt with the defaults: row-major, streaming, cse = 1, shard 0 of 1, no limit,
-   peel_align = 1, fuse_leaf_level = 1. */
+   peel_align = 1, fuse_leaf_level = 0, collapse_levels = 1. */
 void fmm_plan_options_default(fmm_plan_options* opt);
 
 /* ---- algorithms ------------------------------------------------------------------------- */
@@ -153,7 +159,8 @@ fmm_status_t fmm_plan_stats(const fmm_plan_t* plan, double out[8]);
    [11] addition bytes of the separate formation kernels (levels below the fused one)
    [12] addition bytes of the separate assembly kernels
    [13] flops of the peel-strip products
-   [14..15] 0 (reserved) */
+   [14] 1 if the last two levels are collapsed (collapse_levels), else 0
+   [15] 0 (reserved) */
 fmm_status_t fmm_plan_stats_ex(const fmm_plan_t* plan, double out[16]);
 
 /* Cost model (host only, no allocation): predicted milliseconds of a plan of `alg` for the problem

@@ -513,6 +513,173 @@ void fused_launch(const FusedKernel& k, const GemmTask* d_tasks, const void* d_m
 
 std::string fused_source(const FusedKernel& k) { return k.source; }
 
+// ---- two collapsed levels ------------------------------------------------------------------------
+namespace {
+std::string generate_two_level(const TwoLevelSpec& sp, LincombCost& cost) {
+  const int rows = sp.rows, R = sp.R, V = sp.vec;
+  const std::string T = V == 2 ? "double2" : "double";
+  std::vector<std::string> comps = V == 2 ? std::vector<std::string>{".x", ".y"} : std::vector<std::string>{""};
+  auto X = [&](int i, int r) { return sp.X[(size_t)i * R + r]; };
+  auto nz = [&](int r) {
+    std::vector<int> v;
+    for (int i = 0; i < rows; ++i)
+      if (X(i, r) != 0.0) v.push_back(i);
+    return v;
+  };
+  const bool asm_ = sp.side == 2;
+  const int nin = asm_ ? R * R : rows * rows, nout = asm_ ? rows * rows : R * R;
+  std::ostringstream o;
+  o << "// generated by fmm_codegen.cpp: two collapsed levels, side=" << sp.side << " rows=" << rows << " R=" << R << " vec=" << V
+    << "\n";
+  o << "struct Node { const double* in[" << nin << "]; double* out[" << nout << "]; long long ld_in; long long ld_out; };\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(128) lincomb(const Node* __restrict__ nodes, int nrows, int cvec) {\n";
+  o << "  const Node& nd = nodes[blockIdx.z];\n";
+  o << "  const int cv = blockIdx.x * blockDim.x + threadIdx.x;\n";
+  o << "  if (cv >= cvec) return;\n";
+  o << "  for (int row = blockIdx.y; row < nrows; row += gridDim.y) {\n";
+  o << "    const long long pi = (long long)row * nd.ld_in + (long long)cv * " << V << ";\n";
+  o << "    const long long po = (long long)row * nd.ld_out + (long long)cv * " << V << ";\n";
+  // chain over named terms (first-term initialisation; --fmad=false keeps products separate)
+  auto chain = [&](const std::string& dst, const std::vector<std::pair<std::string, double>>& terms) {
+    for (auto& c : comps) {
+      bool first = true;
+      for (const auto& t : terms) {
+        const std::string v = t.first + c;
+        const double k = t.second;
+        if (first) {
+          o << "    " << dst << c << " = " << (k == 1.0 ? v : k == -1.0 ? "-" + v : dlit(k) + " * " + v) << ";\n";
+          first = false;
+        } else {
+          o << "    " << dst << c << " = " << dst << c << (k == 1.0 ? " + " + v : k == -1.0 ? " - " + v : " + " + dlit(k) + " * " + v) << ";\n";
+        }
+      }
+      if (first) o << "    " << dst << c << " = 0.0;\n";
+    }
+  };
+  double adds = 0, reads = 0, writes = 0;
+  if (!asm_) {
+    // which inputs are used: all x[i1][i2] for i1 in nz(r1) of a needed r1 (or singleton i1s)
+    std::set<int> used;
+    for (int r1 = 0; r1 < R; ++r1) {
+      bool any = false;
+      for (int r2 = 0; r2 < R; ++r2) any |= sp.materialize[(size_t)r1 * R + r2] != 0;
+      if (!any) continue;
+      for (int i1 : nz(r1))
+        for (int i2 = 0; i2 < rows; ++i2) used.insert(i1 * rows + i2);
+    }
+    for (int i : used) o << "    const " << T << " x" << i << " = __ldg((const " << T << "*)(nd.in[" << i << "] + pi));\n";
+    reads = (double)used.size();
+    for (int r1 = 0; r1 < R; ++r1) {
+      bool any = false;
+      for (int r2 = 0; r2 < R; ++r2) any |= sp.materialize[(size_t)r1 * R + r2] != 0;
+      if (!any) continue;
+      const std::vector<int> n1 = nz(r1);
+      // T[r1][i2] for the i2 some materialised output of r1 needs
+      std::set<int> need_i2;
+      for (int r2 = 0; r2 < R; ++r2)
+        if (sp.materialize[(size_t)r1 * R + r2])
+          for (int i2 : nz(r2)) need_i2.insert(i2);
+      for (int i2 : need_i2) {
+        const std::string t = "t" + std::to_string(r1) + "_" + std::to_string(i2);
+        if (n1.size() == 1) {
+          o << "    const " << T << "& " << t << " = x" << n1[0] * rows + i2 << ";\n";  // singleton r1: unscaled alias
+        } else {
+          std::vector<std::pair<std::string, double>> terms;
+          for (int i1 : n1) terms.push_back({"x" + std::to_string(i1 * rows + i2), X(i1, r1)});
+          o << "    " << T << " " << t << ";\n";
+          chain(t, terms);
+          adds += (double)n1.size() - 1;
+        }
+      }
+      for (int r2 = 0; r2 < R; ++r2) {
+        const int q = r1 * R + r2;
+        if (!sp.materialize[(size_t)q]) continue;
+        const std::vector<int> n2 = nz(r2);
+        o << "    if (nd.out[" << q << "]) {\n    " << T << " y;\n";
+        if (n2.size() == 1) {
+          for (auto& c : comps) o << "    y" << c << " = t" << r1 << "_" << n2[0] << c << ";\n";  // singleton r2: unscaled
+        } else {
+          std::vector<std::pair<std::string, double>> terms;
+          for (int i2 : n2) terms.push_back({"t" + std::to_string(r1) + "_" + std::to_string(i2), X(i2, r2)});
+          chain("y", terms);
+          adds += (double)n2.size() - 1;
+        }
+        o << "    *(" << T << "*)(nd.out[" << q << "] + po) = y;\n    }\n";
+        writes += 1;
+      }
+    }
+  } else {
+    // C[k1][k2] = sum_r1 X[k1][r1] M1[r1][k2],  M1[r1][k2] = sum_r2 X[k2][r2] M[r1][r2]
+    for (int k = 0; k < nout; ++k) o << "    " << T << " c" << k << ";\n";
+    std::vector<char> started(nout, 0);
+    for (int r1 = 0; r1 < R; ++r1) {
+      std::vector<int> ks;  // k1 with X[k1][r1] != 0
+      for (int k1 = 0; k1 < rows; ++k1)
+        if (X(k1, r1) != 0.0) ks.push_back(k1);
+      if (ks.empty()) continue;
+      o << "    {\n";
+      std::set<int> r2s;
+      for (int k2 = 0; k2 < rows; ++k2)
+        for (int r2 = 0; r2 < R; ++r2)
+          if (X(k2, r2) != 0.0) r2s.insert(r2);
+      for (int r2 : r2s)
+        o << "    const " << T << " m" << r2 << " = __ldcg((const " << T << "*)(nd.in[" << r1 * R + r2 << "] + pi));\n";
+      reads += (double)r2s.size();
+      for (int k2 = 0; k2 < rows; ++k2) {
+        std::vector<std::pair<std::string, double>> terms;
+        for (int r2 = 0; r2 < R; ++r2)
+          if (X(k2, r2) != 0.0) terms.push_back({"m" + std::to_string(r2), X(k2, r2)});
+        o << "    " << T << " u" << k2 << ";\n";
+        chain("u" + std::to_string(k2), terms);
+        adds += terms.empty() ? 0 : (double)terms.size() - 1;
+        for (int k1 : ks) {
+          const int k = k1 * rows + k2;
+          const double w = X(k1, r1);
+          const std::string v = "u" + std::to_string(k2);
+          for (auto& c : comps) {
+            const std::string d = "c" + std::to_string(k) + c, vv = v + c;
+            if (!started[k]) o << "    " << d << " = " << (w == 1.0 ? vv : w == -1.0 ? "-" + vv : dlit(w) + " * " + vv) << ";\n";
+            else o << "    " << d << " = " << d << (w == 1.0 ? " + " + vv : w == -1.0 ? " - " + vv : " + " + dlit(w) + " * " + vv) << ";\n";
+          }
+          if (started[k]) adds += 1;
+          started[k] = 1;
+        }
+      }
+      o << "    }\n";
+    }
+    for (int k = 0; k < nout; ++k) {
+      if (!started[k])
+        for (auto& c : comps) o << "    c" << k << c << " = 0.0;\n";
+      o << "    *(" << T << "*)(nd.out[" << k << "] + po) = c" << k << ";\n";
+      writes += 1;
+    }
+  }
+  o << "  }\n}\n";
+  cost.adds_per_elem = adds;
+  cost.reads_per_elem = reads;
+  cost.writes_per_elem = writes;
+  return o.str();
+}
+}  // namespace
+
+std::shared_ptr<LincombKernel> twolevel_get(const TwoLevelSpec& spec) {
+  if (spec.rows < 1 || spec.R < 1 || (int)spec.X.size() != spec.rows * spec.R ||
+      (spec.side != 2 && (int)spec.materialize.size() != spec.R * spec.R))
+    throw Error(FMM_E_INVALID_ARG, "bad two-level spec");
+  auto k = std::make_shared<LincombKernel>();
+  k->spec.nin = spec.side == 2 ? spec.R * spec.R : spec.rows * spec.rows;
+  k->spec.nout = spec.side == 2 ? spec.rows * spec.rows : spec.R * spec.R;
+  k->spec.vec = spec.vec;
+  k->spec.strategy = FMM_ADD_STREAMING;
+  k->source = generate_two_level(spec, k->cost);
+  std::lock_guard<std::mutex> lock(g_mu);
+  auto it = g_cache.find(k->source);
+  if (it != g_cache.end()) return it->second;
+  compile(*k);
+  g_cache[k->source] = k;
+  return k;
+}
+
 LincombCost lincomb_cost(const LincombKernel& k) { return k.cost; }
 const LincombSpec& lincomb_spec(const LincombKernel& k) { return k.spec; }
 int lincomb_cse_temps(const LincombKernel& k) { return k.temps; }

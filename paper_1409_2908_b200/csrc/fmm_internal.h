@@ -130,6 +130,22 @@ struct LincombCost {
   double reads_per_elem;   // elements read (inputs) per element position
   double writes_per_elem;  // elements written per element position
 };
+// Two recursion levels in one streaming pass (the last two levels collapsed).
+// Formation (side 0 / 1): inputs are the rows^2 sub-sub-blocks x[i1][i2] (index i1 * rows + i2) of
+// a grandparent block; for every level-(L-1) column r1 the intermediate T[r1][i2] = sum_i1 X[i1][r1]
+// x[i1][i2] (or x[i1s][i2] unscaled for a singleton r1), then output (r1, r2) (index r1 * R + r2) =
+// sum_i2 X[i2][r2] T[r1][i2] (or T[r1][i2s] unscaled for a singleton r2) when materialize[r1 R + r2].
+// Assembly (side 2): inputs are the R^2 leaf products M[r1][r2]; M1[r1][k2] = sum_r2 X[k2][r2]
+// M[r1][r2], output (k1, k2) (index k1 * rows + k2) = sum_r1 X[k1][r1] M1[r1][k2].  Every chain is
+// ascending-index with first-term initialisation, i.e. the oracle's two levels exactly.
+struct TwoLevelSpec {
+  int side = 0;               // 0 = A formation, 1 = B formation, 2 = assembly
+  int rows = 0, R = 0;        // rows of X (MK, KN or MN), rank
+  std::vector<double> X;      // rows x R, row-major (U, V or W)
+  std::vector<char> materialize;  // formation: R*R flags
+  int vec = 2;
+};
+std::shared_ptr<LincombKernel> twolevel_get(const TwoLevelSpec& spec);
 LincombCost lincomb_cost(const LincombKernel& k);
 int lincomb_cse_temps(const LincombKernel& k);
 std::string lincomb_source(const LincombKernel& k);

@@ -110,6 +110,7 @@ struct fmm_plan_s {
 
   bool use_tma = true;  // FMM_NO_TMA=1 forces the cp.async GEMM (diagnostics)
   bool fuse = true;     // fuse_leaf_level option (FMM_NO_FUSE=1 overrides)
+  bool collapse = false;  // the last two levels' formation / assembly in one pass each (sec. 6c)
   unsigned long long* d_ctr = nullptr;  // fused launch counters: claim0, claim1, ready[np], tiles[np]
   size_t ctr_bytes = 0;
   // kernels (vec 2 / vec 1 variants created lazily)
@@ -264,14 +265,19 @@ struct fmm_plan_s {
       offT[l].assign(nodes_at[l], -1);
       offM[l].assign(nodes_at[l], -1);
       bool any_unneeded = false;
+      if (collapse && l == L - 1) continue;  // never materialised (sec. 6c)
       for (long long z = 0; z < nodes_at[l]; ++z) {
         const int r = (int)(z % R);
         if (!needed[l][z]) {
           any_unneeded = true;
           continue;
         }
-        if (idxU[r] >= 0) offS[l][z] = take(d.P * ldS[l]);
-        if (idxV[r] >= 0) offT[l][z] = take(d.Q * ldT[l]);
+        const int r1 = (int)((z / R) % R);
+        // collapsed leaves: materialised unless both levels' columns are singletons (then an alias)
+        const bool formA = collapse && l == L ? (idxU[r] >= 0 || idxU[r1] >= 0) : idxU[r] >= 0;
+        const bool formB = collapse && l == L ? (idxV[r] >= 0 || idxV[r1] >= 0) : idxV[r] >= 0;
+        if (formA) offS[l][z] = take(d.P * ldS[l]);
+        if (formB) offT[l][z] = take(d.Q * ldT[l]);
         offM[l][z] = take(d.P * ldM[l]);
       }
       if (any_unneeded) offZero[l] = take(d.P * ldM[l]);
@@ -296,15 +302,47 @@ struct fmm_plan_s {
   View opA(int l, long long z, const View& root) const;
   View opB(int l, long long z, const View& root) const;
 
+  // the execute arguments of the build in progress (row-major orientation)
+  const double *cur_A = nullptr, *cur_B = nullptr;
+  double* cur_C = nullptr;
+  long long cur_lda = 0, cur_ldb = 0, cur_ldc = 0;
+  size_t push_tab(const void* p, size_t n) {
+    const size_t off = h_tab.size();
+    h_tab.resize(align256(off + n));
+    if (p && n) std::memcpy(h_tab.data() + off, p, n);
+    return off;
+  }
+  // output block of node z at level l (C itself at the root; a shared zero block for nodes this
+  // shard does not compute)
+  View out_view(int l, long long z) const {
+    if (l == 0) return View{cur_C, cur_ldc, 1.0};
+    if (offM[l][z] >= 0) return View{ws + offM[l][z], ldM[l], 1.0};
+    return View{offZero[l] >= 0 ? ws + offZero[l] : nullptr, ldM[l], 1.0};
+  }
+
   // Build every launch and its table for the given execute arguments (row-major orientation).
   void build(const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc, bool lazy_kernels);
   // Replace the level-L formation, leaf GEMM and level-L assembly launches by one fused launch.
   void fuse_leaf_level(bool lazy_kernels);
+  // Collapsed levels L-1 and L (sec. 6c): one formation launch per side and one assembly launch
+  // over the level-(L-2) nodes.
+  void emit_two_level_formation(bool lazy_kernels);
+  void emit_two_level_assembly(bool lazy_kernels);
 };
 
 View fmm_plan_s::opA(int l, long long z, const View& root) const {
   if (l == 0) return root;
   const int r = (int)(z % R);
+  if (collapse && l == L) {  // leaf of two collapsed levels: relative to the grandparent
+    const int r1 = (int)((z / R) % R);
+    const View g = opA(L - 2, z / R / R, root);
+    const double sig = g.sigma * (idxU[r1] < 0 ? coefU[r1] : 1.0) * (idxU[r] < 0 ? coefU[r] : 1.0);
+    if (idxU[r1] >= 0 || idxU[r] >= 0) return View{offS[l][z] >= 0 ? ws + offS[l][z] : nullptr, ldS[l], sig};
+    const int i1 = singU[r1], i2 = singU[r];
+    const Dims &d1 = dims[L - 1], &d2 = dims[L];
+    const long long off = (i1 / alg->K) * d1.P * g.ld + (i1 % alg->K) * d1.Q + (i2 / alg->K) * d2.P * g.ld + (i2 % alg->K) * d2.Q;
+    return View{g.ptr ? g.ptr + off : nullptr, g.ld, sig};
+  }
   const View par = opA(l - 1, z / R, root);
   if (idxU[r] >= 0) return View{offS[l][z] >= 0 ? ws + offS[l][z] : nullptr, ldS[l], par.sigma};
   const int i = singU[r];
@@ -316,6 +354,16 @@ View fmm_plan_s::opA(int l, long long z, const View& root) const {
 View fmm_plan_s::opB(int l, long long z, const View& root) const {
   if (l == 0) return root;
   const int r = (int)(z % R);
+  if (collapse && l == L) {
+    const int r1 = (int)((z / R) % R);
+    const View g = opB(L - 2, z / R / R, root);
+    const double sig = g.sigma * (idxV[r1] < 0 ? coefV[r1] : 1.0) * (idxV[r] < 0 ? coefV[r] : 1.0);
+    if (idxV[r1] >= 0 || idxV[r] >= 0) return View{offT[l][z] >= 0 ? ws + offT[l][z] : nullptr, ldT[l], sig};
+    const int j1 = singV[r1], j2 = singV[r];
+    const Dims &d1 = dims[L - 1], &d2 = dims[L];
+    const long long off = (j1 / alg->N) * d1.Q * g.ld + (j1 % alg->N) * d1.N + (j2 / alg->N) * d2.Q * g.ld + (j2 % alg->N) * d2.N;
+    return View{g.ptr ? g.ptr + off : nullptr, g.ld, sig};
+  }
   const View par = opB(l - 1, z / R, root);
   if (idxV[r] >= 0) return View{offT[l][z] >= 0 ? ws + offT[l][z] : nullptr, ldT[l], par.sigma};
   const int j = singV[r];
@@ -330,8 +378,8 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
                        bool lazy_kernels) {
   launches.clear();
   h_tab.clear();
+  cur_A = A, cur_B = B, cur_C = C, cur_lda = lda, cur_ldb = ldb, cur_ldc = ldc;
   const View rootA{const_cast<double*>(A), lda, 1.0}, rootB{const_cast<double*>(B), ldb, 1.0};
-  const View rootC{C, ldc, 1.0};
   const int M = alg->M, K = alg->K, Nb = alg->N;
   auto push = [&](const void* p, size_t n) {
     size_t off = h_tab.size();
@@ -397,15 +445,16 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
       launches.push_back(ln);
     }
   };
-  auto outView = [&](int l, long long z) -> View {
-    if (l == 0) return rootC;
-    if (offM[l][z] >= 0) return View{ws + offM[l][z], ldM[l], 1.0};
-    return View{offZero[l] >= 0 ? ws + offZero[l] : nullptr, ldM[l], 1.0};
-  };
+  auto outView = [&](int l, long long z) -> View { return out_view(l, z); };
 
   // ---- formation, levels 1..L ----
   for (int l = 1; l <= L; ++l) {
     const Dims& d = dims[l];
+    if (collapse && l == L) break;  // emitted with level L-1
+    if (collapse && l == L - 1) {
+      emit_two_level_formation(lazy_kernels);
+      break;
+    }
     for (int side = 0; side < 2; ++side) {
       const auto& form = side == 0 ? formU : formV;
       if (form.empty()) continue;
@@ -503,7 +552,8 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
   for (int l = L; l >= 1; --l) {
     const Dims& d = dims[l];
     const Dims& dp = dims[l - 1];
-    if (d.P > 0 && d.N > 0) {
+    if (collapse && l == L) emit_two_level_assembly(lazy_kernels);
+    if (!(collapse && l >= L - 1) && d.P > 0 && d.N > 0) {
       std::vector<char> tab;
       std::vector<int> node_ids;
       const int nin = R, nout = M * Nb;
@@ -772,6 +822,143 @@ void fmm_plan_s::fuse_leaf_level(bool lazy_kernels) {
   launches.swap(keep);
 }
 
+void fmm_plan_s::emit_two_level_formation(bool lazy_kernels) {
+  const int M = alg->M, K = alg->K, Nb = alg->N;
+  const Dims &d1 = dims[L - 1], &d2 = dims[L];
+  const View rootA{const_cast<double*>(cur_A), cur_lda, 1.0}, rootB{const_cast<double*>(cur_B), cur_ldb, 1.0};
+  for (int side = 0; side < 2; ++side) {
+    const int rows = side == 0 ? M * K : K * Nb, inner = side == 0 ? K : Nb;
+    const auto& idx = side == 0 ? idxU : idxV;
+    const long long brow = side == 0 ? d2.P : d2.Q, bcol = side == 0 ? d2.Q : d2.N;
+    if (brow <= 0 || bcol <= 0) continue;
+    std::vector<char> mat((size_t)R * R, 0);
+    bool any_mat = false;
+    for (int r1 = 0; r1 < R; ++r1)
+      for (int r2 = 0; r2 < R; ++r2) any_mat |= (mat[(size_t)r1 * R + r2] = (idx[r1] >= 0 || idx[r2] >= 0));
+    if (!any_mat) continue;
+    const int nin = rows * rows, nout = R * R;
+    const size_t nb = lincomb_node_bytes(nin, nout);
+    std::vector<char> tab;
+    std::vector<int> node_ids;
+    bool aligned = (bcol % 2) == 0;
+    int count = 0;
+    double writes = 0;
+    for (long long zg = 0; zg < nodes_at[L - 2]; ++zg) {
+      if (!needed[L - 2][zg]) continue;
+      const View g = side == 0 ? opA(L - 2, zg, rootA) : opB(L - 2, zg, rootB);
+      std::vector<char> e(nb, 0);
+      auto** in = reinterpret_cast<const double**>(e.data());
+      auto** out = reinterpret_cast<double**>(e.data() + sizeof(void*) * nin);
+      auto* lds = reinterpret_cast<long long*>(e.data() + sizeof(void*) * (nin + nout));
+      bool anyout = false;
+      for (int i1 = 0; i1 < rows; ++i1)
+        for (int i2 = 0; i2 < rows; ++i2) {
+          const long long off = side == 0 ? (i1 / inner) * d1.P * g.ld + (i1 % inner) * d1.Q + (i2 / inner) * d2.P * g.ld + (i2 % inner) * d2.Q
+                                          : (i1 / inner) * d1.Q * g.ld + (i1 % inner) * d1.N + (i2 / inner) * d2.Q * g.ld + (i2 % inner) * d2.N;
+          in[i1 * rows + i2] = g.ptr + off;
+          aligned &= ((reinterpret_cast<uintptr_t>(in[i1 * rows + i2]) & 15) == 0);
+        }
+      for (int q = 0; q < nout; ++q) {
+        const long long z = (zg * R + q / R) * R + q % R;
+        const long long offv = side == 0 ? offS[L][z] : offT[L][z];
+        out[q] = mat[(size_t)q] && needed[L][z] && offv >= 0 ? ws + offv : nullptr;
+        if (out[q]) writes += 1, anyout = true;
+      }
+      if (!anyout) continue;
+      lds[0] = g.ld;
+      lds[1] = side == 0 ? ldS[L] : ldT[L];
+      aligned &= (lds[0] % 2 == 0) && (lds[1] % 2 == 0);
+      tab.insert(tab.end(), e.begin(), e.end());
+      node_ids.push_back((int)zg);
+      ++count;
+    }
+    if (!count) continue;
+    TwoLevelSpec sp;
+    sp.side = side;
+    sp.rows = rows;
+    sp.R = R;
+    sp.X = side == 0 ? alg->Ud : alg->Vd;
+    sp.materialize = mat;
+    sp.vec = aligned ? 2 : 1;
+    Launch ln;
+    ln.kind = side == 0 ? Launch::FORM_A : Launch::FORM_B;
+    ln.level = L - 1;
+    ln.count = count;
+    ln.rows = brow;
+    ln.cols = bcol;
+    ln.aligned16 = aligned;
+    ln.node_ids = node_ids;
+    ln.kern = twolevel_get(sp);  // cheap when cached; needed for the cost numbers in dry builds too
+    const LincombCost c = lincomb_cost(*ln.kern);
+    const double elems = (double)brow * bcol;
+    ln.elem_adds = c.adds_per_elem * elems * count;
+    ln.elem_reads = c.reads_per_elem * elems * count;
+    ln.elem_writes = writes * elems;
+    ln.table_off = push_tab(tab.data(), tab.size());
+    launches.push_back(ln);
+  }
+  (void)lazy_kernels;
+}
+
+void fmm_plan_s::emit_two_level_assembly(bool lazy_kernels) {
+  const int M = alg->M, Nb = alg->N;
+  const Dims &d1 = dims[L - 1], &d2 = dims[L];
+  if (d2.P <= 0 || d2.N <= 0) return;
+  const int rows = M * Nb, nin = R * R, nout = rows * rows;
+  const size_t nb = lincomb_node_bytes(nin, nout);
+  std::vector<char> tab;
+  std::vector<int> node_ids;
+  bool aligned = (d2.N % 2) == 0;
+  int count = 0;
+  for (long long zg = 0; zg < nodes_at[L - 2]; ++zg) {
+    if (!needed[L - 2][zg]) continue;
+    const View par = out_view(L - 2, zg);
+    std::vector<char> e(nb, 0);
+    auto** in = reinterpret_cast<const double**>(e.data());
+    auto** out = reinterpret_cast<double**>(e.data() + sizeof(void*) * nin);
+    auto* lds = reinterpret_cast<long long*>(e.data() + sizeof(void*) * (nin + nout));
+    for (int q = 0; q < nin; ++q) {
+      in[q] = out_view(L, zg * R * R + q).ptr;
+      aligned &= ((reinterpret_cast<uintptr_t>(in[q]) & 15) == 0);
+    }
+    for (int k1 = 0; k1 < rows; ++k1)
+      for (int k2 = 0; k2 < rows; ++k2) {
+        out[k1 * rows + k2] = par.ptr + (k1 / Nb) * d1.P * par.ld + (k1 % Nb) * d1.N + (k2 / Nb) * d2.P * par.ld + (k2 % Nb) * d2.N;
+        aligned &= ((reinterpret_cast<uintptr_t>(out[k1 * rows + k2]) & 15) == 0);
+      }
+    lds[0] = ldM[L];
+    lds[1] = par.ld;
+    aligned &= (lds[0] % 2 == 0) && (lds[1] % 2 == 0);
+    tab.insert(tab.end(), e.begin(), e.end());
+    node_ids.push_back((int)zg);
+    ++count;
+  }
+  if (!count) return;
+  TwoLevelSpec sp;
+  sp.side = 2;
+  sp.rows = rows;
+  sp.R = R;
+  sp.X = alg->Wd;
+  sp.vec = aligned ? 2 : 1;
+  Launch ln;
+  ln.kind = Launch::ASSEMBLE;
+  ln.level = L - 1;
+  ln.count = count;
+  ln.rows = d2.P;
+  ln.cols = d2.N;
+  ln.aligned16 = aligned;
+  ln.node_ids = node_ids;
+  ln.kern = twolevel_get(sp);
+  const LincombCost c = lincomb_cost(*ln.kern);
+  const double elems = (double)d2.P * d2.N;
+  ln.elem_adds = c.adds_per_elem * elems * count;
+  ln.elem_reads = c.reads_per_elem * elems * count;
+  ln.elem_writes = c.writes_per_elem * elems * count;
+  ln.table_off = push_tab(tab.data(), tab.size());
+  launches.push_back(ln);
+  (void)lazy_kernels;
+}
+
 namespace {
 
 void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long long Nc, int levels,
@@ -854,6 +1041,16 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
   };
   cols(a->Ud, M * K, p->formU, p->idxU, p->singU, p->coefU);
   cols(a->Vd, K * Nb, p->formV, p->idxV, p->singV, p->coefV);
+  // collapse the last two levels (sec. 6c) where the streaming two-level pass applies: small base
+  // case (the pass keeps (MK)^2 inputs in registers), no peeling at level L-1 (its strips would
+  // need the level-(L-1) operands the pass never writes)
+  {
+    const char* e = getenv("FMM_NO_COLLAPSE");
+    const Dims& dl = p->dims[L >= 1 ? L - 1 : 0];
+    p->collapse = p->opt.collapse_levels && !(e && e[0] == '1') && L >= 2 && p->opt.strategy == FMM_ADD_STREAMING &&
+                  M * K <= 4 && K * Nb <= 4 && M * Nb <= 4 && dl.P1 == dl.P && dl.Q1 == dl.Q && dl.N1 == dl.N;
+    if (p->collapse) p->fuse = false;
+  }
   p->setup_sharding();
   p->setup_workspace();
   // compile the streaming/write-once kernels for the 16-byte variant now (NVRTC)
@@ -1012,7 +1209,8 @@ void fmm_plan_options_default(fmm_plan_options* o) {
   o->shard_count = 1;
   o->workspace_limit_bytes = 0;
   o->peel_align = 1;
-  o->fuse_leaf_level = 0;  // experimental until the fused addition CTAs beat the separate kernels
+  o->fuse_leaf_level = 0;  // within +-2 % of the separate kernels on B200
+  o->collapse_levels = 1;
 }
 
 fmm_status_t fmm_plan_create(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels,
@@ -1122,15 +1320,39 @@ double predict_seconds(const fmm_alg& a, long long P, long long Q, long long N, 
     ++L;
   }
   if (used_levels) *used_levels = L;
+  // collapsed last two levels (collapse_levels, as plan_init decides it)
+  const bool collapse = L >= 2 && M * K <= 4 && K * Nb <= 4 && M * Nb <= 4 && dims[L - 1].P1 == dims[L - 1].P &&
+                        dims[L - 1].Q1 == dims[L - 1].Q && dims[L - 1].N1 == dims[L - 1].N;
+  auto materialized = [&](const std::vector<double>& X, int rows) {
+    std::vector<int> sing(R);
+    for (int r = 0; r < R; ++r) {
+      int nz = 0;
+      for (int i = 0; i < rows; ++i) nz += X[(size_t)i * R + r] != 0.0;
+      sing[r] = nz == 1;
+    }
+    int n = 0;
+    for (int r1 = 0; r1 < R; ++r1)
+      for (int r2 = 0; r2 < R; ++r2) n += !(sing[r1] && sing[r2]);
+    return n;
+  };
   double nodes = 1, t = 0;
   for (int l = 1; l <= L; ++l) {
     const D& c = dims[l];
     const D& pd = dims[l - 1];
     // formation and assembly of level l (streaming bytes)
-    const double bytes = 8.0 * nodes *
-                         ((double)(M * K + fu) * c.P * c.Q * (fu > 0) + (double)(K * Nb + fv) * c.Q * c.N * (fv > 0) +
-                          (double)(R + M * Nb) * c.P * c.N);
-    t += bytes / cm.add_bw + cm.launch * (1 + (fu > 0) + (fv > 0));
+    double bytes = 8.0 * nodes *
+                   ((double)(M * K + fu) * c.P * c.Q * (fu > 0) + (double)(K * Nb + fv) * c.Q * c.N * (fv > 0) +
+                    (double)(R + M * Nb) * c.P * c.N);
+    if (collapse && l == L - 1) {
+      const D& c2 = dims[L];
+      bytes = 8.0 * nodes *
+              ((double)(M * K * M * K + materialized(a.Ud, M * K)) * c2.P * c2.Q +
+               (double)(K * Nb * K * Nb + materialized(a.Vd, K * Nb)) * c2.Q * c2.N +
+               (double)(R * R + M * Nb * M * Nb) * c2.P * c2.N);
+    } else if (collapse && l == L) {
+      bytes = 0;
+    }
+    t += bytes / cm.add_bw + (collapse && l == L ? 0.0 : cm.launch * (1 + (fu > 0) + (fv > 0)));
     // peel strips of the level-(l-1) nodes
     t += gemm_time(nodes, pd.P1, pd.N1, pd.Q - pd.Q1, cm);
     t += gemm_time(nodes, pd.P - pd.P1, pd.N, pd.Q, cm);
@@ -1248,6 +1470,7 @@ fmm_status_t fmm_plan_stats_ex(const fmm_plan_t* p, double out[16]) {
     if (ln.kind == Launch::ASSEMBLE) s[12] += bytes;
     if (!leaf && (ln.kind == Launch::STRIPS || ln.kind == Launch::SKINNY)) s[13] += ln.flops;
   }
+  s[14] = p->collapse ? 1.0 : 0.0;
   std::memcpy(out, s, sizeof(s));
   return FMM_OK;
   FMM_API_END

@@ -30,7 +30,7 @@ class _Options(ctypes.Structure):
     _fields_ = [("layout", ctypes.c_int), ("strategy", ctypes.c_int), ("cse", ctypes.c_int),
                 ("shard_rank", ctypes.c_int), ("shard_count", ctypes.c_int),
                 ("workspace_limit_bytes", ctypes.c_size_t), ("peel_align", ctypes.c_int),
-                ("fuse_leaf_level", ctypes.c_int)]
+                ("fuse_leaf_level", ctypes.c_int), ("collapse_levels", ctypes.c_int)]
 
 
 def _load():
@@ -195,7 +195,7 @@ class Plan:
     def __init__(self, alg: Algorithm, P: int, Q: int, N: int, levels: int, layout: str = "row",
                  strategy: str = "streaming", cse: bool = True, shard_rank: int = 0, shard_count: int = 1,
                  device: Optional[int] = None, workspace_limit_bytes: int = 0, peel_align: bool = True,
-                 fuse: bool = False):
+                 fuse: bool = False, collapse: bool = True):
         import torch
         self.alg, self.P, self.Q, self.N, self.levels = alg, P, Q, N, levels
         self.layout = ROW_MAJOR if layout == "row" else COL_MAJOR
@@ -208,6 +208,7 @@ class Plan:
         o.workspace_limit_bytes = workspace_limit_bytes
         o.peel_align = int(bool(peel_align))
         o.fuse_leaf_level = int(bool(fuse))
+        o.collapse_levels = int(bool(collapse))
         self.device = torch.cuda.current_device() if device is None else device
         h = ctypes.c_void_p()
         _check(_lib.fmm_plan_create(alg._h, P, Q, N, levels, ctypes.byref(o), self.device, ctypes.byref(h)))
@@ -228,7 +229,8 @@ class Plan:
         s = (ctypes.c_double * 16)()
         _check(_lib.fmm_plan_stats_ex(self._h, s))
         keys = ["gemm_flops", "add_flops", "add_bytes", "gemm_bytes", "launches", "levels", "leaves", "paper_flops",
-                "leaf_flops", "fused_add_bytes", "fused_launches", "formation_bytes", "assembly_bytes", "strip_flops"]
+                "leaf_flops", "fused_add_bytes", "fused_launches", "formation_bytes", "assembly_bytes", "strip_flops",
+                "collapsed"]
         return dict(zip(keys, list(s)))
 
     def new_output(self):

@@ -1,0 +1,90 @@
+"""Collapsed levels (collapse_levels = 1): the formation and assembly of the last
+two recursion levels in one streaming pass each; the level-(L-1) S_r, T_r, M_r are never written.
+
+The two-level chains are the oracle's two levels in the oracle's order, so with CSE off the
+collapsed and the one-level-per-launch schedules agree bitwise; both meet the north-star tolerance
+against the oracle; integer inputs are exact; leaf shards still sum to the product; a plan that
+cannot collapse (peeling at level L-1, a large base case, write-once) silently uses the separate
+kernels.
+"""
+import numpy as np
+import pytest
+
+import fmm_inputs as I
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _lib():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1409_2908_b200 as F
+    return F
+
+
+def _run(F, name, A, B, L, layout="row", **kw):
+    import torch
+    P, Q = A.shape
+    N = B.shape[1]
+
+    def dev(x):
+        if layout == "row":
+            return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+        return torch.from_numpy(np.ascontiguousarray(x.T)).cuda().t()
+    p = F.Plan(F.load_alg(name), P, Q, N, L, layout=layout, **kw)
+    C = p.execute(dev(A), dev(B))
+    torch.cuda.synchronize()
+    return C.cpu().numpy(), p.stats()
+
+
+CASES = [("strassen_222_7", 256, 256, 256, 2, "row"), ("winograd_class_222_7", 1024, 1024, 1024, 2, "col"),
+         ("winograd_class_222_7", 2048, 512, 1536, 2, "row"), ("strassen_222_7", 1000, 992, 1008, 2, "row"),  # odd-width leaves
+         ("strassen_222_7", 1024, 512, 768, 3, "col"), ("winograd_class_222_7", 64, 64, 64, 2, "row")]
+
+
+@pytest.mark.parametrize("name,P,Q,N,L,layout", CASES)
+def test_collapsed_equals_separate_and_oracle(name, P, Q, N, L, layout):
+    F = _lib()
+    A, B = I.problem(P, Q, N, seed=P + L)
+    Cc, sc = _run(F, name, A, B, L, layout, cse=False, collapse=True)
+    Cs, ss = _run(F, name, A, B, L, layout, cse=False, collapse=False)
+    assert sc["add_bytes"] < ss["add_bytes"] and sc["launches"] < ss["launches"]  # it did collapse
+    assert np.array_equal(Cc, Cs)
+    nrm = np.linalg.norm(A) * np.linalg.norm(B)
+    assert np.max(np.abs(Cc - O.fast(A, B, O.load_alg(F.alg_path(name)), L))) <= 1e-12 * nrm
+    assert np.max(np.abs(Cc - O.classical(A, B))) <= 1e-10 * nrm
+
+
+@pytest.mark.parametrize("name", ["strassen_222_7", "winograd_class_222_7"])
+def test_collapsed_integer_exact(name):
+    F = _lib()
+    A, B = I.problem(384, 256, 320, seed=3, kind="integers")
+    C, st = _run(F, name, A, B, 2)
+    assert np.array_equal(C, A @ B)
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_collapsed_shards_sum_to_product(G):
+    F = _lib()
+    A, B = I.problem(256, 192, 320, seed=8, kind="integers")
+    total = np.zeros((256, 320))
+    for g in range(G):
+        C, _ = _run(F, "winograd_class_222_7", A, B, 2, shard_rank=g, shard_count=G)
+        total += C
+    assert np.array_equal(total, A @ B)
+
+
+def test_not_collapsed_where_it_does_not_apply():
+    F = _lib()
+    A, B = I.problem(250, 250, 250, seed=4, kind="integers")  # 250 -> 125: peeled at level 1 = L-1
+    Ca, sa = _run(F, "strassen_222_7", A, B, 2, collapse=True)
+    Cb, sb = _run(F, "strassen_222_7", A, B, 2, collapse=False)
+    assert sa["launches"] == sb["launches"] and np.array_equal(Ca, A @ B) and np.array_equal(Cb, A @ B)
+    A, B = I.problem(270, 180, 270, seed=5, kind="integers")  # <3,2,3>: base case too large
+    Ca, sa = _run(F, "hk_class_323_15", A, B, 2, collapse=True)
+    _, sb = _run(F, "hk_class_323_15", A, B, 2, collapse=False)
+    assert sa["launches"] == sb["launches"] and np.array_equal(Ca, A @ B)
+    A, B = I.problem(256, 256, 256, seed=6, kind="integers")  # write-once strategy
+    Ca, sa = _run(F, "strassen_222_7", A, B, 2, strategy="write_once")
+    assert np.array_equal(Ca, A @ B)

@@ -26,7 +26,7 @@ for name, P, Q, N, L, lay in cases:
     alg = F.load_alg(name)
     res = {}
     for fuse in (True, False):
-        p = F.Plan(alg, P, Q, N, L, layout=lay, cse=False, fuse=fuse)
+        p = F.Plan(alg, P, Q, N, L, layout=lay, cse=False, fuse=fuse, collapse=False)
         C = p.execute(dev(A), dev(B))
         torch.cuda.synchronize()
         t0 = time.time()

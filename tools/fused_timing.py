@@ -15,7 +15,7 @@ A_np, B_np = bench.gen_inputs(w)
 A = bench.to_device(A_np, w["layout"], "cuda")
 B = bench.to_device(B_np, w["layout"], "cuda")
 fuse = os.environ.get("FMM_NO_FUSE", "0") != "1"
-p = F.Plan(F.load_alg(w["alg"]), w["P"], w["Q"], w["N"], w["L"], layout=w["layout"], fuse=fuse)
+p = F.Plan(F.load_alg(w["alg"]), w["P"], w["Q"], w["N"], w["L"], layout=w["layout"], fuse=fuse, collapse=os.environ.get("FMM_NO_COLLAPSE", "0") != "1" and not fuse)
 C = p.new_output()
 for _ in range(3):
     p.execute(A, B, C)
