@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -1548,11 +1550,14 @@ static void host_async(fmm_plan_t* p, const double* A, long long lda, const doub
     }
   }
   const int b = (int)(p->host_iter++ & 1);
-  if (!p->sA[b]) {
-    FMM_CUDA(cudaMalloc(&p->sA[b], std::max<size_t>(8, (size_t)aR * aC * 8)));
-    FMM_CUDA(cudaMalloc(&p->sB[b], std::max<size_t>(8, (size_t)bR * bC * 8)));
-    FMM_CUDA(cudaMalloc(&p->sC[b], std::max<size_t>(8, (size_t)cR * cC * 8)));
+  if (!p->sA[0]) {  // both staging sets at once: a cudaMalloc later would stall the pipeline
+    for (int q = 0; q < 2; ++q) {
+      FMM_CUDA(cudaMalloc(&p->sA[q], std::max<size_t>(8, (size_t)aR * aC * 8)));
+      FMM_CUDA(cudaMalloc(&p->sB[q], std::max<size_t>(8, (size_t)bR * bC * 8)));
+      FMM_CUDA(cudaMalloc(&p->sC[q], std::max<size_t>(8, (size_t)cR * cC * 8)));
+    }
   }
+
   // copy in, once compute i-2 has released set b
   FMM_CUDA(cudaStreamWaitEvent(p->s_in, p->ev_comp[b], 0));
   if (aR && aC) FMM_CUDA(cudaMemcpy2DAsync(p->sA[b], aC * 8, A, lda * 8, aC * 8, aR, cudaMemcpyHostToDevice, p->s_in));

@@ -28,3 +28,8 @@ def pipe(k=6):
     for _ in range(k): plan.execute_host(At, Bt, Ct, asynchronous=True)
     plan.sync()
 print(json.dumps({"pipelined_ms_per_step": wall(pipe, reps=2) / 6}))
+s_user = torch.cuda.Stream()
+def pipe_stream(k=6):
+    for _ in range(k): plan.execute_host(At, Bt, Ct, asynchronous=True, stream=s_user)
+    plan.sync()
+print(json.dumps({"pipelined_ms_per_step_user_stream": wall(pipe_stream, reps=2) / 6}))
