@@ -1049,6 +1049,8 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
   {
     const char* e = getenv("FMM_NO_COLLAPSE");
     const Dims& dl = p->dims[L >= 1 ? L - 1 : 0];
+    // (a variant reloading the inputs of larger base cases from L1/L2 was measured 2-40 % slower
+    // than one level per launch on c4, c5, c5t: the pass is only worth it with every input in registers)
     p->collapse = p->opt.collapse_levels && !(e && e[0] == '1') && L >= 2 && p->opt.strategy == FMM_ADD_STREAMING &&
                   M * K <= 4 && K * Nb <= 4 && M * Nb <= 4 && dl.P1 == dl.P && dl.Q1 == dl.Q && dl.N1 == dl.N;
     if (p->collapse) p->fuse = false;
