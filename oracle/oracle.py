@@ -19,6 +19,10 @@ Contents
       fast(A, B, alg, L)          the recursive evaluation with peeling
       fast_entries(A, B, alg, L, rows, cols)  sampled entries of exactly fast(...)
       flops(P,Q,N, alg, L)        operation count of fast(...)
+  * error_bound(alg, Q, L, a, b)  a worst-case forward error bound on max|fl(C) - C| derived from
+                                  (U, V, W) ("theoretical bounds can be derived from each
+                                  algorithm's <U,V,W> representation"); pins check (d) of SURVEY 8(c)
+                                  in place of the empirical growth figure the paper does not state.
 """
 from __future__ import annotations
 
@@ -328,3 +332,61 @@ def classical_entries(A: np.ndarray, B: np.ndarray, rows, cols) -> np.ndarray:
 def flops(P: int, Q: int, Nc: int, alg: Alg, L: int) -> float:
     U, V, W = _alg_arrays(alg)
     return _L().oracle_flops(P, Q, Nc, alg.M, alg.K, alg.N, alg.R, _dp(U), _dp(V), _dp(W), L)
+
+
+# --------------------------------------------------------------------------------------------
+# check (d): a worst-case forward error bound derived from (U, V, W)
+# --------------------------------------------------------------------------------------------
+UNIT_ROUNDOFF = 2.0 ** -53
+
+
+def _gamma(n: int) -> float:
+    """gamma_n = n u / (1 - n u): the standard bound for n roundings in a sum or product chain."""
+    nu = n * UNIT_ROUNDOFF
+    return nu / (1.0 - nu)
+
+
+def _chain_roundings(coefs) -> int:
+    """Roundings of a chain sum_i c_i x_i evaluated term by term: one per addition, plus one per
+    product c_i x_i whose coefficient is not a power of two (those products are exact)."""
+    nz = [Fraction(c) for c in coefs if c != 0]
+    def pow2(c):
+        c = abs(c)
+        return c.numerator & (c.numerator - 1) == 0 and c.denominator & (c.denominator - 1) == 0
+    return max(0, len(nz) - 1) + sum(0 if pow2(c) else 1 for c in nz)
+
+
+def error_bound(alg: Alg, Q: int, L: int, a: float = 1.0, b: float = 1.0) -> float:
+    """Upper bound on max_ij |fl(C)_ij - (AB)_ij| for L recursive steps of `alg` (no peeling: Q a
+    multiple of K^L) with ||A||_max <= a, ||B||_max <= b, any summation order inside each chain
+    and a classical leaf of inner dimension Q / K^L (dot products with or without FMA).
+    Recursion (max-norm, first order in the roundings but with exact gamma factors):
+      leaf:  gamma_q q a b
+      level: S_r = sum_i u_ir A_i  ->  |S_r| <= ||u_r||_1 a,  |fl(S_r) - S_r| <= gamma_{n_r} ||u_r||_1 a
+             M_r = S_r T_r (recursively, on the rounded operands), plus the operand-error term
+             q' (eS (|T| + eT) + |S| eT);   C_k = sum_r w_kr M_r rounded by gamma_{n_k}."""
+    K = alg.K
+    if L == 0:
+        return _gamma(Q) * Q * a * b
+    assert Q % K == 0, "error_bound covers unpeeled shapes"
+    q = Q // K
+    R = alg.R
+    errM, magM = [], []
+    for r in range(R):
+        ucol = [alg.U[i][r] for i in range(alg.M * alg.K)]
+        vcol = [alg.V[j][r] for j in range(alg.K * alg.N)]
+        sa = float(sum(abs(Fraction(c)) for c in ucol)) * a
+        tb = float(sum(abs(Fraction(c)) for c in vcol)) * b
+        ea = _gamma(_chain_roundings(ucol)) * sa
+        eb = _gamma(_chain_roundings(vcol)) * tb
+        inner = error_bound(alg, q, L - 1, sa + ea, tb + eb)
+        errM.append(inner + q * (ea * (tb + eb) + sa * eb))
+        magM.append(q * sa * tb)
+    worst = 0.0
+    for k in range(alg.M * alg.N):
+        wrow = [alg.W[k][r] for r in range(R)]
+        absw = [float(abs(Fraction(c))) for c in wrow]
+        e = sum(w * em for w, em in zip(absw, errM))
+        e += _gamma(_chain_roundings(wrow)) * sum(w * (m + em) for w, m, em in zip(absw, magM, errM))
+        worst = max(worst, e)
+    return worst

@@ -270,3 +270,17 @@ def test_execute_host_async_pipeline():
     p.sync()
     for (Ah, Bh, Ch), ref in zip(outs, refs):
         assert np.max(np.abs(Ch.numpy() - ref)) <= bound(Ah.numpy(), Bh.numpy(), 1e-12)
+
+
+# ---- check (d) on the GPU: the error stays within the bound derived from (U, V, W) -------------
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("L", [1, 2])
+@pytest.mark.parametrize("layout", ["row", "col"])
+def test_gpu_error_within_derived_bound(name, L, layout):
+    a = oalg(name)
+    P, Q, N = a.M ** L * 40, a.K ** L * 48, a.N ** L * 36
+    A, B = I.problem(P, Q, N, seed=40 + L)
+    C, _ = run(name, A, B, L, layout=layout)
+    exact = A.astype(np.longdouble) @ B.astype(np.longdouble)
+    err = float(np.max(np.abs(C.astype(np.longdouble) - exact)))
+    assert err <= O.error_bound(a, Q, L, float(np.abs(A).max()), float(np.abs(B).max()))

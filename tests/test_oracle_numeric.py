@@ -144,3 +144,54 @@ def test_flop_count_closed_forms():
         n = 2 ** k
         assert O.flops(n, n, n, s, 0) == 2 * n ** 3 - n ** 2
         assert O.flops(n, n, n, s, k) == round(7 * n ** math.log2(7) - 6 * n ** 2)
+
+
+# ---- check (d): error growth within the bound derived from (U, V, W) ------------
+def _higham_strassen(n, n0):
+    """Higham, Accuracy and Stability of Numerical Algorithms (cited at P:80), the Strassen bound:
+    ||C - fl(C)||_max <= [(n/n0)^log2(12) (n0^2 + 5 n0) - 5 n] u ||A||_max ||B||_max + O(u^2)."""
+    return ((n / n0) ** np.log2(12) * (n0 * n0 + 5 * n0) - 5 * n) * 2.0 ** -53
+
+
+@pytest.mark.parametrize("n0", [16, 64, 256])
+@pytest.mark.parametrize("L", [1, 2, 3])
+def test_error_bound_reduces_to_highams_strassen_bound(n0, L):
+    a = O.load_alg(os.path.join(ALGS, "strassen_222_7.txt"))
+    n = n0 * 2 ** L
+    ours, textbook = O.error_bound(a, n, L), _higham_strassen(n, n0)
+    # the leading terms agree; ours counts left-to-right chains (3 additions in C11 / C22), so its
+    # O(n0) lower-order term is slightly larger, never smaller
+    assert 1.0 <= ours / textbook < 1.05
+
+
+def test_error_bound_classical_leaf():
+    a = O.load_alg(os.path.join(ALGS, "strassen_222_7.txt"))
+    for q in (1, 7, 1000):
+        assert O.error_bound(a, q, 0, 2.0, 3.0) == pytest.approx(q * 2.0 ** -53 / (1 - q * 2.0 ** -53) * q * 6.0)
+
+
+def _exact(A, B):
+    return (A.astype(np.longdouble) @ B.astype(np.longdouble))
+
+
+@pytest.mark.parametrize("name", sorted(ALGS_BY_NAME))
+@pytest.mark.parametrize("L", [1, 2])
+def test_fast_error_within_derived_bound(name, L):
+    alg = ALGS_BY_NAME[name]
+    P, Q, N = alg.M ** L * 12, alg.K ** L * 16, alg.N ** L * 12
+    A, B = I.problem(P, Q, N, seed=31 + L)
+    err = float(np.max(np.abs(O.fast(A, B, alg, L).astype(np.longdouble) - _exact(A, B))))
+    bound = O.error_bound(alg, Q, L, float(np.abs(A).max()), float(np.abs(B).max()))
+    assert err <= bound
+    assert bound <= 1e-10 * np.linalg.norm(A) * np.linalg.norm(B)  # consistent with BJ's gate
+
+
+def test_error_bound_catches_a_broken_algorithm():
+    alg = O.load_alg(os.path.join(ALGS, "winograd_class_222_7.txt"))
+    bad = O.Alg(alg.M, alg.K, alg.N, alg.R, [list(r) for r in alg.U], [list(r) for r in alg.V],
+                [list(r) for r in alg.W], name="broken")
+    r = next(r for r in range(alg.R) if bad.W[0][r] != 0)
+    bad.W[0][r] = -bad.W[0][r]  # one flipped sign
+    A, B = I.problem(64, 64, 64, seed=5)
+    err = float(np.max(np.abs(O.fast(A, B, bad, 2).astype(np.longdouble) - _exact(A, B))))
+    assert err > O.error_bound(alg, 64, 2, float(np.abs(A).max()), float(np.abs(B).max()))
