@@ -46,6 +46,7 @@ typedef enum {
 
 typedef struct fmm_alg_s fmm_alg;   /* immutable after creation; safe to share between threads */
 typedef struct fmm_plan_s fmm_plan_t; /* owns its workspace; one fmm_execute in flight per plan */
+typedef struct fmm_comm_s fmm_comm;   /* an NCCL communicator, one rank per process and GPU */
 
 typedef enum { FMM_ROW_MAJOR = 0, FMM_COL_MAJOR = 1 } fmm_layout;
 
@@ -136,6 +137,24 @@ void fmm_alg_destroy(fmm_alg* alg);
    opt may be NULL (defaults). */
 fmm_status_t fmm_plan_create(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels,
                              const fmm_plan_options* opt, int device, fmm_plan_t** out);
+
+/* ---- multi-GPU (not in the paper, P:1126 future work) --------------------------
+   One process per GPU.  Rank 0 calls fmm_nccl_unique_id and shares the 128 bytes with every rank
+   (e.g. torch.distributed.broadcast_object_list); every rank then calls fmm_comm_create on its
+   own GPU.  NCCL is loaded at run time (libnccl.so.2); FMM_E_NCCL if it is unavailable. */
+fmm_status_t fmm_nccl_unique_id(unsigned char id[128]);
+fmm_status_t fmm_comm_create(const unsigned char id[128], int nranks, int rank, int device, fmm_comm** out);
+fmm_status_t fmm_comm_info(const fmm_comm* comm, int* nranks, int* rank);
+void fmm_comm_destroy(fmm_comm* comm);  /* after every plan using it is destroyed */
+
+/* A distributed plan: rank `rank` of `nranks` computes its HYBRID share of the R^L leaves (Sec. 4.3
+   arithmetic, with GPUs in place of threads: opt->shard_rank / shard_count are set from
+   the communicator) into a partial C, and fmm_execute ends with one in-place NCCL sum-reduce of C
+   to `root` on the execute's stream (the C_k combination is linear in the partials).  C must be
+   contiguous (ldc = Nc row-major, ldc = P column-major) on every rank, else FMM_E_UNSUPPORTED at
+   execute.  The result is complete on `root` only.  The plan keeps `comm` (not owned). */
+fmm_status_t fmm_plan_create_dist(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels,
+                                  const fmm_plan_options* opt, fmm_comm* comm, int root, fmm_plan_t** out);
 
 /* Workspace bytes held by the plan. */
 fmm_status_t fmm_plan_workspace_bytes(const fmm_plan_t* plan, size_t* bytes);

@@ -1,0 +1,121 @@
+// a7: the multi-GPU combine inside the library.  One process per GPU; each
+// rank's plan computes its HYBRID leaf share (GPUs in place of threads) into a partial
+// C, and fmm_execute of a distributed plan ends with one in-place ncclReduce (fp64 sum) of C to
+// the root on the execute's stream -- the C_k combination is linear in the partials.
+// NCCL is loaded at run time (dlopen "libnccl.so.2": the copy PyTorch already loaded when present)
+// so the library has no link-time dependency on a particular NCCL build.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <mutex>
+
+#include "fmm_internal.h"
+
+struct fmm_comm_s {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0, device = 0;
+};
+
+namespace fmm {
+namespace {
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+  std::string err;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      api.err = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return;
+    }
+    api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    api.reduce = reinterpret_cast<decltype(api.reduce)>(dlsym(h, "ncclReduce"));
+    api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+    if (!api.get_unique_id || !api.comm_init_rank || !api.comm_destroy || !api.reduce || !api.error_string)
+      api.err = "libnccl.so.2 lacks an expected symbol";
+  });
+  if (!api.err.empty()) throw Error(FMM_E_NCCL, api.err);
+  return api;
+}
+
+void check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw Error(FMM_E_NCCL, std::string(what) + ": " + nccl().error_string(r));
+}
+}  // namespace
+
+void dist_reduce(void* comm, double* C, size_t count, int root, cudaStream_t stream) {
+  check(nccl().reduce(C, C, count, ncclDouble, ncclSum, root, static_cast<ncclComm_t>(comm), stream), "ncclReduce");
+}
+}  // namespace fmm
+
+using namespace fmm;
+
+extern "C" {
+
+fmm_status_t fmm_nccl_unique_id(unsigned char id[128]) {
+  FMM_API_BEGIN
+  if (!id) throw Error(FMM_E_INVALID_ARG, "null argument");
+  ncclUniqueId u;
+  check(nccl().get_unique_id(&u), "ncclGetUniqueId");
+  static_assert(sizeof(u.internal) == 128, "NCCL unique id size");
+  std::memcpy(id, u.internal, 128);
+  return FMM_OK;
+  FMM_API_END
+}
+
+fmm_status_t fmm_comm_create(const unsigned char id[128], int nranks, int rank, int device, fmm_comm** out) {
+  FMM_API_BEGIN
+  if (!id || !out) throw Error(FMM_E_INVALID_ARG, "null argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(FMM_E_INVALID_ARG, "bad rank / nranks");
+  *out = nullptr;
+  FMM_CUDA(cudaSetDevice(device));
+  ncclUniqueId u;
+  std::memcpy(u.internal, id, 128);
+  std::unique_ptr<fmm_comm> c(new fmm_comm);
+  check(nccl().comm_init_rank(&c->comm, nranks, u, rank), "ncclCommInitRank");
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  *out = c.release();
+  return FMM_OK;
+  FMM_API_END
+}
+
+void fmm_comm_destroy(fmm_comm* c) {
+  if (!c) return;
+  try {
+    if (c->comm) nccl().comm_destroy(c->comm);
+  } catch (...) {
+  }
+  delete c;
+}
+
+fmm_status_t fmm_comm_info(const fmm_comm* c, int* nranks, int* rank) {
+  FMM_API_BEGIN
+  if (!c || !nranks || !rank) throw Error(FMM_E_INVALID_ARG, "null argument");
+  *nranks = c->nranks;
+  *rank = c->rank;
+  return FMM_OK;
+  FMM_API_END
+}
+
+}  // extern "C"
+
+// used by fmm_plan.cpp
+namespace fmm {
+void* comm_handle(const fmm_comm* c) { return c ? static_cast<void*>(c->comm) : nullptr; }
+int comm_nranks(const fmm_comm* c) { return c ? c->nranks : 1; }
+int comm_rank(const fmm_comm* c) { return c ? c->rank : 0; }
+int comm_device(const fmm_comm* c) { return c ? c->device : 0; }
+}  // namespace fmm

@@ -65,6 +65,13 @@ struct fmm_alg_s {
 
 namespace fmm {
 
+// multi-GPU combine (fmm_dist.cpp): in-place NCCL sum-reduce of a contiguous C to `root`
+void dist_reduce(void* comm, double* C, size_t count, int root, cudaStream_t stream);
+void* comm_handle(const fmm_comm* c);
+int comm_nranks(const fmm_comm* c);
+int comm_rank(const fmm_comm* c);
+int comm_device(const fmm_comm* c);
+
 fmm_alg* alg_transpose_prop1(const fmm_alg& a);  // Prop. 1: <N,K,M>
 fmm_alg* alg_cycle_prop2(const fmm_alg& a);      // Prop. 2: <N,M,K>
 void alg_validate_exact(const fmm_alg& a);        // throws FMM_E_NOT_EXACT

@@ -80,6 +80,8 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct fmm_plan_s {
   int device = 0;
+  void* dist_comm = nullptr;  // distributed plan: NCCL communicator (not owned) and root
+  int dist_root = 0;
   fmm_plan_options opt{};
   bool colmajor = false;
   std::unique_ptr<fmm_alg> alg_t;  // Prop. 1 transpose (column-major plans)
@@ -1194,6 +1196,11 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
         break;
     }
   }
+  if (p->dist_comm) {  // a7: the partial products of all ranks summed on the root
+    const long long rows = p->colmajor ? p->userN : p->userP, cols = p->colmajor ? p->userP : p->userN;
+    if (rows > 1 && ldc != cols) throw Error(FMM_E_UNSUPPORTED, "a distributed plan needs a contiguous C");
+    if (rows * cols > 0) dist_reduce(p->dist_comm, C, (size_t)rows * cols, p->dist_root, stream);
+  }
   if (timed) {
     for (int q = phase + 1; q <= 3; ++q) FMM_CUDA(cudaEventRecord(evs[q], stream));
   }
@@ -1224,6 +1231,26 @@ fmm_status_t fmm_plan_create(const fmm_alg* alg, int64_t P, int64_t Q, int64_t N
   *out = nullptr;
   std::unique_ptr<fmm_plan_t> p(new fmm_plan_t);
   plan_init(p.get(), alg, P, Q, Nc, levels, opt, device);
+  *out = p.release();
+  return FMM_OK;
+  FMM_API_END
+}
+
+fmm_status_t fmm_plan_create_dist(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels,
+                                  const fmm_plan_options* opt, fmm_comm* comm, int root, fmm_plan_t** out) {
+  FMM_API_BEGIN
+  if (!out || !comm) throw Error(FMM_E_INVALID_ARG, "null argument");
+  if (root < 0 || root >= comm_nranks(comm)) throw Error(FMM_E_INVALID_ARG, "bad root");
+  *out = nullptr;
+  fmm_plan_options o;
+  if (opt) o = *opt;
+  else fmm_plan_options_default(&o);
+  o.shard_rank = comm_rank(comm);
+  o.shard_count = comm_nranks(comm);
+  std::unique_ptr<fmm_plan_t> p(new fmm_plan_t);
+  plan_init(p.get(), alg, P, Q, Nc, levels, &o, comm_device(comm));
+  p->dist_comm = comm_handle(comm);
+  p->dist_root = root;
   *out = p.release();
   return FMM_OK;
   FMM_API_END

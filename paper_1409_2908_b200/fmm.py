@@ -51,6 +51,10 @@ def _load():
         "fmm_plan_stats_ex": [vp, ctypes.POINTER(dp)],
         "fmm_fused_compile_check": [vp, i32, i32, i32],
         "fmm_alg_permute": [vp, i32, ctypes.POINTER(vp)],
+        "fmm_nccl_unique_id": [ctypes.c_char_p],
+        "fmm_comm_create": [ctypes.c_char_p, i32, i32, i32, ctypes.POINTER(vp)],
+        "fmm_comm_info": [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)],
+        "fmm_plan_create_dist": [vp, i64, i64, i64, i32, ctypes.POINTER(_Options), vp, i32, ctypes.POINTER(vp)],
         "fmm_plan_predict": [vp, i64, i64, i64, i32, i32, ctypes.POINTER(dp), ctypes.POINTER(i32)],
         "fmm_select": [vp, i32, i64, i64, i64, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32),
                        ctypes.POINTER(dp)],
@@ -188,6 +192,39 @@ def _stream_ptr(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
+# ---- multi-GPU -------------------------------------------------------------------------------
+def nccl_unique_id() -> bytes:
+    """fmm_nccl_unique_id: 128 bytes for rank 0 to share with every rank."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.fmm_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Comm:
+    """An NCCL communicator owned by the library (fmm_comm_create), one rank per process and GPU."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: Optional[int] = None):
+        import torch
+        self.device = torch.cuda.current_device() if device is None else device
+        h = ctypes.c_void_p()
+        _check(_lib.fmm_comm_create(ctypes.create_string_buffer(uid, 128), nranks, rank, self.device, ctypes.byref(h)))
+        self._h = h
+        self.nranks, self.rank = nranks, rank
+
+    @classmethod
+    def from_torch_distributed(cls, group=None, device: Optional[int] = None) -> "Comm":
+        """Bootstrap through an initialised torch.distributed group (rank 0's id is broadcast)."""
+        import torch.distributed as dist
+        obj = [nccl_unique_id() if dist.get_rank(group) == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(obj[0], dist.get_world_size(group), dist.get_rank(group), device)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.fmm_comm_destroy(self._h)
+            self._h = None
+
+
 # ---- plans ----------------------------------------------------------------------------------
 class Plan:
     """C (P x N) = A (P x Q) @ B (Q x N) with `levels` recursive steps of `alg` (fmm_plan_create)."""
@@ -195,7 +232,7 @@ class Plan:
     def __init__(self, alg: Algorithm, P: int, Q: int, N: int, levels: int, layout: str = "row",
                  strategy: str = "streaming", cse: bool = True, shard_rank: int = 0, shard_count: int = 1,
                  device: Optional[int] = None, workspace_limit_bytes: int = 0, peel_align: bool = True,
-                 fuse: bool = False, collapse: bool = True):
+                 fuse: bool = False, collapse: bool = True, comm: Optional[Comm] = None, root: int = 0):
         import torch
         self.alg, self.P, self.Q, self.N, self.levels = alg, P, Q, N, levels
         self.layout = ROW_MAJOR if layout == "row" else COL_MAJOR
@@ -211,7 +248,12 @@ class Plan:
         o.collapse_levels = int(bool(collapse))
         self.device = torch.cuda.current_device() if device is None else device
         h = ctypes.c_void_p()
-        _check(_lib.fmm_plan_create(alg._h, P, Q, N, levels, ctypes.byref(o), self.device, ctypes.byref(h)))
+        self.comm = comm  # a distributed plan keeps its communicator alive
+        if comm is None:
+            _check(_lib.fmm_plan_create(alg._h, P, Q, N, levels, ctypes.byref(o), self.device, ctypes.byref(h)))
+        else:
+            self.device = comm.device
+            _check(_lib.fmm_plan_create_dist(alg._h, P, Q, N, levels, ctypes.byref(o), comm._h, root, ctypes.byref(h)))
         self._h = h
 
     def __del__(self):

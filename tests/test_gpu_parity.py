@@ -284,3 +284,19 @@ def test_gpu_error_within_derived_bound(name, L, layout):
     exact = A.astype(np.longdouble) @ B.astype(np.longdouble)
     err = float(np.max(np.abs(C.astype(np.longdouble) - exact)))
     assert err <= O.error_bound(a, Q, L, float(np.abs(A).max()), float(np.abs(B).max()))
+
+
+# ---- the library's own multi-GPU combine (fmm_comm_create / fmm_plan_create_dist) -------------
+def test_distributed_plan_single_rank():
+    # one rank: the NCCL reduce to the root is a no-op copy, so the distributed plan must equal the
+    # local one; a non-contiguous C is refused
+    A, B = I.problem(300, 200, 250, seed=21, kind="integers")
+    comm = F.Comm(F.nccl_unique_id(), 1, 0)
+    p = F.Plan(falg("winograd_class_222_7"), 300, 200, 250, 2, comm=comm, root=0)
+    C = p.execute(dev(A), dev(B))
+    torch.cuda.synchronize()
+    assert np.array_equal(C.cpu().numpy(), A @ B)
+    Cb = torch.zeros(300, 260, dtype=torch.float64, device="cuda")
+    with pytest.raises(F.FmmError) as e:
+        p.execute(dev(A), dev(B), Cb[:, :250])
+    assert e.value.status == "FMM_E_UNSUPPORTED"

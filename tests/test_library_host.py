@@ -100,3 +100,11 @@ def test_hybrid_split_matches_paper(F):
         for G in (1, 2, 4, 8):
             b, d = F.hybrid_split(R, 2, G)
             assert b + d == R * R and b % G == 0 and d < G
+
+
+def test_nccl_unique_id_host_only():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1409_2908_b200 as F
+    a, b = F.nccl_unique_id(), F.nccl_unique_id()
+    assert len(a) == 128 and len(b) == 128 and a != b
