@@ -346,10 +346,20 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
   for (int tile = blockIdx.x; tile < total_tiles; tile += gemm_ctas) {
     const TileCoord tc = locate<BN>(tasks, ntasks, tile, uni);
     const GemmTask& t = tasks[tc.task];
-    const int KT = (__ldg(&t.k) + BK - 1) / BK;
+    const int kdim = __ldg(&t.k);
+    const int KT = (kdim + BK - 1) / BK;
     // epilogue parameters, fetched now so their latency hides behind the main loop
     const double alpha = __ldg(&t.alpha), beta = __ldg(&t.beta);
     const int m = __ldg(&t.m), n = __ldg(&t.n);
+    // ragged edge tiles: a warp whose sub-tile lies beyond m or n may skip its DMMAs.  That only
+    // shortens the tile when every SM sub-partition loses work (consumer warps cw and cw + 4 share
+    // one), so warps skip only when no sub-partition keeps both of its warps busy; otherwise all run
+    // (zero fill costs nothing extra there, and a lone early warp was measured to cost ~1 %).
+    auto in_range = [&](int w) { return (tc.m0 + (w / WGN) * WTM < m) && (tc.n0 + (w % WGN) * WTN < n); };
+    bool full_pair = false;
+#pragma unroll
+    for (int q = 0; q < CONSUMERS / 2; ++q) full_pair |= in_range(q) && in_range(q + CONSUMERS / 2);
+    const bool active = full_pair || in_range(cw);
     const long long ldc = __ldg(&t.ldc);
     double* C = t.C;
     double acc[MI][NI][2];
@@ -358,32 +368,49 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
 #pragma unroll
       for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    for (int kt = 0; kt < KT; ++kt) {
-      mbar_wait(full_bar(stage), phase);
-      const unsigned sa = base + stage * STAGE_T, sb = sa + A_BYTES;
+    // one 4-deep k-slice of a stage: fragments from shared memory, MI x NI DMMAs
+    auto slice = [&](unsigned sa, unsigned sb, int s) {
+      double a[MI], b[NI];
 #pragma unroll
-      for (int s = 0; s < BK / 4; ++s) {
-        double a[MI], b[NI];
-#pragma unroll
-        for (int i = 0; i < MI; ++i) {
-          const unsigned x = (i & 1) ? xa1 : xa0;
-          const unsigned chunk = ((unsigned)(2 * s) + ca) ^ x;
-          a[i] = lds64(sa + a_row0 + (unsigned)(16 * (i >> 1) + (i & 1)) * 128u + chunk * 16u + ha);
-        }
-        const unsigned krow = (unsigned)(4 * s + c);
-#pragma unroll
-        for (int jj = 0; jj < NI; ++jj) {
-          const unsigned chunk = (cb0 + 2u * (jj & 1)) ^ (krow & 7u);
-          b[jj] = lds64(sb + b_box0 + (unsigned)(jj >> 1) * 2048u + krow * 128u + chunk * 16u + hb * 8u);
-        }
-#pragma unroll
-        for (int i = 0; i < MI; ++i)
-#pragma unroll
-          for (int jj = 0; jj < NI; ++jj) dmma(acc[i][jj], a[i], b[jj]);
+      for (int i = 0; i < MI; ++i) {
+        const unsigned x = (i & 1) ? xa1 : xa0;
+        const unsigned chunk = ((unsigned)(2 * s) + ca) ^ x;
+        a[i] = lds64(sa + a_row0 + (unsigned)(16 * (i >> 1) + (i & 1)) * 128u + chunk * 16u + ha);
       }
+      const unsigned krow = (unsigned)(4 * s + c);
+#pragma unroll
+      for (int jj = 0; jj < NI; ++jj) {
+        const unsigned chunk = (cb0 + 2u * (jj & 1)) ^ (krow & 7u);
+        b[jj] = lds64(sb + b_box0 + (unsigned)(jj >> 1) * 2048u + krow * 128u + chunk * 16u + hb * 8u);
+      }
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int jj = 0; jj < NI; ++jj) dmma(acc[i][jj], a[i], b[jj]);
+    };
+    auto release = [&]() {
       __syncwarp();
       if (lane == 0) mbar_arrive(empty_bar(stage));
       if (++stage == STAGES) stage = 0, phase ^= 1u;
+    };
+    // full stages run the plain pipelined loop; then a ragged last k-step runs only the 4-deep slices
+    // that hold data (the rest is zero fill), and a warp whose sub-tile lies beyond m or n (ragged
+    // edge tiles) issues no DMMA at all but waits for and releases every stage with the others
+    const int KF = active ? kdim / BK : 0;
+    for (int kt = 0; kt < KF; ++kt) {
+      mbar_wait(full_bar(stage), phase);
+      const unsigned sa = base + stage * STAGE_T, sb = sa + A_BYTES;
+#pragma unroll
+      for (int s = 0; s < BK / 4; ++s) slice(sa, sb, s);
+      release();
+    }
+    for (int kt = KF; kt < KT; ++kt) {
+      mbar_wait(full_bar(stage), phase);
+      const unsigned sa = base + stage * STAGE_T, sb = sa + A_BYTES;
+      const int ks = active ? (kdim - kt * BK + 3) / 4 : 0;
+#pragma unroll 1
+      for (int s = 0; s < ks; ++s) slice(sa, sb, s);
+      release();
     }
 
     // ---- epilogue: C = alpha * acc (+ beta * C), from registers ----
