@@ -173,6 +173,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fuse", type=int, default=0, help="fused leaf level (formation/GEMM/assembly in one launch)")
     ap.add_argument("--collapse", type=int, default=1, help="last two levels' formation / assembly in one pass each")
+    ap.add_argument("--shard-mode", default="leaf", choices=["leaf", "top"],
+                    help="N > 1: leaf-level HYBRID sharding or the top-level products in contiguous ranges")
     ap.add_argument("--combine", default="torch", choices=["torch", "lib"],
                     help="N > 1: partial-C reduce by torch.distributed (NCCL) or inside fmm_execute (fmm_plan_create_dist)")
     ap.add_argument("--no-other", action="store_true", help="skip timing the other leaf-level schedule (fused vs separate)")
@@ -209,7 +211,7 @@ def main():
     lib_comm = F.Comm.from_torch_distributed(device=device.index) if (world > 1 and args.combine == "lib") else None
     plan = F.Plan(alg, P, Q, N, L, layout=w["layout"], strategy=args.strategy, cse=bool(args.cse),
                   shard_rank=rank, shard_count=world, fuse=bool(args.fuse), collapse=bool(args.collapse),
-                  comm=lib_comm, root=0)
+                  comm=lib_comm, root=0, shard_mode=args.shard_mode)
     C = plan.new_output()
     st = plan.stats()
     dmma_peak, dfma_peak = F.probe_fp64_peak()
@@ -416,7 +418,7 @@ def main():
                        "strategy": args.strategy, "cse": bool(args.cse),
                        "l2": "inputs larger than L2 (A, B, C 0.54 GB each vs 126 MB); no flush"
                        if args.workload != "c1" else "small config: L2-resident",
-                       "parallelism": (f"leaf shards x{world} + NCCL reduce ({'fmm_execute' if lib_comm else 'torch.distributed'})"
+                       "parallelism": (f"{args.shard_mode}-level shards x{world} + NCCL reduce ({'fmm_execute' if lib_comm else 'torch.distributed'})"
                                        if world > 1 else "1 GPU"),
                        "fused_leaf_level": fused, "collapsed_levels": bool(st.get("collapsed", 0))},
             "roofline": roofline,

@@ -82,6 +82,10 @@ typedef struct {
                                (streaming strategy only; needs TMA-eligible leaf views and no thin
                                leaves, else the plan silently runs the separate kernels).
                                0: separate formation / GEMM / assembly launches. */
+  int shard_mode;           /* with shard_count > 1: 0 = leaf-level HYBRID sharding (the default:
+                               balanced to one leaf row); 1 = the top-level products r1 in contiguous
+                               balanced ranges (SURVEY 8(e) mode (i): a rank needs only the A / B
+                               blocks of its r1, but R mod G makes it uneven) */
   int collapse_levels;      /* 1: evaluate the last two recursion levels' formation and assembly in
                                one streaming pass each (the level-(L-1) S_r, T_r and M_r are never
                                written to HBM: DESIGN.md sec. 6c), where it applies: streaming,

@@ -206,6 +206,11 @@ struct fmm_plan_s {
     for (int q = l; q < L; ++q) f *= R;
     return f;
   }
+  long long node_leaf_span_from(int l) const {  // level-l nodes under one level-1 node
+    long long f = 1;
+    for (int q = 1; q < l; ++q) f *= R;
+    return f;
+  }
   long long node_leaf_span(int l) const {
     long long f = 1;
     for (int q = l; q < L; ++q) f *= R;
@@ -218,8 +223,22 @@ struct fmm_plan_s {
     const long long dfs = leaves % G, bfs = leaves - dfs;
     const long long per = bfs / G;
     std::vector<int64_t> r0(leaves), r1(leaves);
-    if (fmm_shard_leaf_rows(leaves, dims[L].P, G, g, r0.data(), r1.data()) != FMM_OK)
+    // top-level ownership (shard_mode 1): rank of top-level product r1 (contiguous balanced ranges)
+    auto top_owner = [&](long long r) {
+      const long long base = R / G, extra = R % G;
+      const long long cut = extra * (base + 1);
+      return r < cut ? r / (base + 1) : extra + (base > 0 ? (r - cut) / base : 0);
+    };
+    if (opt.shard_mode == 1 && L >= 1) {
+      const long long span = node_leaf_span(1);  // leaves under one top-level product
+      for (long long z = 0; z < leaves; ++z) {
+        const bool own = top_owner(z / span) == g;
+        r0[z] = 0;
+        r1[z] = own ? dims[L].P : 0;
+      }
+    } else if (fmm_shard_leaf_rows(leaves, dims[L].P, G, g, r0.data(), r1.data()) != FMM_OK) {
       throw Error(FMM_E_INVALID_ARG, "bad shard arguments");
+    }
     leaf_r0.assign(r0.begin(), r0.end());
     leaf_r1.assign(r1.begin(), r1.end());
     needed.assign(L + 1, {});
@@ -236,7 +255,8 @@ struct fmm_plan_s {
       if (!has_strips) continue;
       for (long long z = 0; z < nodes_at[l]; ++z) {
         const long long f = node_first_leaf(l, z);
-        const long long owner = f < bfs ? (per > 0 ? f / per : 0) : 0;
+        long long owner = f < bfs ? (per > 0 ? f / per : 0) : 0;
+        if (opt.shard_mode == 1) owner = l == 0 ? 0 : top_owner(z / node_leaf_span_from(l));
         if (owner == g) strip_owner[l][z] = 1, needed[l][z] = 1;
       }
     }
@@ -975,6 +995,7 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
   else fmm_plan_options_default(&p->opt);
   if (p->opt.shard_count < 1) p->opt.shard_count = 1;
   if (p->opt.shard_rank < 0 || p->opt.shard_rank >= p->opt.shard_count) throw Error(FMM_E_INVALID_ARG, "bad shard_rank");
+  if (p->opt.shard_mode != 0 && p->opt.shard_mode != 1) throw Error(FMM_E_INVALID_ARG, "bad shard_mode");
   if (p->opt.layout != FMM_ROW_MAJOR && p->opt.layout != FMM_COL_MAJOR) throw Error(FMM_E_INVALID_ARG, "bad layout");
   if (p->opt.strategy != FMM_ADD_STREAMING && p->opt.strategy != FMM_ADD_WRITE_ONCE)
     throw Error(FMM_E_INVALID_ARG, "bad strategy");

@@ -30,7 +30,7 @@ class _Options(ctypes.Structure):
     _fields_ = [("layout", ctypes.c_int), ("strategy", ctypes.c_int), ("cse", ctypes.c_int),
                 ("shard_rank", ctypes.c_int), ("shard_count", ctypes.c_int),
                 ("workspace_limit_bytes", ctypes.c_size_t), ("peel_align", ctypes.c_int),
-                ("fuse_leaf_level", ctypes.c_int), ("collapse_levels", ctypes.c_int)]
+                ("fuse_leaf_level", ctypes.c_int), ("shard_mode", ctypes.c_int), ("collapse_levels", ctypes.c_int)]
 
 
 def _load():
@@ -232,7 +232,8 @@ class Plan:
     def __init__(self, alg: Algorithm, P: int, Q: int, N: int, levels: int, layout: str = "row",
                  strategy: str = "streaming", cse: bool = True, shard_rank: int = 0, shard_count: int = 1,
                  device: Optional[int] = None, workspace_limit_bytes: int = 0, peel_align: bool = True,
-                 fuse: bool = False, collapse: bool = True, comm: Optional[Comm] = None, root: int = 0):
+                 fuse: bool = False, collapse: bool = True, comm: Optional[Comm] = None, root: int = 0,
+                 shard_mode: str = "leaf"):
         import torch
         self.alg, self.P, self.Q, self.N, self.levels = alg, P, Q, N, levels
         self.layout = ROW_MAJOR if layout == "row" else COL_MAJOR
@@ -246,6 +247,7 @@ class Plan:
         o.peel_align = int(bool(peel_align))
         o.fuse_leaf_level = int(bool(fuse))
         o.collapse_levels = int(bool(collapse))
+        o.shard_mode = {"leaf": 0, "top": 1}[shard_mode]
         self.device = torch.cuda.current_device() if device is None else device
         h = ctypes.c_void_p()
         self.comm = comm  # a distributed plan keeps its communicator alive

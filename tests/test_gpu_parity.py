@@ -152,12 +152,26 @@ def test_quantized_inputs_exact_at_scale():
 
 # ---- sharding (HYBRID arithmetic): shards sum to the product ----------------------
 @pytest.mark.parametrize("G", [2, 3, 8])
-def test_shards_sum_to_product(G):
-    name, L, P, Q, N = "winograd_class_222_7", 2, 300, 200, 250
-    Ai, Bi = I.problem(P, Q, N, seed=8, kind="integers")
-    total = np.zeros((P, N))
-    for g in range(G):
-        C, _ = run(name, Ai, Bi, L, shard_rank=g, shard_count=G)
+@pytest.mark.parametrize("mode", ["leaf", "top"])
+def test_shards_sum_to_product(G, mode):
+    for name, L, P, Q, N in [("winograd_class_222_7", 2, 300, 200, 250), ("hk_class_323_15", 2, 271, 181, 269),
+                             ("alg_424_26", 2, 320, 64, 320)]:
+        Ai, Bi = I.problem(P, Q, N, seed=8, kind="integers")
+        total = np.zeros((P, N))
+        for g in range(G):
+            C, _ = run(name, Ai, Bi, L, shard_rank=g, shard_count=G, shard_mode=mode)
+            total += C
+        assert np.array_equal(total, Ai @ Bi)
+
+
+def test_top_level_shards_more_ranks_than_products():
+    # G > R: ranks beyond R own nothing and return zeros
+    Ai, Bi = I.problem(96, 64, 80, seed=9, kind="integers")
+    total = np.zeros((96, 80))
+    for g in range(9):
+        C, _ = run("strassen_222_7", Ai, Bi, 1, shard_rank=g, shard_count=9, shard_mode="top")
+        if g >= 7:
+            assert not C.any()
         total += C
     assert np.array_equal(total, Ai @ Bi)
 
