@@ -84,7 +84,37 @@ def test_not_collapsed_where_it_does_not_apply():
     A, B = I.problem(270, 180, 270, seed=5, kind="integers")  # <3,2,3>: base case too large
     Ca, sa = _run(F, "hk_class_323_15", A, B, 2, collapse=True)
     _, sb = _run(F, "hk_class_323_15", A, B, 2, collapse=False)
-    assert sa["launches"] == sb["launches"] and np.array_equal(Ca, A @ B)
+    assert sa["collapsed"] == 0 and sa["launches"] == sb["launches"] and np.array_equal(Ca, A @ B)
     A, B = I.problem(256, 256, 256, seed=6, kind="integers")  # write-once strategy
     Ca, sa = _run(F, "strassen_222_7", A, B, 2, strategy="write_once")
     assert np.array_equal(Ca, A @ B)
+
+
+@pytest.mark.parametrize("layout", ["row", "col"])
+def test_collapsed_strided_views(layout):
+    # padded leading dimensions on A, B and C; nothing outside C is written
+    import torch
+    F = _lib()
+    P, Q, N = 256, 128, 192
+    A, B = I.problem(P, Q, N, seed=11, kind="integers")
+    if layout == "row":
+        Ab = torch.zeros(P, Q + 6, dtype=torch.float64, device="cuda"); Ab[:, 2:Q + 2] = torch.from_numpy(A).cuda()
+        Bb = torch.zeros(Q, N + 10, dtype=torch.float64, device="cuda"); Bb[:, 4:N + 4] = torch.from_numpy(B).cuda()
+        Cb = torch.full((P, N + 8), 5.0, dtype=torch.float64, device="cuda")
+        Av, Bv, Cv = Ab[:, 2:Q + 2], Bb[:, 4:N + 4], Cb[:, 2:N + 2]
+    else:
+        Ab = torch.zeros(Q, P + 6, dtype=torch.float64, device="cuda"); Ab[:, 2:P + 2] = torch.from_numpy(A.T.copy()).cuda()
+        Bb = torch.zeros(N, Q + 10, dtype=torch.float64, device="cuda"); Bb[:, 4:Q + 4] = torch.from_numpy(B.T.copy()).cuda()
+        Cb = torch.full((N, P + 8), 5.0, dtype=torch.float64, device="cuda")
+        Av, Bv, Cv = Ab[:, 2:P + 2].t(), Bb[:, 4:Q + 4].t(), Cb[:, 2:P + 2].t()
+    p = F.Plan(F.load_alg("winograd_class_222_7"), P, Q, N, 2, layout=layout)
+    assert p.stats()["collapsed"] == 1
+    p.execute(Av, Bv, Cv)
+    torch.cuda.synchronize()
+    assert np.array_equal(Cv.cpu().numpy(), A @ B)
+    rest = Cb.clone()
+    if layout == "row":
+        rest[:, 2:N + 2] = 5.0
+    else:
+        rest[:, 2:P + 2] = 5.0
+    assert bool((rest == 5.0).all())
