@@ -1665,14 +1665,6 @@ fmm_status_t fmm_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const doub
   if (m == 0 || n == 0) return FMM_OK;
   if (!A || !B || !C) throw Error(FMM_E_INVALID_ARG, "null matrix pointer");
   if (lda < std::max<int64_t>(k, 1) || ldb < n || ldc < n) throw Error(FMM_E_SHAPE, "leading dimension too small");
-  thread_local GemmTask* d_task = nullptr;
-  thread_local int d_task_dev = -1;
-  int dev = 0;
-  FMM_CUDA(cudaGetDevice(&dev));
-  if (!d_task || d_task_dev != dev) {
-    FMM_CUDA(cudaMalloc(&d_task, 4096));
-    d_task_dev = dev;
-  }
   std::vector<GemmTask> t(1);
   t[0].A = A;
   t[0].B = B;
@@ -1693,11 +1685,15 @@ fmm_status_t fmm_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const doub
   alignas(128) char buf[1024];
   std::memcpy(buf, t.data(), sizeof(GemmTask));
   if (tma) gemm_tma_maps(t, buf + 512);
+  // a stream-ordered descriptor per call: calls on different streams never share one
+  GemmTask* d_task = nullptr;
+  FMM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_task), sizeof(buf), s));
   FMM_CUDA(cudaMemcpyAsync(d_task, buf, sizeof(buf), cudaMemcpyHostToDevice, s));
   if (tma)
     gemm_tma_launch(d_task, reinterpret_cast<char*>(d_task) + 512, 1, tiles, bn, t[0].tiles_m, t[0].tiles_n, s);
   else
     gemm_launch(d_task, 1, tiles, gemm_tasks_aligned16(t), s);
+  FMM_CUDA(cudaFreeAsync(d_task, s));
   return FMM_OK;
   FMM_API_END
 }
