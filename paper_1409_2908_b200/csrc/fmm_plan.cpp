@@ -569,6 +569,31 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
       t.node = (int)(z / R);
       if (t.m > 0 && t.n > 0) tasks.push_back(t);
     }
+    if (L == 0 && opt.shard_count > 1) {
+      // the root is the only leaf: a shard writes its rows of C and zeros in the rest (k = 0 tasks;
+      // deeper levels get zeros from the zero-initialised workspace instead)
+      const View c = outView(0, 0);
+      auto zero = [&](long long r0, long long r1) {
+        if (r1 <= r0 || d.N <= 0) return;
+        GemmTask t{};
+        t.A = rootA.ptr;
+        t.B = rootB.ptr;
+        t.C = c.ptr + r0 * c.ld;
+        t.lda = rootA.ld;
+        t.ldb = rootB.ld;
+        t.ldc = c.ld;
+        t.m = (int)(r1 - r0);
+        t.n = (int)d.N;
+        t.k = 0;
+        t.alpha = 1.0;
+        t.beta = 0.0;
+        t.node = -1;
+        tasks.push_back(t);
+      };
+      const long long r0 = leaf_r0[0], r1 = leaf_r1[0];
+      if (r1 <= r0) zero(0, d.P);
+      else zero(0, r0), zero(r1, d.P);
+    }
     emit_gemm(Launch::GEMM, L, tasks);
   }
 

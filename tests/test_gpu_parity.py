@@ -314,3 +314,20 @@ def test_distributed_plan_single_rank():
     with pytest.raises(F.FmmError) as e:
         p.execute(dev(A), dev(B), Cb[:, :250])
     assert e.value.status == "FMM_E_UNSUPPORTED"
+
+
+def test_classical_root_shards_write_zeros_elsewhere():
+    # L = 0 (or a problem below the base case): the root is the only leaf and its rows are split
+    # across shards; every shard must write zeros in the rows it does not own (found by
+    # tests/test_gpu_random.py: a 1 x 1 x 1 problem over 2 shards summed uninitialised memory)
+    for (P, Q, N, L) in [(1, 1, 1, 2), (5, 3, 4, 0), (300, 64, 70, 0)]:
+        A, B = I.problem(P, Q, N, seed=P, kind="integers")
+        for G in (2, 3):
+            total = np.zeros((P, N))
+            for g in range(G):
+                p = F.Plan(falg("alg_424_26"), P, Q, N, L, shard_rank=g, shard_count=G)
+                C = torch.full((P, N), float("nan"), dtype=torch.float64, device="cuda")
+                p.execute(dev(A), dev(B), C)
+                torch.cuda.synchronize()
+                total += C.cpu().numpy()
+            assert np.array_equal(total, A @ B)

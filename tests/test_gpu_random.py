@@ -1,0 +1,82 @@
+"""Randomised GPU parity: random algorithm, shape (ragged at any level), levels, layout and plan
+options (strategy, CSE, collapsed levels, fused leaf level, shards) on integer inputs, where every
+schedule must reproduce A*B exactly; and on uniform inputs against the oracle's tolerance.
+Seeded (derandomized) so failures reproduce."""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+import fmm_inputs as I
+from conftest import ALGS
+from oracle import oracle as O
+
+hypothesis = pytest.importorskip("hypothesis")
+from hypothesis import HealthCheck, given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+NAMES = [os.path.basename(p)[:-4] for p in sorted(glob.glob(os.path.join(ALGS, "*.txt")))]
+
+
+def _lib():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1409_2908_b200 as F
+    return F
+
+
+def _dev(x, layout):
+    import torch
+    if layout == "row":
+        return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    return torch.from_numpy(np.ascontiguousarray(x.T)).cuda().t()
+
+
+cases = st.fixed_dictionaries({
+    "name": st.sampled_from(NAMES),
+    "L": st.integers(0, 3),
+    "P": st.integers(1, 700), "Q": st.integers(1, 400), "N": st.integers(1, 700),
+    "layout": st.sampled_from(["row", "col"]),
+    "strategy": st.sampled_from(["streaming", "write_once"]),
+    "cse": st.booleans(), "collapse": st.booleans(), "fuse": st.booleans(), "peel_align": st.booleans(),
+    "G": st.sampled_from([1, 1, 2, 3]), "mode": st.sampled_from(["leaf", "top"]),
+    "seed": st.integers(0, 2 ** 16),
+})
+
+
+N_INT = int(os.environ.get("FMM_RANDOM_EXAMPLES", "60"))
+DERAND = os.environ.get("FMM_RANDOM_SEED") is None
+
+
+@settings(max_examples=N_INT, deadline=None, derandomize=DERAND, suppress_health_check=list(HealthCheck))
+@given(c=cases)
+def test_random_plans_integer_exact(c):
+    import torch
+    F = _lib()
+    A, B = I.problem(c["P"], c["Q"], c["N"], seed=c["seed"], kind="integers")
+    total = np.zeros((c["P"], c["N"]))
+    for g in range(c["G"]):
+        p = F.Plan(F.load_alg(c["name"]), c["P"], c["Q"], c["N"], c["L"], layout=c["layout"], strategy=c["strategy"],
+                   cse=c["cse"], collapse=c["collapse"], fuse=c["fuse"], peel_align=c["peel_align"], shard_rank=g,
+                   shard_count=c["G"], shard_mode=c["mode"])
+        C = p.execute(_dev(A, c["layout"]), _dev(B, c["layout"]))
+        torch.cuda.synchronize()
+        total += C.cpu().numpy()
+    assert np.array_equal(total, A @ B), c
+
+
+@settings(max_examples=max(1, N_INT // 2), deadline=None, derandomize=DERAND, suppress_health_check=list(HealthCheck))
+@given(c=cases)
+def test_random_plans_float_parity(c):
+    import torch
+    F = _lib()
+    A, B = I.problem(c["P"], c["Q"], c["N"], seed=c["seed"])
+    p = F.Plan(F.load_alg(c["name"]), c["P"], c["Q"], c["N"], c["L"], layout=c["layout"], strategy=c["strategy"],
+               cse=c["cse"], collapse=c["collapse"], fuse=c["fuse"], peel_align=c["peel_align"])
+    C = p.execute(_dev(A, c["layout"]), _dev(B, c["layout"])).cpu().numpy()
+    torch.cuda.synchronize()
+    nrm = np.linalg.norm(A) * np.linalg.norm(B)
+    assert np.max(np.abs(C - O.fast(A, B, O.load_alg(F.alg_path(c["name"])), c["L"]))) <= 1e-12 * nrm + 1e-300, c
+    assert np.max(np.abs(C - O.classical(A, B))) <= 1e-10 * nrm + 1e-300, c
