@@ -221,14 +221,16 @@ def main():
         if evs is None:
             plan.execute(A, B, C, stream=stream)
         else:
-            plan.execute_events(A, B, C, evs, stream=stream)
+            plan.execute_events(A, B, C, evs[:4], stream=stream)
         if lib_comm is None:
             combine_partials(C)  # (a distributed plan reduced inside fmm_execute)
+        if evs is not None:
+            evs[4].record(stream)  # after the combine: the comm share of a step (N > 1)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     for e in (x for row in evs for x in row):
         e.record(stream)  # torch creates the underlying cudaEvent_t lazily, at the first record
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -256,8 +258,9 @@ def main():
     value = flops / (ms_step * 1e-3) / 1e9
 
     # per-phase device times measured on the launching stream during the timed region
-    ph = np.array([[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3])] for e in evs])
-    form_ms, gemm_ms, asm_ms = [float(x) for x in ph.mean(axis=0)]
+    ph = np.array([[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]), e[3].elapsed_time(e[4])]
+                   for e in evs])
+    form_ms, gemm_ms, asm_ms, comm_ms = [float(x) for x in ph.mean(axis=0)]
     add_ms = form_ms + asm_ms
     peaks, peak_src = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", HBM_FALLBACK))
@@ -432,7 +435,8 @@ def main():
             "cpu_baseline": cpu,
             "phases_ms": {"formation_levels_below_L" if fused else "formation": form_ms,
                           "fused_leaf_level" if fused else "leaf_gemm": gemm_ms,
-                          "assembly_and_strips": add_ms - form_ms},
+                          "assembly_and_strips": add_ms - form_ms,
+                          "combine_reduce": comm_ms if world > 1 else 0.0},
             "additions": {"algorithmic_bytes_per_step": st["add_bytes"],
                           "bytes_in_fused_launch": st["fused_add_bytes"],
                           "separate_kernel_bytes": sep_bytes, "separate_kernel_gbs": add_gbs, "peak_gbs": hbm,
