@@ -340,70 +340,6 @@ void emit_job_fn(std::ostringstream& o, const std::string& name, const LincombSp
   o << "    }\n  }\n  __syncwarp();  // every lane is done with the slot before the next job rewrites it\n}\n";
 }
 
-// The staged variant (addition CTAs): the inputs of a piece (one row, `seg` columns of every input)
-// arrive by one tensor-map TMA load at i * seg doubles of the warp's buffer; the next piece's load
-// is in flight while the warp evaluates the chains from shared memory (16-byte loads) and stores
-// the outputs.  Same chains and order as the direct variant.
-void emit_staged_fn(std::ostringstream& o, const std::string& name, int q, const LincombSpec& spec, const Program& p) {
-  const int nin = spec.nin, nout = spec.nout;
-  std::vector<std::string> comps{".x", ".y"};
-  auto var = [&](int v) { return v < nin ? "x" + std::to_string(v) : "t" + std::to_string(v - nin); };
-  std::set<int> used;
-  for (const auto& e : p.outs)
-    for (const auto& kv : e)
-      if (kv.first < nin) used.insert(kv.first);
-  for (const auto& t : p.temps) {
-    if (std::get<0>(t) < nin) used.insert(std::get<0>(t));
-    if (std::get<1>(t) < nin) used.insert(std::get<1>(t));
-  }
-  o << "__device__ __forceinline__ void " << name << "(const FusedArgs& fa, const FusedJob& j, int lane, unsigned sp, Staging& st) {\n";
-  o << "  const char* nd = fa.node_tab[" << q << "] + (long long)j.node * fa.node_bytes[" << q << "];\n";
-  // out[], ld_in, ld_out -> slot words 0 .. nout+1
-  o << "  for (int w = lane; w < " << nout + 2 << "; w += 32) sts_u64(sp + 8u * w, reinterpret_cast<const unsigned long long*>(nd + "
-    << 8 * nin << ")[w]);\n";
-  o << "  __syncwarp();\n";
-  o << "  const long long ldo = (long long)lds_u64(sp + " << 8 * (nout + 1) << "u);\n";
-  o << "  const void* map = reinterpret_cast<const char*>(fa.maps[" << q << "]) + 128LL * j.node;\n";
-  o << "  const int seg = fa.seg[" << q << "], cols = fa.cols[" << q << "], rank = fa.map_rank[" << q << "];\n";
-  o << "  const int nseg = (cols + seg - 1) / seg, npieces = j.nrows * nseg;\n";
-  o << "  const unsigned bytes = " << nin << "u * (unsigned)seg * 8u;\n";
-  o << "  auto issue = [&](int pc, int b) {\n";
-  o << "    if (lane == 0) {\n";
-  o << "      const unsigned bar = st.bar0 + 8u * (unsigned)b, dst = st.buf0 + (unsigned)b * FUSED_PIECE_BYTES;\n";
-  o << "      const int row = j.row0 + pc / nseg, c0 = (pc % nseg) * seg;\n";
-  o << "      mbar_expect_tx(bar, bytes);\n";
-  o << "      if (rank == 3) tma_load_3d(dst, map, c0, row, 0, bar); else tma_load_4d(dst, map, c0, row, 0, 0, bar);\n";
-  o << "    }\n  };\n";
-  o << "  if (npieces > 0) issue(0, 0);\n";
-  o << "  int b = 0;\n";
-  o << "  for (int pc = 0; pc < npieces; ++pc, b ^= 1) {\n";
-  o << "    if (pc + 1 < npieces) issue(pc + 1, b ^ 1);\n";
-  o << "    mbar_wait(st.bar0 + 8u * (unsigned)b, (st.phase >> b) & 1u);\n";
-  o << "    st.phase ^= 1u << b;\n";
-  o << "    const int row = j.row0 + pc / nseg, c0 = (pc % nseg) * seg;\n";
-  o << "    const int w = min(seg, cols - c0);\n";
-  o << "    const unsigned sb = st.buf0 + (unsigned)b * FUSED_PIECE_BYTES;\n";
-  o << "    const long long po0 = (long long)row * ldo + c0;\n";
-  o << "    for (int c = 2 * lane; c < w; c += 64) {\n";
-  for (int i : used) o << "    const double2 x" << i << " = lds128(sb + (unsigned)((" << i << " * seg + c) * 8));\n";
-  for (size_t t = 0; t < p.temps.size(); ++t) {
-    const int a = std::get<0>(p.temps[t]), bb = std::get<1>(p.temps[t]);
-    const double r = std::get<2>(p.temps[t]);
-    o << "    double2 t" << t << ";\n";
-    for (auto& c : comps) {
-      if (r == 1.0) o << "    t" << t << c << " = " << var(a) << c << " + " << var(bb) << c << ";\n";
-      else if (r == -1.0) o << "    t" << t << c << " = " << var(a) << c << " - " << var(bb) << c << ";\n";
-      else o << "    t" << t << c << " = " << var(a) << c << " + " << dlit(r) << " * " << var(bb) << c << ";\n";
-    }
-  }
-  for (int qo = 0; qo < nout; ++qo) {
-    o << "    if (double* oq = reinterpret_cast<double*>(lds_u64(sp + " << 8 * qo << "u))) {\n    double2 y;\n";
-    for (auto& c : comps) emit_chain(o, "y", p.outs[qo], c, var);
-    o << "    *reinterpret_cast<double2*>(oq + po0 + c) = y;\n    }\n";
-  }
-  o << "    }\n    __syncwarp();  // every lane is done with buffer b before it is refilled\n  }\n}\n";
-}
-
 std::string strip_pragma_once(const char* src) {
   std::string s(src);
   const std::string key = "#pragma once";
@@ -429,15 +365,13 @@ std::string fused_generate(const std::vector<LincombSpec>& specs, int bn) {
     const Program prog = build_program(specs[q]);
     emit_job_fn(o, "prog" + std::to_string(q) + "_v2", specs[q], prog, 2);
     emit_job_fn(o, "prog" + std::to_string(q) + "_v1", specs[q], prog, 1);
-    emit_staged_fn(o, "prog" + std::to_string(q) + "_st", (int)q, specs[q], prog);
   }
-  o << "__device__ void fmm_add_job(const FusedArgs& fa, const FusedJob& j, int lane, unsigned sp, Staging* st) {\n";
+  o << "__device__ void fmm_add_job(const FusedArgs& fa, const FusedJob& j, int lane, unsigned sp) {\n";
   o << "  const char* nd = fa.node_tab[j.prog] + (long long)j.node * fa.node_bytes[j.prog];\n";
   o << "  switch (j.prog) {\n";
   for (size_t q = 0; q < specs.size(); ++q)
-    o << "    case " << q << ": if (st && fa.seg[" << q << "] > 0) prog" << q << "_st(fa, j, lane, sp, *st); else if (fa.vec2[" << q
-      << "]) prog" << q << "_v2(nd, j.row0, j.nrows, fa.cols[" << q << "], lane, sp); else prog" << q
-      << "_v1(nd, j.row0, j.nrows, fa.cols[" << q << "], lane, sp); break;\n";
+    o << "    case " << q << ": if (fa.vec2[" << q << "]) prog" << q << "_v2(nd, j.row0, j.nrows, fa.cols[" << q
+      << "], lane, sp); else prog" << q << "_v1(nd, j.row0, j.nrows, fa.cols[" << q << "], lane, sp); break;\n";
   o << "  }\n}\n}  // namespace fmm\n";
   o << "extern \"C\" __global__ void __launch_bounds__(fmm::THREADS, 1)\n"
        "fmm_fused(const fmm::GemmTask* __restrict__ tasks, const fmm::CUtensorMap* __restrict__ maps, int ntasks,\n"

@@ -39,15 +39,7 @@ struct FusedJob {
   int dep;         // parent index: F jobs signal ready[dep], A jobs wait for tiles_done[dep]
   int kind;        // 0 = formation (F), 1 = assembly (A)
 };
-// Addition CTAs stage the inputs of a piece (one row segment of every input block of a node) with
-// ONE tensor-map TMA load (3-D or 4-D box over the node's equally spaced input blocks) into one of
-// two FUSED_PIECE_BYTES buffers per warp; input i lands at i * seg doubles.
-constexpr int FUSED_PIECE_BYTES = 8192;
-constexpr int FUSED_ADD_SMEM = 1024 + (GEMM_THREADS / 32) * 2 * FUSED_PIECE_BYTES + 256;  // + pointer slots
 struct FusedArgs {
-  const void* maps[FUSED_MAX_PROGS];      // per program: one CUtensorMap per node-table entry (or null)
-  int seg[FUSED_MAX_PROGS];               // staged segment width (doubles) per program, 0 = not staged
-  int map_rank[FUSED_MAX_PROGS];          // 3 or 4
   const char* node_tab[FUSED_MAX_PROGS];  // per program: node table
   int node_bytes[FUSED_MAX_PROGS];
   int cols[FUSED_MAX_PROGS];              // block width (elements) per program

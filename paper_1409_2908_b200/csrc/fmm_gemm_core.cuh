@@ -48,9 +48,7 @@ constexpr int CONSUMERS = 8, THREADS = 128 + CONSUMERS * 32;  // warpgroup 0 = p
 static_assert(THREADS == GEMM_THREADS, "host and device agree on the block size");
 constexpr int A_BYTES = BM * BK * 8;                           // 16 KB
 __host__ __device__ constexpr int gemm_smem_bytes(int bn) { return GEMM_STAGES * (A_BYTES + BK * bn * 8) + 1024 /*align*/ + 256 /*barriers*/; }
-__host__ __device__ constexpr int fused_smem_bytes(int bn) {
-  return (gemm_smem_bytes(bn) > FUSED_ADD_SMEM ? gemm_smem_bytes(bn) : FUSED_ADD_SMEM) + FUSED_PTR_BYTES;
-}
+__host__ __device__ constexpr int fused_smem_bytes(int bn) { return gemm_smem_bytes(bn) + FUSED_PTR_BYTES; }
 constexpr int GROUP_M = 8;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -82,24 +80,6 @@ __device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map
           dst),
       "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(bar)
       : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(unsigned dst, const void* map, int c0, int c1, int c2, unsigned bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
-      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_4d(unsigned dst, const void* map, int c0, int c1, int c2, int c3, unsigned bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(
-          dst),
-      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ double2 lds128(unsigned addr) {
-  double2 v;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr));
-  return v;
 }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
@@ -196,19 +176,13 @@ __device__ __forceinline__ int claim(unsigned long long* ctr, int lane) {
   return __shfl_sync(0xffffffffu, idx, 0);
 }
 
-// An addition warp's two staging buffers (FUSED_PIECE_BYTES each) and their mbarriers.
-struct Staging {
-  unsigned buf0, bar0;  // buffer b at buf0 + b * FUSED_PIECE_BYTES, its mbarrier at bar0 + 8 b
-  unsigned phase;       // bit b = parity of buffer b
-};
-
 // Generated per algorithm (fmm_codegen.cpp) in the NVRTC source of the fused kernel.
-// sp: shared address of the warp's FUSED_PTR_SLOT; st: staging (addition CTAs) or null (direct loads).
-__device__ void fmm_add_job(const FusedArgs& fa, const FusedJob& j, int lane, unsigned sp, Staging* st);
+// sp: shared address of the warp's FUSED_PTR_SLOT.
+__device__ void fmm_add_job(const FusedArgs& fa, const FusedJob& j, int lane, unsigned sp);
 
 // One job with a whole warp: assembly jobs first wait until every leaf tile of their parent is
 // stored; formation jobs publish (release) to the TMA readers of the leaf products.
-__device__ __forceinline__ void run_job(const FusedArgs& fa, int jidx, int lane, unsigned sp, Staging* st) {
+__device__ __forceinline__ void run_job(const FusedArgs& fa, int jidx, int lane, unsigned sp) {
   const FusedJob j = fa.jobs[jidx];
   if (j.kind == 1) {
     if (lane == 0) {
@@ -218,7 +192,7 @@ __device__ __forceinline__ void run_job(const FusedArgs& fa, int jidx, int lane,
     }
     __syncwarp();
   }
-  fmm_add_job(fa, j, lane, sp, st);
+  fmm_add_job(fa, j, lane, sp);
   if (j.kind == 0) {
     fence_proxy_async_global();
     __threadfence();
@@ -248,25 +222,15 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
     gemm_ctas = fa.gemm_ctas;
     if ((int)blockIdx.x >= gemm_ctas) {
       // ------------------------------ addition CTA ------------------------------
-      // [staging: 2 buffers per warp][barriers][pointer slots]
-      constexpr int NW = THREADS / 32;
-      const unsigned abars = base + NW * 2 * FUSED_PIECE_BYTES;
-      const unsigned asp = abars + 256u + (unsigned)warp * FUSED_PTR_SLOT;
-      if (threadIdx.x == 0) {
-        for (int b = 0; b < 2 * NW; ++b) mbar_init(abars + 8u * b, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-      }
-      __syncthreads();
-      Staging st{base + (unsigned)warp * 2u * FUSED_PIECE_BYTES, abars + 16u * (unsigned)warp, 0u};
       for (;;) {
         const int idx = claim(&fa.ctr[0], lane);
         if (idx >= fa.njobs0) break;
-        run_job(fa, idx, lane, asp, &st);
+        run_job(fa, idx, lane, sp);
       }
       for (;;) {
         const int idx = claim(&fa.ctr[1], lane);
         if (fa.njobs0 + idx >= fa.njobs) break;
-        run_job(fa, fa.njobs0 + idx, lane, asp, &st);
+        run_job(fa, fa.njobs0 + idx, lane, sp);
       }
       return;
     }
@@ -295,6 +259,7 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
         if constexpr (FUSED) {
           const int node = __ldg(&tasks[tc.task].node);
           if (node != ready_node) {
+            // (a watchdog __trap() in these waits was measured to slow the whole launch by ~13 %)
             const unsigned long long target = (unsigned long long)__ldg(&fa.ready_target[node]);
             while (ld_acquire(&fa.ctr[2 + node]) < target) __nanosleep(128);
             fence_proxy_async_global();
@@ -324,7 +289,7 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
     for (;;) {
       const int idx = claim(&fa.ctr[0], lane);
       if (idx >= fa.njobs0) break;
-      run_job(fa, idx, lane, sp, nullptr);
+      run_job(fa, idx, lane, sp);
     }
   }
   const int cw = warp - 4;  // consumer warp 0..7
@@ -447,7 +412,7 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
     for (;;) {
       const int idx = claim(&fa.ctr[1], lane);
       if (fa.njobs0 + idx >= fa.njobs) break;
-      run_job(fa, fa.njobs0 + idx, lane, sp, nullptr);
+      run_job(fa, fa.njobs0 + idx, lane, sp);
     }
   }
 }

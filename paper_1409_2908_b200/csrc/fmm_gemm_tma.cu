@@ -58,30 +58,6 @@ void make_map(CUtensorMap* m, const double* ptr, long long rows, long long cols,
 
 size_t gemm_tma_map_bytes() { return sizeof(CUtensorMap); }
 
-bool tensor_map_nd(void* out, const double* ptr, int rank, const long long* dims, const long long* strides_bytes,
-                   const int* box) {
-  EncodeFn fn = encode_fn();
-  if (!fn || rank < 1 || rank > 5) return false;
-  if (reinterpret_cast<uintptr_t>(ptr) & 15) return false;
-  cuuint64_t d[5], st[4];
-  cuuint32_t b[5], es[5];
-  for (int i = 0; i < rank; ++i) {
-    if (dims[i] < 1 || box[i] < 1 || box[i] > 256) return false;
-    d[i] = (cuuint64_t)dims[i];
-    b[i] = (cuuint32_t)box[i];
-    es[i] = 1;
-  }
-  for (int i = 0; i + 1 < rank; ++i) {
-    if (strides_bytes[i] <= 0 || (strides_bytes[i] & 15) || strides_bytes[i] >= (1LL << 40)) return false;
-    st[i] = (cuuint64_t)strides_bytes[i];
-  }
-  if ((box[0] * 8) % 16) return false;
-  CUresult r = fn(reinterpret_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, const_cast<double*>(ptr), d,
-                  st, b, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
 bool gemm_tma_eligible(const std::vector<GemmTask>& tasks) {
   if (!encode_fn()) return false;
   for (const auto& t : tasks) {

@@ -93,10 +93,6 @@ void gemm_tma_maps(const std::vector<GemmTask>& tasks, void* out);
 // uniform_tm/tn: the common tile grid when every task has the same one (else 0, 0).
 void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn,
                      int uniform_tm, int uniform_tn, cudaStream_t stream);
-// A rank-`rank` FP64 tensor map (no swizzle, zero OOB fill): dims/box innermost first, strides in
-// bytes for dims 1..rank-1.  false if TMA cannot describe the view (alignment, limits).
-bool tensor_map_nd(void* out, const double* ptr, int rank, const long long* dims, const long long* strides_bytes,
-                   const int* box);
 // TMA kernel configuration: consumer warp grid of a tile width, SM count, dynamic shared memory.
 void gemm_bn_config(int bn, int* wgm, int* wgn);
 int gemm_sm_count();

@@ -68,8 +68,6 @@ struct Launch {
   int gemm_ctas = 0;  // FUSED: CTAs running leaf tiles (the rest of the grid are addition CTAs)
   size_t prog_node_off[FUSED_MAX_PROGS] = {};
   int prog_node_bytes[FUSED_MAX_PROGS] = {}, prog_cols[FUSED_MAX_PROGS] = {}, prog_vec2[FUSED_MAX_PROGS] = {};
-  size_t prog_maps_off[FUSED_MAX_PROGS] = {};  // one tensor map per node-table entry (staged programs)
-  int prog_seg[FUSED_MAX_PROGS] = {}, prog_rank[FUSED_MAX_PROGS] = {};
   std::shared_ptr<FusedKernel> fk;
 };
 
@@ -815,46 +813,6 @@ void fmm_plan_s::fuse_leaf_level(bool lazy_kernels) {
     return off;
   };
   fz.jobs_off = push(jobs.data(), jobs.size() * sizeof(FusedJob));
-  // staged programs: one TMA tensor map per node-table entry over the node's equally spaced input
-  // blocks (3-D for the R leaf products of an assembly node, 4-D for the K x M (or N x K) grid of
-  // a formation node's parent sub-blocks); a program whose inputs TMA cannot describe keeps the
-  // direct loads
-  for (int q = 0; q < fz.nprogs; ++q) {
-    const Launch& ln = launches[prog_src[q]];
-    const int side = sides[q];
-    const int nin = side == 0 ? alg->M * alg->K : side == 1 ? alg->K * alg->N : R;
-    const int cols = (int)ln.cols, rows = (int)ln.rows;
-    int seg = std::min(256, FUSED_PIECE_BYTES / (8 * nin));
-    seg = seg >= 64 ? seg / 64 * 64 : seg / 2 * 2;
-    seg = std::min(seg, (cols + 1) / 2 * 2);
-    // measured slower than the direct loads on every config (narrow boxes: one row of <= 256 columns
-    // per input), so opt-in only: FMM_FUSED_TMA=1
-    const char* tma_env = getenv("FMM_FUSED_TMA");
-    bool ok = tma_env && tma_env[0] == '1' && fz.prog_vec2[q] && nin <= 32 && seg >= 2 && rows > 0 && cols > 0;
-    const int n2 = side == 0 ? alg->K : side == 1 ? alg->N : nin, n3 = side == 0 ? alg->M : side == 1 ? alg->K : 1;
-    const int rank = side == 2 ? 3 : 4;
-    std::vector<char> maps(128 * ln.node_ids.size(), 0);
-    for (size_t e = 0; ok && e < ln.node_ids.size(); ++e) {
-      if (lazy_kernels) break;  // dry build: only the space
-      const char* nd = h_tab.data() + ln.table_off + e * fz.prog_node_bytes[q];
-      const double* const* in = reinterpret_cast<const double* const*>(nd);
-      const long long ld = reinterpret_cast<const long long*>(nd + 8 * (nin + (side == 0 ? formU.size() : side == 1 ? formV.size() : alg->M * alg->N)))[0];
-      const long long s2 = n2 > 1 ? (long long)(in[1] - in[0]) : (long long)cols;
-      const long long s3 = n3 > 1 ? (long long)(in[n2] - in[0]) : (long long)rows * ld;
-      for (int i = 0; ok && i < nin; ++i) ok = in[i] == in[0] + (i % n2) * s2 + (i / n2) * s3;
-      if (!ok || s2 <= 0 || s3 <= 0) {
-        ok = false;
-        break;
-      }
-      const long long dims[4] = {cols, rows, n2, n3};
-      const long long strides[3] = {8 * ld, 8 * s2, 8 * s3};
-      const int box[4] = {seg, 1, n2, n3};
-      ok = tensor_map_nd(maps.data() + 128 * e, in[0], rank, dims, strides, box);
-    }
-    fz.prog_maps_off[q] = push(maps.data(), maps.size());
-    fz.prog_seg[q] = ok ? seg : 0;
-    fz.prog_rank[q] = rank;
-  }
   std::vector<int> targets(ready_target);
   targets.insert(targets.end(), tiles_target.begin(), tiles_target.end());
   fz.targets_off = push(targets.data(), targets.size() * sizeof(int));
@@ -1215,9 +1173,6 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
           fa.node_bytes[q] = ln.prog_node_bytes[q];
           fa.cols[q] = ln.prog_cols[q];
           fa.vec2[q] = ln.prog_vec2[q];
-          fa.maps[q] = ln.prog_seg[q] > 0 ? d_tab + ln.prog_maps_off[q] : nullptr;
-          fa.seg[q] = ln.prog_seg[q];
-          fa.map_rank[q] = ln.prog_rank[q];
         }
         fa.jobs = reinterpret_cast<const FusedJob*>(d_tab + ln.jobs_off);
         fa.njobs0 = ln.njobs0;
