@@ -130,7 +130,8 @@ void fmm_alg_destroy(fmm_alg* alg);
 /* ---- plans ------------------------------------------------------------------------------ */
 
 /* Plan C (P x Nc) = A (P x Q) * B (Q x Nc) with `levels` recursive steps (0 = one classical
-   DMMA GEMM).  The recursion stops early at a level whose sub-problem is smaller than the base
+   DMMA GEMM; -1 = the fastest levels <= 4 by the cost model of fmm_plan_predict, the paper's
+   cutoff question, Sec. 3.4).  The recursion stops early at a level whose sub-problem is smaller than the base
    case (reading R10/R18 of DESIGN.md).  Column-major problems are planned through the
    transposed algorithm of Prop. 1: a column-major P x Q array is the row-major
    Q x P array of its transpose, so C^T = B^T A^T runs with <N,K,M> and no data moves.

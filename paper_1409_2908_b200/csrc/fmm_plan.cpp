@@ -968,12 +968,28 @@ void fmm_plan_s::emit_two_level_assembly(bool lazy_kernels) {
 
 namespace {
 
+double predict_seconds(const fmm_alg& a, long long P, long long Q, long long N, int levels, int* used_levels);
+
 void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long long Nc, int levels,
                const fmm_plan_options* opt, int device) {
   if (!alg) throw Error(FMM_E_INVALID_ARG, "null algorithm");
   if (P < 0 || Q < 0 || Nc < 0) throw Error(FMM_E_SHAPE, "negative dimension");
   if (P > INT32_MAX || Q > INT32_MAX || Nc > INT32_MAX) throw Error(FMM_E_UNSUPPORTED, "dimension above 2^31-1");
-  if (levels < 0 || levels > 8) throw Error(FMM_E_UNSUPPORTED, "levels must be in [0, 8]");
+  if (levels < -1 || levels > 8) throw Error(FMM_E_UNSUPPORTED, "levels must be in [0, 8], or -1 (automatic)");
+  if (levels == -1) {  // the cutoff rule (Sec. 3.4) by the cost model: the fastest L <= 4
+    const bool cm = opt && opt->layout == FMM_COL_MAJOR;
+    std::unique_ptr<fmm_alg> t;
+    const fmm_alg* a = alg;
+    if (cm) t.reset(alg_transpose_prop1(*alg)), a = t.get();
+    double best = 1e300;
+    levels = 0;
+    for (int L = 0; L <= 4; ++L) {
+      int used = 0;
+      const double tt = predict_seconds(*a, cm ? Nc : P, Q, cm ? P : Nc, L, &used);
+      if (used < L) break;
+      if (tt < best * (1 - 1e-9)) best = tt, levels = L;
+    }
+  }
   if (opt) p->opt = *opt;
   else fmm_plan_options_default(&p->opt);
   if (p->opt.shard_count < 1) p->opt.shard_count = 1;

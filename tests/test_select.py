@@ -121,3 +121,21 @@ def test_selected_plan_parity(shape):
     C = p.execute(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()).cpu().numpy()
     nrm = np.linalg.norm(A) * np.linalg.norm(B)
     assert np.max(np.abs(C - O.classical(A, B))) <= 1e-10 * nrm
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,P,Q,N,layout", [("strassen_222_7", 2048, 2048, 2048, "row"), ("alg_424_26", 3000, 600, 3000, "col"),
+                                               ("strassen_222_7", 200, 200, 200, "row")])
+def test_automatic_levels(name, P, Q, N, layout):
+    # levels = -1: the plan takes the cost model's fastest L <= 4, and still multiplies exactly
+    import torch
+    F = _lib()
+    a = F.load_alg(name)
+    preds = [a.predict_ms(P, Q, N, L, layout) for L in range(5)]
+    p = F.Plan(a, P, Q, N, -1, layout=layout)
+    assert p.stats()["levels"] == int(np.argmin(preds)) or preds[int(p.stats()["levels"])] <= min(preds) * (1 + 1e-9)
+    A, B = I.problem(P, Q, N, seed=7, kind="integers")
+    dev = (lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()) if layout == "row" else \
+          (lambda x: torch.from_numpy(np.ascontiguousarray(x.T)).cuda().t())
+    C = p.execute(dev(A), dev(B)).cpu().numpy()
+    assert np.array_equal(C, A @ B)
