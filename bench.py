@@ -165,7 +165,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--strategy", default="streaming", choices=["streaming", "write_once"])
+    ap.add_argument("--strategy", default="streaming", choices=["streaming", "write_once", "pairwise"])
     ap.add_argument("--cse", type=int, default=1)
     ap.add_argument("--cpu-frac", type=float, default=1.0, help="oracle sample size (fraction of each dim)")
     ap.add_argument("--ref-frac", type=float, default=0.25, help="reference-arm sample (fraction of each dim)")

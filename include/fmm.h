@@ -53,8 +53,11 @@ typedef enum { FMM_ROW_MAJOR = 0, FMM_COL_MAJOR = 1 } fmm_layout;
 /* Addition-chain implementations (Sec. 3.2).  STREAMING: one kernel per phase reads
    every input block once and writes every formed S_r / T_r (or C_k) once.
    WRITE_ONCE: one output stream per S_r / T_r / C_k, each reading the blocks of its chain
-   (P:628-632).  (Pairwise daxpy chains, are not offered.) */
-typedef enum { FMM_ADD_STREAMING = 0, FMM_ADD_WRITE_ONCE = 1 } fmm_add_strategy;
+   (P:628-632).  PAIRWISE: the paper's daxpy chains (footnote): per output, a copy
+   of the first term then one y <- y + c x pass per further term, i.e. one launch per chain
+   position, each reading two blocks and writing one.  Kept for the Fig. 2 study; all
+   three round identically (ascending-index chains) when cse = 0. */
+typedef enum { FMM_ADD_STREAMING = 0, FMM_ADD_WRITE_ONCE = 1, FMM_ADD_PAIRWISE = 2 } fmm_add_strategy;
 
 typedef struct {
   int layout;               /* fmm_layout of A, B and C (all three share it) */

@@ -39,11 +39,16 @@ typedef struct {
 /* taken q ascending starting from 0.0.  Parallel over rows only, so the per-entry order is    */
 /* fixed.                                                                                       */
 /* ---------------------------------------------------------------------------------------- */
+/* Small loops run on one thread: the threads only partition independent element positions, so
+   this changes nothing in the arithmetic, but an oversubscribed host otherwise spends seconds per
+   tiny parallel region waiting for descheduled threads. */
+#define OMP_MIN_WORK (1 << 16)
+
 void oracle_classical(int64_t P, int64_t Q, int64_t Nc,
                       const double* A, int64_t ars, int64_t acs,
                       const double* B, int64_t brs, int64_t bcs,
                       double* C, int64_t crs, int64_t ccs) {
-#pragma omp parallel for schedule(dynamic, 1)
+#pragma omp parallel for schedule(dynamic, 1) if (P * Q * Nc >= OMP_MIN_WORK)
   for (int64_t i = 0; i < P; ++i) {
     double* acc = (double*)malloc(sizeof(double) * (Nc > 0 ? Nc : 1));
     for (int64_t j = 0; j < Nc; ++j) acc[j] = 0.0;
@@ -102,7 +107,7 @@ static void fast_rec(const oalg* g, int L, int64_t P, int64_t Q, int64_t Nc,
       const double u = g->U[i * R + r];
       if (u == 0.0) continue;
       const double* blk = A + (i / K) * p * ars + (i % K) * q * acs;
-#pragma omp parallel for
+#pragma omp parallel for if (p * q >= OMP_MIN_WORK)
       for (int64_t x = 0; x < p; ++x)
         for (int64_t y = 0; y < q; ++y) {
           const double v = blk[x * ars + y * acs];
@@ -116,7 +121,7 @@ static void fast_rec(const oalg* g, int L, int64_t P, int64_t Q, int64_t Nc,
       const double v = g->V[j * R + r];
       if (v == 0.0) continue;
       const double* blk = B + (j / N) * q * brs + (j % N) * n * bcs;
-#pragma omp parallel for
+#pragma omp parallel for if (q * n >= OMP_MIN_WORK)
       for (int64_t x = 0; x < q; ++x)
         for (int64_t y = 0; y < n; ++y) {
           const double b = blk[x * brs + y * bcs];
@@ -134,7 +139,7 @@ static void fast_rec(const oalg* g, int L, int64_t P, int64_t Q, int64_t Nc,
       const double w = g->W[k * R + r];
       if (w == 0.0) continue;
       const double* mb = Mr + (size_t)r * p * n;
-#pragma omp parallel for
+#pragma omp parallel for if (p * n >= OMP_MIN_WORK)
       for (int64_t x = 0; x < p; ++x)
         for (int64_t y = 0; y < n; ++y) {
           const double m = mb[x * n + y];
@@ -257,7 +262,7 @@ void oracle_fast_entries(int64_t P, int64_t Q, int64_t Nc,
                          int M, int K, int N, int R, const double* U, const double* V, const double* W, int L,
                          int64_t count, const int64_t* rows, const int64_t* cols, double* out) {
   oalg g = {M, K, N, R, U, V, W};
-#pragma omp parallel for schedule(dynamic, 1)
+#pragma omp parallel for schedule(dynamic, 1) if (count >= 64)
   for (int64_t e = 0; e < count; ++e) {
     ectx c;
     memset(&c, 0, sizeof(c));

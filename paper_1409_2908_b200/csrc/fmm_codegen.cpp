@@ -139,10 +139,14 @@ std::string generate(const LincombSpec& s, const Program& p, LincombCost& cost) 
   std::vector<std::string> comps = V == 2 ? std::vector<std::string>{".x", ".y"} : std::vector<std::string>{""};
   std::ostringstream o;
   o << "// generated by fmm_codegen.cpp: nin=" << nin << " nout=" << nout << " vec=" << V
-    << " strategy=" << (s.strategy == FMM_ADD_STREAMING ? "streaming" : "write_once") << " cse=" << s.cse << "\n";
+    << " strategy="
+    << (s.strategy == FMM_ADD_STREAMING ? "streaming" : s.strategy == FMM_ADD_WRITE_ONCE ? "write_once" : "pairwise")
+    << " cse=" << s.cse << "\n";
   o << "struct Node { const double* in[" << nin << "]; double* out[" << nout << "]; long long ld_in; long long ld_out; };\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(128) lincomb(const Node* __restrict__ nodes, int rows, int cvec) {\n";
-  const bool wo = s.strategy == FMM_ADD_WRITE_ONCE;
+  const bool pw = s.strategy == FMM_ADD_PAIRWISE;
+  o << "extern \"C\" __global__ void __launch_bounds__(128) lincomb(const Node* __restrict__ nodes, int rows, int cvec"
+    << (pw ? ", int step" : "") << ") {\n";
+  const bool wo = s.strategy != FMM_ADD_STREAMING;
   if (wo) o << "  const int z = blockIdx.z / " << nout << ", oi = blockIdx.z % " << nout << ";\n";
   else o << "  const int z = blockIdx.z;\n";
   o << "  const Node& nd = nodes[z];\n";
@@ -180,6 +184,43 @@ std::string generate(const LincombSpec& s, const Program& p, LincombCost& cost) 
       adds += p.outs[q].empty() ? 0 : (double)p.outs[q].size() - 1;
       writes += 1;
     }
+  } else if (pw) {
+    // pairwise: launch `step` applies the step-th term of every chain, y <- x (times
+    // its coefficient) for the first term and y <- y + c x after it: one daxpy-like pass per term,
+    // each term in ascending index order as in emit_chain, so the sums round identically
+    o << "    switch (oi) {\n";
+    for (int q = 0; q < nout; ++q) {
+      o << "    case " << q << ": {\n    if (!nd.out[" << q << "]) return;\n    switch (step) {\n";
+      int t = 0;
+      for (const auto& kv : p.outs[q]) {
+        const std::string v = "x" + std::to_string(kv.first);
+        const double c = kv.second;
+        o << "    case " << t << ": {\n";
+        o << "    const " << T << " " << v << " = __ldg((const " << T << "*)(nd.in[" << kv.first << "] + pi));\n";
+        o << "    " << T << " y";
+        if (t > 0) o << " = *(const " << T << "*)(nd.out[" << q << "] + po)";
+        o << ";\n";
+        for (auto& cp : comps) {
+          const std::string x = v + cp, y = "y" + cp;
+          if (t == 0) {
+            if (c == 1.0) o << "    " << y << " = " << x << ";\n";
+            else if (c == -1.0) o << "    " << y << " = -" << x << ";\n";
+            else o << "    " << y << " = " << dlit(c) << " * " << x << ";\n";
+          } else {
+            if (c == 1.0) o << "    " << y << " = " << y << " + " << x << ";\n";
+            else if (c == -1.0) o << "    " << y << " = " << y << " - " << x << ";\n";
+            else o << "    " << y << " = " << y << " + " << dlit(c) << " * " << x << ";\n";
+          }
+        }
+        o << "    *(" << T << "*)(nd.out[" << q << "] + po) = y;\n    } break;\n";
+        reads += t == 0 ? 1.0 : 2.0;
+        writes += 1;
+        ++t;
+      }
+      o << "    default: return;\n    }\n    } break;\n";
+      adds += p.outs[q].empty() ? 0 : (double)p.outs[q].size() - 1;
+    }
+    o << "    }\n";
   } else {
     o << "    switch (oi) {\n";
     for (int q = 0; q < nout; ++q) {
@@ -257,11 +298,19 @@ void lincomb_launch(const LincombKernel& k, const void* d_nodes, int nnodes, lon
   if (nnodes <= 0 || rows <= 0 || cols <= 0) return;
   const long long cvec = cols / k.spec.vec;
   if (cvec * k.spec.vec != cols) throw Error(FMM_E_INVALID_ARG, "lincomb: cols not a multiple of vec");
-  const long long zdim = (long long)nnodes * (k.spec.strategy == FMM_ADD_WRITE_ONCE ? k.spec.nout : 1);
+  const long long zdim = (long long)nnodes * (k.spec.strategy != FMM_ADD_STREAMING ? k.spec.nout : 1);
   if (zdim > 65535) throw Error(FMM_E_UNSUPPORTED, "lincomb: too many nodes in one launch");
   dim3 grid((unsigned)((cvec + k.threads - 1) / k.threads), (unsigned)std::min<long long>(rows, 65535),
             (unsigned)zdim);
   int r = (int)rows, c = (int)cvec;
+  if (k.spec.strategy == FMM_ADD_PAIRWISE) {
+    // one launch per chain position: a term's pass must see the previous term's stores
+    for (int step = 0; step < lincomb_steps(k); ++step) {
+      void* args[] = {(void*)&d_nodes, &r, &c, &step};
+      FMM_CUDA(cudaLaunchKernel((const void*)k.kern, grid, dim3(k.threads), args, 0, stream));
+    }
+    return;
+  }
   void* args[] = {(void*)&d_nodes, &r, &c};
   FMM_CUDA(cudaLaunchKernel((const void*)k.kern, grid, dim3(k.threads), args, 0, stream));
 }
@@ -615,6 +664,13 @@ std::shared_ptr<LincombKernel> twolevel_get(const TwoLevelSpec& spec) {
 }
 
 LincombCost lincomb_cost(const LincombKernel& k) { return k.cost; }
+int lincomb_steps(const LincombKernel& k) {
+  if (k.spec.strategy != FMM_ADD_PAIRWISE) return 1;
+  size_t n = 0;
+  for (const auto& e : k.prog.outs) n = std::max(n, e.size());
+  return (int)n;
+}
+int lincomb_out_terms(const LincombKernel& k, int q) { return (int)k.prog.outs.at((size_t)q).size(); }
 const LincombSpec& lincomb_spec(const LincombKernel& k) { return k.spec; }
 int lincomb_cse_temps(const LincombKernel& k) { return k.temps; }
 std::string lincomb_source(const LincombKernel& k) { return k.source; }

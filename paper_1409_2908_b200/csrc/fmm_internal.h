@@ -150,6 +150,8 @@ struct TwoLevelSpec {
 };
 std::shared_ptr<LincombKernel> twolevel_get(const TwoLevelSpec& spec);
 LincombCost lincomb_cost(const LincombKernel& k);
+int lincomb_steps(const LincombKernel& k);               // launches per lincomb_launch (pairwise: max chain length)
+int lincomb_out_terms(const LincombKernel& k, int q);   // terms in output q's chain
 int lincomb_cse_temps(const LincombKernel& k);
 std::string lincomb_source(const LincombKernel& k);
 

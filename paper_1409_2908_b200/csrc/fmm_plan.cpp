@@ -490,6 +490,7 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
       bool aligned = (cols % 2) == 0;
       int count = 0;
       double writes = 0;
+      std::vector<double> mat_count(nout, 0.0);  // nodes materialising output o
       for (long long zp = 0; zp < nodes_at[l - 1]; ++zp) {
         if (!needed[l - 1][zp]) continue;
         bool any = false;
@@ -509,7 +510,7 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
           const long long z = zp * R + form[o];
           const long long offv = side == 0 ? offS[l][z] : offT[l][z];
           out[o] = needed[l][z] && offv >= 0 ? ws + offv : nullptr;
-          if (out[o]) writes += 1;
+          if (out[o]) writes += 1, mat_count[o] += 1;
         }
         lds[0] = par.ld;
         lds[1] = side == 0 ? ldS[l] : ldT[l];
@@ -532,11 +533,18 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
       const LincombCost c = lincomb_cost(*k);
       const double elems = (double)rows * cols;
       ln.elem_adds = c.adds_per_elem * elems * count;
-      if (opt.strategy == FMM_ADD_STREAMING) {
-        ln.elem_reads = c.reads_per_elem * elems * count;
-        ln.elem_writes = writes * elems;
+      if (opt.strategy == FMM_ADD_PAIRWISE) {
+        // per materialised chain of n terms: a copy (1 read, 1 write), then n - 1 daxpy passes
+        // (2 reads, 1 write each) -- P:638-640
+        ln.elem_reads = ln.elem_writes = 0;
+        for (int o = 0; o < nout; ++o) {
+          const double n = lincomb_out_terms(*k, o);
+          ln.elem_reads += mat_count[o] * (2 * n - 1) * elems;
+          ln.elem_writes += mat_count[o] * n * elems;
+        }
       } else {
-        ln.elem_reads = c.reads_per_elem * elems * count;  // sum of chain lengths per node
+        // streaming: every used input once; write-once: the sum of chain lengths per node
+        ln.elem_reads = c.reads_per_elem * elems * count;
         ln.elem_writes = writes * elems;
       }
       ln.table_off = push(tab.data(), tab.size());
@@ -996,7 +1004,8 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
   if (p->opt.shard_rank < 0 || p->opt.shard_rank >= p->opt.shard_count) throw Error(FMM_E_INVALID_ARG, "bad shard_rank");
   if (p->opt.shard_mode != 0 && p->opt.shard_mode != 1) throw Error(FMM_E_INVALID_ARG, "bad shard_mode");
   if (p->opt.layout != FMM_ROW_MAJOR && p->opt.layout != FMM_COL_MAJOR) throw Error(FMM_E_INVALID_ARG, "bad layout");
-  if (p->opt.strategy != FMM_ADD_STREAMING && p->opt.strategy != FMM_ADD_WRITE_ONCE)
+  if (p->opt.strategy != FMM_ADD_STREAMING && p->opt.strategy != FMM_ADD_WRITE_ONCE &&
+      p->opt.strategy != FMM_ADD_PAIRWISE)
     throw Error(FMM_E_INVALID_ARG, "bad strategy");
   p->device = device;
   FMM_CUDA(cudaSetDevice(device));

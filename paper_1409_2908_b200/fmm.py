@@ -16,7 +16,8 @@ FMM_OK = 0
 _STATUS = {1: "FMM_E_INVALID_ARG", 2: "FMM_E_NOT_EXACT", 3: "FMM_E_SHAPE", 4: "FMM_E_NO_MEMORY",
            5: "FMM_E_CUDA", 6: "FMM_E_NCCL", 7: "FMM_E_UNSUPPORTED", 8: "FMM_E_PARSE"}
 ROW_MAJOR, COL_MAJOR = 0, 1
-STREAMING, WRITE_ONCE = 0, 1
+STREAMING, WRITE_ONCE, PAIRWISE = 0, 1, 2
+_STRATEGIES = {"streaming": STREAMING, "write_once": WRITE_ONCE, "pairwise": PAIRWISE}
 
 
 class FmmError(RuntimeError):
@@ -240,7 +241,9 @@ class Plan:
         o = _Options()
         _lib.fmm_plan_options_default(ctypes.byref(o))
         o.layout = self.layout
-        o.strategy = STREAMING if strategy == "streaming" else WRITE_ONCE
+        if strategy not in _STRATEGIES:
+            raise ValueError(f"strategy must be one of {sorted(_STRATEGIES)}")
+        o.strategy = _STRATEGIES[strategy]
         o.cse = int(bool(cse))
         o.shard_rank, o.shard_count = shard_rank, shard_count
         o.workspace_limit_bytes = workspace_limit_bytes

@@ -128,7 +128,7 @@ def test_fast_float_parity(name, L, P, Q, N, layout):
     assert np.max(np.abs(C - O.classical(A, B))) <= bound(A, B, 1e-10)
 
 
-@pytest.mark.parametrize("strategy", ["streaming", "write_once"])
+@pytest.mark.parametrize("strategy", ["streaming", "write_once", "pairwise"])
 @pytest.mark.parametrize("cse", [False, True])
 def test_strategies_and_cse(strategy, cse):
     for name, L, P, Q, N in [("alg_424_26", 2, 320, 64, 320), ("winograd_class_222_7", 2, 512, 512, 512)]:
@@ -138,6 +138,30 @@ def test_strategies_and_cse(strategy, cse):
         Ai, Bi = I.problem(P, Q, N, seed=6, kind="integers")
         Ci, _ = run(name, Ai, Bi, L, strategy=strategy, cse=cse)
         assert np.array_equal(Ci, Ai @ Bi)
+
+
+@pytest.mark.parametrize("name,L,P,Q,N", [("strassen_222_7", 2, 256, 256, 256), ("alg_424_26", 2, 328, 66, 330),
+                                           ("laderman_class_333_23", 1, 99, 96, 93)])
+def test_three_strategies_round_identically(name, L, P, Q, N):
+    # without CSE every strategy sums each chain in ascending index order: bitwise equal
+    A, B = I.problem(P, Q, N, seed=12)
+    Cs, _ = run(name, A, B, L, strategy="streaming", cse=False)
+    for strategy in ("write_once", "pairwise"):
+        C, _ = run(name, A, B, L, strategy=strategy, cse=False)
+        assert np.array_equal(C, Cs), strategy
+
+
+def test_pairwise_traffic_is_the_papers_count():
+    # pairwise reads 2 nnz(U,V,W) - 2R - MN and writes nnz(U,V,W) sub-blocks per node.
+    # Strassen: nnz = 12 + 12 + 12, R = 7, MN = 4 -> 54 reads, 36 writes; the two singleton columns
+    # of U and of V are aliased, not copied, which removes 4 reads and 4 writes.
+    b = 256
+    A, B = I.problem(2 * b, 2 * b, 2 * b, seed=13)
+    C, p = run("strassen_222_7", A, B, 1, strategy="pairwise", cse=False)
+    assert p.stats()["add_bytes"] == 8 * (50 + 32) * b * b
+    assert np.max(np.abs(C - O.fast(A, B, oalg("strassen_222_7"), 1))) <= bound(A, B, 1e-12)
+    _, pw = run("strassen_222_7", A, B, 1, strategy="write_once", cse=False)
+    assert pw.stats()["add_bytes"] < p.stats()["add_bytes"]
 
 
 def test_quantized_inputs_exact_at_scale():

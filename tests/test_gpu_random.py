@@ -39,7 +39,7 @@ cases = st.fixed_dictionaries({
     "L": st.integers(0, 3),
     "P": st.integers(1, 700), "Q": st.integers(1, 400), "N": st.integers(1, 700),
     "layout": st.sampled_from(["row", "col"]),
-    "strategy": st.sampled_from(["streaming", "write_once"]),
+    "strategy": st.sampled_from(["streaming", "write_once", "pairwise"]),
     "cse": st.booleans(), "collapse": st.booleans(), "fuse": st.booleans(), "peel_align": st.booleans(),
     "G": st.sampled_from([1, 1, 2, 3]), "mode": st.sampled_from(["leaf", "top"]),
     "seed": st.integers(0, 2 ** 16),
