@@ -177,6 +177,8 @@ def main():
                     help="N > 1: leaf-level HYBRID sharding or the top-level products in contiguous ranges")
     ap.add_argument("--combine", default="torch", choices=["torch", "lib"],
                     help="N > 1: partial-C reduce by torch.distributed (NCCL) or inside fmm_execute (fmm_plan_create_dist)")
+    ap.add_argument("--output", default="root", choices=["root", "slabs"],
+                    help="N > 1: C summed onto rank 0, or slab-distributed (slab g of C summed onto rank g)")
     ap.add_argument("--no-other", action="store_true", help="skip timing the other leaf-level schedule (fused vs separate)")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -201,7 +203,7 @@ def main():
     import __graft_entry__
     __graft_entry__.build()
     import paper_1409_2908_b200 as F
-    from paper_1409_2908_b200.dist import combine_partials
+    from paper_1409_2908_b200.dist import combine_partials, scatter_partials
 
     P, Q, N, L = w["P"], w["Q"], w["N"], w["L"]
     A_np, B_np = gen_inputs(w)
@@ -211,7 +213,7 @@ def main():
     lib_comm = F.Comm.from_torch_distributed(device=device.index) if (world > 1 and args.combine == "lib") else None
     plan = F.Plan(alg, P, Q, N, L, layout=w["layout"], strategy=args.strategy, cse=bool(args.cse),
                   shard_rank=rank, shard_count=world, fuse=bool(args.fuse), collapse=bool(args.collapse),
-                  comm=lib_comm, root=0, shard_mode=args.shard_mode)
+                  comm=lib_comm, root="slabs" if args.output == "slabs" else 0, shard_mode=args.shard_mode)
     C = plan.new_output()
     st = plan.stats()
     dmma_peak, dfma_peak = F.probe_fp64_peak()
@@ -222,8 +224,11 @@ def main():
             plan.execute(A, B, C, stream=stream)
         else:
             plan.execute_events(A, B, C, evs[:4], stream=stream)
-        if lib_comm is None:
-            combine_partials(C)  # (a distributed plan reduced inside fmm_execute)
+        if lib_comm is None:  # (a distributed plan reduces inside fmm_execute)
+            if args.output == "slabs":
+                scatter_partials(C)
+            else:
+                combine_partials(C)
         if evs is not None:
             evs[4].record(stream)  # after the combine: the comm share of a step (N > 1)
 
@@ -408,6 +413,28 @@ def main():
                       "copy-out of consecutive steps overlap)" if world == 1 else
                "H2D + fmm_execute + NCCL reduce + D2H"}
 
+    # N > 1: the replication of A and B from rank 0, timed on its own after the timed
+    # region (every rank holds the seeded inputs, so the steps above do not include it)
+    bcast = None
+    if world > 1:
+        from paper_1409_2908_b200.dist import storage_view
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        dist.barrier()
+        torch.cuda.synchronize()
+        b0.record(stream)
+        for _ in range(reps):
+            dist.broadcast(storage_view(A), src=0)
+            dist.broadcast(storage_view(B), src=0)
+        b1.record(stream)
+        torch.cuda.synchronize()
+        tb = torch.tensor([b0.elapsed_time(b1) / reps], dtype=torch.float64, device=device)
+        dist.all_reduce(tb, op=dist.ReduceOp.MAX)
+        bms = float(tb.item())
+        bbytes = 8.0 * (P * Q + Q * N)
+        bcast = {"ms": bms, "bytes": bbytes, "algbw_gbs": bbytes / (bms * 1e-3) / 1e9,
+                 "value_with_broadcast": flops / ((ms_step + bms) * 1e-3) / 1e9}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle import oracle as O
@@ -425,7 +452,9 @@ def main():
                        "strategy": args.strategy, "cse": bool(args.cse),
                        "l2": "inputs larger than L2 (A, B, C 0.54 GB each vs 126 MB); no flush"
                        if args.workload != "c1" else "small config: L2-resident",
-                       "parallelism": (f"{args.shard_mode}-level shards x{world} + NCCL reduce ({'fmm_execute' if lib_comm else 'torch.distributed'})"
+                       "parallelism": (f"{args.shard_mode}-level shards x{world} + NCCL "
+                                       f"{'reduce to rank 0' if args.output == 'root' else 'slab reduce-scatter'} "
+                                       f"({'fmm_execute' if lib_comm else 'torch.distributed'})"
                                        if world > 1 else "1 GPU"),
                        "fused_leaf_level": fused, "collapsed_levels": bool(st.get("collapsed", 0))},
             "roofline": roofline,
@@ -437,6 +466,8 @@ def main():
                           "fused_leaf_level" if fused else "leaf_gemm": gemm_ms,
                           "assembly_and_strips": add_ms - form_ms,
                           "combine_reduce": comm_ms if world > 1 else 0.0},
+            "input_broadcast": bcast,
+            "combine_algbw_gbs": (8.0 * P * N / (comm_ms * 1e-3) / 1e9) if world > 1 and comm_ms else None,
             "additions": {"algorithmic_bytes_per_step": st["add_bytes"],
                           "bytes_in_fused_launch": st["fused_add_bytes"],
                           "separate_kernel_bytes": sep_bytes, "separate_kernel_gbs": add_gbs, "peak_gbs": hbm,

@@ -160,9 +160,18 @@ void fmm_comm_destroy(fmm_comm* comm);  /* after every plan using it is destroye
    the communicator) into a partial C, and fmm_execute ends with one in-place NCCL sum-reduce of C
    to `root` on the execute's stream (the C_k combination is linear in the partials).  C must be
    contiguous (ldc = Nc row-major, ldc = P column-major) on every rank, else FMM_E_UNSUPPORTED at
-   execute.  The result is complete on `root` only.  The plan keeps `comm` (not owned). */
+   execute.  The result is complete on `root` only.  The plan keeps `comm` (not owned).
+   root = FMM_DIST_SLABS instead gives slab-distributed output (reduce-scatter): the
+   contiguous C is cut along its outer storage dimension (rows of C when row-major, columns when
+   column-major) into nranks slabs as even as integers allow (fmm_dist_slab), and slab g is summed
+   onto rank g -- one grouped set of ncclReduce calls, the same bytes sent as the single reduce.
+   Outside its own slab a rank's C holds its partial product. */
+#define FMM_DIST_SLABS (-1)
 fmm_status_t fmm_plan_create_dist(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels,
                                   const fmm_plan_options* opt, fmm_comm* comm, int root, fmm_plan_t** out);
+/* The slab of C that rank `rank` of `nranks` holds after a FMM_DIST_SLABS execute: rows
+   [*first, *last) of C (row-major) or columns [*first, *last) (column-major).  Host only. */
+fmm_status_t fmm_dist_slab(int64_t P, int64_t Nc, int layout, int nranks, int rank, int64_t* first, int64_t* last);
 
 /* Workspace bytes held by the plan. */
 fmm_status_t fmm_plan_workspace_bytes(const fmm_plan_t* plan, size_t* bytes);

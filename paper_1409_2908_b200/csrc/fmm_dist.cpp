@@ -23,6 +23,8 @@ struct NcclApi {
   ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
   ncclResult_t (*reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
   std::string err;
 };
@@ -42,7 +44,10 @@ const NcclApi& nccl() {
     api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
     api.reduce = reinterpret_cast<decltype(api.reduce)>(dlsym(h, "ncclReduce"));
     api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
-    if (!api.get_unique_id || !api.comm_init_rank || !api.comm_destroy || !api.reduce || !api.error_string)
+    api.group_start = reinterpret_cast<decltype(api.group_start)>(dlsym(h, "ncclGroupStart"));
+    api.group_end = reinterpret_cast<decltype(api.group_end)>(dlsym(h, "ncclGroupEnd"));
+    if (!api.get_unique_id || !api.comm_init_rank || !api.comm_destroy || !api.reduce || !api.error_string ||
+        !api.group_start || !api.group_end)
       api.err = "libnccl.so.2 lacks an expected symbol";
   });
   if (!api.err.empty()) throw Error(FMM_E_NCCL, api.err);
@@ -56,6 +61,33 @@ void check(ncclResult_t r, const char* what) {
 
 void dist_reduce(void* comm, double* C, size_t count, int root, cudaStream_t stream) {
   check(nccl().reduce(C, C, count, ncclDouble, ncclSum, root, static_cast<ncclComm_t>(comm), stream), "ncclReduce");
+}
+
+void dist_slab_range(long long outer, int nranks, int rank, long long* r0, long long* r1) {
+  *r0 = outer * rank / nranks;
+  *r1 = outer * (rank + 1) / nranks;
+}
+
+// Reduce-scatter by slabs (SURVEY 8(e) "ncclReduceScatter for row-slab-distributed output"): slab g
+// of the contiguous C (outer x inner, outer split as evenly as integers allow) is summed onto rank
+// g.  One grouped set of ncclReduce calls, so ragged slabs need no padding; every rank sends the
+// whole partial C once, as in the single reduce, but the result is spread over all ranks.
+void dist_reduce_slabs(void* comm, int nranks, double* C, long long outer, long long inner, cudaStream_t stream) {
+  const NcclApi& api = nccl();
+  check(api.group_start(), "ncclGroupStart");
+  ncclResult_t first = ncclSuccess;
+  for (int g = 0; g < nranks; ++g) {
+    long long r0, r1;
+    dist_slab_range(outer, nranks, g, &r0, &r1);
+    if (r1 <= r0 || inner <= 0) continue;
+    double* p = C + r0 * inner;
+    const ncclResult_t r = api.reduce(p, p, (size_t)((r1 - r0) * inner), ncclDouble, ncclSum, g,
+                                      static_cast<ncclComm_t>(comm), stream);
+    if (first == ncclSuccess) first = r;
+  }
+  const ncclResult_t e = api.group_end();
+  check(first, "ncclReduce (slab)");
+  check(e, "ncclGroupEnd");
 }
 }  // namespace fmm
 

@@ -67,6 +67,8 @@ namespace fmm {
 
 // multi-GPU combine (fmm_dist.cpp): in-place NCCL sum-reduce of a contiguous C to `root`
 void dist_reduce(void* comm, double* C, size_t count, int root, cudaStream_t stream);
+void dist_reduce_slabs(void* comm, int nranks, double* C, long long outer, long long inner, cudaStream_t stream);
+void dist_slab_range(long long outer, int nranks, int rank, long long* r0, long long* r1);
 void* comm_handle(const fmm_comm* c);
 int comm_nranks(const fmm_comm* c);
 int comm_rank(const fmm_comm* c);

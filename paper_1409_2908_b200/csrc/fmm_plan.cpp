@@ -1225,7 +1225,10 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
   if (p->dist_comm) {  // a7: the partial products of all ranks summed on the root
     const long long rows = p->colmajor ? p->userN : p->userP, cols = p->colmajor ? p->userP : p->userN;
     if (rows > 1 && ldc != cols) throw Error(FMM_E_UNSUPPORTED, "a distributed plan needs a contiguous C");
-    if (rows * cols > 0) dist_reduce(p->dist_comm, C, (size_t)rows * cols, p->dist_root, stream);
+    if (rows * cols > 0) {
+      if (p->dist_root == FMM_DIST_SLABS) dist_reduce_slabs(p->dist_comm, p->opt.shard_count, C, rows, cols, stream);
+      else dist_reduce(p->dist_comm, C, (size_t)rows * cols, p->dist_root, stream);
+    }
   }
   if (timed) {
     for (int q = phase + 1; q <= 3; ++q) FMM_CUDA(cudaEventRecord(evs[q], stream));
@@ -1266,7 +1269,7 @@ fmm_status_t fmm_plan_create_dist(const fmm_alg* alg, int64_t P, int64_t Q, int6
                                   const fmm_plan_options* opt, fmm_comm* comm, int root, fmm_plan_t** out) {
   FMM_API_BEGIN
   if (!out || !comm) throw Error(FMM_E_INVALID_ARG, "null argument");
-  if (root < 0 || root >= comm_nranks(comm)) throw Error(FMM_E_INVALID_ARG, "bad root");
+  if (root != FMM_DIST_SLABS && (root < 0 || root >= comm_nranks(comm))) throw Error(FMM_E_INVALID_ARG, "bad root");
   *out = nullptr;
   fmm_plan_options o;
   if (opt) o = *opt;
@@ -1278,6 +1281,20 @@ fmm_status_t fmm_plan_create_dist(const fmm_alg* alg, int64_t P, int64_t Q, int6
   p->dist_comm = comm_handle(comm);
   p->dist_root = root;
   *out = p.release();
+  return FMM_OK;
+  FMM_API_END
+}
+
+fmm_status_t fmm_dist_slab(int64_t P, int64_t Nc, int layout, int nranks, int rank, int64_t* first, int64_t* last) {
+  FMM_API_BEGIN
+  if (!first || !last) throw Error(FMM_E_INVALID_ARG, "null argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(FMM_E_INVALID_ARG, "bad rank / nranks");
+  if (layout != FMM_ROW_MAJOR && layout != FMM_COL_MAJOR) throw Error(FMM_E_INVALID_ARG, "bad layout");
+  if (P < 0 || Nc < 0) throw Error(FMM_E_SHAPE, "negative dimension");
+  long long r0, r1;
+  dist_slab_range(layout == FMM_ROW_MAJOR ? P : Nc, nranks, rank, &r0, &r1);
+  *first = r0;
+  *last = r1;
   return FMM_OK;
   FMM_API_END
 }
@@ -1305,7 +1322,9 @@ fmm_status_t fmm_plan_stats(const fmm_plan_t* p, double out[8]) {
     s[1] += ln.elem_adds;
     s[2] += 8.0 * (ln.elem_reads + ln.elem_writes);
     s[3] += ln.gemm_bytes;
-    s[4] += 1;
+    s[4] += (ln.kind == Launch::FORM_A || ln.kind == Launch::FORM_B || ln.kind == Launch::ASSEMBLE) && ln.kern
+                ? lincomb_steps(*ln.kern)  // pairwise: one launch per chain position
+                : 1;
     if (ln.kind == Launch::GEMM || ln.kind == Launch::FUSED || (ln.kind == Launch::SKINNY && ln.level == p->L))
       s[6] += ln.count;
     if (ln.kind == Launch::SKINNY) s[4] += (ln.nrow > 0) + (ln.ncol > 0) - 1;

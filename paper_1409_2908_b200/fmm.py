@@ -17,6 +17,7 @@ _STATUS = {1: "FMM_E_INVALID_ARG", 2: "FMM_E_NOT_EXACT", 3: "FMM_E_SHAPE", 4: "F
            5: "FMM_E_CUDA", 6: "FMM_E_NCCL", 7: "FMM_E_UNSUPPORTED", 8: "FMM_E_PARSE"}
 ROW_MAJOR, COL_MAJOR = 0, 1
 STREAMING, WRITE_ONCE, PAIRWISE = 0, 1, 2
+DIST_SLABS = -1  # fmm_plan_create_dist root: slab-distributed output (FMM_DIST_SLABS)
 _STRATEGIES = {"streaming": STREAMING, "write_once": WRITE_ONCE, "pairwise": PAIRWISE}
 
 
@@ -69,6 +70,7 @@ def _load():
         "fmm_sync": [vp],
         "fmm_hybrid_split": [i64, i32, i64, p64, p64],
         "fmm_shard_leaf_rows": [i64, i64, i64, i64, p64, p64],
+        "fmm_dist_slab": [i64, i64, i32, i32, i32, p64, p64],
         "fmm_dgemm": [i64, i64, i64, dp, vp, i64, vp, i64, dp, vp, i64, vp],
     }
     for name, args in sig.items():
@@ -258,6 +260,8 @@ class Plan:
             _check(_lib.fmm_plan_create(alg._h, P, Q, N, levels, ctypes.byref(o), self.device, ctypes.byref(h)))
         else:
             self.device = comm.device
+            if root == "slabs":
+                root = DIST_SLABS
             _check(_lib.fmm_plan_create_dist(alg._h, P, Q, N, levels, ctypes.byref(o), comm._h, root, ctypes.byref(h)))
         self._h = h
 
@@ -384,6 +388,15 @@ def shard_leaf_rows(leaves: int, rows: int, G: int, g: int):
     r1 = (ctypes.c_int64 * leaves)()
     _check(_lib.fmm_shard_leaf_rows(leaves, rows, G, g, r0, r1))
     return list(zip(r0, r1))
+
+
+def dist_slab(P: int, N: int, layout: str, nranks: int, rank: int):
+    """(first, last): the rows (row-major) or columns (column-major) of C that `rank` holds after a
+    slab-distributed combine (root="slabs"; fmm_dist_slab)."""
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    _check(_lib.fmm_dist_slab(P, N, ROW_MAJOR if layout == "row" else COL_MAJOR, nranks, rank, ctypes.byref(a),
+                              ctypes.byref(b)))
+    return a.value, b.value
 
 
 def hybrid_split(R: int, L: int, G: int):

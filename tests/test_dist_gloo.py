@@ -24,7 +24,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, alg_name, q):
+def _worker(rank, world, port, alg_name, q, mode="root"):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -32,7 +32,7 @@ def _worker(rank, world, port, alg_name, q):
     try:
         import fmm_inputs as I
         import paper_1409_2908_b200 as F
-        from paper_1409_2908_b200.dist import combine_partials
+        from paper_1409_2908_b200.dist import combine_partials, scatter_partials
         from oracle import oracle as O
         a = O.load_alg(os.path.join(ALGS, alg_name + ".txt"))
         U, V, W = (np.array(X, dtype=np.float64) for X in a.as_float())
@@ -51,10 +51,25 @@ def _worker(rank, world, port, alg_name, q):
             Mr[r0:r1] = S[r0:r1] @ T
             for k in range(M * N):
                 C[(k // N) * p:(k // N + 1) * p, (k % N) * n:(k % N + 1) * n] += W[k, r] * Mr
-        Ct = torch.from_numpy(C)
-        combine_partials(Ct, root=0)
         owns = [None] * world
         dist.all_gather_object(owns, own)
+        if mode != "root":
+            # slab-distributed output: row slabs of a row-major C, column slabs of a column-major C
+            Ct = torch.from_numpy(C) if mode == "slabs_row" else torch.from_numpy(np.ascontiguousarray(C.T)).t()
+            first, last = scatter_partials(Ct)
+            lay = "row" if mode == "slabs_row" else "col"
+            assert (first, last) == F.dist_slab(C.shape[0], C.shape[1], lay, world, rank)
+            want = A @ B
+            got = Ct.numpy()
+            ok = np.array_equal(got[first:last], want[first:last]) if lay == "row" else \
+                np.array_equal(got[:, first:last], want[:, first:last])
+            ok_all = [None] * world
+            dist.all_gather_object(ok_all, ok)
+            if rank == 0:
+                q.put((all(ok_all), True))
+            return
+        Ct = torch.from_numpy(C)
+        combine_partials(Ct, root=0)
         if rank == 0:
             cover = np.zeros((R, p), dtype=int)
             for o in owns:
@@ -65,14 +80,16 @@ def _worker(rank, world, port, alg_name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,alg", [(2, "strassen_222_7"), (3, "hk_class_323_15"), (2, "alg_433_29")])
-def test_sharded_partials_reduce_to_product(world, alg):
+@pytest.mark.parametrize("world,alg,mode", [(2, "strassen_222_7", "root"), (3, "hk_class_323_15", "root"),
+                                           (2, "alg_433_29", "root"), (3, "alg_424_26", "slabs_row"),
+                                           (2, "hk_class_323_15", "slabs_col")])
+def test_sharded_partials_reduce_to_product(world, alg, mode):
     import __graft_entry__
     __graft_entry__.build()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, alg, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, alg, q, mode)) for r in range(world)]
     for pr in procs:
         pr.start()
     for pr in procs:

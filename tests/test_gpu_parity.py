@@ -159,6 +159,8 @@ def test_pairwise_traffic_is_the_papers_count():
     A, B = I.problem(2 * b, 2 * b, 2 * b, seed=13)
     C, p = run("strassen_222_7", A, B, 1, strategy="pairwise", cse=False)
     assert p.stats()["add_bytes"] == 8 * (50 + 32) * b * b
+    # one launch per chain position: longest S chain 2, T chain 2, C chain 4, plus the leaf GEMM
+    assert p.stats()["launches"] == 2 + 2 + 1 + 4
     assert np.max(np.abs(C - O.fast(A, B, oalg("strassen_222_7"), 1))) <= bound(A, B, 1e-12)
     _, pw = run("strassen_222_7", A, B, 1, strategy="write_once", cse=False)
     assert pw.stats()["add_bytes"] < p.stats()["add_bytes"]
@@ -338,6 +340,18 @@ def test_distributed_plan_single_rank():
     with pytest.raises(F.FmmError) as e:
         p.execute(dev(A), dev(B), Cb[:, :250])
     assert e.value.status == "FMM_E_UNSUPPORTED"
+
+
+@pytest.mark.parametrize("layout", ["row", "col"])
+def test_distributed_plan_single_rank_slabs(layout):
+    # root = "slabs" (FMM_DIST_SLABS) at one rank: the only slab is all of C
+    A, B = I.problem(260, 130, 190, seed=22, kind="integers")
+    comm = F.Comm(F.nccl_unique_id(), 1, 0)
+    p = F.Plan(falg("alg_424_26"), 260, 130, 190, 2, layout=layout, comm=comm, root="slabs")
+    C = p.execute(dev(A, layout), dev(B, layout))
+    torch.cuda.synchronize()
+    assert np.array_equal(C.cpu().numpy(), A @ B)
+    assert F.dist_slab(260, 190, layout, 1, 0) == (0, 260 if layout == "row" else 190)
 
 
 def test_classical_root_shards_write_zeros_elsewhere():

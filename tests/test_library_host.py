@@ -108,3 +108,16 @@ def test_nccl_unique_id_host_only():
     import paper_1409_2908_b200 as F
     a, b = F.nccl_unique_id(), F.nccl_unique_id()
     assert len(a) == 128 and len(b) == 128 and a != b
+
+
+@pytest.mark.parametrize("outer,G", [(0, 3), (1, 2), (7, 3), (12000, 8), (8192, 5)])
+def test_dist_slabs_partition_the_outer_dimension(F, outer, G):
+    # FMM_DIST_SLABS: rank g owns [first, last); the slabs tile [0, outer) in order, sizes differ by <= 1
+    for lay, (P, N) in (("row", (outer, 5)), ("col", (5, outer))):
+        spans = [F.dist_slab(P, N, lay, G, g) for g in range(G)]
+        assert spans[0][0] == 0 and spans[-1][1] == outer
+        assert all(spans[g][1] == spans[g + 1][0] for g in range(G - 1))
+        sizes = [b - a for a, b in spans]
+        assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(F.FmmError):
+        F.dist_slab(4, 4, "row", 2, 2)
