@@ -133,6 +133,16 @@ void emit_chain(std::ostringstream& o, const std::string& dst, const Expr& e, co
   }
 }
 
+// Thread -> element position: one thread per V-vector position of the rows x cvec block, flattened
+// (row-major) so that narrow blocks (a few hundred columns at deep levels) still fill whole CTAs;
+// a warp touches at most two row segments.  rows * cvec < 2^32 (checked by lincomb_launch).
+void emit_flat_position(std::ostringstream& o, const char* rows) {
+  o << "  const unsigned e = blockIdx.x * blockDim.x + threadIdx.x;\n";
+  o << "  if (e >= (unsigned)" << rows << " * (unsigned)cvec) return;\n";
+  o << "  {\n";
+  o << "    const int row = (int)(e / (unsigned)cvec), cv = (int)(e - (unsigned)row * (unsigned)cvec);\n";
+}
+
 std::string generate(const LincombSpec& s, const Program& p, LincombCost& cost) {
   const int nin = s.nin, nout = s.nout, V = s.vec;
   const std::string T = V == 2 ? "double2" : "double";
@@ -150,9 +160,7 @@ std::string generate(const LincombSpec& s, const Program& p, LincombCost& cost) 
   if (wo) o << "  const int z = blockIdx.z / " << nout << ", oi = blockIdx.z % " << nout << ";\n";
   else o << "  const int z = blockIdx.z;\n";
   o << "  const Node& nd = nodes[z];\n";
-  o << "  const int cv = blockIdx.x * blockDim.x + threadIdx.x;\n";
-  o << "  if (cv >= cvec) return;\n";
-  o << "  for (int row = blockIdx.y; row < rows; row += gridDim.y) {\n";
+  emit_flat_position(o, "rows");
   o << "    const long long pi = (long long)row * nd.ld_in + (long long)cv * " << V << ";\n";
   o << "    const long long po = (long long)row * nd.ld_out + (long long)cv * " << V << ";\n";
   auto var = [&](int v) { return v < nin ? "x" + std::to_string(v) : "t" + std::to_string(v - nin); };
@@ -300,8 +308,9 @@ void lincomb_launch(const LincombKernel& k, const void* d_nodes, int nnodes, lon
   if (cvec * k.spec.vec != cols) throw Error(FMM_E_INVALID_ARG, "lincomb: cols not a multiple of vec");
   const long long zdim = (long long)nnodes * (k.spec.strategy != FMM_ADD_STREAMING ? k.spec.nout : 1);
   if (zdim > 65535) throw Error(FMM_E_UNSUPPORTED, "lincomb: too many nodes in one launch");
-  dim3 grid((unsigned)((cvec + k.threads - 1) / k.threads), (unsigned)std::min<long long>(rows, 65535),
-            (unsigned)zdim);
+  const long long total = rows * cvec;
+  if (total >= (1ll << 32)) throw Error(FMM_E_UNSUPPORTED, "lincomb: block too large for one launch");
+  dim3 grid((unsigned)((total + k.threads - 1) / k.threads), 1, (unsigned)zdim);
   int r = (int)rows, c = (int)cvec;
   if (k.spec.strategy == FMM_ADD_PAIRWISE) {
     // one launch per chain position: a term's pass must see the previous term's stores
@@ -517,9 +526,7 @@ std::string generate_two_level(const TwoLevelSpec& sp, LincombCost& cost) {
   o << "struct Node { const double* in[" << nin << "]; double* out[" << nout << "]; long long ld_in; long long ld_out; };\n";
   o << "extern \"C\" __global__ void __launch_bounds__(128) lincomb(const Node* __restrict__ nodes, int nrows, int cvec) {\n";
   o << "  const Node& nd = nodes[blockIdx.z];\n";
-  o << "  const int cv = blockIdx.x * blockDim.x + threadIdx.x;\n";
-  o << "  if (cv >= cvec) return;\n";
-  o << "  for (int row = blockIdx.y; row < nrows; row += gridDim.y) {\n";
+  emit_flat_position(o, "nrows");
   o << "    const long long pi = (long long)row * nd.ld_in + (long long)cv * " << V << ";\n";
   o << "    const long long po = (long long)row * nd.ld_out + (long long)cv * " << V << ";\n";
   // chain over named terms (first-term initialisation; --fmad=false keeps products separate)
