@@ -74,7 +74,8 @@ typedef struct {
   size_t workspace_limit_bytes; /* 0 = no limit */
   int peel_align;           /* 1: when the paper's core N' = N floor(Nc/N) gives an odd column-block
                                width, peel to N' = 2N floor(Nc/(2N)) instead (one extra column
-                               block in the classical strip), so every sub-block view is 16-byte
+                               block in the classical strip), and likewise Q' = 2K floor(Q/(2K))
+                               for an odd A column-block width, so every sub-block view is 16-byte
                                aligned and TMA / 16-byte vector paths apply (R7b).
                                0: the paper's minimal peeling everywhere. */
   int fuse_leaf_level;      /* 1: run the last level's formation (S_r, T_r of the leaves), the leaf

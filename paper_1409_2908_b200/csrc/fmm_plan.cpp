@@ -978,6 +978,13 @@ namespace {
 
 double predict_seconds(const fmm_alg& a, long long P, long long Q, long long N, int levels, int* used_levels);
 
+// R7b's peel: widen the peeled strip so the child block widths Q1 / K and N1 / Nb are even
+template <class D>
+void peel_even(D& d, int K, int Nb) {
+  if ((d.Q1 / K) % 2 == 1 && d.Q / (2 * K) >= 1) d.Q1 = 2 * K * (d.Q / (2 * K));
+  if ((d.N1 / Nb) % 2 == 1 && d.N / (2 * Nb) >= 1) d.N1 = 2 * Nb * (d.N / (2 * Nb));
+}
+
 void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long long Nc, int levels,
                const fmm_plan_options* opt, int device) {
   if (!alg) throw Error(FMM_E_INVALID_ARG, "null algorithm");
@@ -1039,8 +1046,9 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
     d.P1 = M * (d.P / M);
     d.Q1 = K * (d.Q / K);
     d.N1 = Nb * (d.N / Nb);
-    // R7b: keep column-block widths even so sub-block views stay 16-byte aligned (TMA)
-    if (p->opt.peel_align && L < levels && (d.N1 / Nb) % 2 == 1 && d.N / (2 * Nb) >= 1) d.N1 = 2 * Nb * (d.N / (2 * Nb));
+    // R7b: keep column-block widths even so sub-block views stay 16-byte aligned (TMA): the
+    // column offsets of A's blocks are multiples of Q / K, of B's and C's multiples of N / Nb
+    if (p->opt.peel_align && L < levels) peel_even(d, K, Nb);
     p->dims.push_back(d);
     if (L == levels || d.P < M || d.Q < K || d.N < Nb) break;
     d = Dims{d.P1 / M, d.Q1 / K, d.N1 / Nb, 0, 0, 0};
@@ -1390,6 +1398,7 @@ double predict_seconds(const fmm_alg& a, long long P, long long Q, long long N, 
     d.P1 = M * (d.P / M);
     d.Q1 = K * (d.Q / K);
     d.N1 = Nb * (d.N / Nb);
+    if (L < levels) peel_even(d, K, Nb);  // as plan_init with the default peel_align
     dims.push_back(d);
     if (L == levels || d.P < M || d.Q < K || d.N < Nb) break;
     d = D{d.P1 / M, d.Q1 / K, d.N1 / Nb, 0, 0, 0};
