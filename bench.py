@@ -111,6 +111,18 @@ def to_device(x, layout, device):
     return torch.from_numpy(np.ascontiguousarray(x.T)).to(device).t()
 
 
+def cpu_model():
+    """The host CPU's model name (/proc/cpuinfo), for the cpu_baseline record."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_oracle_sample(w, A, B, frac):
     """The oracle as it stands (oracle_fast, same algorithm and L) on the leading
     (frac P) x (frac Q) x (frac N) sub-problem of the workload's own A and B.  One run."""
@@ -124,7 +136,7 @@ def cpu_oracle_sample(w, A, B, frac):
     dt = time.perf_counter() - t0
     cores = len(os.sched_getaffinity(0))
     return {"value": 2.0 * p * q * n / dt / 1e9, "unit": "GFLOPS", "cores": cores, "kind": "oracle",
-            "seconds": dt,
+            "seconds": dt, "cpu_model": cpu_model(),
             "sample": f"oracle_fast ({w['alg']}, L={w['L']}) on the leading {p}x{q}x{n} sub-problem of the "
                       f"workload's A,B (one run, OpenMP over {cores} threads); value = 2pqn/t"}
 
@@ -153,7 +165,7 @@ def run_reference(args, w):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": w["desc"], "sample": last["sample"]},
             "cpu_baseline": {"value": value, "unit": "GFLOPS", "cores": last["cores"], "kind": "oracle",
-                             "sample": last["sample"]},
+                             "sample": last["sample"], "cpu_model": last["cpu_model"]},
             "e2e": {"value": value, "unit": "GFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
