@@ -378,6 +378,41 @@ def main():
         cub = flops / (best * 1e-3) / 1e9
         del ref
 
+    # the classical comparison on our own DMMA GEMM (L = 0): at N > 1 each rank multiplies its row
+    # slab of A by B with no exchange (SURVEY f1's classical row-slab split), timed as max over ranks
+    own = None
+    try:
+        if w["layout"] == "row":
+            r0, r1 = F.dist_slab(P, N, "row", world, rank)
+            As = A[r0:r1]
+        else:  # column-major: the slab of C's columns, i.e. B's columns
+            r0, r1 = F.dist_slab(P, N, "col", world, rank)
+            As = None
+        m_rows = (r1 - r0) if As is not None else P
+        n_cols = N if As is not None else (r1 - r0)
+        cp = F.Plan(alg, m_rows, Q, n_cols, 0, layout=w["layout"])
+        Aa, Bb = (As, B) if As is not None else (A, B[:, r0:r1])
+        Cc = cp.new_output()
+        for _ in range(2):
+            cp.execute(Aa, Bb, Cc, stream=stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(3):
+            cp.execute(Aa, Bb, Cc, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        tt = torch.tensor([e0.elapsed_time(e1) / 3], dtype=torch.float64, device=device)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        own = {"ms": float(tt.item()), "value": flops / (float(tt.item()) * 1e-3) / 1e9,
+               "what": "classical DMMA GEMM (L = 0, this library)" + (f", row slabs x{world}, no exchange" if world > 1 else "")}
+        del cp, Cc
+    except Exception as ex:  # noqa: BLE001  (a comparison leg only)
+        own = {"error": str(ex)[:200]}
+
     # end-to-end through the public host-buffer API: H2D of A and B, execute, D2H of C per step
     e2e = None
     if not args.no_e2e:
@@ -489,6 +524,7 @@ def main():
             "fp64_peak_tflops": {"dmma_measured": dmma_peak, "dfma_measured": dfma_peak, "nameplate": 37.2},
             "effective_frac_of_fp64_peak": value / 1e3 / dmma_peak,
             "cublas_dgemm_gflops_same_inputs": cub,
+            "classical_own_dgemm": own,
             "paper_effective_gflops": (2.0 * P * Q * N - P * N) / (ms_step * 1e-3) / 1e9,
             "plan": {k: st[k] for k in ("gemm_flops", "add_flops", "add_bytes", "launches", "leaves")},
         }
