@@ -191,6 +191,8 @@ def main():
                     help="N > 1: partial-C reduce by torch.distributed (NCCL) or inside fmm_execute (fmm_plan_create_dist)")
     ap.add_argument("--output", default="root", choices=["root", "slabs"],
                     help="N > 1: C summed onto rank 0, or slab-distributed (slab g of C summed onto rank g)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N > 1: gloo only to exercise the multi-rank control flow where ranks share a GPU (not a measurement)")
     ap.add_argument("--no-other", action="store_true", help="skip timing the other leaf-level schedule (fused vs separate)")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -207,8 +209,15 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        if args.dist_backend == "gloo":
+            # control-flow check of the N > 1 path on a box with fewer GPUs than ranks (ranks share
+            # devices; gloo carries the collectives): its numbers are not measurements
+            local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if args.dist_backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     else:
         torch.cuda.set_device(0)
     device = torch.device(f"cuda:{torch.cuda.current_device()}")
@@ -273,6 +282,26 @@ def main():
     ms_step = ms / args.steps
     flops = 2.0 * P * Q * N
     value = flops / (ms_step * 1e-3) / 1e9
+
+    # result check after the timed steps (C holds the last step's combined product): sampled rows
+    # of rank 0's part of C against a cuBLAS product of the same rows (a check, not a timing), at the
+    # north-star tolerance max |C - AB| <= 1e-10 ||A||_F ||B||_F
+    check = None
+    if rank == 0:
+        if args.output == "slabs" and world > 1:
+            lo, hi = F.dist_slab(P, N, w["layout"], world, 0)
+        else:
+            lo, hi = 0, (P if w["layout"] == "row" else N)
+        g = torch.Generator().manual_seed(7)
+        idx = torch.randint(lo, max(lo + 1, hi), (min(64, max(hi - lo, 1)),), generator=g).to(device)
+        if hi > lo:
+            if w["layout"] == "row":
+                err = (C[idx] - A[idx] @ B).abs().max().item()
+            else:  # slabs of C's columns
+                err = (C[:, idx] - A @ B[:, idx]).abs().max().item()
+            tol = 1e-10 * torch.linalg.norm(A).item() * torch.linalg.norm(B).item()
+            check = {"sampled": int(idx.numel()), "of": "rows" if w["layout"] == "row" else "columns",
+                     "max_abs_err": err, "tolerance": tol, "ok": bool(err <= tol)}
 
     # per-phase device times measured on the launching stream during the timed region
     ph = np.array([[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]), e[3].elapsed_time(e[4])]
@@ -499,11 +528,13 @@ def main():
                        "strategy": args.strategy, "cse": bool(args.cse),
                        "l2": "inputs larger than L2 (A, B, C 0.54 GB each vs 126 MB); no flush"
                        if args.workload != "c1" else "small config: L2-resident",
-                       "parallelism": (f"{args.shard_mode}-level shards x{world} + NCCL "
+                       "parallelism": (f"{args.shard_mode}-level shards x{world} + {args.dist_backend.upper()} "
                                        f"{'reduce to rank 0' if args.output == 'root' else 'slab reduce-scatter'} "
                                        f"({'fmm_execute' if lib_comm else 'torch.distributed'})"
                                        if world > 1 else "1 GPU"),
-                       "fused_leaf_level": fused, "collapsed_levels": bool(st.get("collapsed", 0))},
+                       "fused_leaf_level": fused, "collapsed_levels": bool(st.get("collapsed", 0)),
+                       **({"dist_backend": "gloo (control-flow check, ranks share a GPU: NOT a measurement)"}
+                          if world > 1 and args.dist_backend == "gloo" else {})},
             "roofline": roofline,
             "clocks": clk,
             "e2e": e2e,
@@ -525,6 +556,7 @@ def main():
             "effective_frac_of_fp64_peak": value / 1e3 / dmma_peak,
             "cublas_dgemm_gflops_same_inputs": cub,
             "classical_own_dgemm": own,
+            "result_check": check,
             "paper_effective_gflops": (2.0 * P * Q * N - P * N) / (ms_step * 1e-3) / 1e9,
             "plan": {k: st[k] for k in ("gemm_flops", "add_flops", "add_bytes", "launches", "leaves")},
         }
