@@ -471,7 +471,7 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        n_e2e = max(3, min(args.steps, 30))
+        n_e2e = max(3, min(max(args.steps, 30), 60))  # fill and drain of the copy pipeline amortised over >= 30 steps
         h0 = time.perf_counter()
         for _ in range(n_e2e):
             e2e_step()
