@@ -16,8 +16,8 @@
 // file in algs/ independently with fractions.Fraction.
 //
 //   g++ -O2 -std=c++17 -o tools/flipsearch tools/flipsearch.cpp
-//   tools/flipsearch M K N TARGET [--seed S] [--plateau P] [--seconds T] [--out FILE]
-// (about 3.5 M flips/s on one core at R ~ 40; a plateau of 5e6-2e7 flips works for <2,3,4> / <3,4,4>)
+//   tools/flipsearch M K N TARGET [--seed S] [--plateau P] [--seconds T] [--out FILE] [--from FILE]
+// (about 3.5 M flips/s on one core at R ~ 40; a plateau of 5e6 flips finds <2,3,4;20> in seconds to minutes)
 #include <algorithm>
 #include <array>
 #include <chrono>
@@ -181,14 +181,70 @@ struct Walker {
   }
 };
 
-void write_file(const char* path, const Problem& pr, const std::vector<Term>& t, unsigned long long seed) {
+// a scheme in the S:190 text format (comments after '#'; header "M K N R ..."; MK rows of U, KN rows of
+// V, MN rows of W, R entries each, all in {-1, 0, 1}), e.g. a direct sum to start from
+std::vector<Term> read_file(const char* path, const Problem& pr) {
+  FILE* f = fopen(path, "r");
+  if (!f) {
+    perror(path);
+    exit(2);
+  }
+  std::vector<std::vector<int>> rows;
+  std::vector<int> header;
+  char line[1 << 14];
+  while (fgets(line, sizeof line, f)) {
+    if (char* h = strchr(line, '#')) *h = 0;
+    std::vector<int> v;
+    for (char* tok = strtok(line, " \t\r\n"); tok; tok = strtok(nullptr, " \t\r\n")) {
+      char* end = nullptr;
+      const long x = strtol(tok, &end, 10);
+      if (end && *end == 0) v.push_back((int)x);
+    }
+    if (v.empty()) continue;
+    if (header.empty()) header = v;
+    else rows.push_back(v);
+  }
+  fclose(f);
+  if (header.size() < 4 || header[0] != pr.M || header[1] != pr.K || header[2] != pr.N) {
+    fprintf(stderr, "%s: not a <%d,%d,%d> scheme\n", path, pr.M, pr.K, pr.N);
+    exit(2);
+  }
+  const int R = header[3];
+  if ((int)rows.size() != pr.dim(0) + pr.dim(1) + pr.dim(2)) {
+    fprintf(stderr, "%s: expected %d coefficient rows\n", path, pr.dim(0) + pr.dim(1) + pr.dim(2));
+    exit(2);
+  }
+  std::vector<Term> t(R);
+  int row = 0;
+  for (int s = 0; s < 3; ++s)
+    for (int i = 0; i < pr.dim(s); ++i, ++row) {
+      if ((int)rows[row].size() != R) {
+        fprintf(stderr, "%s: row %d has %zu entries, want %d\n", path, row, rows[row].size(), R);
+        exit(2);
+      }
+      for (int r = 0; r < R; ++r) {
+        const int x = rows[row][r];
+        if (x < -1 || x > 1) {
+          fprintf(stderr, "%s: entry %d outside {-1, 0, 1}\n", path, x);
+          exit(2);
+        }
+        if (x == 1) t[r].f[s].p |= 1ull << i;
+        if (x == -1) t[r].f[s].n |= 1ull << i;
+      }
+    }
+  return t;
+}
+
+void write_file(const char* path, const Problem& pr, const std::vector<Term>& t, unsigned long long seed,
+                const char* from_desc) {
   FILE* f = fopen(path, "w");
   if (!f) {
     perror(path);
     exit(1);
   }
   fprintf(f, "# <%d,%d,%d;%zu> exact bilinear algorithm, entries in {-1,0,1}.\n", pr.M, pr.K, pr.N, t.size());
-  fprintf(f, "# Found by tools/flipsearch.cpp (exact integer flip-graph walk from the classical algorithm, seed %llu).\n", seed);
+  fprintf(f, "# Found by tools/flipsearch.cpp (exact integer flip-graph walk from %s, seed %llu).\n",
+          from_desc, seed);
   fprintf(f, "# Rows: U (A-blocks row-major), blank, V, blank, W.  Exact by tests/test_oracle_algebra.py.\n");
   fprintf(f, "%d %d %d %zu exact\n", pr.M, pr.K, pr.N, t.size());
   for (int s = 0; s < 3; ++s) {
@@ -205,7 +261,7 @@ void write_file(const char* path, const Problem& pr, const std::vector<Term>& t,
 
 int main(int argc, char** argv) {
   if (argc < 5) {
-    fprintf(stderr, "usage: %s M K N TARGET [--seed S] [--plateau P] [--seconds T] [--out FILE]\n", argv[0]);
+    fprintf(stderr, "usage: %s M K N TARGET [--seed S] [--plateau P] [--seconds T] [--out FILE] [--from FILE]\n", argv[0]);
     return 2;
   }
   Problem pr{atoi(argv[1]), atoi(argv[2]), atoi(argv[3])};
@@ -213,17 +269,23 @@ int main(int argc, char** argv) {
   unsigned long long seed = 1, plateau = 100000;
   double seconds = 600;
   const char* out = nullptr;
+  const char* from = nullptr;
   for (int i = 5; i + 1 < argc; i += 2) {
     if (!strcmp(argv[i], "--seed")) seed = strtoull(argv[i + 1], nullptr, 10);
     else if (!strcmp(argv[i], "--plateau")) plateau = strtoull(argv[i + 1], nullptr, 10);
     else if (!strcmp(argv[i], "--seconds")) seconds = atof(argv[i + 1]);
     else if (!strcmp(argv[i], "--out")) out = argv[i + 1];
+    else if (!strcmp(argv[i], "--from")) from = argv[i + 1];
   }
   if (pr.dim(0) > MAXD || pr.dim(1) > MAXD || pr.dim(2) > MAXD) {
     fprintf(stderr, "dimensions too large\n");
     return 2;
   }
-  Walker w{pr, classical(pr), std::mt19937_64(seed)};
+  Walker w{pr, from ? read_file(from, pr) : classical(pr), std::mt19937_64(seed)};
+  if (!verify(pr, w.t)) {
+    fprintf(stderr, "the starting scheme is not exact\n");
+    return 2;
+  }
   size_t best = w.t.size();
   std::vector<Term> best_t = w.t;
   unsigned long long since = 0, flips = 0;
@@ -259,6 +321,6 @@ int main(int argc, char** argv) {
     return 1;
   }
   fprintf(stderr, "best rank %zu (target %zu), exact\n", best, target);
-  if (out && best <= target) write_file(out, pr, best_t, seed);
+  if (out && best <= target) write_file(out, pr, best_t, seed, from ? from : "the classical algorithm");
   return best <= target ? 0 : 3;
 }
