@@ -96,10 +96,15 @@ typedef struct {
                                L >= 2, a base case with MK, KN, MN <= 4, no peeling at level L-1.
                                The chains are the oracle's two levels exactly (CSE is not used
                                there).  0: one level per launch. */
+  int cuda_graphs;          /* 1: the second and later fmm_execute calls with the same A/B/C
+                               pointers and leading dimensions replay the plan's launch sequence
+                               as one CUDA graph (captured once per cached pointer set), which
+                               removes the per-launch host overhead.  Not used for distributed,
+                               fused or timed executes.  0: plain launches every time. */
 } fmm_plan_options;
 
 /* Fill *opt with the defaults: row-major, streaming, cse = 1, shard 0 of 1, no limit,
-   peel_align = 1, fuse_leaf_level = 0, collapse_levels = 1. */
+   peel_align = 1, fuse_leaf_level = 0, collapse_levels = 1, cuda_graphs = 1. */
 void fmm_plan_options_default(fmm_plan_options* opt);
 
 /* ---- algorithms ------------------------------------------------------------------------- */

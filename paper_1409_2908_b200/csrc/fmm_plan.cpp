@@ -134,7 +134,10 @@ struct fmm_plan_s {
     long long lda = -1, ldb = -1, ldc = -1;
     std::vector<Launch> launches;
     unsigned long long used = 0;
+    int runs = 0;                     // executes served by this slot
+    cudaGraphExec_t gexec = nullptr;  // its launch sequence as a CUDA graph (cuda_graphs option)
   } slot[2];
+  cudaStream_t s_cap = nullptr;  // private stream the graphs are captured on
   unsigned long long use_clock = 0;
   cudaEvent_t upload_done = nullptr;
   cudaEvent_t ev[8] = {};
@@ -153,8 +156,11 @@ struct fmm_plan_s {
     cudaDeviceSynchronize();
     if (ws) cudaFree(ws);
     if (d_ctr) cudaFree(d_ctr);
-    for (auto& sl : slot)
+    for (auto& sl : slot) {
       if (sl.d_tab) cudaFree(sl.d_tab);
+      if (sl.gexec) cudaGraphExecDestroy(sl.gexec);
+    }
+    if (s_cap) cudaStreamDestroy(s_cap);
     if (h_pinned) cudaFreeHost(h_pinned);
     for (int b = 0; b < 2; ++b) {
       if (sA[b]) cudaFree(sA[b]);
@@ -1158,6 +1164,9 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
     // stream-ordered: kernels of earlier executes on this stream that read the slot finish first
     FMM_CUDA(cudaMemcpyAsync(sl->d_tab, p->h_pinned, p->h_tab.size(), cudaMemcpyHostToDevice, stream));
     FMM_CUDA(cudaEventRecord(p->upload_done, stream));
+    if (sl->gexec) FMM_CUDA(cudaGraphExecDestroy(sl->gexec));
+    sl->gexec = nullptr;
+    sl->runs = 0;
     sl->valid = true;
     sl->A = a;
     sl->B = b;
@@ -1171,6 +1180,34 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
   char* d_tab = sl->d_tab;
   if (timed) FMM_CUDA(cudaEventRecord(evs[0], stream));
   int phase = 0;  // 0 formation, 1 gemm, 2 assembly/strips
+  // CUDA-graph replay of a cached slot (option cuda_graphs): captured on the slot's second use,
+  // on a private stream, then launched on the caller's stream (kernels only: the table upload
+  // happened when the slot was built; fused launches need their counter reset and stay plain)
+  bool graphable = p->opt.cuda_graphs && !timed && !p->dist_comm;
+  for (const Launch& ln : sl->launches) graphable &= ln.kind != Launch::FUSED;
+  if (graphable && sl->gexec) {
+    FMM_CUDA(cudaGraphLaunch(sl->gexec, stream));
+    ++sl->runs;
+    return;
+  }
+  const bool capture = graphable && sl->runs >= 1;
+  cudaStream_t ls = stream;  // the stream the launches below go to
+  if (capture) {
+    if (!p->s_cap) FMM_CUDA(cudaStreamCreateWithFlags(&p->s_cap, cudaStreamNonBlocking));
+    ls = p->s_cap;
+    FMM_CUDA(cudaStreamBeginCapture(ls, cudaStreamCaptureModeThreadLocal));
+  }
+  struct CaptureGuard {  // a launch that throws mid-capture must not leave the stream capturing
+    cudaStream_t s;
+    bool on;
+    ~CaptureGuard() {
+      if (!on) return;
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(s, &g);
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+    }
+  } guard{ls, capture};
   for (const Launch& ln : sl->launches) {
     const int ph = (ln.kind == Launch::FORM_A || ln.kind == Launch::FORM_B) ? 0
                    : (ln.kind == Launch::GEMM || ln.kind == Launch::FUSED || (ln.kind == Launch::SKINNY && ln.level == p->L))
@@ -1183,7 +1220,7 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
         phase = ph;
       }
       skinny_launch(reinterpret_cast<const GemmTask*>(d_tab + ln.table_off), ids, ln.nrow, ln.max_n, ids + ln.nrow,
-                    ln.ncol, ln.max_m, stream);
+                    ln.ncol, ln.max_m, ls);
       continue;
     }
     if (timed && ph != phase) {
@@ -1195,7 +1232,7 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
       case Launch::FORM_A:
       case Launch::FORM_B:
       case Launch::ASSEMBLE:
-        lincomb_launch(*ln.kern, tab, ln.count, ln.rows, ln.cols, stream);
+        lincomb_launch(*ln.kern, tab, ln.count, ln.rows, ln.cols, ls);
         break;
       case Launch::SKINNY:
         break;
@@ -1224,12 +1261,22 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
       case Launch::STRIPS:
         if (ln.tma)
           gemm_tma_launch(reinterpret_cast<const GemmTask*>(tab), d_tab + ln.maps_off, ln.count, ln.tiles, ln.bn,
-                          ln.uni_tm, ln.uni_tn, stream);
+                          ln.uni_tm, ln.uni_tn, ls);
         else
-          gemm_launch(reinterpret_cast<const GemmTask*>(tab), ln.count, ln.tiles, ln.aligned16, stream);
+          gemm_launch(reinterpret_cast<const GemmTask*>(tab), ln.count, ln.tiles, ln.aligned16, ls);
         break;
     }
   }
+  if (capture) {
+    cudaGraph_t g = nullptr;
+    guard.on = false;
+    FMM_CUDA(cudaStreamEndCapture(ls, &g));
+    const cudaError_t e = cudaGraphInstantiate(&sl->gexec, g, 0);
+    cudaGraphDestroy(g);
+    FMM_CUDA(e);
+    FMM_CUDA(cudaGraphLaunch(sl->gexec, stream));
+  }
+  ++sl->runs;
   if (p->dist_comm) {  // a7: the partial products of all ranks summed on the root
     const long long rows = p->colmajor ? p->userN : p->userP, cols = p->colmajor ? p->userP : p->userN;
     if (rows > 1 && ldc != cols) throw Error(FMM_E_UNSUPPORTED, "a distributed plan needs a contiguous C");
@@ -1259,6 +1306,7 @@ void fmm_plan_options_default(fmm_plan_options* o) {
   o->peel_align = 1;
   o->fuse_leaf_level = 0;  // within +-2 % of the separate kernels on B200
   o->collapse_levels = 1;
+  o->cuda_graphs = 1;
 }
 
 fmm_status_t fmm_plan_create(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels,

@@ -32,7 +32,8 @@ class _Options(ctypes.Structure):
     _fields_ = [("layout", ctypes.c_int), ("strategy", ctypes.c_int), ("cse", ctypes.c_int),
                 ("shard_rank", ctypes.c_int), ("shard_count", ctypes.c_int),
                 ("workspace_limit_bytes", ctypes.c_size_t), ("peel_align", ctypes.c_int),
-                ("fuse_leaf_level", ctypes.c_int), ("shard_mode", ctypes.c_int), ("collapse_levels", ctypes.c_int)]
+                ("fuse_leaf_level", ctypes.c_int), ("shard_mode", ctypes.c_int), ("collapse_levels", ctypes.c_int),
+                ("cuda_graphs", ctypes.c_int)]
 
 
 def _load():
@@ -236,7 +237,7 @@ class Plan:
                  strategy: str = "streaming", cse: bool = True, shard_rank: int = 0, shard_count: int = 1,
                  device: Optional[int] = None, workspace_limit_bytes: int = 0, peel_align: bool = True,
                  fuse: bool = False, collapse: bool = True, comm: Optional[Comm] = None, root: int = 0,
-                 shard_mode: str = "leaf"):
+                 shard_mode: str = "leaf", cuda_graphs: bool = True):
         import torch
         self.alg, self.P, self.Q, self.N, self.levels = alg, P, Q, N, levels
         self.layout = ROW_MAJOR if layout == "row" else COL_MAJOR
@@ -246,6 +247,7 @@ class Plan:
         if strategy not in _STRATEGIES:
             raise ValueError(f"strategy must be one of {sorted(_STRATEGIES)}")
         o.strategy = _STRATEGIES[strategy]
+        o.cuda_graphs = int(bool(cuda_graphs))
         o.cse = int(bool(cse))
         o.shard_rank, o.shard_count = shard_rank, shard_count
         o.workspace_limit_bytes = workspace_limit_bytes
