@@ -16,7 +16,7 @@
 // file in algs/ independently with fractions.Fraction.
 //
 //   g++ -O2 -std=c++17 -o tools/flipsearch tools/flipsearch.cpp
-//   tools/flipsearch M K N TARGET [--seed S] [--plateau P] [--seconds T] [--out FILE] [--from FILE]
+//   tools/flipsearch M K N TARGET [--seed S] [--plateau P] [--seconds T] [--out FILE] [--from FILE] [--best FILE]
 // (about 3.5 M flips/s on one core at R ~ 40; a plateau of 5e6 flips finds <2,3,4;20> in seconds to minutes)
 #include <algorithm>
 #include <array>
@@ -261,7 +261,7 @@ void write_file(const char* path, const Problem& pr, const std::vector<Term>& t,
 
 int main(int argc, char** argv) {
   if (argc < 5) {
-    fprintf(stderr, "usage: %s M K N TARGET [--seed S] [--plateau P] [--seconds T] [--out FILE] [--from FILE]\n", argv[0]);
+    fprintf(stderr, "usage: %s M K N TARGET [--seed S] [--plateau P] [--seconds T] [--out FILE] [--from FILE] [--best FILE]\n", argv[0]);
     return 2;
   }
   Problem pr{atoi(argv[1]), atoi(argv[2]), atoi(argv[3])};
@@ -270,12 +270,14 @@ int main(int argc, char** argv) {
   double seconds = 600;
   const char* out = nullptr;
   const char* from = nullptr;
+  const char* best_out = nullptr;  // --best FILE: rewritten at every new best rank
   for (int i = 5; i + 1 < argc; i += 2) {
     if (!strcmp(argv[i], "--seed")) seed = strtoull(argv[i + 1], nullptr, 10);
     else if (!strcmp(argv[i], "--plateau")) plateau = strtoull(argv[i + 1], nullptr, 10);
     else if (!strcmp(argv[i], "--seconds")) seconds = atof(argv[i + 1]);
     else if (!strcmp(argv[i], "--out")) out = argv[i + 1];
     else if (!strcmp(argv[i], "--from")) from = argv[i + 1];
+    else if (!strcmp(argv[i], "--best")) best_out = argv[i + 1];
   }
   if (pr.dim(0) > MAXD || pr.dim(1) > MAXD || pr.dim(2) > MAXD) {
     fprintf(stderr, "dimensions too large\n");
@@ -304,6 +306,7 @@ int main(int argc, char** argv) {
       since = 0;
       const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       fprintf(stderr, "rank %zu after %llu flips, %.1f s\n", best, flips, el);
+      if (best_out && verify(pr, best_t)) write_file(best_out, pr, best_t, seed, from ? from : "the classical algorithm");
     } else if (++since > plateau) {
       // plateau: restart from the best scheme found, then escape with a rank + 1 move
       w.t = best_t;
