@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "fmm_internal.h"
 
@@ -220,11 +221,14 @@ bool gemm_tasks_aligned16(const std::vector<GemmTask>& tasks) {
 
 void gemm_launch(const GemmTask* d_tasks, int ntasks, long long total_tiles, bool aligned16, cudaStream_t stream) {
   if (total_tiles <= 0 || ntasks <= 0) return;
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<unsigned long long> configured{0};  // bit d: attribute set on device d
+  int dev_ = 0;
+  FMM_CUDA(cudaGetDevice(&dev_));
+  const unsigned long long bit = 1ull << (dev_ & 63);
+  if (!(configured.load() & bit)) {
     FMM_CUDA(cudaFuncSetAttribute(grouped_dgemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
     FMM_CUDA(cudaFuncSetAttribute(grouped_dgemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
-    configured = true;
+    configured.fetch_or(bit);
   }
   if (aligned16)
     grouped_dgemm<true><<<(unsigned)total_tiles, THREADS, SMEM_BYTES, stream>>>(d_tasks, ntasks);

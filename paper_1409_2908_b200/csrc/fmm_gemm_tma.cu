@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
@@ -79,12 +80,15 @@ void gemm_tma_maps(const std::vector<GemmTask>& tasks, void* out) {
 template <int BN, int WGM, int WGN>
 static void launch_cfg(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int sms,
                        Uniform uni, cudaStream_t stream) {
-  static bool configured = false;  // per process; one device per process (torchrun)
+  static std::atomic<unsigned long long> configured{0};  // bit d: attribute set on device d
+  int dev_ = 0;
+  FMM_CUDA(cudaGetDevice(&dev_));
+  const unsigned long long bit = 1ull << (dev_ & 63);
   auto kern = grouped_dgemm_tma<BN, WGM, WGN>;
   const size_t smem = (size_t)gemm_smem_bytes(BN);
-  if (!configured) {
+  if (!(configured.load() & bit)) {
     FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
+    configured.fetch_or(bit);
   }
   const int grid = (int)std::min<long long>(total_tiles, sms);
   kern<<<grid, THREADS, smem, stream>>>(d_tasks, reinterpret_cast<const CUtensorMap*>(d_maps), ntasks, (int)total_tiles,
