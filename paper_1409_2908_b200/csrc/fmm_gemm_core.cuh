@@ -43,7 +43,10 @@ typedef CUtensorMap_opaque CUtensorMap;
 #endif
 
 constexpr int BM = 128, BK = 16;
-constexpr int GEMM_STAGES = 6;
+#ifndef FMM_GEMM_STAGES
+#define FMM_GEMM_STAGES 6
+#endif
+constexpr int GEMM_STAGES = FMM_GEMM_STAGES;
 constexpr int CONSUMERS = 8, THREADS = 128 + CONSUMERS * 32;  // warpgroup 0 = producer, 1-2 = consumers
 static_assert(THREADS == GEMM_THREADS, "host and device agree on the block size");
 constexpr int A_BYTES = BM * BK * 8;                           // 16 KB
