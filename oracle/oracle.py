@@ -335,6 +335,52 @@ def flops(P: int, Q: int, Nc: int, alg: Alg, L: int) -> float:
 
 
 # --------------------------------------------------------------------------------------------
+# addition-chain traffic per recursion node, in sub-block reads and writes (Sec. 3.2)
+# --------------------------------------------------------------------------------------------
+def addition_traffic(alg: Alg, strategy: str, alias_singletons: bool = False):
+    """(reads, writes) of one recursion node's addition chains, counted chain by chain as the three
+    implementations of P:622-636 perform them: the S_r chains (U columns), the T_r chains (V columns)
+    and the C_k chains (W rows).
+      pairwise   -- per chain of n terms: a copy (1 read, 1 write) then n - 1 daxpy calls (2 reads,
+                    1 write each), P:622-626 and the footnote;
+      write_once -- per chain: n reads, 1 write; U / V chains of one term are not written (P:644);
+      streaming  -- every A, B and M_r block a chain uses is read once; every formed S_r, T_r
+                    (more than one term) and every C_k is written once.
+    alias_singletons: one-term U / V chains cost nothing at all, neither read nor write (the GPU
+    path hands the block itself to the leaf product; SURVEY 8(d)'s "actual HBM traffic")."""
+    U, V, W = alg.U, alg.V, alg.W
+    R = alg.R
+    ucols = [[i for i in range(len(U)) if U[i][r] != 0] for r in range(R)]
+    vcols = [[j for j in range(len(V)) if V[j][r] != 0] for r in range(R)]
+    wrows = [[r for r in range(R) if W[k][r] != 0] for k in range(len(W))]
+    reads = writes = 0
+    for side, chains in (("u", ucols), ("v", vcols), ("w", wrows)):
+        if strategy == "streaming":
+            used = set()
+            for c in chains:
+                if side != "w" and len(c) == 1 and alias_singletons:
+                    continue
+                used.update(c)
+            reads += len(used)
+        for c in chains:
+            n = len(c)
+            single = side != "w" and n == 1
+            if single and alias_singletons:
+                continue
+            if strategy == "pairwise":
+                reads += 2 * n - 1
+                writes += n
+            elif strategy == "write_once":
+                reads += n
+                writes += 0 if single else 1
+            elif strategy == "streaming":
+                writes += 0 if single else 1
+            else:
+                raise ValueError(strategy)
+    return reads, writes
+
+
+# --------------------------------------------------------------------------------------------
 # check (d): a worst-case forward error bound derived from (U, V, W)  (P:1133-1134)
 # --------------------------------------------------------------------------------------------
 UNIT_ROUNDOFF = 2.0 ** -53

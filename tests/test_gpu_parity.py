@@ -166,6 +166,21 @@ def test_pairwise_traffic_is_the_papers_count():
     assert pw.stats()["add_bytes"] < p.stats()["add_bytes"]
 
 
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("strategy", ["streaming", "write_once", "pairwise"])
+def test_addition_bytes_equal_the_oracles_chain_count(name, strategy):
+    # one level on b x b blocks: the plan's algorithmic addition bytes are the oracle's chain-by-chain
+    # sub-block count (singleton chains aliased, as the kernels do) x 8 b^2
+    a = falg(name)
+    b = 64
+    P, Q, N = a.M * b, a.K * b, a.N * b
+    A, B = I.problem(P, Q, N, seed=14, kind="integers")
+    C, p = run(name, A, B, 1, strategy=strategy, cse=False)
+    reads, writes = O.addition_traffic(oalg(name), strategy, alias_singletons=True)
+    assert p.stats()["add_bytes"] == 8 * b * b * (reads + writes)
+    assert np.array_equal(C, A @ B)
+
+
 def test_quantized_inputs_exact_at_scale():
     # g = 11 grid: every partial sum of classical and fast algorithms is exact
     for name, L, P, Q, N in [("winograd_class_222_7", 2, 2048, 2048, 2048), ("alg_433_29", 2, 1800, 360, 360)]:

@@ -195,3 +195,31 @@ def test_error_bound_catches_a_broken_algorithm():
     A, B = I.problem(64, 64, 64, seed=5)
     err = float(np.max(np.abs(O.fast(A, B, bad, 2).astype(np.longdouble) - _exact(A, B))))
     assert err > O.error_bound(alg, 64, 2, float(np.abs(A).max()), float(np.abs(B).max()))
+
+
+# ---- addition-chain traffic per recursion node (Sec. 3.2) ----------------------------
+@pytest.mark.parametrize("name", sorted(ALGS_BY_NAME))
+def test_addition_traffic_matches_the_papers_closed_forms(name):
+    # the chain-by-chain count against the paper's closed forms
+    a = ALGS_BY_NAME[name]
+    nu, nv, nw = a.nnz()
+    nnz, R, MN = nu + nv + nw, a.R, a.M * a.N
+    single = sum(1 for X in (a.U, a.V) for r in range(R) if sum(1 for row in X if row[r] != 0) == 1)
+    assert O.addition_traffic(a, "pairwise") == (2 * nnz - 2 * R - MN, nnz)
+    rw, ww = O.addition_traffic(a, "write_once")
+    assert rw == nnz and ww == 2 * R + MN - single and ww <= 2 * R + MN
+    rs, ws = O.addition_traffic(a, "streaming")
+    every_block_used = all(any(v != 0 for v in row) for X in (a.U, a.V) for row in X)
+    assert every_block_used and rs == a.M * a.K + a.K * a.N + R
+    assert ws == ww
+    # aliasing the one-term U / V chains removes exactly one read (and, pairwise, one write) each
+    assert O.addition_traffic(a, "pairwise", True) == (2 * nnz - 2 * R - MN - single, nnz - single)
+    assert O.addition_traffic(a, "write_once", True) == (nnz - single, ww)
+
+
+def test_addition_traffic_strassen_and_winograd_values():
+    # SURVEY 8(d)'s verified counts (paper convention, then with singleton chains aliased)
+    s, w = ALGS_BY_NAME["strassen_222_7"], ALGS_BY_NAME["winograd_class_222_7"]
+    assert [O.addition_traffic(s, k) for k in ("pairwise", "write_once", "streaming")] == [(54, 36), (36, 14), (15, 14)]
+    assert [O.addition_traffic(w, k) for k in ("pairwise", "write_once", "streaming")] == [(66, 42), (42, 12), (15, 12)]
+    assert O.addition_traffic(s, "write_once", True) == (32, 14) and O.addition_traffic(w, "write_once", True) == (36, 12)
