@@ -19,6 +19,9 @@ Contents
       fast(A, B, alg, L)          the recursive evaluation with peeling
       fast_entries(A, B, alg, L, rows, cols)  sampled entries of exactly fast(...)
       flops(P,Q,N, alg, L)        operation count of fast(...)
+  * addition_traffic(alg, strategy, alias_singletons)  sub-block reads / writes of one recursion
+                                  node's addition chains, counted chain by chain for the pairwise,
+                                  write-once and streaming implementations
   * error_bound(alg, Q, L, a, b)  a worst-case forward error bound on max|fl(C) - C| derived from
                                   (U, V, W) ("theoretical bounds can be derived from each
                                   algorithm's <U,V,W> representation"); pins check (d) of SURVEY 8(c)
