@@ -265,6 +265,23 @@ def test_errors_are_reported():
     assert e.value.status == "FMM_E_SHAPE"
 
 
+def test_option_errors_are_reported():
+    # the workspace limit (the message states the R-fold requirement)
+    with pytest.raises(F.FmmError) as e:
+        F.Plan(falg("strassen_222_7"), 512, 512, 512, 2, workspace_limit_bytes=1 << 20)
+    assert e.value.status == "FMM_E_NO_MEMORY" and "workspace bytes" in str(e.value)
+    F.Plan(falg("strassen_222_7"), 512, 512, 512, 2, workspace_limit_bytes=1 << 30)  # fits
+    with pytest.raises(F.FmmError) as e:
+        F.Plan(falg("strassen_222_7"), 64, 64, 64, 1, shard_rank=3, shard_count=2)
+    assert e.value.status == "FMM_E_INVALID_ARG"
+    with pytest.raises(ValueError):
+        F.Plan(falg("strassen_222_7"), 64, 64, 64, 1, strategy="daxpy")
+    comm = F.Comm(F.nccl_unique_id(), 1, 0)
+    with pytest.raises(F.FmmError) as e:
+        F.Plan(falg("strassen_222_7"), 64, 64, 64, 1, comm=comm, root=1)
+    assert e.value.status == "FMM_E_INVALID_ARG"
+
+
 def test_execute_host_end_to_end():
     A, B = I.problem(300, 200, 310, seed=10)
     p = F.Plan(falg("hk_class_323_15"), 300, 200, 310, 2)
