@@ -1,6 +1,7 @@
 """Randomised GPU parity: random algorithm, shape (ragged at any level), levels, layout and plan
 options (strategy, CSE, collapsed levels, fused leaf level, shards) on integer inputs, where every
-schedule must reproduce A*B exactly; and on uniform inputs against the oracle's tolerance.
+schedule must reproduce A*B exactly (three executes per plan: plain, graph capture, graph replay);
+and on uniform inputs against the oracle's tolerance.
 Seeded (derandomized) so failures reproduce."""
 import glob
 import os
@@ -61,7 +62,11 @@ def test_random_plans_integer_exact(c):
         p = F.Plan(F.load_alg(c["name"]), c["P"], c["Q"], c["N"], c["L"], layout=c["layout"], strategy=c["strategy"],
                    cse=c["cse"], collapse=c["collapse"], fuse=c["fuse"], peel_align=c["peel_align"], shard_rank=g,
                    shard_count=c["G"], shard_mode=c["mode"])
-        C = p.execute(_dev(A, c["layout"]), _dev(B, c["layout"]))
+        Ad, Bd = _dev(A, c["layout"]), _dev(B, c["layout"])
+        C = p.new_output()
+        for _ in range(3):  # plain launches, then the CUDA-graph capture, then a replay
+            C.fill_(float("nan"))
+            p.execute(Ad, Bd, C)
         torch.cuda.synchronize()
         total += C.cpu().numpy()
     assert np.array_equal(total, A @ B), c
