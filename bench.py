@@ -187,7 +187,7 @@ def main():
     ap.add_argument("--collapse", type=int, default=1, help="last two levels' formation / assembly in one pass each")
     ap.add_argument("--shard-mode", default="leaf", choices=["leaf", "top"],
                     help="N > 1: leaf-level HYBRID sharding or the top-level products in contiguous ranges")
-    ap.add_argument("--combine", default="torch", choices=["torch", "lib"],
+    ap.add_argument("--combine", default="torch", choices=["torch", "lib", "p2p"],
                     help="N > 1: partial-C reduce by torch.distributed (NCCL) or inside fmm_execute (fmm_plan_create_dist)")
     ap.add_argument("--output", default="root", choices=["root", "slabs"],
                     help="N > 1: C summed onto rank 0, or slab-distributed (slab g of C summed onto rank g)")
@@ -235,21 +235,41 @@ def main():
     plan = F.Plan(alg, P, Q, N, L, layout=w["layout"], strategy=args.strategy, cse=bool(args.cse),
                   shard_rank=rank, shard_count=world, fuse=bool(args.fuse), collapse=bool(args.collapse),
                   comm=lib_comm, root="slabs" if args.output == "slabs" else 0, shard_mode=args.shard_mode)
-    C = plan.new_output()
+    # --combine p2p: the partial C lives in a peer-mapped buffer and one pull-reduce kernel per rank
+    # sums its slab over every rank's partial (fmm_p2p_*, CUDA IPC over NVLink, no NCCL data path)
+    p2p = out_slab = None
+    outer, inner = (P, N) if w["layout"] == "row" else (N, P)
+    if world > 1 and args.combine == "p2p":
+        p2p = F.P2P.from_torch_distributed(8 * P * N, device=device.index)
+        C = p2p.partial(P, N, w["layout"])
+        s0, s1 = F.dist_slab(P, N, w["layout"], world, rank)
+        out_slab = torch.empty(s1 - s0, inner, dtype=torch.float64, device=device)
+    else:
+        C = plan.new_output()
     st = plan.stats()
     dmma_peak, dfma_peak = F.probe_fp64_peak()
     stream = torch.cuda.current_stream()
+
+    def combine():
+        if lib_comm is not None:  # a distributed plan reduces inside fmm_execute
+            return
+        if p2p is not None:
+            stream.synchronize()
+            dist.barrier()  # every partial complete
+            p2p.reduce_slab(outer, inner, out_slab, stream=stream)
+            stream.synchronize()
+            dist.barrier()  # every slab read before the next step overwrites a partial
+        elif args.output == "slabs":
+            scatter_partials(C)
+        else:
+            combine_partials(C)
 
     def step(evs=None):
         if evs is None:
             plan.execute(A, B, C, stream=stream)
         else:
             plan.execute_events(A, B, C, evs[:4], stream=stream)
-        if lib_comm is None:  # (a distributed plan reduces inside fmm_execute)
-            if args.output == "slabs":
-                scatter_partials(C)
-            else:
-                combine_partials(C)
+        combine()
         if evs is not None:
             evs[4].record(stream)  # after the combine: the comm share of a step (N > 1)
 
@@ -288,17 +308,20 @@ def main():
     # north-star tolerance max |C - AB| <= 1e-10 ||A||_F ||B||_F
     check = None
     if rank == 0:
-        if args.output == "slabs" and world > 1:
+        if (args.output == "slabs" or p2p is not None) and world > 1:
             lo, hi = F.dist_slab(P, N, w["layout"], world, 0)
         else:
             lo, hi = 0, (P if w["layout"] == "row" else N)
         g = torch.Generator().manual_seed(7)
         idx = torch.randint(lo, max(lo + 1, hi), (min(64, max(hi - lo, 1)),), generator=g).to(device)
         if hi > lo:
+            # rank 0's result: C itself, or (p2p) its reduced slab of C's storage rows
+            got = (lambda rows: out_slab[rows - lo]) if p2p is not None else (
+                (lambda rows: C[rows]) if w["layout"] == "row" else (lambda cols: C[:, cols].t()))
             if w["layout"] == "row":
-                err = (C[idx] - A[idx] @ B).abs().max().item()
+                err = (got(idx) - A[idx] @ B).abs().max().item()
             else:  # slabs of C's columns
-                err = (C[:, idx] - A @ B[:, idx]).abs().max().item()
+                err = (got(idx) - (A @ B[:, idx]).t()).abs().max().item()
             tol = 1e-10 * torch.linalg.norm(A).item() * torch.linalg.norm(B).item()
             check = {"sampled": int(idx.numel()), "of": "rows" if w["layout"] == "row" else "columns",
                      "max_abs_err": err, "tolerance": tol, "ok": bool(err <= tol)}
@@ -454,6 +477,10 @@ def main():
         Ah, Bh, Ch = pinned(A_np, P, Q), pinned(B_np, Q, N), pinned(None, P, N)
         h2d = 8 * (P * Q + Q * N)
         d2h = 8 * P * N if rank == 0 else 0
+        slab_h = None
+        if p2p is not None and rank == 0:  # rank 0's result is its reduced slab
+            slab_h = torch.empty(tuple(out_slab.shape), dtype=torch.float64, pin_memory=True)
+            d2h = 8 * out_slab.numel()
         def e2e_step():
             if world == 1:
                 # pipelined public host API: H2D of this step, compute, D2H of its C
@@ -461,10 +488,12 @@ def main():
             else:
                 A.copy_(Ah, non_blocking=True); B.copy_(Bh, non_blocking=True)
                 plan.execute(A, B, C, stream=stream)
-                if lib_comm is None:
-                    combine_partials(C)
+                combine()
                 if rank == 0:
-                    Ch.copy_(C, non_blocking=True)
+                    if slab_h is not None:
+                        slab_h.copy_(out_slab, non_blocking=True)
+                    else:
+                        Ch.copy_(C, non_blocking=True)
                 torch.cuda.synchronize()
         e2e_step()
         plan.sync()
@@ -528,9 +557,11 @@ def main():
                        "strategy": args.strategy, "cse": bool(args.cse),
                        "l2": "inputs larger than L2 (A, B, C 0.54 GB each vs 126 MB); no flush"
                        if args.workload != "c1" else "small config: L2-resident",
-                       "parallelism": (f"{args.shard_mode}-level shards x{world} + {args.dist_backend.upper()} "
-                                       f"{'reduce to rank 0' if args.output == 'root' else 'slab reduce-scatter'} "
-                                       f"({'fmm_execute' if lib_comm else 'torch.distributed'})"
+                       "parallelism": ((f"{args.shard_mode}-level shards x{world} + peer-memory slab reduce "
+                                        "(fmm_p2p: one pull kernel per rank over CUDA IPC)") if p2p is not None else
+                                       (f"{args.shard_mode}-level shards x{world} + {args.dist_backend.upper()} "
+                                        f"{'reduce to rank 0' if args.output == 'root' else 'slab reduce-scatter'} "
+                                        f"({'fmm_execute' if lib_comm else 'torch.distributed'})")
                                        if world > 1 else "1 GPU"),
                        "fused_leaf_level": fused, "collapsed_levels": bool(st.get("collapsed", 0)),
                        **({"dist_backend": "gloo (control-flow check, ranks share a GPU: NOT a measurement)"}

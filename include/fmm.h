@@ -175,6 +175,25 @@ void fmm_comm_destroy(fmm_comm* comm);  /* after every plan using it is destroye
 #define FMM_DIST_SLABS (-1)
 fmm_status_t fmm_plan_create_dist(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels,
                                   const fmm_plan_options* opt, fmm_comm* comm, int root, fmm_plan_t** out);
+/* ---- the combine over peer memory (no NCCL in the data path) -------------
+   One process per GPU.  Each rank owns a partial-product buffer of `bytes` (cudaMalloc, returned in
+   *local): pass it as C to fmm_execute of its shard plan.  Ranks exchange the 64-byte CUDA IPC
+   handles of their buffers (fmm_p2p_handle; e.g. torch.distributed all_gather_object) and map
+   every peer's with fmm_p2p_open (over NVLink / NVSwitch between GPUs).  fmm_p2p_reduce_slab then
+   runs ONE kernel on `stream` that reads the slab of every rank's partial that this rank owns
+   (fmm_dist_slab's split of the `outer` dimension; rows of `inner` doubles, leading dimension
+   `ld` in the partials) and writes their sum, ranks in ascending order (deterministic), to `out`
+   (row r of the slab at out + r * ldo).  Ordering is the caller's: every partial complete before
+   any rank reduces, every reduce complete before the next fmm_execute overwrites a partial (e.g.
+   stream synchronise + barrier).  At most 16 ranks. */
+typedef struct fmm_p2p_s fmm_p2p;
+fmm_status_t fmm_p2p_create(int nranks, int rank, int device, size_t bytes, fmm_p2p** out, double** local);
+fmm_status_t fmm_p2p_handle(const fmm_p2p* p, unsigned char handle[64]);
+fmm_status_t fmm_p2p_open(fmm_p2p* p, const unsigned char* handles /* nranks x 64 bytes */);
+fmm_status_t fmm_p2p_reduce_slab(fmm_p2p* p, int64_t outer, int64_t inner, int64_t ld, double* out, int64_t ldo,
+                                 void* stream);
+void fmm_p2p_destroy(fmm_p2p* p);
+
 /* The slab of C that rank `rank` of `nranks` holds after a FMM_DIST_SLABS execute: rows
    [*first, *last) of C (row-major) or columns [*first, *last) (column-major).  Host only. */
 fmm_status_t fmm_dist_slab(int64_t P, int64_t Nc, int layout, int nranks, int rank, int64_t* first, int64_t* last);

@@ -2,7 +2,7 @@
 (include/fmm.h) with sm_100a kernels, and its thin Python binding."""
 import os
 
-from .fmm import (Algorithm, Comm, DIST_SLABS, FmmError, dist_slab, Plan, dgemm, nccl_unique_id, select, hybrid_split, plan, probe_fp64_peak, shard_leaf_rows, version, LIB_PATH,  # noqa: F401
+from .fmm import (Algorithm, Comm, DIST_SLABS, FmmError, P2P, dist_slab, Plan, dgemm, nccl_unique_id, select, hybrid_split, plan, probe_fp64_peak, shard_leaf_rows, version, LIB_PATH,  # noqa: F401
                   ROW_MAJOR, COL_MAJOR, STREAMING, WRITE_ONCE)
 
 ALGS_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "algs")

@@ -72,6 +72,10 @@ def _load():
         "fmm_hybrid_split": [i64, i32, i64, p64, p64],
         "fmm_shard_leaf_rows": [i64, i64, i64, i64, p64, p64],
         "fmm_dist_slab": [i64, i64, i32, i32, i32, p64, p64],
+        "fmm_p2p_create": [i32, i32, i32, ctypes.c_size_t, ctypes.POINTER(vp), ctypes.POINTER(vp)],
+        "fmm_p2p_handle": [vp, ctypes.c_char_p],
+        "fmm_p2p_open": [vp, ctypes.c_char_p],
+        "fmm_p2p_reduce_slab": [vp, i64, i64, i64, vp, i64, vp],
         "fmm_dgemm": [i64, i64, i64, dp, vp, i64, vp, i64, dp, vp, i64, vp],
     }
     for name, args in sig.items():
@@ -80,6 +84,8 @@ def _load():
         f.restype = ctypes.c_int
     lib.fmm_alg_destroy.argtypes = [vp]
     lib.fmm_alg_destroy.restype = None
+    lib.fmm_p2p_destroy.argtypes = [vp]
+    lib.fmm_p2p_destroy.restype = None
     lib.fmm_plan_destroy.argtypes = [vp]
     lib.fmm_plan_destroy.restype = None
     lib.fmm_plan_options_default.argtypes = [ctypes.POINTER(_Options)]
@@ -390,6 +396,82 @@ def shard_leaf_rows(leaves: int, rows: int, G: int, g: int):
     r1 = (ctypes.c_int64 * leaves)()
     _check(_lib.fmm_shard_leaf_rows(leaves, rows, G, g, r0, r1))
     return list(zip(r0, r1))
+
+
+class _CudaBuffer:
+    """A raw device allocation seen by torch through __cuda_array_interface__ (no copy)."""
+
+    def __init__(self, ptr: int, shape, owner):
+        self.owner = owner  # keeps the allocation alive while a tensor views it
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f8", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class P2P:
+    """The multi-GPU combine over peer memory (fmm_p2p_*): each rank's partial C
+    lives in a library buffer mapped into every peer by CUDA IPC, and reduce_slab sums this rank's
+    slab of all partials in ONE kernel (pull-based reduce-scatter, no NCCL in the data path).  The
+    caller orders the ranks: all partials written (synchronise + barrier) before any reduce_slab,
+    all reduces finished before a partial is overwritten."""
+
+    def __init__(self, nranks: int, rank: int, nbytes: int, device: Optional[int] = None):
+        import torch
+        self.nranks, self.rank = nranks, rank
+        self.device = torch.cuda.current_device() if device is None else device
+        h, local = ctypes.c_void_p(), ctypes.c_void_p()
+        _check(_lib.fmm_p2p_create(nranks, rank, self.device, nbytes, ctypes.byref(h), ctypes.byref(local)))
+        self._h, self.local_ptr, self.nbytes = h, local.value, nbytes
+
+    def handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        _check(_lib.fmm_p2p_handle(self._h, buf))
+        return buf.raw
+
+    def open(self, handles) -> None:
+        """Map every rank's partial (handles: one 64-byte handle per rank, rank order)."""
+        if len(handles) != self.nranks or any(len(x) != 64 for x in handles):
+            raise ValueError("need one 64-byte handle per rank")
+        blob = b"".join(handles)
+        _check(_lib.fmm_p2p_open(self._h, ctypes.create_string_buffer(blob, len(blob))))
+
+    @classmethod
+    def from_torch_distributed(cls, nbytes: int, group=None, device: Optional[int] = None) -> "P2P":
+        import torch.distributed as dist
+        p = cls(dist.get_world_size(group), dist.get_rank(group), nbytes, device)
+        hs = [None] * p.nranks
+        dist.all_gather_object(hs, p.handle(), group=group)
+        p.open(hs)
+        return p
+
+    def partial(self, P: int, N: int, layout: str = "row"):
+        """The P x N partial-product view (row- or column-major) over this rank's buffer: the C
+        to pass to the shard plan's execute."""
+        import torch
+        if 8 * P * N > self.nbytes:
+            raise ValueError("the buffer is smaller than P x N doubles")
+        if layout == "row":
+            return torch.as_tensor(_CudaBuffer(self.local_ptr, (P, N), self), device=f"cuda:{self.device}")
+        return torch.as_tensor(_CudaBuffer(self.local_ptr, (N, P), self), device=f"cuda:{self.device}").t()
+
+    def reduce_slab(self, outer: int, inner: int, out, ld: Optional[int] = None, stream=None):
+        """out (this rank's fmm_dist_slab rows of the outer x inner partial storage, a float64 CUDA
+        tensor with unit column stride) <- the sum over ranks.  Asynchronous on the stream."""
+        if out.dtype != torch_float64() or not out.is_cuda or (out.dim() == 2 and out.shape[0] > 1 and out.stride(1) != 1):
+            raise TypeError("out must be a float64 CUDA tensor with unit column stride")
+        ldo = out.stride(0) if out.dim() == 2 else inner
+        _check(_lib.fmm_p2p_reduce_slab(self._h, outer, inner, inner if ld is None else ld,
+                                        ctypes.c_void_p(out.data_ptr()), ldo, _stream_ptr(stream)))
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.fmm_p2p_destroy(self._h)
+            self._h = None
+
+
+def torch_float64():
+    import torch
+    return torch.float64
 
 
 def dist_slab(P: int, N: int, layout: str, nranks: int, rank: int):

@@ -1,0 +1,88 @@
+"""The combine over peer memory (fmm_p2p_*): world-size 2 and 3 processes, each
+with its HYBRID leaf shard written into its IPC-exported partial buffer, then ONE
+reduce kernel per rank pulling its slab from every rank's partial.  The ranks share the one GPU of
+this box (CUDA IPC works between processes on one device), gloo carries only the handle exchange
+and the two barriers; no kernel waits on another rank's kernel.  Integer inputs: the slabs must
+equal the exact product bit for bit, in both layouts."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, layout, alg_name, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ok = False
+    try:
+        import fmm_inputs as I
+        import paper_1409_2908_b200 as F
+        torch.cuda.set_device(0)
+        P, Q, N = 300, 200, 250
+        A, B = I.problem(P, Q, N, seed=31, kind="integers")
+
+        def dev(x):
+            if layout == "row":
+                return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+            return torch.from_numpy(np.ascontiguousarray(x.T)).cuda().t()
+        p2p = F.P2P.from_torch_distributed(8 * P * N)
+        plan = F.Plan(F.load_alg(alg_name), P, Q, N, 2, layout=layout, shard_rank=rank, shard_count=world)
+        C = p2p.partial(P, N, layout)
+        for it in range(2):  # twice: the buffers are reused across executes
+            plan.execute(dev(A), dev(B), C)
+            torch.cuda.synchronize()
+            dist.barrier()  # every partial complete
+            outer, inner = (P, N) if layout == "row" else (N, P)
+            r0, r1 = F.dist_slab(P, N, layout, world, rank)
+            out = torch.empty(r1 - r0, inner, dtype=torch.float64, device="cuda")
+            p2p.reduce_slab(outer, inner, out)
+            torch.cuda.synchronize()
+            dist.barrier()  # every reduce done before a partial is overwritten
+            want = (A @ B)[r0:r1] if layout == "row" else (A @ B)[:, r0:r1].T
+            ok = bool(np.array_equal(out.cpu().numpy(), want))
+            if not ok:
+                break
+        oks = [None] * world
+        dist.all_gather_object(oks, ok)
+        if rank == 0:
+            q.put(all(oks))
+        del C, plan
+        dist.barrier()
+        del p2p
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,layout,alg", [(2, "row", "winograd_class_222_7"), (3, "col", "alg_424_26"),
+                                              (2, "col", "hk_class_323_15")])
+def test_p2p_slab_combine(world, layout, alg):
+    import __graft_entry__
+    __graft_entry__.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, layout, alg, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=300)
+    assert all(pr.exitcode == 0 for pr in procs), [pr.exitcode for pr in procs]
+    assert q.get(timeout=5), "reduced slabs differ from A*B"
