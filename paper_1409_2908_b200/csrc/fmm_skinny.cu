@@ -5,10 +5,11 @@
 // run here instead, on the FP64 CUDA cores, HBM/L2-bound:
 //   row strips (m <= 8): a block covers 32 output columns x 8 k-slices; each thread keeps all
 //       m rows of its column in registers over its k-slice (B read once, coalesced; A[i][k] a
-//       warp-uniform broadcast), and the slices are reduced through shared memory.
-//   column strips (n <= 8): two output rows per warp; lanes split k (A rows read coalesced,
-//       4 loads in flight), the B strip is staged transposed in shared memory per k-chunk, each
-//       lane accumulates all n outputs, then a warp shuffle reduction.
+//       warp-uniform broadcast), and the slices are reduced through shared memory.  (A 64-column
+//       variant with 16-byte loads was measured slower on c3: 0.19 vs 0.16 ms.)
+//   column strips (n <= 8): four output rows per warp; lanes split k (A rows read coalesced,
+//       16-byte loads, up to 16 in flight), the B strip is staged transposed in shared memory per
+//       k-chunk, each lane accumulates all n outputs, then a warp shuffle reduction.
 // C = alpha * A B + beta * C, same task table as the GEMM kernels.
 #include <cuda_runtime.h>
 
@@ -68,9 +69,10 @@ __global__ void __launch_bounds__(256) skinny_rows(const GemmTask* __restrict__ 
   }
 }
 
-// Column strips: 16 rows per block (2 per warp); the B strip (k x n, n <= 8) is staged
-// transposed through shared memory in k-chunks, so lane reads of B are conflict-free and A rows
-// are read coalesced with 4 loads in flight per lane.
+// Column strips: 16 rows per block (2 per warp); the B strip (k x n, n <= 8) is staged transposed
+// through shared memory in k-chunks; lanes split k and read A rows coalesced, 16 bytes at a time
+// when A is 16-byte aligned with an even lda, with up to 16 loads in flight per lane; each lane
+// accumulates all n outputs of its rows, then a warp shuffle reduction.
 constexpr int KC = 256, ROWS_PER_WARP = 2;
 __global__ void __launch_bounds__(256) skinny_cols(const GemmTask* __restrict__ tasks, const int* __restrict__ ids,
                                                    int count) {
@@ -78,6 +80,7 @@ __global__ void __launch_bounds__(256) skinny_cols(const GemmTask* __restrict__ 
   const GemmTask t = tasks[ids[blockIdx.y]];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int row0 = (blockIdx.x * 8 + warp) * ROWS_PER_WARP;
+  const bool v2 = ((reinterpret_cast<uintptr_t>(t.A) & 15) == 0) && ((t.lda & 1) == 0);
   double acc[ROWS_PER_WARP][THIN];
 #pragma unroll
   for (int q = 0; q < ROWS_PER_WARP; ++q)
@@ -91,21 +94,50 @@ __global__ void __launch_bounds__(256) skinny_cols(const GemmTask* __restrict__ 
       bt[j][kk] = __ldg(t.B + (long long)(k0 + kk) * t.ldb + j);
     }
     __syncthreads();
+    if (v2) {
+      // lane covers k pairs kk = 2 lane + 64 s, s = 0..3 (the 256-wide chunk)
+      double2 a[ROWS_PER_WARP][4];
 #pragma unroll
-    for (int q = 0; q < ROWS_PER_WARP; ++q) {
-      const int i = row0 + q;
-      if (i >= t.m) continue;
-      const double* arow = t.A + (long long)i * t.lda + k0;
-      for (int kk = lane; kk < kc; kk += 128) {
-        double a[4];
+      for (int q = 0; q < ROWS_PER_WARP; ++q) {
+        const int i = row0 + q;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) a[u] = kk + 32 * u < kc ? __ldg(arow + kk + 32 * u) : 0.0;
+        for (int s4 = 0; s4 < 4; ++s4) {
+          const int kk = 2 * lane + 64 * s4;
+          const double* ap = t.A + (long long)i * t.lda + k0 + kk;
+          a[q][s4] = (i < t.m && kk + 1 < kc) ? __ldg(reinterpret_cast<const double2*>(ap))
+                     : (i < t.m && kk < kc) ? make_double2(__ldg(ap), 0.0) : make_double2(0.0, 0.0);
+        }
+      }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (kk + 32 * u < kc)
+      for (int s4 = 0; s4 < 4; ++s4) {
+        const int kk = 2 * lane + 64 * s4;
+        if (kk >= kc) continue;
+        const bool second = kk + 1 < kc;
 #pragma unroll
-            for (int j = 0; j < THIN; ++j)
-              if (j < t.n) acc[q][j] = fma(a[u], bt[j][kk + 32 * u], acc[q][j]);
+        for (int j = 0; j < THIN; ++j)
+          if (j < t.n) {
+            const double b0 = bt[j][kk], b1 = second ? bt[j][kk + 1] : 0.0;
+#pragma unroll
+            for (int q = 0; q < ROWS_PER_WARP; ++q) acc[q][j] = fma(a[q][s4].y, b1, fma(a[q][s4].x, b0, acc[q][j]));
+          }
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < ROWS_PER_WARP; ++q) {
+        const int i = row0 + q;
+        if (i >= t.m) continue;
+        const double* arow = t.A + (long long)i * t.lda + k0;
+        for (int kk = lane; kk < kc; kk += 128) {
+          double a[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) a[u] = kk + 32 * u < kc ? __ldg(arow + kk + 32 * u) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (kk + 32 * u < kc)
+#pragma unroll
+              for (int j = 0; j < THIN; ++j)
+                if (j < t.n) acc[q][j] = fma(a[u], bt[j][kk + 32 * u], acc[q][j]);
+        }
       }
     }
   }
