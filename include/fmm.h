@@ -101,10 +101,15 @@ typedef struct {
                                as one CUDA graph (captured once per cached pointer set), which
                                removes the per-launch host overhead.  Not used for distributed,
                                fused or timed executes.  0: plain launches every time. */
+  int peel_tiles;           /* 1: when the leaves' row count r is not a multiple of the GEMM's 128-row
+                               tile, peel r mod 128 rows of every leaf into the last split's
+                               classical strips instead, if the cost model predicts that faster
+                               (R7c; measured slower on c3, so off by default).  Exact
+                               either way.  0 (default): the paper's minimal peeling of rows. */
 } fmm_plan_options;
 
 /* Fill *opt with the defaults: row-major, streaming, cse = 1, shard 0 of 1, no limit,
-   peel_align = 1, fuse_leaf_level = 0, collapse_levels = 1, cuda_graphs = 1. */
+   peel_align = 1, fuse_leaf_level = 0, collapse_levels = 1, cuda_graphs = 1, peel_tiles = 0. */
 void fmm_plan_options_default(fmm_plan_options* opt);
 
 /* ---- algorithms ------------------------------------------------------------------------- */
@@ -221,7 +226,7 @@ fmm_status_t fmm_plan_stats(const fmm_plan_t* plan, double out[8]);
    [12] addition bytes of the separate assembly kernels
    [13] flops of the peel-strip products
    [14] 1 if the last two levels are collapsed (collapse_levels), else 0
-   [15] 0 (reserved) */
+   [15] 1 if the last split's rows were peeled to 128-row-aligned leaves (peel_tiles, R7c) */
 fmm_status_t fmm_plan_stats_ex(const fmm_plan_t* plan, double out[16]);
 
 /* Cost model (host only, no allocation): predicted milliseconds of a plan of `alg` for the problem

@@ -43,6 +43,7 @@ struct Dims {
   long long P, Q, N;     // node problem at this level: (P x Q) * (Q x N)
   long long P1, Q1, N1;  // divisible core (only meaningful below the last level)
 };
+using PlanDims = Dims;
 
 struct Launch {
   enum Kind { FORM_A, FORM_B, GEMM, ASSEMBLE, STRIPS, SKINNY, FUSED } kind;
@@ -113,6 +114,7 @@ struct fmm_plan_s {
   bool use_tma = true;  // FMM_NO_TMA=1 forces the cp.async GEMM (diagnostics)
   bool fuse = true;     // fuse_leaf_level option (FMM_NO_FUSE=1 overrides)
   bool collapse = false;  // the last two levels' formation / assembly in one pass each (sec. 6c)
+  bool tiled_peel = false;  // R7c: the last split's rows were peeled to 128-row-aligned leaves
   unsigned long long* d_ctr = nullptr;  // fused launch counters: claim0, claim1, ready[np], tiles[np]
   size_t ctr_bytes = 0;
   // kernels (vec 2 / vec 1 variants created lazily)
@@ -983,6 +985,8 @@ void fmm_plan_s::emit_two_level_assembly(bool lazy_kernels) {
 namespace {
 
 double predict_seconds(const fmm_alg& a, long long P, long long Q, long long N, int levels, int* used_levels);
+std::vector<PlanDims> plan_dims(const fmm_alg& a, long long P, long long Q, long long N, int levels, bool peel_align,
+                                bool peel_tiles, bool* tiled);
 
 // R7b's peel: widen the peeled strip so the child block widths Q1 / K and N1 / Nb are even
 template <class D>
@@ -1045,21 +1049,11 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
   p->R = a->R;
   const int M = a->M, K = a->K, Nb = a->N, R = a->R;
   // effective levels (R10/R18): stop at a level whose problem is smaller than the base case
-  p->dims.clear();
-  Dims d{p->P, p->Q, p->N, 0, 0, 0};
-  int L = 0;
-  while (true) {
-    d.P1 = M * (d.P / M);
-    d.Q1 = K * (d.Q / K);
-    d.N1 = Nb * (d.N / Nb);
-    // R7b: keep column-block widths even so sub-block views stay 16-byte aligned (TMA): the
-    // column offsets of A's blocks are multiples of Q / K, of B's and C's multiples of N / Nb
-    if (p->opt.peel_align && L < levels) peel_even(d, K, Nb);
-    p->dims.push_back(d);
-    if (L == levels || d.P < M || d.Q < K || d.N < Nb) break;
-    d = Dims{d.P1 / M, d.Q1 / K, d.N1 / Nb, 0, 0, 0};
-    ++L;
-  }
+  // R7b: keep column-block widths even so sub-block views stay 16-byte aligned (TMA): the column
+  // offsets of A's blocks are multiples of Q / K, of B's and C's multiples of N / Nb.  R7c: the
+  // tile-aware row peel of the last split, where the cost model predicts it faster.
+  p->dims = plan_dims(*a, p->P, p->Q, p->N, levels, p->opt.peel_align != 0, p->opt.peel_tiles != 0, &p->tiled_peel);
+  const int L = (int)p->dims.size() - 1;
   p->L = L;
   p->nodes_at.assign(L + 1, 1);
   for (int l = 1; l <= L; ++l) {
@@ -1307,6 +1301,7 @@ void fmm_plan_options_default(fmm_plan_options* o) {
   o->fuse_leaf_level = 0;  // within +-2 % of the separate kernels on B200
   o->collapse_levels = 1;
   o->cuda_graphs = 1;
+  o->peel_tiles = 0;  // measured: c3 12.60 -> 12.78 ms, c5 258.0 -> 257.3 (R7c)
 }
 
 fmm_status_t fmm_plan_create(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels,
@@ -1434,25 +1429,13 @@ int formed_columns(const std::vector<double>& X, int rows, int R) {
 }
 
 // seconds; levels beyond the base case are not taken (R10), as in plan_init
-double predict_seconds(const fmm_alg& a, long long P, long long Q, long long N, int levels, int* used_levels) {
+// seconds of a plan with the given per-level dims (dims[0..L]) on one B200
+double predict_dims(const fmm_alg& a, const std::vector<PlanDims>& dims) {
   const CostModel cm;
   const int M = a.M, K = a.K, Nb = a.N, R = a.R;
+  const int L = (int)dims.size() - 1;
   const int fu = formed_columns(a.Ud, M * K, R), fv = formed_columns(a.Vd, K * Nb, R);
-  struct D { long long P, Q, N, P1, Q1, N1; };
-  std::vector<D> dims;
-  D d{P, Q, N, 0, 0, 0};
-  int L = 0;
-  while (true) {
-    d.P1 = M * (d.P / M);
-    d.Q1 = K * (d.Q / K);
-    d.N1 = Nb * (d.N / Nb);
-    if (L < levels) peel_even(d, K, Nb);  // as plan_init with the default peel_align
-    dims.push_back(d);
-    if (L == levels || d.P < M || d.Q < K || d.N < Nb) break;
-    d = D{d.P1 / M, d.Q1 / K, d.N1 / Nb, 0, 0, 0};
-    ++L;
-  }
-  if (used_levels) *used_levels = L;
+  using D = PlanDims;
   // collapsed last two levels (collapse_levels, as plan_init decides it)
   const bool collapse = L >= 2 && M * K <= 4 && K * Nb <= 4 && M * Nb <= 4 && dims[L - 1].P1 == dims[L - 1].P &&
                         dims[L - 1].Q1 == dims[L - 1].Q && dims[L - 1].N1 == dims[L - 1].N;
@@ -1494,6 +1477,49 @@ double predict_seconds(const fmm_alg& a, long long P, long long Q, long long N, 
   }
   t += gemm_time(nodes, dims[L].P, dims[L].N, dims[L].Q, cm);
   return t;
+}
+
+// the per-level dims of plan_init (R10 effective levels, R7 peeling, R7b alignment peel with the
+// default peel_align), then R7c: the tile-aware row peel of the last split when the cost model
+// predicts it faster (peel_tiles)
+std::vector<PlanDims> plan_dims(const fmm_alg& a, long long P, long long Q, long long N, int levels, bool peel_align,
+                                bool peel_tiles, bool* tiled) {
+  const int M = a.M, K = a.K, Nb = a.N;
+  std::vector<PlanDims> dims;
+  PlanDims d{P, Q, N, 0, 0, 0};
+  int L = 0;
+  while (true) {
+    d.P1 = M * (d.P / M);
+    d.Q1 = K * (d.Q / K);
+    d.N1 = Nb * (d.N / Nb);
+    if (peel_align && L < levels) peel_even(d, K, Nb);
+    dims.push_back(d);
+    if (L == levels || d.P < M || d.Q < K || d.N < Nb) break;
+    d = PlanDims{d.P1 / M, d.Q1 / K, d.N1 / Nb, 0, 0, 0};
+    ++L;
+  }
+  if (tiled) *tiled = false;
+  // R7c: the leaves' rows run in 128-row GEMM tiles, so r rows cost ceil(r / 128) tiles.  Peeling
+  // the remainder r mod 128 of every leaf into the level-(L-1) classical strips leaves 128-aligned
+  // leaves; taken only when the cost model says so (the strips are classical work)
+  if (peel_tiles && L >= 1 && dims[L].P >= 128 && dims[L].P % 128 != 0) {
+    std::vector<PlanDims> alt = dims;
+    const long long rt = 128 * (dims[L].P / 128);
+    alt[L - 1].P1 = M * rt;
+    alt[L].P = rt;
+    alt[L].P1 = M * (rt / M);
+    if (predict_dims(a, alt) < 0.995 * predict_dims(a, dims)) {
+      dims.swap(alt);
+      if (tiled) *tiled = true;
+    }
+  }
+  return dims;
+}
+
+double predict_seconds(const fmm_alg& a, long long P, long long Q, long long N, int levels, int* used_levels) {
+  const std::vector<PlanDims> dims = plan_dims(a, P, Q, N, levels, true, false, nullptr);  // the default options
+  if (used_levels) *used_levels = (int)dims.size() - 1;
+  return predict_dims(a, dims);
 }
 }  // namespace
 
@@ -1604,6 +1630,7 @@ fmm_status_t fmm_plan_stats_ex(const fmm_plan_t* p, double out[16]) {
     if (!leaf && (ln.kind == Launch::STRIPS || ln.kind == Launch::SKINNY)) s[13] += ln.flops;
   }
   s[14] = p->collapse ? 1.0 : 0.0;
+  s[15] = p->tiled_peel ? 1.0 : 0.0;
   std::memcpy(out, s, sizeof(s));
   return FMM_OK;
   FMM_API_END

@@ -33,7 +33,7 @@ class _Options(ctypes.Structure):
                 ("shard_rank", ctypes.c_int), ("shard_count", ctypes.c_int),
                 ("workspace_limit_bytes", ctypes.c_size_t), ("peel_align", ctypes.c_int),
                 ("fuse_leaf_level", ctypes.c_int), ("shard_mode", ctypes.c_int), ("collapse_levels", ctypes.c_int),
-                ("cuda_graphs", ctypes.c_int)]
+                ("cuda_graphs", ctypes.c_int), ("peel_tiles", ctypes.c_int)]
 
 
 def _load():
@@ -243,7 +243,7 @@ class Plan:
                  strategy: str = "streaming", cse: bool = True, shard_rank: int = 0, shard_count: int = 1,
                  device: Optional[int] = None, workspace_limit_bytes: int = 0, peel_align: bool = True,
                  fuse: bool = False, collapse: bool = True, comm: Optional[Comm] = None, root: int = 0,
-                 shard_mode: str = "leaf", cuda_graphs: bool = True):
+                 shard_mode: str = "leaf", cuda_graphs: bool = True, peel_tiles: bool = False):
         import torch
         self.alg, self.P, self.Q, self.N, self.levels = alg, P, Q, N, levels
         self.layout = ROW_MAJOR if layout == "row" else COL_MAJOR
@@ -254,6 +254,7 @@ class Plan:
             raise ValueError(f"strategy must be one of {sorted(_STRATEGIES)}")
         o.strategy = _STRATEGIES[strategy]
         o.cuda_graphs = int(bool(cuda_graphs))
+        o.peel_tiles = int(bool(peel_tiles))
         o.cse = int(bool(cse))
         o.shard_rank, o.shard_count = shard_rank, shard_count
         o.workspace_limit_bytes = workspace_limit_bytes
@@ -289,7 +290,7 @@ class Plan:
         _check(_lib.fmm_plan_stats_ex(self._h, s))
         keys = ["gemm_flops", "add_flops", "add_bytes", "gemm_bytes", "launches", "levels", "leaves", "paper_flops",
                 "leaf_flops", "fused_add_bytes", "fused_launches", "formation_bytes", "assembly_bytes", "strip_flops",
-                "collapsed"]
+                "collapsed", "tiled_peel"]
         return dict(zip(keys, list(s)))
 
     def new_output(self):

@@ -265,6 +265,18 @@ def test_errors_are_reported():
     assert e.value.status == "FMM_E_SHAPE"
 
 
+@pytest.mark.parametrize("layout", ["row", "col"])
+def test_tile_aware_row_peel(layout):
+    # R7c: leaves of 130 rows would take two 128-row tiles; with peel_tiles the plan peels 2 rows of
+    # every leaf into the classical strips (the cost model prefers it here) -- still exact
+    P, Q, N = 9 * 130, 4 * 64, 9 * 130
+    A, B = I.problem(P, Q, N, seed=15, kind="integers")
+    C, p = run("hk_class_323_15", A, B, 2, layout=layout, peel_tiles=True)
+    assert p.stats()["tiled_peel"] == 1 and np.array_equal(C, A @ B)
+    C, p = run("hk_class_323_15", A, B, 2, layout=layout)
+    assert p.stats()["tiled_peel"] == 0 and np.array_equal(C, A @ B)
+
+
 def test_option_errors_are_reported():
     # the workspace limit (the message states the R-fold requirement)
     with pytest.raises(F.FmmError) as e:
