@@ -1141,6 +1141,20 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
   if ((!A && p->userP * p->userQ > 0) || (!B && p->userQ * p->userN > 0) || (!C && p->userP * p->userN > 0))
     throw Error(FMM_E_INVALID_ARG, "null matrix pointer");
   check_ld(p, lda, ldb, ldc);
+  {  // C must not overlap A or B (fmm.h): compare the byte spans of the three storages
+    const bool cm = p->colmajor;
+    auto span = [](const double* x, long long rows, long long cols, long long ld) {
+      const uintptr_t lo = reinterpret_cast<uintptr_t>(x);
+      return std::make_pair(lo, rows > 0 && cols > 0 ? lo + (uintptr_t)(((rows - 1) * ld + cols) * 8) : lo);
+    };
+    const auto sa = span(A, cm ? p->userQ : p->userP, cm ? p->userP : p->userQ, lda);
+    const auto sb = span(B, cm ? p->userN : p->userQ, cm ? p->userQ : p->userN, ldb);
+    const auto sc = span(C, cm ? p->userN : p->userP, cm ? p->userP : p->userN, ldc);
+    auto overlap = [](std::pair<uintptr_t, uintptr_t> x, std::pair<uintptr_t, uintptr_t> y) {
+      return x.first < x.second && y.first < y.second && x.first < y.second && y.first < x.second;
+    };
+    if (overlap(sc, sa) || overlap(sc, sb)) throw Error(FMM_E_INVALID_ARG, "C must not overlap A or B");
+  }
   FMM_CUDA(cudaSetDevice(p->device));
   // row-major orientation: for column-major, C^T = B^T A^T (Prop. 1)
   const double* a = p->colmajor ? B : A;

@@ -292,6 +292,16 @@ def test_option_errors_are_reported():
     with pytest.raises(F.FmmError) as e:
         F.Plan(falg("strassen_222_7"), 64, 64, 64, 1, comm=comm, root=1)
     assert e.value.status == "FMM_E_INVALID_ARG"
+    # C overlapping A or B is refused before any device work
+    p = F.Plan(falg("strassen_222_7"), 64, 64, 64, 1)
+    X = torch.zeros(64, 64, dtype=torch.float64, device="cuda")
+    Y = torch.zeros(64, 64, dtype=torch.float64, device="cuda")
+    for args in [(X, Y, X), (X, Y, Y)]:
+        with pytest.raises(F.FmmError) as e:
+            p.execute(*args)
+        assert e.value.status == "FMM_E_INVALID_ARG"
+    big = torch.zeros(128, 64, dtype=torch.float64, device="cuda")
+    p.execute(big[:64], Y, big[64:])  # adjacent, not overlapping: fine
 
 
 def test_execute_host_end_to_end():
