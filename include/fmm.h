@@ -62,10 +62,13 @@ typedef enum { FMM_ADD_STREAMING = 0, FMM_ADD_WRITE_ONCE = 1, FMM_ADD_PAIRWISE =
 typedef struct {
   int layout;               /* fmm_layout of A, B and C (all three share it) */
   int strategy;             /* fmm_add_strategy */
-  int cse;                  /* 1: greedy length-two common-subexpression elimination in the
-                               streaming kernels (Sec. 3.3); temporaries live in
-                               registers.  0: every chain is summed in ascending index order
-                               (bit-identical to the oracle's order). */
+  int cse;                  /* 1: greedy length-two common-subexpression elimination (Sec. 3.3,
+                               P:662-720).  Streaming keeps the temporaries in registers;
+                               write-once and pairwise write each one to memory once per node
+                               (its own launch) and read it in the chains, with the
+                               temporaries in a workspace arena counted by
+                               fmm_plan_workspace_bytes.  0: every chain is summed in ascending
+                               index order (bit-identical to the oracle's order). */
   int shard_rank;           /* multi-GPU leaf sharding (Sec. 4.3 HYBRID arithmetic, P:823-829,
                                with GPUs in place of threads): this plan computes the partial
                                product of its share of the R^L leaves; summing the C of all

@@ -741,6 +741,22 @@ std::shared_ptr<LincombKernel> twolevel_get(const TwoLevelSpec& spec) {
   return k;
 }
 
+// The greedy length-two CSE of a spec as data, for strategies that keep the common
+// subexpressions in memory (write-once / pairwise with CSE): temps[t] = (a, b, ratio)
+// means Y_t = x_a + ratio * x_b, variables nin + t being Y_t; outs[o] is output o's chain over
+// inputs and temporaries, ascending variable index.
+void lincomb_cse_program(const LincombSpec& spec, std::vector<std::tuple<int, int, double>>* temps,
+                         std::vector<std::vector<std::pair<int, double>>>* outs) {
+  LincombSpec s = spec;
+  s.strategy = FMM_ADD_STREAMING;  // build_program applies CSE only in the streaming form
+  s.cse = 1;
+  const Program p = build_program(s);
+  *temps = p.temps;
+  outs->assign(p.outs.size(), {});
+  for (size_t o = 0; o < p.outs.size(); ++o)
+    for (const auto& kv : p.outs[o]) (*outs)[o].push_back({kv.first, kv.second});
+}
+
 LincombCost lincomb_cost(const LincombKernel& k) { return k.cost; }
 int lincomb_steps(const LincombKernel& k) {
   if (k.spec.strategy != FMM_ADD_PAIRWISE) return 1;

@@ -6,6 +6,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/fmm.h"
@@ -154,6 +155,8 @@ std::shared_ptr<LincombKernel> twolevel_get(const TwoLevelSpec& spec);
 LincombCost lincomb_cost(const LincombKernel& k);
 int lincomb_steps(const LincombKernel& k);               // launches per lincomb_launch (pairwise: max chain length)
 int lincomb_out_terms(const LincombKernel& k, int q);   // terms in output q's chain
+void lincomb_cse_program(const LincombSpec& spec, std::vector<std::tuple<int, int, double>>* temps,
+                         std::vector<std::vector<std::pair<int, double>>>* outs);
 int lincomb_cse_temps(const LincombKernel& k);
 std::string lincomb_source(const LincombKernel& k);
 

@@ -157,6 +157,7 @@ struct fmm_plan_s {
     if (upload_done) cudaEventSynchronize(upload_done);
     cudaDeviceSynchronize();
     if (ws) cudaFree(ws);
+    if (scratch) cudaFree(scratch);
     if (d_ctr) cudaFree(d_ctr);
     for (auto& sl : slot) {
       if (sl.d_tab) cudaFree(sl.d_tab);
@@ -182,6 +183,10 @@ struct fmm_plan_s {
   std::shared_ptr<LincombKernel> kernel(int side, int vec) {
     auto* slot = side == 0 ? kU : side == 1 ? kV : kW;
     if (slot[vec]) return slot[vec];
+    slot[vec] = lincomb_get(spec_for(side, vec));
+    return slot[vec];
+  }
+  LincombSpec spec_for(int side, int vec) const {
     LincombSpec s;
     s.strategy = opt.strategy;
     s.cse = opt.cse;
@@ -203,8 +208,7 @@ struct fmm_plan_s {
       for (int k = 0; k < M * Nb; ++k)
         for (int r = 0; r < R; ++r) s.coef[(size_t)k * R + r] = alg->Wd[(size_t)k * R + r];
     }
-    slot[vec] = lincomb_get(s);
-    return slot[vec];
+    return s;
   }
 
   long long node_first_leaf(int l, long long z) const {
@@ -329,6 +333,18 @@ struct fmm_plan_s {
     }
   }
 
+  // memory-CSE temporaries (write-once / pairwise with CSE): an arena laid out by
+  // every build in the same order, allocated after the dry build
+  double* scratch = nullptr;
+  size_t scratch_elems = 0, scratch_used = 0;
+  double* scratch_take(long long elems) {
+    const size_t off = scratch_used;
+    scratch_used += (size_t)round_up(elems, 32);
+    return scratch ? scratch + off : reinterpret_cast<double*>((uintptr_t)0x400000 + off * 8);  // dry build
+  }
+  bool emit_mcse(Launch::Kind kind, int level, int side, const std::vector<char>& tab, int nin, int nout, int count,
+                 long long rows, long long cols, bool aligned, const std::vector<int>& node_ids);
+
   View opA(int l, long long z, const View& root) const;
   View opB(int l, long long z, const View& root) const;
 
@@ -408,6 +424,7 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
                        bool lazy_kernels) {
   launches.clear();
   h_tab.clear();
+  scratch_used = 0;
   cur_A = A, cur_B = B, cur_C = C, cur_lda = lda, cur_ldb = ldb, cur_ldc = ldc;
   const View rootA{const_cast<double*>(A), lda, 1.0}, rootB{const_cast<double*>(B), ldb, 1.0};
   const int M = alg->M, K = alg->K, Nb = alg->N;
@@ -528,6 +545,9 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
         ++count;
       }
       if (!count) continue;
+      if (emit_mcse(side == 0 ? Launch::FORM_A : Launch::FORM_B, l, side, tab, nin, nout, count, rows, cols, aligned,
+                    node_ids))
+        continue;
       Launch ln;
       ln.node_ids = node_ids;
       ln.kind = side == 0 ? Launch::FORM_A : Launch::FORM_B;
@@ -645,7 +665,7 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
         node_ids.push_back((int)zp);
         ++count;
       }
-      if (count) {
+      if (count && !emit_mcse(Launch::ASSEMBLE, l, 2, tab, nin, nout, count, d.P, d.N, aligned, node_ids)) {
         Launch ln;
         ln.node_ids = node_ids;
         ln.kind = Launch::ASSEMBLE;
@@ -843,6 +863,115 @@ void fmm_plan_s::fuse_leaf_level(bool lazy_kernels) {
   for (int q = 0; q < (int)launches.size(); ++q)
     if (q != ia && q != ib && q != ias) keep.push_back(launches[q]);
   launches.swap(keep);
+}
+
+// Write-once / pairwise with CSE: the greedy length-two subexpressions Y_t = x_a + r x_b
+// (the same ones the streaming kernels keep in registers) are written to memory once per node by
+// their own launches, in creation order (a later Y may use an earlier one), then the main launch
+// evaluates every chain over the inputs and the Y_t.  Each Y_t has the node's input leading
+// dimension, so one ld serves all inputs of the main launch.  Returns false (nothing emitted)
+// for streaming, without CSE, or when the chains share no subexpression.
+bool fmm_plan_s::emit_mcse(Launch::Kind kind, int level, int side, const std::vector<char>& tab, int nin, int nout,
+                           int count, long long rows, long long cols, bool aligned, const std::vector<int>& node_ids) {
+  if (opt.strategy == FMM_ADD_STREAMING || !opt.cse) return false;
+  std::vector<std::tuple<int, int, double>> temps;
+  std::vector<std::vector<std::pair<int, double>>> outs;
+  const LincombSpec base = spec_for(side, 2);
+  lincomb_cse_program(base, &temps, &outs);
+  const int T = (int)temps.size();
+  if (T == 0) return false;
+  const size_t nb = lincomb_node_bytes(nin, nout);
+  const int vec = aligned ? 2 : 1;
+  const double elems = (double)rows * cols;
+  // per node: its input pointers, output pointers, leading dimensions; temporaries from the arena
+  std::vector<std::vector<const double*>> var(count);  // nin inputs then T temporaries
+  std::vector<std::vector<double*>> outp(count);
+  std::vector<long long> ldi(count), ldo(count);
+  for (int z = 0; z < count; ++z) {
+    const char* e = tab.data() + (size_t)z * nb;
+    const double* const* in = reinterpret_cast<const double* const*>(e);
+    double* const* out = reinterpret_cast<double* const*>(e + sizeof(void*) * nin);
+    auto* lds = reinterpret_cast<const long long*>(e + sizeof(void*) * (nin + nout));
+    ldi[z] = lds[0];
+    ldo[z] = lds[1];
+    var[z].assign(in, in + nin);
+    outp[z].assign(out, out + nout);
+    for (int t = 0; t < T; ++t) var[z].push_back(scratch_take(rows * ldi[z]));
+  }
+  auto emit = [&](const LincombSpec& sp, const std::vector<char>& t2, double reads, double writes) {
+    Launch ln;
+    ln.node_ids = node_ids;
+    ln.kind = kind;
+    ln.level = level;
+    ln.count = count;
+    ln.rows = rows;
+    ln.cols = cols;
+    ln.aligned16 = aligned;
+    ln.kern = lincomb_get(sp);
+    ln.elem_adds = lincomb_cost(*ln.kern).adds_per_elem * elems * count;
+    ln.elem_reads = reads * elems;
+    ln.elem_writes = writes * elems;
+    ln.table_off = push_tab(t2.data(), t2.size());
+    launches.push_back(ln);
+  };
+  const bool pw = opt.strategy == FMM_ADD_PAIRWISE;
+  // the temporaries, Y_t = x_a + r x_b: a two-term chain (pairwise: a copy and one daxpy)
+  for (int t = 0; t < T; ++t) {
+    LincombSpec sp;
+    sp.nin = 2;
+    sp.nout = 1;
+    sp.coef = {1.0, std::get<2>(temps[t])};
+    sp.strategy = opt.strategy;
+    sp.cse = 0;
+    sp.vec = vec;
+    std::vector<char> t2;
+    const size_t nb2 = lincomb_node_bytes(2, 1);
+    for (int z = 0; z < count; ++z) {
+      std::vector<char> e(nb2, 0);
+      auto** in = reinterpret_cast<const double**>(e.data());
+      auto** out = reinterpret_cast<double**>(e.data() + sizeof(void*) * 2);
+      auto* lds = reinterpret_cast<long long*>(e.data() + sizeof(void*) * 3);
+      in[0] = var[z][std::get<0>(temps[t])];
+      in[1] = var[z][std::get<1>(temps[t])];
+      out[0] = const_cast<double*>(var[z][nin + t]);
+      lds[0] = ldi[z];
+      lds[1] = ldi[z];
+      t2.insert(t2.end(), e.begin(), e.end());
+    }
+    emit(sp, t2, (pw ? 3.0 : 2.0) * count, (pw ? 2.0 : 1.0) * count);
+  }
+  // the chains over inputs and temporaries
+  LincombSpec sp;
+  sp.nin = nin + T;
+  sp.nout = nout;
+  sp.coef.assign((size_t)sp.nin * nout, 0.0);
+  for (int o = 0; o < nout; ++o)
+    for (const auto& kv : outs[o]) sp.coef[(size_t)o * sp.nin + kv.first] = kv.second;
+  sp.strategy = opt.strategy;
+  sp.cse = 0;
+  sp.vec = vec;
+  const size_t nbm = lincomb_node_bytes(sp.nin, nout);
+  std::vector<char> tm;
+  double reads = 0, writes = 0;
+  for (int z = 0; z < count; ++z) {
+    std::vector<char> e(nbm, 0);
+    auto** in = reinterpret_cast<const double**>(e.data());
+    auto** out = reinterpret_cast<double**>(e.data() + sizeof(void*) * sp.nin);
+    auto* lds = reinterpret_cast<long long*>(e.data() + sizeof(void*) * (sp.nin + nout));
+    for (int v = 0; v < sp.nin; ++v) in[v] = var[z][v];
+    for (int o = 0; o < nout; ++o) {
+      out[o] = outp[z][o];
+      if (!out[o]) continue;
+      const double n = (double)outs[o].size();
+      reads += pw ? 2 * n - 1 : n;
+      writes += pw ? n : 1;
+    }
+    lds[0] = ldi[z];
+    lds[1] = ldo[z];
+    tm.insert(tm.end(), e.begin(), e.end());
+  }
+  emit(sp, tm, reads, writes);
+  return true;
 }
 
 void fmm_plan_s::emit_two_level_formation(bool lazy_kernels) {
@@ -1106,6 +1235,19 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
   p->build(reinterpret_cast<const double*>(0x100000), std::max<long long>(p->Q, 1), reinterpret_cast<const double*>(0x200000),
            std::max<long long>(p->N, 1), reinterpret_cast<double*>(0x300000), std::max<long long>(p->N, 1), true);
   p->tab_bytes = std::max<size_t>(p->h_tab.size(), 256);
+  p->scratch_elems = p->scratch_used;
+  if (p->scratch_elems) {
+    const size_t bytes = p->scratch_elems * sizeof(double);
+    if (p->opt.workspace_limit_bytes && p->ws_bytes + bytes > p->opt.workspace_limit_bytes)
+      throw Error(FMM_E_NO_MEMORY, "plan needs " + std::to_string(p->ws_bytes + bytes) +
+                                       " workspace bytes with its memory CSE temporaries > limit");
+    if (cudaMalloc(reinterpret_cast<void**>(&p->scratch), bytes) != cudaSuccess) {
+      cudaGetLastError();
+      p->scratch = nullptr;
+      throw Error(FMM_E_NO_MEMORY, "cudaMalloc of " + std::to_string(bytes) + " CSE temporary bytes failed");
+    }
+    p->ws_bytes += bytes;
+  }
   for (auto& sl : p->slot) FMM_CUDA(cudaMalloc(&sl.d_tab, p->tab_bytes));
   FMM_CUDA(cudaMallocHost(&p->h_pinned, p->tab_bytes));
   FMM_CUDA(cudaEventCreateWithFlags(&p->upload_done, cudaEventDisableTiming));

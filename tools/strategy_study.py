@@ -1,6 +1,7 @@
 """Strategy x CSE study on B200 (the paper's Fig. 2 question):
-pairwise (daxpy chains) vs write-once vs streaming addition kernels, CSE on / off (streaming only:
-the other two never share subexpressions), for <4,2,4;26> on N x 1600 x N (the paper's outer-product
+pairwise (daxpy chains) vs write-once vs streaming addition kernels, CSE on / off (streaming keeps
+the common subexpressions in registers; write-once and pairwise write them to memory once per
+node), for <4,2,4;26> on N x 1600 x N (the paper's outer-product
 family), <4,2,3;20> on N x N x N (Fig. 2's second panel; the <2,3,4;20> of algs/ under Prop. 2) and
 the c2 / c4 workloads.  One JSON line per (workload, strategy, cse)."""
 import json
@@ -34,7 +35,7 @@ for name, P, Q, N, L, lay in WL:
     A = bench.to_device(A_np, lay, "cuda")
     B = bench.to_device(B_np, lay, "cuda")
     for strategy in ("streaming", "write_once", "pairwise"):
-        for cse in ((False, True) if strategy == "streaming" else (False,)):
+        for cse in (False, True):
             p = F.Plan(load(name), P, Q, N, L, layout=lay, strategy=strategy, cse=cse)
             st = p.stats()
             C = p.new_output()
