@@ -67,7 +67,8 @@ typedef struct {
                                write-once and pairwise write each one to memory once per node
                                (its own launch) and read it in the chains, with the
                                temporaries in a workspace arena counted by
-                               fmm_plan_workspace_bytes.  0: every chain is summed in ascending
+                               fmm_plan_workspace_bytes (each has its node's input leading
+                               dimension, so it can exceed the S_r / T_r storage).  0: every chain is summed in ascending
                                index order (bit-identical to the oracle's order). */
   int shard_rank;           /* multi-GPU leaf sharding (Sec. 4.3 HYBRID arithmetic, P:823-829,
                                with GPUs in place of threads): this plan computes the partial
