@@ -202,399 +202,465 @@ def main():
         run_reference(args, w)
         return
 
-    import numpy as np
-    import torch
-    import torch.distributed as dist
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        if args.dist_backend == "gloo":
-            # control-flow check of the N > 1 path on a box with fewer GPUs than ranks (ranks share
-            # devices; gloo carries the collectives): its numbers are not measurements
-            local = local % torch.cuda.device_count()
-        torch.cuda.set_device(local)
-        if args.dist_backend == "gloo":
-            dist.init_process_group("gloo")
+    Run(args, w).go()
+
+
+class Run:
+    """One bench invocation of our arm: set-up, the timed steps, the comparison legs, the JSON line.
+    State shared by the legs lives on the instance."""
+
+    def __init__(self, args, w):
+        import torch
+        import torch.distributed as dist
+        self.args, self.w = args, w
+        self.torch, self.dist = torch, dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        if self.world > 1:
+            if args.dist_backend == "gloo":
+                # control-flow check of the N > 1 path on a box with fewer GPUs than ranks (ranks share
+                # devices; gloo carries the collectives): its numbers are not measurements
+                local = local % torch.cuda.device_count()
+            torch.cuda.set_device(local)
+            if args.dist_backend == "gloo":
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         else:
-            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    else:
-        torch.cuda.set_device(0)
-    device = torch.device(f"cuda:{torch.cuda.current_device()}")
-    import __graft_entry__
-    __graft_entry__.build()
-    import paper_1409_2908_b200 as F
-    from paper_1409_2908_b200.dist import combine_partials, scatter_partials
+            torch.cuda.set_device(0)
+        self.device = torch.device(f"cuda:{torch.cuda.current_device()}")
+        import __graft_entry__
+        __graft_entry__.build()
+        import paper_1409_2908_b200 as F
+        self.F = F
+        self.P, self.Q, self.N, self.L = w["P"], w["Q"], w["N"], w["L"]
+        self.flops = 2.0 * self.P * self.Q * self.N
 
-    P, Q, N, L = w["P"], w["Q"], w["N"], w["L"]
-    A_np, B_np = gen_inputs(w)
-    A = to_device(A_np, w["layout"], device)
-    B = to_device(B_np, w["layout"], device)
-    alg = F.load_alg(w["alg"])
-    lib_comm = F.Comm.from_torch_distributed(device=device.index) if (world > 1 and args.combine == "lib") else None
-    plan = F.Plan(alg, P, Q, N, L, layout=w["layout"], strategy=args.strategy, cse=bool(args.cse),
-                  shard_rank=rank, shard_count=world, fuse=bool(args.fuse), collapse=bool(args.collapse),
-                  comm=lib_comm, root="slabs" if args.output == "slabs" else 0, shard_mode=args.shard_mode)
-    # --combine p2p: the partial C lives in a peer-mapped buffer and one pull-reduce kernel per rank
-    # sums its slab over every rank's partial (fmm_p2p_*, CUDA IPC over NVLink, no NCCL data path)
-    p2p = out_slab = None
-    outer, inner = (P, N) if w["layout"] == "row" else (N, P)
-    if world > 1 and args.combine == "p2p":
-        p2p = F.P2P.from_torch_distributed(8 * P * N, device=device.index)
-        C = p2p.partial(P, N, w["layout"])
-        s0, s1 = F.dist_slab(P, N, w["layout"], world, rank)
-        out_slab = torch.empty(s1 - s0, inner, dtype=torch.float64, device=device)
-    else:
-        C = plan.new_output()
-    st = plan.stats()
-    dmma_peak, dfma_peak = F.probe_fp64_peak()
-    stream = torch.cuda.current_stream()
+    # ---- set-up ------------------------------------------------------------------------------
+    def setup(self):
+        args, w, F, torch = self.args, self.w, self.F, self.torch
+        P, Q, N, L, world, rank, device = self.P, self.Q, self.N, self.L, self.world, self.rank, self.device
+        self.A_np, self.B_np = gen_inputs(w)
+        self.A = to_device(self.A_np, w["layout"], device)
+        self.B = to_device(self.B_np, w["layout"], device)
+        self.alg = F.load_alg(w["alg"])
+        self.lib_comm = F.Comm.from_torch_distributed(device=device.index) if (world > 1 and args.combine == "lib") else None
+        self.plan = F.Plan(self.alg, P, Q, N, L, layout=w["layout"], strategy=args.strategy, cse=bool(args.cse),
+                           shard_rank=rank, shard_count=world, fuse=bool(args.fuse), collapse=bool(args.collapse),
+                           comm=self.lib_comm, root="slabs" if args.output == "slabs" else 0, shard_mode=args.shard_mode)
+        # --combine p2p: the partial C lives in a peer-mapped buffer and one pull-reduce kernel per rank
+        # sums its slab over every rank's partial (fmm_p2p_*, CUDA IPC over NVLink, no NCCL data path)
+        self.p2p = self.out_slab = None
+        self.outer, self.inner = (P, N) if w["layout"] == "row" else (N, P)
+        if world > 1 and args.combine == "p2p":
+            self.p2p = F.P2P.from_torch_distributed(8 * P * N, device=device.index)
+            self.C = self.p2p.partial(P, N, w["layout"])
+            s0, s1 = F.dist_slab(P, N, w["layout"], world, rank)
+            self.out_slab = torch.empty(s1 - s0, self.inner, dtype=torch.float64, device=device)
+        else:
+            self.C = self.plan.new_output()
+        self.st = self.plan.stats()
+        self.fused = self.st.get("fused_launches", 0) > 0
+        self.dmma_peak, self.dfma_peak = F.probe_fp64_peak()
+        self.stream = torch.cuda.current_stream()
 
-    def combine():
-        if lib_comm is not None:  # a distributed plan reduces inside fmm_execute
+    def combine(self):
+        from paper_1409_2908_b200.dist import combine_partials, scatter_partials
+        if self.lib_comm is not None:  # a distributed plan reduces inside fmm_execute
             return
-        if p2p is not None:
-            stream.synchronize()
-            dist.barrier()  # every partial complete
-            p2p.reduce_slab(outer, inner, out_slab, stream=stream)
-            stream.synchronize()
-            dist.barrier()  # every slab read before the next step overwrites a partial
-        elif args.output == "slabs":
-            scatter_partials(C)
+        if self.p2p is not None:
+            self.stream.synchronize()
+            self.dist.barrier()  # every partial complete
+            self.p2p.reduce_slab(self.outer, self.inner, self.out_slab, stream=self.stream)
+            self.stream.synchronize()
+            self.dist.barrier()  # every slab read before the next step overwrites a partial
+        elif self.args.output == "slabs":
+            scatter_partials(self.C)
         else:
-            combine_partials(C)
+            combine_partials(self.C)
 
-    def step(evs=None):
+    def step(self, evs=None):
         if evs is None:
-            plan.execute(A, B, C, stream=stream)
+            self.plan.execute(self.A, self.B, self.C, stream=self.stream)
         else:
-            plan.execute_events(A, B, C, evs[:4], stream=stream)
-        combine()
+            self.plan.execute_events(self.A, self.B, self.C, evs[:4], stream=self.stream)
+        self.combine()
         if evs is not None:
-            evs[4].record(stream)  # after the combine: the comm share of a step (N > 1)
+            evs[4].record(self.stream)  # after the combine: the comm share of a step (N > 1)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
-    for e in (x for row in evs for x in row):
-        e.record(stream)  # torch creates the underlying cudaEvent_t lazily, at the first record
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = ClockSampler(device.index)
-    clocks.start()
-    time.sleep(0.3)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t0.record(stream)
-    for k in range(args.steps):
-        step(evs[k])
-    t1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clk = clocks.stop()
-    ms = t0.elapsed_time(t1)
-    if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device=device)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
-    ms_step = ms / args.steps
-    flops = 2.0 * P * Q * N
-    value = flops / (ms_step * 1e-3) / 1e9
+    def max_over_ranks(self, ms):
+        if self.world > 1:
+            tt = self.torch.tensor([ms], dtype=self.torch.float64, device=self.device)
+            self.dist.all_reduce(tt, op=self.dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        return ms
 
-    # result check after the timed steps (C holds the last step's combined product): sampled rows
-    # of rank 0's part of C against a cuBLAS product of the same rows (a check, not a timing), at the
-    # north-star tolerance max |C - AB| <= 1e-10 ||A||_F ||B||_F
-    check = None
-    if rank == 0:
-        if (args.output == "slabs" or p2p is not None) and world > 1:
-            lo, hi = F.dist_slab(P, N, w["layout"], world, 0)
+    # ---- the timed region ----------------------------------------------------------------------
+    def timed_steps(self):
+        import numpy as np
+        torch, args, stream = self.torch, self.args, self.stream
+        for _ in range(args.warmup):
+            self.step()
+        torch.cuda.synchronize()
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+        for e in (x for row in evs for x in row):
+            e.record(stream)  # torch creates the underlying cudaEvent_t lazily, at the first record
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clocks = ClockSampler(self.device.index)
+        clocks.start()
+        time.sleep(0.3)
+        if self.world > 1:
+            self.dist.barrier()
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for k in range(args.steps):
+            self.step(evs[k])
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if self.world > 1:
+            self.dist.barrier()
+        self.clk = clocks.stop()
+        self.ms_step = self.max_over_ranks(t0.elapsed_time(t1)) / args.steps
+        self.value = self.flops / (self.ms_step * 1e-3) / 1e9
+        # per-phase device times measured on the launching stream during the timed region
+        ph = np.array([[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]),
+                        e[3].elapsed_time(e[4])] for e in evs])
+        self.form_ms, self.gemm_ms, self.asm_ms, self.comm_ms = [float(x) for x in ph.mean(axis=0)]
+
+    def result_check(self):
+        # after the timed steps C holds the last step's combined product: sampled rows of rank 0's
+        # part of C against a cuBLAS product of the same rows (a check, not a timing), at the
+        # north-star tolerance max |C - AB| <= 1e-10 ||A||_F ||B||_F
+        if self.rank != 0:
+            return None
+        torch, w, F, A, B, C = self.torch, self.w, self.F, self.A, self.B, self.C
+        if (self.args.output == "slabs" or self.p2p is not None) and self.world > 1:
+            lo, hi = F.dist_slab(self.P, self.N, w["layout"], self.world, 0)
         else:
-            lo, hi = 0, (P if w["layout"] == "row" else N)
+            lo, hi = 0, (self.P if w["layout"] == "row" else self.N)
+        if hi <= lo:
+            return None
         g = torch.Generator().manual_seed(7)
-        idx = torch.randint(lo, max(lo + 1, hi), (min(64, max(hi - lo, 1)),), generator=g).to(device)
-        if hi > lo:
-            # rank 0's result: C itself, or (p2p) its reduced slab of C's storage rows
-            got = (lambda rows: out_slab[rows - lo]) if p2p is not None else (
-                (lambda rows: C[rows]) if w["layout"] == "row" else (lambda cols: C[:, cols].t()))
-            if w["layout"] == "row":
-                err = (got(idx) - A[idx] @ B).abs().max().item()
-            else:  # slabs of C's columns
-                err = (got(idx) - (A @ B[:, idx]).t()).abs().max().item()
-            tol = 1e-10 * torch.linalg.norm(A).item() * torch.linalg.norm(B).item()
-            check = {"sampled": int(idx.numel()), "of": "rows" if w["layout"] == "row" else "columns",
-                     "max_abs_err": err, "tolerance": tol, "ok": bool(err <= tol)}
+        idx = torch.randint(lo, max(lo + 1, hi), (min(64, max(hi - lo, 1)),), generator=g).to(self.device)
+        # rank 0's result: C itself, or (p2p) its reduced slab of C's storage rows
+        if self.p2p is not None:
+            got = lambda rows: self.out_slab[rows - lo]  # noqa: E731
+        elif w["layout"] == "row":
+            got = lambda rows: C[rows]  # noqa: E731
+        else:
+            got = lambda cols: C[:, cols].t()  # noqa: E731
+        if w["layout"] == "row":
+            err = (got(idx) - A[idx] @ B).abs().max().item()
+        else:  # slabs of C's columns
+            err = (got(idx) - (A @ B[:, idx]).t()).abs().max().item()
+        tol = 1e-10 * torch.linalg.norm(A).item() * torch.linalg.norm(B).item()
+        return {"sampled": int(idx.numel()), "of": "rows" if w["layout"] == "row" else "columns",
+                "max_abs_err": err, "tolerance": tol, "ok": bool(err <= tol)}
 
-    # per-phase device times measured on the launching stream during the timed region
-    ph = np.array([[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]), e[3].elapsed_time(e[4])]
-                   for e in evs])
-    form_ms, gemm_ms, asm_ms, comm_ms = [float(x) for x in ph.mean(axis=0)]
-    add_ms = form_ms + asm_ms
-    peaks, peak_src = measured_peaks()
-    hbm = float(peaks.get("hbm_gbs", HBM_FALLBACK))
-    fused = st.get("fused_launches", 0) > 0
-    # leaf-product flops of the dominant launch (the fused leaf level, or the plain leaf GEMM)
-    gemm_tf = st["leaf_flops"] / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
-    sep_bytes = st["add_bytes"] - st["fused_add_bytes"]
-    add_gbs = sep_bytes / (add_ms * 1e-3) / 1e9 if add_ms > 0 else None
-
-    # the other leaf-level schedule on the same workload: with --fuse 0 (default) the fused
-    # leaf-level launch (level-L formation / leaf GEMM / level-L assembly in one cooperative
-    # kernel, addition CTAs on their own SMs), with --fuse 1 the separate kernels
-    other = None
-    if not args.no_other and L >= 1:
+    # ---- comparison legs (outside the timed region) --------------------------------------------
+    def other_schedule(self):
+        # the other leaf-level schedule on the same workload: with --fuse 0 (default) the fused
+        # leaf-level launch (level-L formation / leaf GEMM / level-L assembly in one cooperative
+        # kernel, addition CTAs on their own SMs), with --fuse 1 the separate kernels
+        import numpy as np
+        args, torch, stream = self.args, self.torch, self.stream
+        if args.no_other or self.L < 1:
+            return None
         try:
-            plan_o = F.Plan(alg, P, Q, N, L, layout=w["layout"], strategy=args.strategy, cse=bool(args.cse),
-                            shard_rank=rank, shard_count=world, fuse=not fused, collapse=False)
+            plan_o = self.F.Plan(self.alg, self.P, self.Q, self.N, self.L, layout=self.w["layout"],
+                                 strategy=args.strategy, cse=bool(args.cse), shard_rank=self.rank,
+                                 shard_count=self.world, fuse=not self.fused, collapse=False)
             so = plan_o.stats()
             for _ in range(2):
-                plan_o.execute(A, B, C, stream=stream)
+                plan_o.execute(self.A, self.B, self.C, stream=stream)
             nu = max(3, min(args.steps, 10))
             evu = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nu)]
             for e in (x for row in evu for x in row):
                 e.record(stream)  # creates the underlying cudaEvent_t
             torch.cuda.synchronize()
             for k in range(nu):
-                plan_o.execute_events(A, B, C, evu[k], stream=stream)
+                plan_o.execute_events(self.A, self.B, self.C, evu[k], stream=stream)
             torch.cuda.synchronize()
             phu = np.array([[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]),
                              e[0].elapsed_time(e[3])] for e in evu]).mean(axis=0)
-            o_fused = so.get("fused_launches", 0) > 0
-            other = {"fused_leaf_level": o_fused, "collapsed_levels": bool(so.get("collapsed", 0)), "ms_per_step": float(phu[3]), "value": flops / (phu[3] * 1e-3) / 1e9,
+            other = {"fused_leaf_level": so.get("fused_launches", 0) > 0, "collapsed_levels": bool(so.get("collapsed", 0)),
+                     "ms_per_step": float(phu[3]), "value": self.flops / (phu[3] * 1e-3) / 1e9,
                      "steps": nu, "phases_ms": {"formation": float(phu[0]), "leaf_level": float(phu[1]),
                                                 "assembly_and_strips": float(phu[2])},
                      "launches": so["launches"]}
             del plan_o
-            plan.execute(A, B, C, stream=stream)  # C holds the headline path's result again
+            self.plan.execute(self.A, self.B, self.C, stream=stream)  # C holds the headline path's result again
+            return other
         except Exception as e:  # an optional extra measurement must not cost the bench line
-            other = {"error": str(e)[:200]}
             torch.cuda.synchronize()
+            return {"error": str(e)[:200]}
 
-    # shape matching (fmm_select over every algorithm file x its six Prop. 1/2 permutations x L <= 3,
-    # by the library's cost model) on the same inputs: what the paper's "match the shape" buys here
-    shape_matched = None
-    if not args.no_other and rank == 0 and world == 1:
+    def shape_matched(self):
+        # shape matching (fmm_select over every algorithm file x its six Prop. 1/2 permutations x
+        # L <= 3, by the library's cost model) on the same inputs: what the paper's "match the shape"
+        # buys here
         import glob
+        args, torch, stream, F = self.args, self.torch, self.stream, self.F
+        if args.no_other or self.rank != 0 or self.world != 1:
+            return None
         cands = [F.load_alg(os.path.basename(x)[:-4]) for x in sorted(glob.glob(os.path.join(ROOT, "algs", "*.txt")))]
-        sel, sel_L, sel_pred = F.select(cands, P, Q, N, 3, w["layout"])
-        if sel is not None:
-            try:
-                plan_s = F.Plan(sel, P, Q, N, sel_L, layout=w["layout"], strategy=args.strategy, cse=bool(args.cse))
-                for _ in range(2):
-                    plan_s.execute(A, B, C, stream=stream)
-                ns = max(3, min(args.steps, 10))
-                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                s0.record(stream)
-                for _ in range(ns):
-                    plan_s.execute(A, B, C, stream=stream)
-                s1.record(stream)
-                torch.cuda.synchronize()
-                ms_s = s0.elapsed_time(s1) / ns
-                shape_matched = {"algorithm": sel.name, "base_case": [sel.M, sel.K, sel.N], "rank": sel.R, "levels": sel_L,
-                                 "predicted_ms": sel_pred, "ms_per_step": ms_s, "value": flops / (ms_s * 1e-3) / 1e9,
-                                 "steps": ns, "note": "not the headline: BASELINE fixes the algorithm and L"}
-                del plan_s
-                plan.execute(A, B, C, stream=stream)
-            except Exception as e:  # optional, like other_schedule
-                shape_matched = {"algorithm": sel.name, "levels": sel_L, "error": str(e)[:200]}
+        sel, sel_L, sel_pred = F.select(cands, self.P, self.Q, self.N, 3, self.w["layout"])
+        if sel is None:
+            return None
+        try:
+            plan_s = F.Plan(sel, self.P, self.Q, self.N, sel_L, layout=self.w["layout"], strategy=args.strategy,
+                            cse=bool(args.cse))
+            for _ in range(2):
+                plan_s.execute(self.A, self.B, self.C, stream=stream)
+            ns = max(3, min(args.steps, 10))
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            for _ in range(ns):
+                plan_s.execute(self.A, self.B, self.C, stream=stream)
+            s1.record(stream)
+            torch.cuda.synchronize()
+            ms_s = s0.elapsed_time(s1) / ns
+            del plan_s
+            self.plan.execute(self.A, self.B, self.C, stream=stream)
+            return {"algorithm": sel.name, "base_case": [sel.M, sel.K, sel.N], "rank": sel.R, "levels": sel_L,
+                    "predicted_ms": sel_pred, "ms_per_step": ms_s, "value": self.flops / (ms_s * 1e-3) / 1e9,
+                    "steps": ns, "note": "not the headline: BASELINE fixes the algorithm and L"}
+        except Exception as e:  # optional, like other_schedule
+            return {"algorithm": sel.name, "levels": sel_L, "error": str(e)[:200]}
 
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get(args.workload, {}).get("grouped_dgemm_bytes_per_launch")
-    except OSError:
-        pass
-    kname = ("grouped_dgemm_tma<FUSED> (level-L formation + leaf products on DMMA mma.sync.m8n8k4.f64 + "
-             "level-L assembly, one persistent launch)" if fused else
-             "grouped_dgemm_tma (leaf products, mma.sync.m8n8k4.f64 = DMMA)")
-    roofline = {"bound": "tensor", "kernel": kname,
-                "achieved": gemm_tf, "peak": dmma_peak, "unit": "TFLOP/s",
-                "frac": (gemm_tf / dmma_peak) if gemm_tf else None, "traffic": traffic,
-                "peak_source": "in-run DMMA microbenchmark fmm_probe_fp64_peak (MEASURED_PEAKS.json has no FP64 "
-                               "figure; nameplate 148 SM x 128 flop/clk x 1.965 GHz = 37.2)",
-                "algorithmic_flops_per_launch": st["leaf_flops"],
-                "hidden_addition_bytes_per_launch": st["fused_add_bytes"]}
-
-    # cuBLAS DGEMM (classical) on the same inputs, same box: the comparison point
-    cub = None
-    if rank == 0:
+    def cublas(self):
+        # cuBLAS DGEMM (classical) on the same inputs, same box: the comparison point
+        if self.rank != 0:
+            return None
+        torch, A, B = self.torch, self.A, self.B
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ref = torch.matmul(A, B)
+        torch.matmul(A, B)
         torch.cuda.synchronize()
         best = 1e30
         for _ in range(3):
-            e0.record(); torch.matmul(A, B); e1.record()
+            e0.record()
+            torch.matmul(A, B)
+            e1.record()
             e1.synchronize()
             best = min(best, e0.elapsed_time(e1))
-        cub = flops / (best * 1e-3) / 1e9
-        del ref
+        return self.flops / (best * 1e-3) / 1e9
 
-    # the classical comparison on our own DMMA GEMM (L = 0): at N > 1 each rank multiplies its row
-    # slab of A by B with no exchange (SURVEY f1's classical row-slab split), timed as max over ranks
-    own = None
-    try:
-        if w["layout"] == "row":
-            r0, r1 = F.dist_slab(P, N, "row", world, rank)
-            As = A[r0:r1]
-        else:  # column-major: the slab of C's columns, i.e. B's columns
-            r0, r1 = F.dist_slab(P, N, "col", world, rank)
-            As = None
-        m_rows = (r1 - r0) if As is not None else P
-        n_cols = N if As is not None else (r1 - r0)
-        cp = F.Plan(alg, m_rows, Q, n_cols, 0, layout=w["layout"])
-        Aa, Bb = (As, B) if As is not None else (A, B[:, r0:r1])
-        Cc = cp.new_output()
-        for _ in range(2):
-            cp.execute(Aa, Bb, Cc, stream=stream)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(3):
-            cp.execute(Aa, Bb, Cc, stream=stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        tt = torch.tensor([e0.elapsed_time(e1) / 3], dtype=torch.float64, device=device)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        own = {"ms": float(tt.item()), "value": flops / (float(tt.item()) * 1e-3) / 1e9,
-               "what": "classical DMMA GEMM (L = 0, this library)" + (f", row slabs x{world}, no exchange" if world > 1 else "")}
-        del cp, Cc
-    except Exception as ex:  # noqa: BLE001  (a comparison leg only)
-        own = {"error": str(ex)[:200]}
+    def own_classical(self):
+        # the classical comparison on our own DMMA GEMM (L = 0): at N > 1 each rank multiplies its
+        # row slab of A by B with no exchange (SURVEY f1's classical row-slab split), max over ranks
+        torch, F, w, A, B, stream = self.torch, self.F, self.w, self.A, self.B, self.stream
+        try:
+            lay = w["layout"]
+            r0, r1 = F.dist_slab(self.P, self.N, lay, self.world, self.rank)
+            if lay == "row":
+                cp = F.Plan(self.alg, r1 - r0, self.Q, self.N, 0, layout=lay)
+                Aa, Bb = A[r0:r1], B
+            else:  # column-major: the slab of C's columns, i.e. B's columns
+                cp = F.Plan(self.alg, self.P, self.Q, r1 - r0, 0, layout=lay)
+                Aa, Bb = A, B[:, r0:r1]
+            Cc = cp.new_output()
+            for _ in range(2):
+                cp.execute(Aa, Bb, Cc, stream=stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if self.world > 1:
+                self.dist.barrier()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(3):
+                cp.execute(Aa, Bb, Cc, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = self.max_over_ranks(e0.elapsed_time(e1) / 3)
+            del cp, Cc
+            return {"ms": ms, "value": self.flops / (ms * 1e-3) / 1e9,
+                    "what": "classical DMMA GEMM (L = 0, this library)" +
+                            (f", row slabs x{self.world}, no exchange" if self.world > 1 else "")}
+        except Exception as ex:  # noqa: BLE001  (a comparison leg only)
+            return {"error": str(ex)[:200]}
 
-    # end-to-end through the public host-buffer API: H2D of A and B, execute, D2H of C per step
-    e2e = None
-    if not args.no_e2e:
+    def e2e(self):
+        # end to end through the public host-buffer API: H2D of A and B, execute, D2H of C per step
+        import numpy as np
+        args, torch, w, world, rank = self.args, self.torch, self.w, self.world, self.rank
+        if args.no_e2e:
+            return None
+        P, Q, N = self.P, self.Q, self.N
+
         def pinned(x, rows, cols):
             if w["layout"] == "row":
                 return (torch.from_numpy(np.ascontiguousarray(x)) if x is not None
                         else torch.empty(rows, cols, dtype=torch.float64)).pin_memory()
             return (torch.from_numpy(np.ascontiguousarray(x.T)) if x is not None
                     else torch.empty(cols, rows, dtype=torch.float64)).pin_memory().t()
-        Ah, Bh, Ch = pinned(A_np, P, Q), pinned(B_np, Q, N), pinned(None, P, N)
+        Ah, Bh, Ch = pinned(self.A_np, P, Q), pinned(self.B_np, Q, N), pinned(None, P, N)
         h2d = 8 * (P * Q + Q * N)
         d2h = 8 * P * N if rank == 0 else 0
         slab_h = None
-        if p2p is not None and rank == 0:  # rank 0's result is its reduced slab
-            slab_h = torch.empty(tuple(out_slab.shape), dtype=torch.float64, pin_memory=True)
-            d2h = 8 * out_slab.numel()
+        if self.p2p is not None and rank == 0:  # rank 0's result is its reduced slab
+            slab_h = torch.empty(tuple(self.out_slab.shape), dtype=torch.float64, pin_memory=True)
+            d2h = 8 * self.out_slab.numel()
+
         def e2e_step():
             if world == 1:
                 # pipelined public host API: H2D of this step, compute, D2H of its C
-                plan.execute_host(Ah, Bh, Ch, stream=stream, asynchronous=True)
+                self.plan.execute_host(Ah, Bh, Ch, stream=self.stream, asynchronous=True)
             else:
-                A.copy_(Ah, non_blocking=True); B.copy_(Bh, non_blocking=True)
-                plan.execute(A, B, C, stream=stream)
-                combine()
+                self.A.copy_(Ah, non_blocking=True)
+                self.B.copy_(Bh, non_blocking=True)
+                self.plan.execute(self.A, self.B, self.C, stream=self.stream)
+                self.combine()
                 if rank == 0:
                     if slab_h is not None:
-                        slab_h.copy_(out_slab, non_blocking=True)
+                        slab_h.copy_(self.out_slab, non_blocking=True)
                     else:
-                        Ch.copy_(C, non_blocking=True)
+                        Ch.copy_(self.C, non_blocking=True)
                 torch.cuda.synchronize()
         e2e_step()
-        plan.sync()
+        self.plan.sync()
         if world > 1:
-            dist.barrier()
+            self.dist.barrier()
         torch.cuda.synchronize()
         n_e2e = max(3, min(max(args.steps, 30), 60))  # fill and drain of the copy pipeline amortised over >= 30 steps
         h0 = time.perf_counter()
         for _ in range(n_e2e):
             e2e_step()
-        plan.sync()
+        self.plan.sync()
         torch.cuda.synchronize()
-        ms_e = (time.perf_counter() - h0) * 1e3
-        if world > 1:
-            tt = torch.tensor([ms_e], dtype=torch.float64, device=device)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ms_e = float(tt.item())
-        e2e = {"value": flops / (ms_e / n_e2e * 1e-3) / 1e9, "unit": "GFLOPS", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": ms_e / n_e2e, "steps": n_e2e,
-               "timing": "host wall clock over the steps, device synchronised on both sides",
-               "api": "fmm_execute_host_async x steps + fmm_sync (pinned host A, B, C; copy-in, compute and "
-                      "copy-out of consecutive steps overlap)" if world == 1 else
-               "H2D + fmm_execute + NCCL reduce + D2H"}
+        ms_e = self.max_over_ranks((time.perf_counter() - h0) * 1e3)
+        combine_name = ("peer-memory slab reduce" if self.p2p is not None else "NCCL reduce")
+        return {"value": self.flops / (ms_e / n_e2e * 1e-3) / 1e9, "unit": "GFLOPS", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e / n_e2e, "steps": n_e2e,
+                "timing": "host wall clock over the steps, device synchronised on both sides",
+                "api": "fmm_execute_host_async x steps + fmm_sync (pinned host A, B, C; copy-in, compute and "
+                       "copy-out of consecutive steps overlap)" if world == 1 else
+                f"H2D + fmm_execute + {combine_name} + D2H"}
 
-    # N > 1: the replication of A and B from rank 0, timed on its own after the timed
-    # region (every rank holds the seeded inputs, so the steps above do not include it)
-    bcast = None
-    if world > 1:
+    def broadcast(self):
+        # N > 1: the replication of A and B from rank 0 (SURVEY 8(e)), timed on its own after the
+        # timed region (every rank holds the seeded inputs, so the steps above do not include it)
+        if self.world == 1:
+            return None
         from paper_1409_2908_b200.dist import storage_view
+        torch, dist, stream = self.torch, self.dist, self.stream
         b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = 3
         dist.barrier()
         torch.cuda.synchronize()
         b0.record(stream)
         for _ in range(reps):
-            dist.broadcast(storage_view(A), src=0)
-            dist.broadcast(storage_view(B), src=0)
+            dist.broadcast(storage_view(self.A), src=0)
+            dist.broadcast(storage_view(self.B), src=0)
         b1.record(stream)
         torch.cuda.synchronize()
-        tb = torch.tensor([b0.elapsed_time(b1) / reps], dtype=torch.float64, device=device)
-        dist.all_reduce(tb, op=dist.ReduceOp.MAX)
-        bms = float(tb.item())
-        bbytes = 8.0 * (P * Q + Q * N)
-        bcast = {"ms": bms, "bytes": bbytes, "algbw_gbs": bbytes / (bms * 1e-3) / 1e9,
-                 "value_with_broadcast": flops / ((ms_step + bms) * 1e-3) / 1e9}
+        bms = self.max_over_ranks(b0.elapsed_time(b1) / reps)
+        bbytes = 8.0 * (self.P * self.Q + self.Q * self.N)
+        return {"ms": bms, "bytes": bbytes, "algbw_gbs": bbytes / (bms * 1e-3) / 1e9,
+                "value_with_broadcast": self.flops / ((self.ms_step + bms) * 1e-3) / 1e9}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    def roofline(self):
+        st = self.st
+        gemm_tf = st["leaf_flops"] / (self.gemm_ms * 1e-3) / 1e12 if self.gemm_ms > 0 else None
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                traffic = json.load(f).get(self.args.workload, {}).get("grouped_dgemm_bytes_per_launch")
+        except OSError:
+            pass
+        kname = ("grouped_dgemm_tma<FUSED> (level-L formation + leaf products on DMMA mma.sync.m8n8k4.f64 + "
+                 "level-L assembly, one persistent launch)" if self.fused else
+                 "grouped_dgemm_tma (leaf products, mma.sync.m8n8k4.f64 = DMMA)")
+        return {"bound": "tensor", "kernel": kname,
+                "achieved": gemm_tf, "peak": self.dmma_peak, "unit": "TFLOP/s",
+                "frac": (gemm_tf / self.dmma_peak) if gemm_tf else None, "traffic": traffic,
+                "peak_source": "in-run DMMA microbenchmark fmm_probe_fp64_peak (MEASURED_PEAKS.json has no FP64 "
+                               "figure; nameplate 148 SM x 128 flop/clk x 1.965 GHz = 37.2)",
+                "algorithmic_flops_per_launch": st["leaf_flops"],
+                "hidden_addition_bytes_per_launch": st["fused_add_bytes"]}
+
+    def cpu_baseline(self):
+        if self.rank != 0 or self.world != 1 or self.args.no_cpu:
+            return None
         from oracle import oracle as O
         O.build()
-        cpu = cpu_oracle_sample(w, A_np, B_np, args.cpu_frac)
+        cpu = cpu_oracle_sample(self.w, self.A_np, self.B_np, self.args.cpu_frac)
         cpu.pop("seconds", None)
+        return cpu
 
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": "GFLOPS", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": w["desc"], "algorithm": w["alg"], "rank": alg.R, "levels": L, "P": P, "Q": Q,
-                       "N": N, "layout": w["layout"], "inputs": "uniform[-1,1) fp64, numpy PCG64 seeds 0 (A), 1 (B)",
-                       "strategy": args.strategy, "cse": bool(args.cse),
-                       "l2": "inputs larger than L2 (A, B, C 0.54 GB each vs 126 MB); no flush"
-                       if args.workload != "c1" else "small config: L2-resident",
-                       "parallelism": ((f"{args.shard_mode}-level shards x{world} + peer-memory slab reduce "
-                                        "(fmm_p2p: one pull kernel per rank over CUDA IPC)") if p2p is not None else
-                                       (f"{args.shard_mode}-level shards x{world} + {args.dist_backend.upper()} "
-                                        f"{'reduce to rank 0' if args.output == 'root' else 'slab reduce-scatter'} "
-                                        f"({'fmm_execute' if lib_comm else 'torch.distributed'})")
-                                       if world > 1 else "1 GPU"),
-                       "fused_leaf_level": fused, "collapsed_levels": bool(st.get("collapsed", 0)),
-                       **({"dist_backend": "gloo (control-flow check, ranks share a GPU: NOT a measurement)"}
-                          if world > 1 and args.dist_backend == "gloo" else {})},
-            "roofline": roofline,
-            "clocks": clk,
-            "e2e": e2e,
-            "gpu_launches": int(st["launches"]) * args.steps,
-            "cpu_baseline": cpu,
-            "phases_ms": {"formation_levels_below_L" if fused else "formation": form_ms,
-                          "fused_leaf_level" if fused else "leaf_gemm": gemm_ms,
-                          "assembly_and_strips": add_ms - form_ms,
-                          "combine_reduce": comm_ms if world > 1 else 0.0},
-            "input_broadcast": bcast,
-            "combine_algbw_gbs": (8.0 * P * N / (comm_ms * 1e-3) / 1e9) if world > 1 and comm_ms else None,
-            "additions": {"algorithmic_bytes_per_step": st["add_bytes"],
-                          "bytes_in_fused_launch": st["fused_add_bytes"],
-                          "separate_kernel_bytes": sep_bytes, "separate_kernel_gbs": add_gbs, "peak_gbs": hbm,
-                          "separate_kernel_frac": (add_gbs / hbm) if add_gbs else None, "peak_source": peak_src},
-            "other_schedule": other,
-            "shape_matched": shape_matched,
-            "fp64_peak_tflops": {"dmma_measured": dmma_peak, "dfma_measured": dfma_peak, "nameplate": 37.2},
-            "effective_frac_of_fp64_peak": value / 1e3 / dmma_peak,
-            "cublas_dgemm_gflops_same_inputs": cub,
-            "classical_own_dgemm": own,
-            "result_check": check,
-            "paper_effective_gflops": (2.0 * P * Q * N - P * N) / (ms_step * 1e-3) / 1e9,
-            "plan": {k: st[k] for k in ("gemm_flops", "add_flops", "add_bytes", "launches", "leaves")},
-        }
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    # ---- the whole run -------------------------------------------------------------------------
+    def go(self):
+        args, w, st, world = self.args, self.w, None, self.world
+        self.setup()
+        st = self.st
+        self.timed_steps()
+        check = self.result_check()
+        add_ms = self.form_ms + self.asm_ms
+        peaks, peak_src = measured_peaks()
+        hbm = float(peaks.get("hbm_gbs", HBM_FALLBACK))
+        sep_bytes = st["add_bytes"] - st["fused_add_bytes"]
+        add_gbs = sep_bytes / (add_ms * 1e-3) / 1e9 if add_ms > 0 else None
+        other = self.other_schedule()
+        shape_matched = self.shape_matched()
+        roofline = self.roofline()
+        cub = self.cublas()
+        own = self.own_classical()
+        e2e = self.e2e()
+        bcast = self.broadcast()
+        cpu = self.cpu_baseline()
+        P, Q, N, ms_step, value = self.P, self.Q, self.N, self.ms_step, self.value
+        if self.rank == 0:
+            gb = lambda rows, cols: 8.0 * rows * cols / 1e9  # noqa: E731
+            l2 = (f"inputs larger than L2 (A {gb(P, Q):.2f} GB, B {gb(Q, N):.2f} GB, C {gb(P, N):.2f} GB vs 126 MB); "
+                  "no flush" if args.workload != "c1" else "small config: L2-resident")
+            if world == 1:
+                parallelism = "1 GPU"
+            elif self.p2p is not None:
+                parallelism = (f"{args.shard_mode}-level shards x{world} + peer-memory slab reduce "
+                               "(fmm_p2p: one pull kernel per rank over CUDA IPC)")
+            else:
+                parallelism = (f"{args.shard_mode}-level shards x{world} + {args.dist_backend.upper()} "
+                               f"{'reduce to rank 0' if args.output == 'root' else 'slab reduce-scatter'} "
+                               f"({'fmm_execute' if self.lib_comm else 'torch.distributed'})")
+            line = {
+                "metric": METRIC, "value": value, "unit": "GFLOPS", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": w["desc"], "algorithm": w["alg"], "rank": self.alg.R, "levels": self.L,
+                           "P": P, "Q": Q, "N": N, "layout": w["layout"],
+                           "inputs": "uniform[-1,1) fp64, numpy PCG64 seeds 0 (A), 1 (B)",
+                           "strategy": args.strategy, "cse": bool(args.cse), "l2": l2, "parallelism": parallelism,
+                           "fused_leaf_level": self.fused, "collapsed_levels": bool(st.get("collapsed", 0)),
+                           **({"dist_backend": "gloo (control-flow check, ranks share a GPU: NOT a measurement)"}
+                              if world > 1 and args.dist_backend == "gloo" else {})},
+                "roofline": roofline,
+                "clocks": self.clk,
+                "e2e": e2e,
+                "gpu_launches": int(st["launches"]) * args.steps,
+                "cpu_baseline": cpu,
+                "phases_ms": {"formation_levels_below_L" if self.fused else "formation": self.form_ms,
+                              "fused_leaf_level" if self.fused else "leaf_gemm": self.gemm_ms,
+                              "assembly_and_strips": self.asm_ms,
+                              "combine_reduce": self.comm_ms if world > 1 else 0.0},
+                "input_broadcast": bcast,
+                "combine_algbw_gbs": (8.0 * P * N / (self.comm_ms * 1e-3) / 1e9) if world > 1 and self.comm_ms else None,
+                "additions": {"algorithmic_bytes_per_step": st["add_bytes"],
+                              "bytes_in_fused_launch": st["fused_add_bytes"],
+                              "separate_kernel_bytes": sep_bytes, "separate_kernel_gbs": add_gbs, "peak_gbs": hbm,
+                              "separate_kernel_frac": (add_gbs / hbm) if add_gbs else None, "peak_source": peak_src},
+                "other_schedule": other,
+                "shape_matched": shape_matched,
+                "fp64_peak_tflops": {"dmma_measured": self.dmma_peak, "dfma_measured": self.dfma_peak, "nameplate": 37.2},
+                "effective_frac_of_fp64_peak": value / 1e3 / self.dmma_peak,
+                "cublas_dgemm_gflops_same_inputs": cub,
+                "classical_own_dgemm": own,
+                "result_check": check,
+                "paper_effective_gflops": (2.0 * P * Q * N - P * N) / (ms_step * 1e-3) / 1e9,
+                "plan": {k: st[k] for k in ("gemm_flops", "add_flops", "add_bytes", "launches", "leaves")},
+            }
+            print(json.dumps(line), flush=True)
+        if world > 1:
+            self.dist.barrier()
+            self.dist.destroy_process_group()
 
 
 if __name__ == "__main__":
