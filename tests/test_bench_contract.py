@@ -1,0 +1,32 @@
+"""The bench contract's host-side pieces, without a GPU: the reference arm (the CPU oracle on a
+bounded sample, BASELINE metric and unit, its own cpu_baseline and a zero-copy e2e record) prints
+one valid JSON line, and the argument checks hold (W >= 3)."""
+import json
+import os
+import subprocess
+import sys
+
+from conftest import ROOT
+
+
+def _bench(*args):
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                          timeout=300, cwd=ROOT)
+
+
+def test_reference_arm_line():
+    r = _bench("--impl", "reference", "--workload", "c1", "--steps", "2", "--warmup", "3")
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    base = json.load(open(os.path.join(ROOT, "BASELINE.json")))
+    assert line["impl"] == "reference" and line["metric"] == base["metric"]
+    assert line["unit"] == "GFLOPS" and line["higher_is_better"] is True and line["value"] > 0
+    assert line["steps"] == 2 and line["warmup"] == 3 and line["n_gpus"] == 1
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == line["value"] and cb["sample"]
+    assert line["e2e"] == {"value": line["value"], "unit": "GFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def test_warmup_below_three_is_refused():
+    r = _bench("--impl", "reference", "--workload", "c1", "--steps", "1", "--warmup", "2")
+    assert r.returncode != 0 and "--warmup must be >= 3" in r.stderr
