@@ -84,11 +84,13 @@ typedef struct {
                                0: the paper's minimal peeling everywhere. */
   int fuse_leaf_level;      /* 1: run the last level's formation (S_r, T_r of the leaves), the leaf
                                products and the last level's assembly C_k = sum_r w_kr M_r as ONE
-                               persistent launch: spare warps of the DMMA GEMM kernel evaluate the
-                               addition chains (ascending index order, no CSE) while the tensor
-                               pipe works, synchronised per parent node through device counters
-                               (streaming strategy only; needs TMA-eligible leaf views and no thin
-                               leaves, else the plan silently runs the separate kernels).
+                               cooperative persistent launch: CTAs on some SMs run the DMMA leaf
+                               tiles, CTAs on the other SMs run the same generated addition chains
+                               as the separate kernels, synchronised per parent node through device
+                               counters (bitwise equal to the separate kernels).
+                               Streaming strategy only; where collapse_levels applies the collapsed
+                               kernels run instead.  Needs TMA-eligible leaf views and no thin
+                               leaves, else the plan silently runs the separate kernels.
                                0: separate formation / GEMM / assembly launches. */
   int shard_mode;           /* with shard_count > 1: 0 = leaf-level HYBRID sharding (the default:
                                balanced to one leaf row); 1 = the top-level products r1 in contiguous
