@@ -6,8 +6,12 @@
 
 One step = one fmm_execute of the whole hot path (S/T formation at every level, the grouped DMMA
 leaf GEMM, C assembly at every level, peel strips) over one synthetic input pair already
-resident in HBM; for N > 1 each rank computes its leaf shard and the partial C are summed with
-one NCCL reduce, inside the timed region.  Prints ONE JSON line on rank 0.
+resident in HBM; for N > 1 each rank computes its leaf shard and the partial C are summed inside
+the same fmm_execute (the library's distributed plan: NCCL reduce in overlapped row chunks, or
+the peer-memory combine), inside the timed region.  Prints ONE JSON line on rank 0.
+
+--gpus N > 1 without torchrun (WORLD_SIZE unset) re-launches this script under
+torch.distributed.run with N ranks; under torchrun, --gpus must equal WORLD_SIZE.
 
 Default workload = BASELINE.json configs[1] (c2): Strassen-Winograd-class <2,2,2;7>, L = 2,
 8192 x 8192 x 8192, column-major, uniform[-1,1] from seeds 0/1.  The other configs are parity
@@ -187,22 +191,52 @@ def main():
     ap.add_argument("--collapse", type=int, default=1, help="last two levels' formation / assembly in one pass each")
     ap.add_argument("--shard-mode", default="leaf", choices=["leaf", "top"],
                     help="N > 1: leaf-level HYBRID sharding or the top-level products in contiguous ranges")
-    ap.add_argument("--combine", default="torch", choices=["torch", "lib", "p2p"],
-                    help="N > 1: partial-C reduce by torch.distributed (NCCL) or inside fmm_execute (fmm_plan_create_dist)")
+    ap.add_argument("--combine", default="auto", choices=["auto", "lib", "p2p", "torch"],
+                    help="N > 1: the partial-C combine.  lib: NCCL inside fmm_execute (fmm_plan_create_dist, "
+                         "row chunks overlapped with the assembly); p2p: the peer-memory pull-reduce inside "
+                         "fmm_execute (fmm_plan_create_p2p); torch: torch.distributed.reduce after fmm_execute.  "
+                         "auto = lib with --dist-backend nccl, p2p with gloo")
     ap.add_argument("--output", default="root", choices=["root", "slabs"],
                     help="N > 1: C summed onto rank 0, or slab-distributed (slab g of C summed onto rank g)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="N > 1: gloo only to exercise the multi-rank control flow where ranks share a GPU (not a measurement)")
     ap.add_argument("--no-other", action="store_true", help="skip timing the other leaf-level schedule (fused vs separate)")
+    ap.add_argument("--configs", default="auto",
+                    help="extra BASELINE configs timed after the headline, one sub-record each (comma list, "
+                         "'none'); auto = c3,c4,c5t,c5 for the default c2 run at N = 1")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if args.combine == "auto":
+        args.combine = "p2p" if args.dist_backend == "gloo" else "lib"
     w = WORKLOADS[args.workload]
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is not None and int(world_env) != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}: launch one rank per GPU\n")
+        sys.exit(2)
+    if world_env is None and args.gpus > 1:
+        sys.exit(relaunch(args.gpus))
     if args.impl == "reference":
         run_reference(args, w)
         return
-
     Run(args, w).go()
+
+
+def relaunch(n: int) -> int:
+    """Run this script again under torch.distributed.run with n ranks (one per GPU, 127.0.0.1)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
 
 
 class Run:
@@ -218,6 +252,9 @@ class Run:
         self.rank = int(os.environ.get("RANK", "0"))
         local = int(os.environ.get("LOCAL_RANK", "0"))
         if self.world > 1:
+            # NCCL's init lines (communicator ranks, NVLS) in the log: the driver counts ranks from them
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             if args.dist_backend == "gloo":
                 # control-flow check of the N > 1 path on a box with fewer GPUs than ranks (ranks share
                 # devices; gloo carries the collectives): its numbers are not measurements
@@ -245,21 +282,16 @@ class Run:
         self.A = to_device(self.A_np, w["layout"], device)
         self.B = to_device(self.B_np, w["layout"], device)
         self.alg = F.load_alg(w["alg"])
+        # N > 1: the combine runs inside fmm_execute -- NCCL (lib, fmm_plan_create_dist) or the
+        # peer-memory pull-reduce over CUDA IPC (p2p, fmm_plan_create_p2p) -- or after it (torch)
         self.lib_comm = F.Comm.from_torch_distributed(device=device.index) if (world > 1 and args.combine == "lib") else None
+        self.p2p = F.P2P.from_torch_distributed(8 * P * N, device=device.index) if (world > 1 and args.combine == "p2p") else None
         self.plan = F.Plan(self.alg, P, Q, N, L, layout=w["layout"], strategy=args.strategy, cse=bool(args.cse),
                            shard_rank=rank, shard_count=world, fuse=bool(args.fuse), collapse=bool(args.collapse),
-                           comm=self.lib_comm, root="slabs" if args.output == "slabs" else 0, shard_mode=args.shard_mode)
-        # --combine p2p: the partial C lives in a peer-mapped buffer and one pull-reduce kernel per rank
-        # sums its slab over every rank's partial (fmm_p2p_*, CUDA IPC over NVLink, no NCCL data path)
-        self.p2p = self.out_slab = None
+                           comm=self.lib_comm, p2p=self.p2p, barrier=(self.dist.barrier if self.p2p else None),
+                           root="slabs" if args.output == "slabs" else 0, shard_mode=args.shard_mode)
         self.outer, self.inner = (P, N) if w["layout"] == "row" else (N, P)
-        if world > 1 and args.combine == "p2p":
-            self.p2p = F.P2P.from_torch_distributed(8 * P * N, device=device.index)
-            self.C = self.p2p.partial(P, N, w["layout"])
-            s0, s1 = F.dist_slab(P, N, w["layout"], world, rank)
-            self.out_slab = torch.empty(s1 - s0, self.inner, dtype=torch.float64, device=device)
-        else:
-            self.C = self.plan.new_output()
+        self.C = self.plan.new_output()
         self.st = self.plan.stats()
         self.fused = self.st.get("fused_launches", 0) > 0
         self.dmma_peak, self.dfma_peak = F.probe_fp64_peak()
@@ -267,27 +299,16 @@ class Run:
 
     def combine(self):
         from paper_1409_2908_b200.dist import combine_partials, scatter_partials
-        if self.lib_comm is not None:  # a distributed plan reduces inside fmm_execute
+        if self.world == 1 or self.args.combine != "torch":  # lib / p2p plans combine inside fmm_execute
             return
-        if self.p2p is not None:
-            self.stream.synchronize()
-            self.dist.barrier()  # every partial complete
-            self.p2p.reduce_slab(self.outer, self.inner, self.out_slab, stream=self.stream)
-            self.stream.synchronize()
-            self.dist.barrier()  # every slab read before the next step overwrites a partial
-        elif self.args.output == "slabs":
+        if self.args.output == "slabs":
             scatter_partials(self.C)
         else:
             combine_partials(self.C)
 
-    def step(self, evs=None):
-        if evs is None:
-            self.plan.execute(self.A, self.B, self.C, stream=self.stream)
-        else:
-            self.plan.execute_events(self.A, self.B, self.C, evs[:4], stream=self.stream)
+    def step(self):
+        self.plan.execute(self.A, self.B, self.C, stream=self.stream)
         self.combine()
-        if evs is not None:
-            evs[4].record(self.stream)  # after the combine: the comm share of a step (N > 1)
 
     def max_over_ranks(self, ms):
         if self.world > 1:
@@ -298,14 +319,12 @@ class Run:
 
     # ---- the timed region ----------------------------------------------------------------------
     def timed_steps(self):
-        import numpy as np
+        # the headline: whole-step events around K plain fmm_execute calls (the library's default
+        # path, CUDA-graph replay where the plan allows it), max over ranks
         torch, args, stream = self.torch, self.args, self.stream
         for _ in range(args.warmup):
             self.step()
         torch.cuda.synchronize()
-        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
-        for e in (x for row in evs for x in row):
-            e.record(stream)  # torch creates the underlying cudaEvent_t lazily, at the first record
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         clocks = ClockSampler(self.device.index)
         clocks.start()
@@ -315,7 +334,7 @@ class Run:
         torch.cuda.synchronize()
         t0.record(stream)
         for k in range(args.steps):
-            self.step(evs[k])
+            self.step()
         t1.record(stream)
         torch.cuda.synchronize()
         if self.world > 1:
@@ -323,10 +342,28 @@ class Run:
         self.clk = clocks.stop()
         self.ms_step = self.max_over_ranks(t0.elapsed_time(t1)) / args.steps
         self.value = self.flops / (self.ms_step * 1e-3) / 1e9
-        # per-phase device times measured on the launching stream during the timed region
-        ph = np.array([[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]),
-                        e[3].elapsed_time(e[4])] for e in evs])
-        self.form_ms, self.gemm_ms, self.asm_ms, self.comm_ms = [float(x) for x in ph.mean(axis=0)]
+
+    def phase_split(self, reps=3):
+        # per-phase device times from a separate pass (fmm_execute_timed: plain launches with an
+        # event after each; formation / leaf products / assembly / peel strips / exposed combine)
+        import numpy as np
+        ph = []
+        for _ in range(reps):
+            if self.world > 1 and self.args.combine == "torch":
+                _, t = self.plan.execute_timed(self.A, self.B, self.C, stream=self.stream)
+                e0 = self.torch.cuda.Event(enable_timing=True)
+                e1 = self.torch.cuda.Event(enable_timing=True)
+                e0.record(self.stream)
+                self.combine()
+                e1.record(self.stream)
+                e1.synchronize()
+                t["total_ms"] += e0.elapsed_time(e1)
+            else:
+                _, t = self.plan.execute_timed(self.A, self.B, self.C, stream=self.stream)
+            ph.append([t["formation_ms"], t["gemm_ms"], t["assembly_ms"], t["strips_ms"], t["total_ms"]])
+        m = np.array(ph).mean(axis=0)
+        self.form_ms, self.gemm_ms, self.asm_ms, self.strip_ms, tot = [float(x) for x in m]
+        self.comm_ms = max(0.0, tot - self.form_ms - self.gemm_ms - self.asm_ms - self.strip_ms) if self.world > 1 else 0.0
 
     def result_check(self):
         # after the timed steps C holds the last step's combined product: sampled rows of rank 0's
@@ -335,7 +372,7 @@ class Run:
         if self.rank != 0:
             return None
         torch, w, F, A, B, C = self.torch, self.w, self.F, self.A, self.B, self.C
-        if (self.args.output == "slabs" or self.p2p is not None) and self.world > 1:
+        if self.args.output == "slabs" and self.world > 1:
             lo, hi = F.dist_slab(self.P, self.N, w["layout"], self.world, 0)
         else:
             lo, hi = 0, (self.P if w["layout"] == "row" else self.N)
@@ -343,10 +380,7 @@ class Run:
             return None
         g = torch.Generator().manual_seed(7)
         idx = torch.randint(lo, max(lo + 1, hi), (min(64, max(hi - lo, 1)),), generator=g).to(self.device)
-        # rank 0's result: C itself, or (p2p) its reduced slab of C's storage rows
-        if self.p2p is not None:
-            got = lambda rows: self.out_slab[rows - lo]  # noqa: E731
-        elif w["layout"] == "row":
+        if w["layout"] == "row":
             got = lambda rows: C[rows]  # noqa: E731
         else:
             got = lambda cols: C[:, cols].t()  # noqa: E731
@@ -375,15 +409,11 @@ class Run:
             for _ in range(2):
                 plan_o.execute(self.A, self.B, self.C, stream=stream)
             nu = max(3, min(args.steps, 10))
-            evu = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(nu)]
-            for e in (x for row in evu for x in row):
-                e.record(stream)  # creates the underlying cudaEvent_t
-            torch.cuda.synchronize()
+            rows = []
             for k in range(nu):
-                plan_o.execute_events(self.A, self.B, self.C, evu[k], stream=stream)
-            torch.cuda.synchronize()
-            phu = np.array([[e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), e[2].elapsed_time(e[3]),
-                             e[0].elapsed_time(e[3])] for e in evu]).mean(axis=0)
+                _, t = plan_o.execute_timed(self.A, self.B, self.C, stream=stream)
+                rows.append([t["formation_ms"], t["gemm_ms"], t["assembly_ms"] + t["strips_ms"], t["total_ms"]])
+            phu = np.array(rows).mean(axis=0)
             other = {"fused_leaf_level": so.get("fused_launches", 0) > 0, "collapsed_levels": bool(so.get("collapsed", 0)),
                      "ms_per_step": float(phu[3]), "value": self.flops / (phu[3] * 1e-3) / 1e9,
                      "steps": nu, "phases_ms": {"formation": float(phu[0]), "leaf_level": float(phu[1]),
@@ -496,10 +526,6 @@ class Run:
         Ah, Bh, Ch = pinned(self.A_np, P, Q), pinned(self.B_np, Q, N), pinned(None, P, N)
         h2d = 8 * (P * Q + Q * N)
         d2h = 8 * P * N if rank == 0 else 0
-        slab_h = None
-        if self.p2p is not None and rank == 0:  # rank 0's result is its reduced slab
-            slab_h = torch.empty(tuple(self.out_slab.shape), dtype=torch.float64, pin_memory=True)
-            d2h = 8 * self.out_slab.numel()
 
         def e2e_step():
             if world == 1:
@@ -511,10 +537,7 @@ class Run:
                 self.plan.execute(self.A, self.B, self.C, stream=self.stream)
                 self.combine()
                 if rank == 0:
-                    if slab_h is not None:
-                        slab_h.copy_(self.out_slab, non_blocking=True)
-                    else:
-                        Ch.copy_(self.C, non_blocking=True)
+                    Ch.copy_(self.C, non_blocking=True)
                 torch.cuda.synchronize()
         e2e_step()
         self.plan.sync()
@@ -528,13 +551,14 @@ class Run:
         self.plan.sync()
         torch.cuda.synchronize()
         ms_e = self.max_over_ranks((time.perf_counter() - h0) * 1e3)
-        combine_name = ("peer-memory slab reduce" if self.p2p is not None else "NCCL reduce")
+        combine_name = {"p2p": "peer-memory combine inside fmm_execute", "lib": "NCCL reduce inside fmm_execute",
+                        "torch": "torch.distributed reduce"}[self.args.combine]
         return {"value": self.flops / (ms_e / n_e2e * 1e-3) / 1e9, "unit": "GFLOPS", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": ms_e / n_e2e, "steps": n_e2e,
                 "timing": "host wall clock over the steps, device synchronised on both sides",
                 "api": "fmm_execute_host_async x steps + fmm_sync (pinned host A, B, C; copy-in, compute and "
                        "copy-out of consecutive steps overlap)" if world == 1 else
-                f"H2D + fmm_execute + {combine_name} + D2H"}
+                f"H2D + fmm_execute ({combine_name}) + D2H"}
 
     def broadcast(self):
         # N > 1: the replication of A and B from rank 0, timed on its own after the
@@ -588,12 +612,91 @@ class Run:
         return cpu
 
     # ---- the whole run -------------------------------------------------------------------------
+    def sub_record(self, name, hbm, steps):
+        """One extra BASELINE config on this GPU (N = 1), its own inputs and plan (configured algorithm
+        and L, default options): effective GFLOPS over whole-step events (plain fmm_execute, graph replay
+        where it applies), the leaf-GEMM fraction of the DMMA peak, the addition kernels' fraction of
+        HBM (peel strips reported separately), cuBLAS on the same inputs, a sampled result check."""
+        import numpy as np
+        torch, F, stream = self.torch, self.F, self.stream
+        w = WORKLOADS[name]
+        P, Q, N, L = w["P"], w["Q"], w["N"], w["L"]
+        flops = 2.0 * P * Q * N
+        A_np, B_np = gen_inputs(w)
+        A, B = to_device(A_np, w["layout"], self.device), to_device(B_np, w["layout"], self.device)
+        del A_np, B_np
+        alg = F.load_alg(w["alg"])
+        plan = F.Plan(alg, P, Q, N, L, layout=w["layout"])
+        st = plan.stats()
+        C = plan.new_output()
+        for _ in range(3):
+            plan.execute(A, B, C, stream=stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            plan.execute(A, B, C, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        ph = np.array([[t["formation_ms"], t["gemm_ms"], t["assembly_ms"], t["strips_ms"], t["total_ms"]]
+                       for t in (plan.execute_timed(A, B, C, stream=stream)[1] for _ in range(2))]).mean(axis=0)
+        form_ms, gemm_ms, asm_ms, strip_ms, tot_ms = (float(x) for x in ph)
+        # sampled rows (columns) of C against cuBLAS on the same rows, then cuBLAS on the whole problem
+        g = torch.Generator().manual_seed(7)
+        outer = P if w["layout"] == "row" else N
+        idx = torch.randint(0, outer, (min(32, outer),), generator=g).to(self.device)
+        err = ((C[idx] - A[idx] @ B) if w["layout"] == "row" else (C[:, idx] - A @ B[:, idx])).abs().max().item()
+        tol = 1e-10 * torch.linalg.norm(A).item() * torch.linalg.norm(B).item()
+        cub = None
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        Cc = torch.matmul(A, B)
+        torch.cuda.synchronize()
+        for _ in range(2):
+            c0.record()
+            torch.matmul(A, B, out=Cc)
+            c1.record()
+            c1.synchronize()
+            cub = min(cub or 1e30, c0.elapsed_time(c1))
+        del Cc
+        add_bytes = st["add_bytes"] - st["fused_add_bytes"]
+        leaf_tf = st["leaf_flops"] / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                traffic = json.load(f).get(name, {}).get("grouped_dgemm_bytes_per_launch")
+        except OSError:
+            pass
+        rec = {"workload": w["desc"], "algorithm": w["alg"], "rank": alg.R, "levels": L, "P": P, "Q": Q, "N": N,
+               "layout": w["layout"], "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOPS", "ms_per_step": ms,
+               "steps": steps, "warmup": 3, "timing": "CUDA events around the steps (plain fmm_execute)",
+               "effective_frac_of_fp64_peak": flops / (ms * 1e-3) / 1e12 / self.dmma_peak,
+               "phases_ms": {"formation": form_ms, "leaf_gemm": gemm_ms, "assembly": asm_ms, "peel_strips": strip_ms,
+                             "sum_of_launches_timed": tot_ms},
+               "leaf_gemm": {"achieved_tflops": leaf_tf, "peak_tflops": self.dmma_peak,
+                             "frac": (leaf_tf / self.dmma_peak) if leaf_tf else None,
+                             "algorithmic_flops": st["leaf_flops"], "traffic_bytes_ncu": traffic},
+               "additions": {"algorithmic_bytes": add_bytes, "ms": form_ms + asm_ms,
+                             "gbs": add_bytes / ((form_ms + asm_ms) * 1e-3) / 1e9 if form_ms + asm_ms > 0 else None,
+                             "frac_of_hbm": (add_bytes / ((form_ms + asm_ms) * 1e-3) / 1e9 / hbm)
+                             if form_ms + asm_ms > 0 else None},
+               "cublas_dgemm_gflops_same_inputs": flops / (cub * 1e-3) / 1e9 if cub else None,
+               "vs_cublas": (cub / ms) if cub else None,
+               "gpu_launches_per_step": int(st["launches"]),
+               "collapsed_levels": bool(st.get("collapsed", 0)),
+               "result_check": {"sampled": int(idx.numel()), "max_abs_err": err, "tolerance": tol, "ok": bool(err <= tol)}}
+        del plan, A, B, C
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        return rec
+
     def go(self):
         args, w, st, world = self.args, self.w, None, self.world
         self.setup()
         st = self.st
         self.timed_steps()
         check = self.result_check()
+        self.phase_split()
         add_ms = self.form_ms + self.asm_ms
         peaks, peak_src = measured_peaks()
         hbm = float(peaks.get("hbm_gbs", HBM_FALLBACK))
@@ -608,19 +711,39 @@ class Run:
         bcast = self.broadcast()
         cpu = self.cpu_baseline()
         P, Q, N, ms_step, value = self.P, self.Q, self.N, self.ms_step, self.value
+        names = args.configs
+        if names == "auto":
+            names = "c1,c3,c4,c5t,c5" if (world == 1 and args.workload == "c2") else "none"
+        subs = None
+        if names != "none" and world == 1:
+            # the headline's buffers go first: c5's plan needs ~72 GB of the 180
+            del self.plan
+            self.A = self.B = self.C = None
+            self.torch.cuda.synchronize()
+            self.torch.cuda.empty_cache()
+            subs = {}
+            for nm in [x.strip() for x in names.split(",") if x.strip()]:
+                try:
+                    subs[nm] = self.sub_record(nm, hbm, max(3, min(args.steps, 10)))
+                except Exception as ex:  # noqa: BLE001  (a sub-record must not cost the headline line)
+                    subs[nm] = {"error": str(ex)[:300]}
+                    self.torch.cuda.synchronize()
+                    self.torch.cuda.empty_cache()
         if self.rank == 0:
             gb = lambda rows, cols: 8.0 * rows * cols / 1e9  # noqa: E731
             l2 = (f"inputs larger than L2 (A {gb(P, Q):.2f} GB, B {gb(Q, N):.2f} GB, C {gb(P, N):.2f} GB vs 126 MB); "
                   "no flush" if args.workload != "c1" else "small config: L2-resident")
+            where = "reduce to rank 0" if args.output == "root" else "slab-distributed output"
             if world == 1:
                 parallelism = "1 GPU"
-            elif self.p2p is not None:
-                parallelism = (f"{args.shard_mode}-level shards x{world} + peer-memory slab reduce "
-                               "(fmm_p2p: one pull kernel per rank over CUDA IPC)")
+            elif args.combine == "p2p":
+                parallelism = (f"{args.shard_mode}-level shards x{world} + peer-memory combine inside fmm_execute "
+                               f"(fmm_plan_create_p2p: one pull-reduce kernel per rank over CUDA IPC), {where}")
+            elif args.combine == "lib":
+                parallelism = (f"{args.shard_mode}-level shards x{world} + NCCL {where} inside fmm_execute "
+                               "(fmm_plan_create_dist; C reduced in row chunks that overlap the assembly where the plan allows)")
             else:
-                parallelism = (f"{args.shard_mode}-level shards x{world} + {args.dist_backend.upper()} "
-                               f"{'reduce to rank 0' if args.output == 'root' else 'slab reduce-scatter'} "
-                               f"({'fmm_execute' if self.lib_comm else 'torch.distributed'})")
+                parallelism = f"{args.shard_mode}-level shards x{world} + {args.dist_backend.upper()} {where} (torch.distributed)"
             line = {
                 "metric": METRIC, "value": value, "unit": "GFLOPS", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
@@ -635,12 +758,14 @@ class Run:
                 "roofline": roofline,
                 "clocks": self.clk,
                 "e2e": e2e,
-                "gpu_launches": int(st["launches"]) * args.steps,
+                "gpu_launches": (int(st["launches"]) + (1 if args.combine == "p2p" and world > 1 else 0)) * args.steps,
                 "cpu_baseline": cpu,
                 "phases_ms": {"formation_levels_below_L" if self.fused else "formation": self.form_ms,
                               "fused_leaf_level" if self.fused else "leaf_gemm": self.gemm_ms,
-                              "assembly_and_strips": self.asm_ms,
-                              "combine_reduce": self.comm_ms if world > 1 else 0.0},
+                              "assembly": self.asm_ms, "peel_strips": self.strip_ms,
+                              "combine_exposed": self.comm_ms if world > 1 else 0.0,
+                              "how": "fmm_execute_timed after the timed steps: plain launches, an event after each, "
+                                     "mean of 3"},
                 "input_broadcast": bcast,
                 "combine_algbw_gbs": (8.0 * P * N / (self.comm_ms * 1e-3) / 1e9) if world > 1 and self.comm_ms else None,
                 "additions": {"algorithmic_bytes_per_step": st["add_bytes"],
@@ -656,6 +781,7 @@ class Run:
                 "result_check": check,
                 "paper_effective_gflops": (2.0 * P * Q * N - P * N) / (ms_step * 1e-3) / 1e9,
                 "plan": {k: st[k] for k in ("gemm_flops", "add_flops", "add_bytes", "launches", "leaves")},
+                "configs": subs,
             }
             print(json.dumps(line), flush=True)
         if world > 1:

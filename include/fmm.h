@@ -112,10 +112,20 @@ typedef struct {
                                classical strips instead, if the cost model predicts that faster
                                (R7c; measured slower on c3, so off by default).  Exact
                                either way.  0 (default): the paper's minimal peeling of rows. */
+  int dist_chunks;          /* NCCL distributed plans (fmm_plan_create_dist): the launch that writes
+                               C (the level-1 assembly, C_k = sum_r w_kr M_r) runs as this
+                               many row chunks, and each chunk's rows of C are reduced on a library
+                               communication stream as soon as the chunk is written, so the
+                               reduce of chunk j overlaps the assembly of chunk j + 1.  Applies
+                               when that launch is one streaming assembly and the top level has no
+                               K peel (its rank-update strip would touch C after the assembly);
+                               otherwise, and with 0 or 1, one reduce of the whole C at the end.
+                               Default 4.  Ignored by single-GPU and peer-memory plans. */
 } fmm_plan_options;
 
 /* Fill *opt with the defaults: row-major, streaming, cse = 1, shard 0 of 1, no limit,
-   peel_align = 1, fuse_leaf_level = 0, collapse_levels = 1, cuda_graphs = 1, peel_tiles = 0. */
+   peel_align = 1, fuse_leaf_level = 0, collapse_levels = 1, cuda_graphs = 1, peel_tiles = 0,
+   dist_chunks = 4. */
 void fmm_plan_options_default(fmm_plan_options* opt);
 
 /* ---- algorithms ------------------------------------------------------------------------- */
@@ -205,6 +215,25 @@ fmm_status_t fmm_p2p_reduce_slab(fmm_p2p* p, int64_t outer, int64_t inner, int64
                                  void* stream);
 void fmm_p2p_destroy(fmm_p2p* p);
 
+/* A distributed plan whose combine runs over peer memory INSIDE fmm_execute (no NCCL in the data
+   path): rank p2p->rank of p2p->nranks computes its HYBRID leaf share (as fmm_plan_create_dist) into
+   the p2p object's partial buffer, which must hold 8 * P * Nc bytes; then, within the same
+   fmm_execute: the stream is synchronised, `barrier(barrier_ctx)` is called (every rank's partial is
+   complete), this rank pulls and sums its part of every rank's partial with one kernel
+   (fmm_p2p_reduce_slab's kernel, ranks in ascending order) into the caller's C with the caller's
+   ldc, the stream is synchronised again and `barrier` is called a second time (no partial is
+   overwritten while a peer still reads it).  So fmm_execute of such a plan is BLOCKING.
+   root >= 0: rank `root` receives the whole C and the other ranks leave their C untouched;
+   root = FMM_DIST_SLABS: every rank receives its fmm_dist_slab slab of C (rows of C when
+   row-major, columns when column-major), the rest of its C untouched.
+   `barrier` is a host barrier over the same ranks (e.g. torch.distributed.barrier through a
+   callback); it returns 0 on success, anything else fails the execute with FMM_E_NCCL.  The plan
+   keeps `p2p` (not owned; destroy the plan first).  CUDA graphs are not used for these plans. */
+typedef int (*fmm_barrier_fn)(void* ctx);
+fmm_status_t fmm_plan_create_p2p(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels,
+                                 const fmm_plan_options* opt, fmm_p2p* p2p, int root, fmm_barrier_fn barrier,
+                                 void* barrier_ctx, fmm_plan_t** out);
+
 /* The slab of C that rank `rank` of `nranks` holds after a FMM_DIST_SLABS execute: rows
    [*first, *last) of C (row-major) or columns [*first, *last) (column-major).  Host only. */
 fmm_status_t fmm_dist_slab(int64_t P, int64_t Nc, int layout, int nranks, int rank, int64_t* first, int64_t* last);
@@ -264,16 +293,19 @@ fmm_status_t fmm_fused_compile_check(const fmm_alg* alg, int layout, int cse, in
 fmm_status_t fmm_execute(fmm_plan_t* plan, const double* A, int64_t lda, const double* B, int64_t ldb,
                          double* C, int64_t ldc, void* stream);
 
-/* Same, timing the phases with CUDA events on `stream` (blocking: synchronises the stream).
-   ms[0] = formation kernels, ms[1] = leaf GEMM kernels, ms[2] = assembly kernels,
-   ms[3] = peel-strip GEMMs, ms[4] = total. */
+/* Same, timing every launch with CUDA events on `stream` (plain launches, no CUDA graph; blocking:
+   synchronises the stream) and summing the launch times by phase: ms[0] = formation kernels,
+   ms[1] = leaf products (GEMM, or the fused leaf-level launch), ms[2] = assembly kernels,
+   ms[3] = peel-strip GEMMs, ms[4] = total from the first launch to the end of the step, including a
+   distributed plan's combine (whose exposed part is ms[4] - ms[0..3]). */
 fmm_status_t fmm_execute_timed(fmm_plan_t* plan, const double* A, int64_t lda, const double* B,
                                int64_t ldb, double* C, int64_t ldc, void* stream, float ms[5]);
 
 /* Same as fmm_execute, additionally recording four caller-created cudaEvent_t on `stream`
    (non-blocking): events[0] before the first kernel, [1] after the formation kernels, [2] after
-   the leaf GEMM, [3] after the assembly and peel-strip kernels.  Used to time the phases inside
-   a timed region without synchronising. */
+   the leaf GEMM, [3] after the assembly and peel-strip kernels, before a distributed plan's
+   combine completes (an event the caller records after the call closes the combine phase).
+   Plain launches (no CUDA graph).  Used to time the phases without synchronising. */
 fmm_status_t fmm_execute_events(fmm_plan_t* plan, const double* A, int64_t lda, const double* B,
                                 int64_t ldb, double* C, int64_t ldc, void* stream, void* events[4]);
 

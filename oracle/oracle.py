@@ -245,9 +245,19 @@ def load_alg(path: str) -> Alg:
 # --------------------------------------------------------------------------------------------
 def build(force: bool = False) -> str:
     """Compile liboracle.so (gcc, OpenMP, no FMA contraction)."""
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-                               "-shared", "-o", _SO, _SRC])
+    import fcntl
+    stale = lambda: not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC)  # noqa: E731
+    if not (force or stale()):
+        return _SO
+    # concurrent builders (one per rank) take turns; the .so is replaced atomically
+    with open(_SO + ".lock", "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if force or stale():
+            tmp = f"{_SO}.{os.getpid()}.tmp"
+            subprocess.check_call(["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
+                                   "-shared", "-o", tmp, _SRC])
+            os.replace(tmp, _SO)
+        fcntl.flock(lk, fcntl.LOCK_UN)
     return _SO
 
 

@@ -20,9 +20,22 @@ static __int128 gcd128(__int128 a, __int128 b) {
   }
   return a;
 }
-static const __int128 kLimit = (__int128)1 << 100;  // guard well below overflow of products
+// Every numerator and denominator stays within +-2^100; each product or sum below is computed with
+// the overflow-checked builtins, so an algorithm whose coefficients outgrow 128 bits is refused
+// (FMM_E_UNSUPPORTED) instead of being misjudged by a wrapped intermediate.
+static const __int128 kLimit = (__int128)1 << 100;
 static void check_range(__int128 v) {
   if (v > kLimit || v < -kLimit) throw Error(FMM_E_UNSUPPORTED, "rational coefficient arithmetic overflow");
+}
+static __int128 mul_checked(__int128 a, __int128 b) {
+  __int128 r;
+  if (__builtin_mul_overflow(a, b, &r)) throw Error(FMM_E_UNSUPPORTED, "rational coefficient arithmetic overflow");
+  return r;
+}
+static __int128 add_checked(__int128 a, __int128 b) {
+  __int128 r;
+  if (__builtin_add_overflow(a, b, &r)) throw Error(FMM_E_UNSUPPORTED, "rational coefficient arithmetic overflow");
+  return r;
 }
 
 Rat rat_make(__int128 n, __int128 d) {
@@ -39,12 +52,12 @@ Rat rat_add(Rat a, Rat b) {
   if (a.n == 0) return b;
   if (b.n == 0) return a;
   __int128 g = gcd128(a.d, b.d);
-  return rat_make(a.n * (b.d / g) + b.n * (a.d / g), a.d / g * b.d);
+  return rat_make(add_checked(mul_checked(a.n, b.d / g), mul_checked(b.n, a.d / g)), mul_checked(a.d / g, b.d));
 }
 Rat rat_mul(Rat a, Rat b) {
   if (a.n == 0 || b.n == 0) return Rat{0, 1};
   __int128 g1 = gcd128(a.n, b.d), g2 = gcd128(b.n, a.d);
-  return rat_make((a.n / g1) * (b.n / g2), (a.d / g2) * (b.d / g1));
+  return rat_make(mul_checked(a.n / g1, b.n / g2), mul_checked(a.d / g2, b.d / g1));
 }
 
 // T_ijk of the <M,K,N> matmul tensor from the index conditions of P:415-421 (0-based).

@@ -7,6 +7,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "fmm_internal.h"
@@ -87,6 +88,34 @@ void dist_reduce_slabs(void* comm, int nranks, double* C, long long outer, long 
   }
   const ncclResult_t e = api.group_end();
   check(first, "ncclReduce (slab)");
+  check(e, "ncclGroupEnd");
+}
+
+void dist_reduce_rows(void* comm, int nranks, double* C, long long rows, long long inner,
+                      const std::vector<std::pair<long long, long long>>& ranges, int root, cudaStream_t stream) {
+  const NcclApi& api = nccl();
+  check(api.group_start(), "ncclGroupStart");
+  ncclResult_t first = ncclSuccess;
+  auto one = [&](long long r0, long long r1, int to) {
+    if (r1 <= r0 || inner <= 0) return;
+    double* p = C + r0 * inner;
+    const ncclResult_t r = api.reduce(p, p, (size_t)((r1 - r0) * inner), ncclDouble, ncclSum, to,
+                                      static_cast<ncclComm_t>(comm), stream);
+    if (first == ncclSuccess) first = r;
+  };
+  for (const auto& rg : ranges) {
+    if (root != FMM_DIST_SLABS) {
+      one(rg.first, rg.second, root);
+      continue;
+    }
+    for (int g = 0; g < nranks; ++g) {
+      long long s0, s1;
+      dist_slab_range(rows, nranks, g, &s0, &s1);
+      one(std::max(rg.first, s0), std::min(rg.second, s1), g);
+    }
+  }
+  const ncclResult_t e = api.group_end();
+  check(first, "ncclReduce (rows)");
   check(e, "ncclGroupEnd");
 }
 }  // namespace fmm

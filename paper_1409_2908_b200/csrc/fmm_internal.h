@@ -70,6 +70,18 @@ namespace fmm {
 void dist_reduce(void* comm, double* C, size_t count, int root, cudaStream_t stream);
 void dist_reduce_slabs(void* comm, int nranks, double* C, long long outer, long long inner, cudaStream_t stream);
 void dist_slab_range(long long outer, int nranks, int rank, long long* r0, long long* r1);
+// grouped in-place NCCL reduces of row ranges [first, second) of a contiguous rows x inner C: each
+// range to `root`, or (root = FMM_DIST_SLABS) each range's intersection with slab g to rank g
+void dist_reduce_rows(void* comm, int nranks, double* C, long long rows, long long inner,
+                      const std::vector<std::pair<long long, long long>>& ranges, int root, cudaStream_t stream);
+// the peer-memory combine (fmm_p2p.cu)
+void p2p_reduce_rows(const fmm_p2p* p, long long outer, long long r0, long long r1, long long inner, long long ld,
+                     double* out, long long ldo, cudaStream_t s);
+int p2p_nranks(const fmm_p2p* p);
+int p2p_rank(const fmm_p2p* p);
+int p2p_device(const fmm_p2p* p);
+double* p2p_local(const fmm_p2p* p);
+size_t p2p_bytes(const fmm_p2p* p);
 void* comm_handle(const fmm_comm* c);
 int comm_nranks(const fmm_comm* c);
 int comm_rank(const fmm_comm* c);

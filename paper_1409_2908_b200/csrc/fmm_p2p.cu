@@ -60,6 +60,42 @@ __global__ void __launch_bounds__(256) p2p_reduce(PeerPtrs src, int G, long long
 }  // namespace
 }  // namespace fmm
 
+namespace fmm {
+// rows [r0, r1) of the outer x inner partials (leading dimension ld) summed over every rank, ranks
+// ascending, into out (row r0 at out, then out + ldo per row)
+void p2p_reduce_rows(const fmm_p2p* p, long long outer, long long r0, long long r1, long long inner, long long ld,
+                     double* out, long long ldo, cudaStream_t s) {
+  if (outer > 1 && ld < inner) throw Error(FMM_E_SHAPE, "ld < inner");
+  if ((size_t)((outer > 0 ? (outer - 1) * ld : 0) + inner) * 8 > p->bytes)
+    throw Error(FMM_E_SHAPE, "the partial does not fit the p2p buffer");
+  for (int g = 0; g < p->nranks; ++g)
+    if (!p->peer[g]) throw Error(FMM_E_INVALID_ARG, "fmm_p2p_open has not mapped every rank");
+  const long long rows = r1 - r0;
+  if (rows <= 0 || inner <= 0) return;
+  if (!out) throw Error(FMM_E_INVALID_ARG, "null output");
+  if (rows > 1 && ldo < inner) throw Error(FMM_E_SHAPE, "ldo < inner");
+  FMM_CUDA(cudaSetDevice(p->device));
+  PeerPtrs src{};
+  for (int g = 0; g < p->nranks; ++g) src.p[g] = p->peer[g];
+  bool vec2 = inner % 2 == 0 && ld % 2 == 0 && ldo % 2 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  for (int g = 0; g < p->nranks; ++g) vec2 &= (reinterpret_cast<uintptr_t>(p->peer[g]) & 15) == 0;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+  const long long work = rows * (vec2 ? inner / 2 : inner);
+  const int grid = (int)std::min<long long>((work + 255) / 256, (long long)sms * 8);
+  if (vec2)
+    p2p_reduce<true><<<grid, 256, 0, s>>>(src, p->nranks, r0, rows, inner, ld, out, ldo);
+  else
+    p2p_reduce<false><<<grid, 256, 0, s>>>(src, p->nranks, r0, rows, inner, ld, out, ldo);
+  FMM_CUDA(cudaGetLastError());
+}
+int p2p_nranks(const fmm_p2p* p) { return p->nranks; }
+int p2p_rank(const fmm_p2p* p) { return p->rank; }
+int p2p_device(const fmm_p2p* p) { return p->device; }
+double* p2p_local(const fmm_p2p* p) { return p->local; }
+size_t p2p_bytes(const fmm_p2p* p) { return p->bytes; }
+}  // namespace fmm
+
 using namespace fmm;
 
 extern "C" {
@@ -124,32 +160,9 @@ fmm_status_t fmm_p2p_reduce_slab(fmm_p2p* p, int64_t outer, int64_t inner, int64
   FMM_API_BEGIN
   if (!p) throw Error(FMM_E_INVALID_ARG, "null argument");
   if (outer < 0 || inner < 0) throw Error(FMM_E_SHAPE, "negative dimension");
-  if (outer > 1 && ld < inner) throw Error(FMM_E_SHAPE, "ld < inner");
-  if ((size_t)((outer > 0 ? (outer - 1) * ld : 0) + inner) * 8 > p->bytes)
-    throw Error(FMM_E_SHAPE, "the partial does not fit the p2p buffer");
-  for (int g = 0; g < p->nranks; ++g)
-    if (!p->peer[g]) throw Error(FMM_E_INVALID_ARG, "fmm_p2p_open has not mapped every rank");
   long long r0, r1;
   dist_slab_range(outer, p->nranks, p->rank, &r0, &r1);
-  const long long rows = r1 - r0;
-  if (rows <= 0 || inner <= 0) return FMM_OK;
-  if (!out) throw Error(FMM_E_INVALID_ARG, "null output");
-  if (rows > 1 && ldo < inner) throw Error(FMM_E_SHAPE, "ldo < inner");
-  FMM_CUDA(cudaSetDevice(p->device));
-  PeerPtrs src{};
-  for (int g = 0; g < p->nranks; ++g) src.p[g] = p->peer[g];
-  bool vec2 = inner % 2 == 0 && ld % 2 == 0 && ldo % 2 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-  for (int g = 0; g < p->nranks; ++g) vec2 &= (reinterpret_cast<uintptr_t>(p->peer[g]) & 15) == 0;
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
-  const long long work = rows * (vec2 ? inner / 2 : inner);
-  const int grid = (int)std::min<long long>((work + 255) / 256, (long long)sms * 8);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (vec2)
-    p2p_reduce<true><<<grid, 256, 0, s>>>(src, p->nranks, r0, rows, inner, ld, out, ldo);
-  else
-    p2p_reduce<false><<<grid, 256, 0, s>>>(src, p->nranks, r0, rows, inner, ld, out, ldo);
-  FMM_CUDA(cudaGetLastError());
+  p2p_reduce_rows(p, outer, r0, r1, inner, ld, out, ldo, static_cast<cudaStream_t>(stream));
   return FMM_OK;
   FMM_API_END
 }

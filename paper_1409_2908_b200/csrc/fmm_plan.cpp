@@ -18,6 +18,7 @@
 // Sharding: HYBRID arithmetic over GPUs: the first R^L - (R^L mod G) leaves are split
 // evenly and contiguously, the remaining R^L mod G leaves are split by rows over all G.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing unless a tool is attached
 
 #include <algorithm>
 #include <array>
@@ -46,7 +47,7 @@ struct Dims {
 using PlanDims = Dims;
 
 struct Launch {
-  enum Kind { FORM_A, FORM_B, GEMM, ASSEMBLE, STRIPS, SKINNY, FUSED } kind;
+  enum Kind { FORM_A, FORM_B, GEMM, ASSEMBLE, STRIPS, SKINNY, FUSED, REDUCE /* no kernel: reduce_rows only */ } kind;
   int level = 0;
   size_t table_off = 0;  // byte offset in the device table buffer
   int count = 0;         // nodes / tasks
@@ -63,6 +64,10 @@ struct Launch {
   double elem_reads = 0, elem_writes = 0, elem_adds = 0;  // totals over the launch (elements)
   double flops = 0, gemm_bytes = 0;
   std::vector<int> node_ids;  // FORM / ASSEMBLE: parent node index of every table entry
+  int nin = 0, nout = 0;      // ASSEMBLE: inputs / outputs per table entry
+  // NCCL distributed plans with dist_chunks: rows [first, second) of C (plan orientation) to reduce
+  // on the communication stream once this launch is done (a chunk of the assembly that writes C)
+  std::vector<std::pair<long long, long long>> reduce_rows;
   // FUSED: byte offsets of the program / job / target tables, and their sizes
   size_t jobs_off = 0, targets_off = 0;
   int njobs0 = 0, njobs = 0, np = 0, nprogs = 0;
@@ -81,6 +86,12 @@ struct fmm_plan_s {
   int device = 0;
   void* dist_comm = nullptr;  // distributed plan: NCCL communicator (not owned) and root
   int dist_root = 0;
+  bool dist_chunked = false;  // the last build split the C-writing assembly into reduced row chunks
+  cudaStream_t s_comm = nullptr;     // NCCL chunk reduces run here, overlapping the next chunk
+  std::vector<cudaEvent_t> ev_chunk;  // one per chunk launch, and the end of the comm stream's work
+  fmm_p2p* p2p = nullptr;     // peer-memory distributed plan (fmm_plan_create_p2p): partial buffer owner
+  fmm_barrier_fn barrier = nullptr;
+  void* barrier_ctx = nullptr;
   fmm_plan_options opt{};
   bool colmajor = false;
   std::unique_ptr<fmm_alg> alg_t;  // Prop. 1 transpose (column-major plans)
@@ -143,6 +154,11 @@ struct fmm_plan_s {
   unsigned long long use_clock = 0;
   cudaEvent_t upload_done = nullptr;
   cudaEvent_t ev[8] = {};
+  // fmm_execute_timed: an event after every launch, and the phase of each launch (0 formation,
+  // 1 leaf products, 2 assembly, 3 peel strips, 4 combine)
+  bool profile_launches = false;
+  std::vector<cudaEvent_t> ev_l;
+  std::vector<int> ev_l_phase;
 
   // host-execute staging: two buffer sets, copy-in / copy-out streams, ordering events
   double *sA[2] = {nullptr, nullptr}, *sB[2] = {nullptr, nullptr}, *sC[2] = {nullptr, nullptr};
@@ -164,6 +180,9 @@ struct fmm_plan_s {
       if (sl.gexec) cudaGraphExecDestroy(sl.gexec);
     }
     if (s_cap) cudaStreamDestroy(s_cap);
+    if (s_comm) cudaStreamDestroy(s_comm);
+    for (auto& e : ev_chunk)
+      if (e) cudaEventDestroy(e);
     if (h_pinned) cudaFreeHost(h_pinned);
     for (int b = 0; b < 2; ++b) {
       if (sA[b]) cudaFree(sA[b]);
@@ -176,6 +195,8 @@ struct fmm_plan_s {
     if (s_out) cudaStreamDestroy(s_out);
     if (upload_done) cudaEventDestroy(upload_done);
     for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : ev_l)
       if (e) cudaEventDestroy(e);
     cudaSetDevice(cur);
   }
@@ -374,6 +395,9 @@ struct fmm_plan_s {
   // over the level-(L-2) nodes.
   void emit_two_level_formation(bool lazy_kernels);
   void emit_two_level_assembly(bool lazy_kernels);
+  // NCCL distributed plans: split the assembly launch that writes C into dist_chunks row chunks,
+  // each followed by the reduce of its rows of C (run() issues it on s_comm)
+  void chunk_final_assembly();
 };
 
 View fmm_plan_s::opA(int l, long long z, const View& root) const {
@@ -670,6 +694,8 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
         ln.node_ids = node_ids;
         ln.kind = Launch::ASSEMBLE;
         ln.level = l;
+        ln.nin = nin;
+        ln.nout = nout;
         ln.count = count;
         ln.rows = d.P;
         ln.cols = d.N;
@@ -738,6 +764,76 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
     emit_gemm(Launch::STRIPS, l - 1, tasks);
   }
   fuse_leaf_level(lazy_kernels);
+  chunk_final_assembly();
+}
+
+void fmm_plan_s::chunk_final_assembly() {
+  dist_chunked = false;
+  if (!dist_comm || opt.dist_chunks <= 1 || L < 1) return;
+  int ia = -1, nasm = 0;
+  for (int q = 0; q < (int)launches.size(); ++q)
+    if (launches[q].kind == Launch::ASSEMBLE && launches[q].level == 1) ia = q, ++nasm;
+  // one streaming assembly writes C (memory-CSE strategies emit several launches), over the root only
+  if (ia < 0 || nasm != 1 || launches[ia].count != 1 || launches[ia].nin <= 0) return;
+  const Dims& d0 = dims[0];
+  if (d0.Q1 < d0.Q) return;  // strip (a) would add into C's core after the assembly
+  for (int q = ia + 1; q < (int)launches.size(); ++q)  // only level-0 strips follow it
+    if (!((launches[q].kind == Launch::STRIPS || launches[q].kind == Launch::SKINNY) && launches[q].level == 0)) return;
+  const Launch base = launches[ia];
+  const long long rows = base.rows;
+  const int nch = (int)std::min<long long>(opt.dist_chunks, std::max<long long>(rows, 1));
+  const size_t nb = lincomb_node_bytes(base.nin, base.nout);
+  std::vector<char> entry(h_tab.begin() + base.table_off, h_tab.begin() + base.table_off + nb);
+  auto** in0 = reinterpret_cast<const double**>(entry.data());
+  auto** out0 = reinterpret_cast<double**>(entry.data() + sizeof(void*) * base.nin);
+  const auto* lds0 = reinterpret_cast<const long long*>(entry.data() + sizeof(void*) * (base.nin + base.nout));
+  // first row of C (plan orientation) of every output block
+  std::vector<long long> starts;
+  for (int k = 0; k < base.nout; ++k) starts.push_back((long long)(out0[k] - cur_C) / std::max<long long>(cur_ldc, 1));
+  std::sort(starts.begin(), starts.end());
+  starts.erase(std::unique(starts.begin(), starts.end()), starts.end());
+  std::vector<Launch> chunks;
+  std::vector<std::pair<long long, long long>> covered;
+  for (int j = 0; j < nch; ++j) {
+    const long long r0 = rows * j / nch, r1 = rows * (j + 1) / nch;
+    if (r1 <= r0) continue;
+    std::vector<char> e = entry;
+    auto** in = reinterpret_cast<const double**>(e.data());
+    auto** out = reinterpret_cast<double**>(e.data() + sizeof(void*) * base.nin);
+    for (int i = 0; i < base.nin; ++i)
+      if (in0[i]) in[i] = in0[i] + r0 * lds0[0];
+    for (int k = 0; k < base.nout; ++k) out[k] = out0[k] + r0 * lds0[1];
+    Launch ln = base;
+    ln.rows = r1 - r0;
+    ln.table_off = push_tab(e.data(), e.size());
+    const double f = (double)(r1 - r0) / (double)rows;
+    ln.elem_adds = base.elem_adds * f, ln.elem_reads = base.elem_reads * f, ln.elem_writes = base.elem_writes * f;
+    ln.reduce_rows.clear();
+    for (long long s0 : starts) {
+      if (!ln.reduce_rows.empty() && ln.reduce_rows.back().second == s0 + r0) ln.reduce_rows.back().second = s0 + r1;
+      else ln.reduce_rows.push_back({s0 + r0, s0 + r1});
+      covered.push_back({s0 + r0, s0 + r1});
+    }
+    chunks.push_back(ln);
+  }
+  // rows no chunk covers (the bottom peel strip (b)) are reduced once everything is written
+  std::sort(covered.begin(), covered.end());
+  Launch tail;
+  tail.kind = Launch::REDUCE;
+  tail.level = 0;
+  long long at = 0;
+  for (const auto& c : covered) {
+    if (c.first > at) tail.reduce_rows.push_back({at, c.first});
+    at = std::max(at, c.second);
+  }
+  if (at < d0.P) tail.reduce_rows.push_back({at, d0.P});
+  // level-0 strips (b) and (c) write C outside the assembled core: launch them first
+  std::vector<Launch> out(launches.begin(), launches.begin() + ia);
+  out.insert(out.end(), launches.begin() + ia + 1, launches.end());
+  out.insert(out.end(), chunks.begin(), chunks.end());
+  if (!tail.reduce_rows.empty()) out.push_back(tail);
+  launches.swap(out);
+  dist_chunked = true;
 }
 
 // The fused leaf level (fmm_gemm_tma.cu, FUSED kernel).  Jobs: formation (F) of the level-L S / T
@@ -1095,6 +1191,8 @@ void fmm_plan_s::emit_two_level_assembly(bool lazy_kernels) {
   Launch ln;
   ln.kind = Launch::ASSEMBLE;
   ln.level = L - 1;
+  ln.nin = nin;
+  ln.nout = nout;
   ln.count = count;
   ln.rows = d2.P;
   ln.cols = d2.N;
@@ -1298,6 +1396,16 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
     if (overlap(sc, sa) || overlap(sc, sb)) throw Error(FMM_E_INVALID_ARG, "C must not overlap A or B");
   }
   FMM_CUDA(cudaSetDevice(p->device));
+  // a peer-memory plan computes its partial product into the p2p buffer (contiguous, plan
+  // orientation) and sums the ranks' partials into the caller's C at the end
+  double* const userC = C;
+  const long long user_ldc = ldc;
+  const long long crows = p->colmajor ? p->userN : p->userP, ccols = p->colmajor ? p->userP : p->userN;
+  if (p->p2p) {
+    if ((size_t)(crows * ccols) * 8 > p2p_bytes(p->p2p)) throw Error(FMM_E_SHAPE, "the p2p partial buffer is smaller than C");
+    C = p2p_local(p->p2p);
+    ldc = std::max<long long>(ccols, 1);
+  }
   // row-major orientation: for column-major, C^T = B^T A^T (Prop. 1)
   const double* a = p->colmajor ? B : A;
   const double* b = p->colmajor ? A : B;
@@ -1333,7 +1441,7 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
   // CUDA-graph replay of a cached slot (option cuda_graphs): captured on the slot's second use,
   // on a private stream, then launched on the caller's stream (kernels only: the table upload
   // happened when the slot was built; fused launches need their counter reset and stay plain)
-  bool graphable = p->opt.cuda_graphs && !timed && !p->dist_comm;
+  bool graphable = p->opt.cuda_graphs && !timed && !p->dist_comm && !p->p2p;
   for (const Launch& ln : sl->launches) graphable &= ln.kind != Launch::FUSED;
   if (graphable && sl->gexec) {
     FMM_CUDA(cudaGraphLaunch(sl->gexec, stream));
@@ -1358,11 +1466,60 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
       cudaGetLastError();
     }
   } guard{ls, capture};
+  // NCCL plans with chunked assembly: a chunk's rows of C are reduced on s_comm right after it
+  const bool chunked = p->dist_comm && ccols > 0 && crows > 0 &&
+                       std::any_of(sl->launches.begin(), sl->launches.end(), [](const Launch& x) { return !x.reduce_rows.empty(); });
+  int nchunk_ev = 0;
+  if (chunked) {
+    if (crows > 1 && ldc != ccols) throw Error(FMM_E_UNSUPPORTED, "a distributed plan needs a contiguous C");
+    if (!p->s_comm) FMM_CUDA(cudaStreamCreateWithFlags(&p->s_comm, cudaStreamNonBlocking));
+  }
+  int nl = 0;  // profile_launches: events recorded so far
+  auto mark = [&](int phase_of_launch) {
+    if (!p->profile_launches) return;
+    if ((int)p->ev_l.size() <= nl) {
+      cudaEvent_t e;
+      FMM_CUDA(cudaEventCreate(&e));
+      p->ev_l.push_back(e);
+      p->ev_l_phase.push_back(0);
+    }
+    p->ev_l_phase[nl] = phase_of_launch;
+    FMM_CUDA(cudaEventRecord(p->ev_l[nl++], ls));
+  };
+  mark(-1);  // start
+  auto reduce_after = [&](const Launch& ln) {
+    if (!chunked || ln.reduce_rows.empty()) return;
+    if ((int)p->ev_chunk.size() <= nchunk_ev) {
+      cudaEvent_t e;
+      FMM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      p->ev_chunk.push_back(e);
+    }
+    cudaEvent_t e = p->ev_chunk[nchunk_ev++];
+    FMM_CUDA(cudaEventRecord(e, ls));
+    FMM_CUDA(cudaStreamWaitEvent(p->s_comm, e, 0));
+    dist_reduce_rows(p->dist_comm, p->opt.shard_count, C, crows, ccols, ln.reduce_rows, p->dist_root, p->s_comm);
+  };
+  // NVTX: one range per launch, named by phase and recursion level (profiling)
+  static const char* const kNvtx[] = {"fmm form A", "fmm form B", "fmm leaf gemm", "fmm assemble", "fmm strips",
+                                      "fmm thin", "fmm fused leaf level", "fmm reduce"};
+  char nvtx_name[64];
+  nvtxRangePushA(p->dist_comm || p->p2p ? "fmm_execute (distributed)" : "fmm_execute");
+  struct NvtxPop {
+    ~NvtxPop() { nvtxRangePop(); }
+  } nvtx_outer;
   for (const Launch& ln : sl->launches) {
+    std::snprintf(nvtx_name, sizeof nvtx_name, "%s L%d", kNvtx[(int)ln.kind], ln.level);
+    nvtxRangePushA(nvtx_name);
+    NvtxPop nvtx_launch;
+    if (ln.kind == Launch::REDUCE) {
+      reduce_after(ln);
+      continue;
+    }
     const int ph = (ln.kind == Launch::FORM_A || ln.kind == Launch::FORM_B) ? 0
                    : (ln.kind == Launch::GEMM || ln.kind == Launch::FUSED || (ln.kind == Launch::SKINNY && ln.level == p->L))
                        ? 1
                        : 2;
+    const int prof_phase = ph < 2 ? ph : ln.kind == Launch::ASSEMBLE ? 2 : 3;
     if (ln.kind == Launch::SKINNY) {
       const int* ids = reinterpret_cast<const int*>(d_tab + ln.ids_off);
       if (timed && ph != phase) {
@@ -1371,6 +1528,7 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
       }
       skinny_launch(reinterpret_cast<const GemmTask*>(d_tab + ln.table_off), ids, ln.nrow, ln.max_n, ids + ln.nrow,
                     ln.ncol, ln.max_m, ls);
+      mark(prof_phase);
       continue;
     }
     if (timed && ph != phase) {
@@ -1385,6 +1543,7 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
         lincomb_launch(*ln.kern, tab, ln.count, ln.rows, ln.cols, ls);
         break;
       case Launch::SKINNY:
+      case Launch::REDUCE:
         break;
       case Launch::FUSED: {
         FusedArgs fa{};
@@ -1416,6 +1575,8 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
           gemm_launch(reinterpret_cast<const GemmTask*>(tab), ln.count, ln.tiles, ln.aligned16, ls);
         break;
     }
+    mark(prof_phase);
+    reduce_after(ln);
   }
   if (capture) {
     cudaGraph_t g = nullptr;
@@ -1427,17 +1588,53 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
     FMM_CUDA(cudaGraphLaunch(sl->gexec, stream));
   }
   ++sl->runs;
-  if (p->dist_comm) {  // a7: the partial products of all ranks summed on the root
-    const long long rows = p->colmajor ? p->userN : p->userP, cols = p->colmajor ? p->userP : p->userN;
+  if (timed) {  // phase [3] ends with the last kernel; a combine after it is the caller's next phase
+    for (int q = phase + 1; q <= 3; ++q) FMM_CUDA(cudaEventRecord(evs[q], stream));
+    phase = 3;
+  }
+  if (chunked) {  // the caller's stream continues once the last chunk reduce is done
+    if ((int)p->ev_chunk.size() <= nchunk_ev) {
+      cudaEvent_t e;
+      FMM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      p->ev_chunk.push_back(e);
+    }
+    cudaEvent_t e = p->ev_chunk[nchunk_ev];
+    FMM_CUDA(cudaEventRecord(e, p->s_comm));
+    FMM_CUDA(cudaStreamWaitEvent(stream, e, 0));
+  } else if (p->dist_comm) {  // a7: the partial products of all ranks summed on the root
+    const long long rows = crows, cols = ccols;
     if (rows > 1 && ldc != cols) throw Error(FMM_E_UNSUPPORTED, "a distributed plan needs a contiguous C");
     if (rows * cols > 0) {
       if (p->dist_root == FMM_DIST_SLABS) dist_reduce_slabs(p->dist_comm, p->opt.shard_count, C, rows, cols, stream);
       else dist_reduce(p->dist_comm, C, (size_t)rows * cols, p->dist_root, stream);
     }
   }
-  if (timed) {
-    for (int q = phase + 1; q <= 3; ++q) FMM_CUDA(cudaEventRecord(evs[q], stream));
+  if (p->p2p) {  // a7 over peer memory: every partial complete -> pull-reduce -> every read done
+    auto bar = [&]() {
+      if (p->barrier(p->barrier_ctx) != 0) throw Error(FMM_E_NCCL, "the peer-memory plan's host barrier failed");
+    };
+    FMM_CUDA(cudaStreamSynchronize(stream));
+    bar();
+    const int g = p2p_rank(p->p2p), G = p2p_nranks(p->p2p);
+    long long r0 = 0, r1 = 0;
+    if (p->dist_root == FMM_DIST_SLABS) dist_slab_range(crows, G, g, &r0, &r1);
+    else if (p->dist_root == g) r0 = 0, r1 = crows;
+    if (r1 > r0 && ccols > 0)
+      p2p_reduce_rows(p->p2p, crows, r0, r1, ccols, ldc, userC + r0 * user_ldc, user_ldc, stream);
+    FMM_CUDA(cudaStreamSynchronize(stream));
+    bar();
   }
+  if (p->profile_launches && (p->dist_comm || p->p2p)) {
+    if ((int)p->ev_l.size() <= nl) {
+      cudaEvent_t e;
+      FMM_CUDA(cudaEventCreate(&e));
+      p->ev_l.push_back(e);
+      p->ev_l_phase.push_back(0);
+    }
+    p->ev_l_phase[nl] = 4;
+    FMM_CUDA(cudaEventRecord(p->ev_l[nl++], stream));
+  }
+  if (p->profile_launches) p->ev_l_phase.resize(nl);
 }
 
 }  // namespace
@@ -1458,6 +1655,7 @@ void fmm_plan_options_default(fmm_plan_options* o) {
   o->collapse_levels = 1;
   o->cuda_graphs = 1;
   o->peel_tiles = 0;  // measured: c3 12.60 -> 12.78 ms, c5 258.0 -> 257.3 (R7c)
+  o->dist_chunks = 4;
 }
 
 fmm_status_t fmm_plan_create(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels,
@@ -1484,9 +1682,34 @@ fmm_status_t fmm_plan_create_dist(const fmm_alg* alg, int64_t P, int64_t Q, int6
   o.shard_rank = comm_rank(comm);
   o.shard_count = comm_nranks(comm);
   std::unique_ptr<fmm_plan_t> p(new fmm_plan_t);
-  plan_init(p.get(), alg, P, Q, Nc, levels, &o, comm_device(comm));
-  p->dist_comm = comm_handle(comm);
+  p->dist_comm = comm_handle(comm);  // before plan_init: its dry build sizes the chunk tables
   p->dist_root = root;
+  plan_init(p.get(), alg, P, Q, Nc, levels, &o, comm_device(comm));
+  *out = p.release();
+  return FMM_OK;
+  FMM_API_END
+}
+
+fmm_status_t fmm_plan_create_p2p(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels,
+                                 const fmm_plan_options* opt, fmm_p2p* p2p, int root, fmm_barrier_fn barrier,
+                                 void* barrier_ctx, fmm_plan_t** out) {
+  FMM_API_BEGIN
+  if (!out || !p2p || !barrier) throw Error(FMM_E_INVALID_ARG, "null argument");
+  if (root != FMM_DIST_SLABS && (root < 0 || root >= p2p_nranks(p2p))) throw Error(FMM_E_INVALID_ARG, "bad root");
+  if (P < 0 || Nc < 0) throw Error(FMM_E_SHAPE, "negative dimension");
+  if ((size_t)P * (size_t)Nc * 8 > p2p_bytes(p2p)) throw Error(FMM_E_SHAPE, "the p2p partial buffer is smaller than P x Nc doubles");
+  *out = nullptr;
+  fmm_plan_options o;
+  if (opt) o = *opt;
+  else fmm_plan_options_default(&o);
+  o.shard_rank = p2p_rank(p2p);
+  o.shard_count = p2p_nranks(p2p);
+  std::unique_ptr<fmm_plan_t> p(new fmm_plan_t);
+  p->p2p = p2p;
+  p->barrier = barrier;
+  p->barrier_ctx = barrier_ctx;
+  p->dist_root = root;
+  plan_init(p.get(), alg, P, Q, Nc, levels, &o, p2p_device(p2p));
   *out = p.release();
   return FMM_OK;
   FMM_API_END
@@ -1529,7 +1752,8 @@ fmm_status_t fmm_plan_stats(const fmm_plan_t* p, double out[8]) {
     s[1] += ln.elem_adds;
     s[2] += 8.0 * (ln.elem_reads + ln.elem_writes);
     s[3] += ln.gemm_bytes;
-    s[4] += (ln.kind == Launch::FORM_A || ln.kind == Launch::FORM_B || ln.kind == Launch::ASSEMBLE) && ln.kern
+    s[4] += ln.kind == Launch::REDUCE ? 0
+            : (ln.kind == Launch::FORM_A || ln.kind == Launch::FORM_B || ln.kind == Launch::ASSEMBLE) && ln.kern
                 ? lincomb_steps(*ln.kern)  // pairwise: one launch per chain position
                 : 1;
     if (ln.kind == Launch::GEMM || ln.kind == Launch::FUSED || (ln.kind == Launch::SKINNY && ln.level == p->L))
@@ -1814,17 +2038,28 @@ fmm_status_t fmm_execute_timed(fmm_plan_t* p, const double* A, int64_t lda, cons
                                int64_t ldc, void* stream, float ms[5]) {
   FMM_API_BEGIN
   if (!p || !ms) throw Error(FMM_E_INVALID_ARG, "null argument");
+  // plain launches (no graph) with an event after each one; every launch's time goes to its phase
+  p->profile_launches = true;
+  struct Off {
+    fmm_plan_t* p;
+    ~Off() { p->profile_launches = false; }
+  } off{p};
   run(p, A, lda, B, ldb, C, ldc, (cudaStream_t)stream, p->ev);
-  FMM_CUDA(cudaEventSynchronize(p->ev[3]));
-  float t01 = 0, t12 = 0, t23 = 0;
-  FMM_CUDA(cudaEventElapsedTime(&t01, p->ev[0], p->ev[1]));
-  FMM_CUDA(cudaEventElapsedTime(&t12, p->ev[1], p->ev[2]));
-  FMM_CUDA(cudaEventElapsedTime(&t23, p->ev[2], p->ev[3]));
-  ms[0] = t01;
-  ms[1] = t12;
-  ms[2] = t23;
-  ms[3] = 0.0f;
-  ms[4] = t01 + t12 + t23;
+  FMM_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  float acc[5] = {0, 0, 0, 0, 0};
+  for (size_t q = 1; q < p->ev_l_phase.size(); ++q) {
+    float t = 0;
+    FMM_CUDA(cudaEventElapsedTime(&t, p->ev_l[q - 1], p->ev_l[q]));
+    const int ph = p->ev_l_phase[q];
+    if (ph >= 0 && ph < 5) acc[ph] += t;
+  }
+  ms[0] = acc[0];
+  ms[1] = acc[1];
+  ms[2] = acc[2];
+  ms[3] = acc[3];
+  float total = 0;
+  if (p->ev_l_phase.size() > 1) FMM_CUDA(cudaEventElapsedTime(&total, p->ev_l[0], p->ev_l[p->ev_l_phase.size() - 1]));
+  ms[4] = total;
   return FMM_OK;
   FMM_API_END
 }

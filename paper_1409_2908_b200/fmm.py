@@ -33,7 +33,11 @@ class _Options(ctypes.Structure):
                 ("shard_rank", ctypes.c_int), ("shard_count", ctypes.c_int),
                 ("workspace_limit_bytes", ctypes.c_size_t), ("peel_align", ctypes.c_int),
                 ("fuse_leaf_level", ctypes.c_int), ("shard_mode", ctypes.c_int), ("collapse_levels", ctypes.c_int),
-                ("cuda_graphs", ctypes.c_int), ("peel_tiles", ctypes.c_int)]
+                ("cuda_graphs", ctypes.c_int), ("peel_tiles", ctypes.c_int), ("dist_chunks", ctypes.c_int)]
+
+
+# fmm_barrier_fn: int (*)(void* ctx), a host barrier over the ranks of a peer-memory plan
+_BARRIER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)
 
 
 def _load():
@@ -58,6 +62,8 @@ def _load():
         "fmm_comm_create": [ctypes.c_char_p, i32, i32, i32, ctypes.POINTER(vp)],
         "fmm_comm_info": [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)],
         "fmm_plan_create_dist": [vp, i64, i64, i64, i32, ctypes.POINTER(_Options), vp, i32, ctypes.POINTER(vp)],
+        "fmm_plan_create_p2p": [vp, i64, i64, i64, i32, ctypes.POINTER(_Options), vp, i32, _BARRIER_FN, vp,
+                                ctypes.POINTER(vp)],
         "fmm_plan_predict": [vp, i64, i64, i64, i32, i32, ctypes.POINTER(dp), ctypes.POINTER(i32)],
         "fmm_select": [vp, i32, i64, i64, i64, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32),
                        ctypes.POINTER(dp)],
@@ -243,7 +249,13 @@ class Plan:
                  strategy: str = "streaming", cse: bool = True, shard_rank: int = 0, shard_count: int = 1,
                  device: Optional[int] = None, workspace_limit_bytes: int = 0, peel_align: bool = True,
                  fuse: bool = False, collapse: bool = True, comm: Optional[Comm] = None, root: int = 0,
-                 shard_mode: str = "leaf", cuda_graphs: bool = True, peel_tiles: bool = False):
+                 shard_mode: str = "leaf", cuda_graphs: bool = True, peel_tiles: bool = False,
+                 p2p: Optional["P2P"] = None, barrier=None, dist_chunks: Optional[int] = None):
+        """comm: an NCCL Comm -> fmm_plan_create_dist (the reduce runs inside execute, in dist_chunks
+        overlapped row chunks where it applies).  p2p + barrier: a P2P object and a zero-argument host
+        barrier over the same ranks (e.g. torch.distributed.barrier) -> fmm_plan_create_p2p (the
+        peer-memory combine runs inside execute, which then blocks).  root: the rank that receives C,
+        or "slabs" for slab-distributed output."""
         import torch
         self.alg, self.P, self.Q, self.N, self.levels = alg, P, Q, N, levels
         self.layout = ROW_MAJOR if layout == "row" else COL_MAJOR
@@ -262,15 +274,34 @@ class Plan:
         o.fuse_leaf_level = int(bool(fuse))
         o.collapse_levels = int(bool(collapse))
         o.shard_mode = {"leaf": 0, "top": 1}[shard_mode]
+        if dist_chunks is not None:
+            o.dist_chunks = int(dist_chunks)
         self.device = torch.cuda.current_device() if device is None else device
         h = ctypes.c_void_p()
-        self.comm = comm  # a distributed plan keeps its communicator alive
-        if comm is None:
+        self.comm = comm  # a distributed plan keeps its communicator / peer buffers alive
+        self.p2p = p2p
+        if root == "slabs":
+            root = DIST_SLABS
+        if comm is not None and p2p is not None:
+            raise ValueError("a plan combines through NCCL (comm) or peer memory (p2p), not both")
+        if p2p is not None:
+            if barrier is None:
+                raise ValueError("a peer-memory plan needs a host barrier over its ranks")
+
+            def _bar(_ctx):
+                try:
+                    barrier()
+                    return 0
+                except Exception:  # noqa: BLE001  (reported to the library as a failed barrier)
+                    return 1
+            self._barrier = _BARRIER_FN(_bar)  # kept alive as long as the plan
+            self.device = p2p.device
+            _check(_lib.fmm_plan_create_p2p(alg._h, P, Q, N, levels, ctypes.byref(o), p2p._h, root, self._barrier,
+                                            None, ctypes.byref(h)))
+        elif comm is None:
             _check(_lib.fmm_plan_create(alg._h, P, Q, N, levels, ctypes.byref(o), self.device, ctypes.byref(h)))
         else:
             self.device = comm.device
-            if root == "slabs":
-                root = DIST_SLABS
             _check(_lib.fmm_plan_create_dist(alg._h, P, Q, N, levels, ctypes.byref(o), comm._h, root, ctypes.byref(h)))
         self._h = h
 
@@ -313,12 +344,15 @@ class Plan:
         return C
 
     def execute_timed(self, A, B, C=None, stream=None):
-        """Blocking; returns (C, {formation, gemm, assembly, total} ms)."""
+        """Blocking, plain launches with an event after each (fmm_execute_timed); returns
+        (C, {formation, gemm (leaf products), assembly, strips (peel GEMMs), total} ms), total
+        including a distributed plan's combine."""
         if C is None:
             C = self.new_output()
         ms = (ctypes.c_float * 5)()
         _check(_lib.fmm_execute_timed(self._h, *self._args(A, B, C), _stream_ptr(stream), ms))
-        return C, {"formation_ms": ms[0], "gemm_ms": ms[1], "assembly_ms": ms[2], "total_ms": ms[4]}
+        return C, {"formation_ms": ms[0], "gemm_ms": ms[1], "assembly_ms": ms[2], "strips_ms": ms[3],
+                   "total_ms": ms[4]}
 
     def execute_events(self, A, B, C, events, stream=None):
         """Asynchronous execute that records 4 torch.cuda.Event on the stream: before, after
@@ -335,19 +369,35 @@ class Plan:
         import torch
 
         def hp(x, rows, cols, what, writable=False):
+            # the same layout rules as _mat(): unit stride along the contiguous dimension, a
+            # non-negative leading dimension, and a writeable output (the library copies whole
+            # rows / columns of ld-strided storage, so any other view would be read or written wrongly)
             if isinstance(x, torch.Tensor):
-                if x.is_cuda or x.dtype != torch.float64:
-                    raise TypeError(f"{what} must be a float64 CPU tensor")
+                if x.is_cuda or x.dtype != torch.float64 or x.dim() != 2:
+                    raise TypeError(f"{what} must be a 2-D float64 CPU tensor")
                 s0, s1 = x.stride()
                 ptr = x.data_ptr()
             else:
-                if x.dtype != np.float64:
-                    raise TypeError(f"{what} must be float64")
+                if not isinstance(x, np.ndarray) or x.dtype != np.float64 or x.ndim != 2:
+                    raise TypeError(f"{what} must be a 2-D float64 array")
+                if x.strides[0] % 8 or x.strides[1] % 8:
+                    raise ValueError(f"{what} has strides that are not whole elements")
                 s0, s1 = x.strides[0] // 8, x.strides[1] // 8
                 ptr = x.ctypes.data
+                if writable and not x.flags.writeable:
+                    raise ValueError(f"{what} is read-only")
             if tuple(x.shape) != (rows, cols):
                 raise ValueError(f"{what} has shape {tuple(x.shape)}, expected {(rows, cols)}")
-            ld = s0 if self.layout == ROW_MAJOR else s1
+            if s0 < 0 or s1 < 0:
+                raise ValueError(f"{what} has a negative stride")
+            if self.layout == ROW_MAJOR:
+                if s1 != 1 and cols > 1:
+                    raise ValueError(f"{what} must be row-major (unit column stride)")
+                ld = s0 if rows > 1 else max(cols, 1)
+            else:
+                if s0 != 1 and rows > 1:
+                    raise ValueError(f"{what} must be column-major (unit row stride)")
+                ld = s1 if cols > 1 else max(rows, 1)
             return ctypes.c_void_p(ptr), int(max(ld, 1))
         a, lda = hp(A, self.P, self.Q, "A")
         b, ldb = hp(B, self.Q, self.N, "B")

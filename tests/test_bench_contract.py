@@ -30,3 +30,26 @@ def test_reference_arm_line():
 def test_warmup_below_three_is_refused():
     r = _bench("--impl", "reference", "--workload", "c1", "--steps", "1", "--warmup", "2")
     assert r.returncode != 0 and "--warmup must be >= 3" in r.stderr
+
+
+def test_gpus_must_match_world_size():
+    env = dict(os.environ, WORLD_SIZE="3", RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", "c1",
+                        "--gpus", "2", "--steps", "1", "--warmup", "3"], capture_output=True, text=True, timeout=120,
+                       cwd=ROOT, env=env)
+    assert r.returncode == 2 and "WORLD_SIZE=3" in r.stderr
+
+
+def test_gpus_n_without_torchrun_launches_n_ranks():
+    # --gpus 2 with WORLD_SIZE unset re-launches bench.py under torch.distributed.run with 2 ranks; the
+    # reference arm runs on rank 0 only, so exactly one JSON line comes back, with n_gpus = 2
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR",
+                                                             "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", "c1",
+                        "--gpus", "2", "--steps", "1", "--warmup", "3"], capture_output=True, text=True, timeout=300,
+                       cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["impl"] == "reference"

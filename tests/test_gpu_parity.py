@@ -423,3 +423,25 @@ def test_classical_root_shards_write_zeros_elsewhere():
                 torch.cuda.synchronize()
                 total += C.cpu().numpy()
             assert np.array_equal(total, A @ B)
+
+
+@pytest.mark.parametrize("alg,shape,layout,chunks,root", [
+    ("winograd_class_222_7", (256, 256, 256), "col", 4, 0),       # collapsed two-level assembly writes C
+    ("winograd_class_222_7", (301, 200, 250), "row", 3, 0),       # bottom peel rows: the tail reduce
+    ("hk_class_323_15", (301, 64, 299), "row", 7, "slabs"),       # top-level row and column strips
+    ("alg_424_26", (257, 131, 190), "col", 4, 0),                 # K peel at the top: one reduce at the end
+    ("alg_433_29", (180, 36, 36), "row", 1, 0)])                  # chunking off
+def test_distributed_plan_chunked_reduce(alg, shape, layout, chunks, root):
+    # NCCL plan, dist_chunks row chunks of the C-writing assembly, each reduced on the library's comm
+    # stream; at one rank every reduce is an in-place copy, so C must be the exact product whatever
+    # the chunking (it checks the chunk tables, the strip reordering and the tail rows)
+    P, Q, N = shape
+    A, B = I.problem(P, Q, N, seed=23, kind="integers")
+    comm = F.Comm(F.nccl_unique_id(), 1, 0)
+    p = F.Plan(falg(alg), P, Q, N, 2, layout=layout, comm=comm, root=root, dist_chunks=chunks)
+    for _ in range(2):
+        C = p.execute(dev(A, layout), dev(B, layout))
+        torch.cuda.synchronize()
+        assert np.array_equal(C.cpu().numpy(), A @ B)
+    _, t = p.execute_timed(dev(A, layout), dev(B, layout), C)
+    assert t["gemm_ms"] > 0 and t["total_ms"] >= t["gemm_ms"]

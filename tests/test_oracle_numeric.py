@@ -146,6 +146,37 @@ def test_flop_count_closed_forms():
         assert O.flops(n, n, n, s, k) == round(7 * n ** math.log2(7) - 6 * n ** 2)
 
 
+def test_flop_count_peeled_and_scaled_by_hand():
+    # the branches the closed forms above do not reach, counted by hand from the paper's
+    # operation rules: a classical p x q x n product costs p n (2q - 1); a chain of k
+    # nonzero coefficients costs k - 1 additions per element, and a non-unit coefficient one multiply
+    # per element ("inactive multiplies"); peeling per S:287-295 (reading R7)
+    import dataclasses
+    from fractions import Fraction as Fr
+    s = ALGS_BY_NAME["strassen_222_7"]
+    # Strassen's 18 block additions: 5 forming S (U), 5 forming T (V), 8 forming C (W)
+    assert sum(sum(1 for v in col if v != 0) - 1 for col in zip(*s.U)) == 5
+    assert sum(sum(1 for v in col if v != 0) - 1 for col in zip(*s.V)) == 5
+    assert sum(sum(1 for v in row if v != 0) - 1 for row in s.W) == 8
+    # 5 x 5 x 5, one step: core 4 x 4 x 4 with 2 x 2 blocks
+    core = 5 * 4 + 5 * 4 + 7 * (2 * 2 * (2 * 2 - 1)) + 8 * 4       # S, T, 7 leaves of 12 flops, C = 156
+    fix_a = 4 * 4 * (2 * 1 - 1) + 4 * 4                             # (a) C'[0:4,0:4] += A[:,4:5] B[4:5,:]
+    fix_b = 1 * 5 * (2 * 5 - 1)                                     # (b) the last row of C, classical
+    fix_c = 4 * 1 * (2 * 5 - 1)                                     # (c) the last column of the first 4 rows
+    assert (core, fix_a, fix_b, fix_c) == (156, 32, 45, 36)
+    assert O.flops(5, 5, 5, s, 1) == core + fix_a + fix_b + fix_c == 269
+    # rational-scaled column: U column 0 (S_1 = A11 + A22) times 2, W column 0 (M_1 in C11 and C22)
+    # times 1/2 -- still exact (Brent), and each scaled coefficient costs one multiply per element
+    U = [[v * (2 if r == 0 else 1) for r, v in enumerate(row)] for row in s.U]
+    W = [[v * (Fr(1, 2) if r == 0 else 1) for r, v in enumerate(row)] for row in s.W]
+    t = dataclasses.replace(s, U=U, W=W)
+    assert O.brent_residuals(t) == 0
+    # S_1: 1 addition + 2 multiplies per element instead of 1 addition: +2 x 4; C11, C22: +1 x 4 each
+    assert O.flops(4, 4, 4, t, 1) == 156 + 2 * 4 + 2 * 4 == 172
+    # and a base case smaller than the problem in one dimension only: classical at that level (R10/R18)
+    assert O.flops(1, 7, 9, s, 2) == 1 * 9 * (2 * 7 - 1)
+
+
 # ---- check (d): error growth within the bound derived from (U, V, W) ------------
 def _higham_strassen(n, n0):
     """Higham, Accuracy and Stability of Numerical Algorithms (cited at P:80), the Strassen bound:

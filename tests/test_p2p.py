@@ -1,6 +1,8 @@
 """The combine over peer memory (fmm_p2p_*): world-size 2 and 3 processes, each
 with its HYBRID leaf shard written into its IPC-exported partial buffer, then ONE
-reduce kernel per rank pulling its slab from every rank's partial.  The ranks share the one GPU of
+reduce kernel per rank pulling its slab from every rank's partial -- called by hand
+(fmm_p2p_reduce_slab) and inside fmm_execute of the library's peer-memory plan
+(fmm_plan_create_p2p, root and slab output).  The ranks share the one GPU of
 this box (CUDA IPC works between processes on one device), gloo carries only the handle exchange
 and the two barriers; no kernel waits on another rank's kernel.  Integer inputs: the slabs must
 equal the exact product bit for bit, in both layouts."""
@@ -86,3 +88,69 @@ def test_p2p_slab_combine(world, layout, alg):
         pr.join(timeout=300)
     assert all(pr.exitcode == 0 for pr in procs), [pr.exitcode for pr in procs]
     assert q.get(timeout=5), "reduced slabs differ from A*B"
+
+
+def _plan_worker(rank, world, port, layout, alg_name, root, q):
+    # the library's own combine: fmm_plan_create_p2p, the reduce inside fmm_execute, the host
+    # barrier supplied as a callback (gloo's torch.distributed.barrier)
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import fmm_inputs as I
+        import paper_1409_2908_b200 as F
+        torch.cuda.set_device(0)
+        P, Q, N = 301, 200, 250  # odd P: a peel strip at the top level
+        A, B = I.problem(P, Q, N, seed=37, kind="integers")
+
+        def dev(x):
+            if layout == "row":
+                return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+            return torch.from_numpy(np.ascontiguousarray(x.T)).cuda().t()
+        p2p = F.P2P.from_torch_distributed(8 * P * N)
+        plan = F.Plan(F.load_alg(alg_name), P, Q, N, 2, layout=layout, p2p=p2p, barrier=dist.barrier, root=root)
+        want = A @ B
+        ok = True
+        for it in range(3):  # the partial buffers are reused across executes
+            C = torch.full((P, N), float("nan"), dtype=torch.float64, device="cuda") if layout == "row" else \
+                torch.full((N, P), float("nan"), dtype=torch.float64, device="cuda").t()
+            plan.execute(dev(A), dev(B), C)
+            torch.cuda.synchronize()
+            got = C.cpu().numpy()
+            if root == "slabs":
+                r0, r1 = F.dist_slab(P, N, layout, world, rank)
+                ok &= bool(np.array_equal(got[r0:r1], want[r0:r1]) if layout == "row" else
+                           np.array_equal(got[:, r0:r1], want[:, r0:r1]))
+            elif rank == root:
+                ok &= bool(np.array_equal(got, want))
+            else:  # other ranks' C is left untouched
+                ok &= bool(np.isnan(got).all())
+        oks = [None] * world
+        dist.all_gather_object(oks, ok)
+        if rank == 0:
+            q.put(all(oks))
+        del plan
+        dist.barrier()
+        del p2p
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,layout,alg,root", [(2, "row", "winograd_class_222_7", 0),
+                                                   (2, "col", "hk_class_323_15", 1),
+                                                   (3, "row", "alg_424_26", "slabs"),
+                                                   (2, "col", "strassen_222_7", "slabs")])
+def test_p2p_plan_combines_inside_execute(world, layout, alg, root):
+    import __graft_entry__
+    __graft_entry__.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_plan_worker, args=(r, world, port, layout, alg, root, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=300)
+    assert all(pr.exitcode == 0 for pr in procs), [pr.exitcode for pr in procs]
+    assert q.get(timeout=5), "the combined C differs from A*B"
