@@ -336,9 +336,8 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
 #pragma unroll
       for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    // one 4-deep k-slice of a stage: fragments from shared memory, MI x NI DMMAs
-    auto slice = [&](unsigned sa, unsigned sb, int s) {
-      double a[MI], b[NI];
+    // fragments of one 4-deep k-slice from shared memory, and its MI x NI DMMAs
+    auto load = [&](double (&a)[MI], double (&b)[NI], unsigned sa, unsigned sb, int s) {
 #pragma unroll
       for (int i = 0; i < MI; ++i) {
         const unsigned x = (i & 1) ? xa1 : xa0;
@@ -351,6 +350,8 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
         const unsigned chunk = (cb0 + 2u * (jj & 1)) ^ (krow & 7u);
         b[jj] = lds64(sb + b_box0 + (unsigned)(jj >> 1) * 2048u + krow * 128u + chunk * 16u + hb * 8u);
       }
+    };
+    auto mma = [&](const double (&a)[MI], const double (&b)[NI]) {
 #pragma unroll
       for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -361,23 +362,47 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
       if (lane == 0) mbar_arrive(empty_bar(stage));
       if (++stage == STAGES) stage = 0, phase ^= 1u;
     };
-    // full stages run the plain pipelined loop; then a ragged last k-step runs only the 4-deep slices
-    // that hold data (the rest is zero fill), and a warp whose sub-tile lies beyond m or n (ragged
-    // edge tiles) issues no DMMA at all but waits for and releases every stage with the others
+    // Full stages: software-pipelined -- the fragments of slice s + 1 (for the last slice, slice 0
+    // of the next stage, after its full barrier) are loaded before the DMMAs of slice s, so the
+    // shared-memory latency hides behind the warp's own DMMAs, not only behind the other warp of
+    // its sub-partition.  A stage is released after the DMMAs that consume its last fragments.
+    // Then a ragged last k-step runs only the 4-deep slices that hold data (the rest is zero fill),
+    // and a warp whose sub-tile lies beyond m or n (ragged edge tiles) issues no DMMA at all but
+    // waits for and releases every stage with the others.
     const int KF = active ? kdim / BK : 0;
-    for (int kt = 0; kt < KF; ++kt) {
+    if (KF > 0) {
+      static_assert(BK / 4 == 4, "four slices per stage");
+      double a0[MI], b0[NI], a1[MI], b1[NI];
       mbar_wait(full_bar(stage), phase);
-      const unsigned sa = base + stage * STAGE_T, sb = sa + A_BYTES;
-#pragma unroll
-      for (int s = 0; s < BK / 4; ++s) slice(sa, sb, s);
-      release();
+      unsigned sa = base + stage * STAGE_T, sb = sa + A_BYTES;
+      load(a0, b0, sa, sb, 0);
+      for (int kt = 0; kt < KF; ++kt) {
+        load(a1, b1, sa, sb, 1);
+        mma(a0, b0);
+        load(a0, b0, sa, sb, 2);
+        mma(a1, b1);
+        load(a1, b1, sa, sb, 3);
+        mma(a0, b0);
+        if (kt + 1 < KF) {
+          const int nx = stage + 1 == STAGES ? 0 : stage + 1;
+          mbar_wait(full_bar(nx), nx == 0 ? phase ^ 1u : phase);
+          sa = base + nx * STAGE_T, sb = sa + A_BYTES;
+          load(a0, b0, sa, sb, 0);
+        }
+        mma(a1, b1);
+        release();
+      }
     }
     for (int kt = KF; kt < KT; ++kt) {
       mbar_wait(full_bar(stage), phase);
       const unsigned sa = base + stage * STAGE_T, sb = sa + A_BYTES;
       const int ks = active ? (kdim - kt * BK + 3) / 4 : 0;
 #pragma unroll 1
-      for (int s = 0; s < ks; ++s) slice(sa, sb, s);
+      for (int s = 0; s < ks; ++s) {
+        double a[MI], b[NI];
+        load(a, b, sa, sb, s);
+        mma(a, b);
+      }
       release();
     }
 

@@ -10,7 +10,8 @@ from fractions import Fraction
 from typing import Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfmm.so")
+# FMM_LIB_PATH: an experiment build of the same library (build.py FMM_BUILD_VARIANT); default libfmm.so
+LIB_PATH = os.environ.get("FMM_LIB_PATH") or os.path.join(_HERE, "libfmm.so")
 
 FMM_OK = 0
 _STATUS = {1: "FMM_E_INVALID_ARG", 2: "FMM_E_NOT_EXACT", 3: "FMM_E_SHAPE", 4: "FMM_E_NO_MEMORY",

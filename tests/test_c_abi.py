@@ -216,6 +216,6 @@ def test_c_program_executes_on_the_gpu(tmp_path):
            f"-L{cuda}/lib64", "-lcudart", f"-Wl,-rpath,{cuda}/lib64", "-lm"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
-    r = subprocess.run([str(exe), str(tmp_path), os.path.join(ROOT, "algs"), repr(tols[0]), repr(tols[1])],
+    r = subprocess.run([str(exe), str(tmp_path), os.path.join(ROOT, "algs"), "%.17g" % tols[0], "%.17g" % tols[1]],
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.strip().endswith("OK"), r.stdout + r.stderr
