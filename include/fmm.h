@@ -121,11 +121,22 @@ typedef struct {
                                K peel (its rank-update strip would touch C after the assembly);
                                otherwise, and with 0 or 1, one reduce of the whole C at the end.
                                Default 4.  Ignored by single-GPU and peer-memory plans. */
+  int fuse_output;          /* 1: K3f -- the last level's output step C_k = sum_r w_kr M_r
+                               fused into the leaf GEMM's epilogue: every leaf tile is staged in
+                               shared memory and reduce-added by TMA (cp.reduce.async.bulk.tensor,
+                               fp64 add in L2) into each level-(L-1) output block its W column
+                               touches, so the leaf products M_r are never written or read back and
+                               the level-L assembly launch disappears (the target blocks are zeroed
+                               first).  The summation order of those adds is not fixed, so results
+                               can differ from run to run by rounding (within the tolerances; exact
+                               on integer inputs).  Applies when W has only 0 / +-1 entries and
+                               MN <= 16, one shard, no fused leaf level; it replaces the collapsed
+                               last two levels.  0 (default): separate assembly kernels. */
 } fmm_plan_options;
 
 /* Fill *opt with the defaults: row-major, streaming, cse = 1, shard 0 of 1, no limit,
    peel_align = 1, fuse_leaf_level = 0, collapse_levels = 1, cuda_graphs = 1, peel_tiles = 0,
-   dist_chunks = 4. */
+   dist_chunks = 4, fuse_output = 0. */
 void fmm_plan_options_default(fmm_plan_options* opt);
 
 /* ---- algorithms ------------------------------------------------------------------------- */
@@ -263,6 +274,10 @@ fmm_status_t fmm_plan_stats(const fmm_plan_t* plan, double out[8]);
    [14] 1 if the last two levels are collapsed (collapse_levels), else 0
    [15] 1 if the last split's rows were peeled to 128-row-aligned leaves (peel_tiles, R7c) */
 fmm_status_t fmm_plan_stats_ex(const fmm_plan_t* plan, double out[16]);
+
+/* The same, extensible: fills out[0 .. min(n, 17) - 1]; out[0..15] as fmm_plan_stats_ex, then
+   [16] 1 if the output step is fused into the leaf GEMM (fuse_output applied), else 0. */
+fmm_status_t fmm_plan_stats_ex2(const fmm_plan_t* plan, double* out, int n);
 
 /* Cost model (host only, no allocation): predicted milliseconds of a plan of `alg` for the problem
    on one B200 -- leaf DMMA GEMM tile schedule (wave quantisation, tile widths), streaming addition

@@ -13,8 +13,24 @@ struct GemmTask {
   int m, n, k;
   int tiles_m, tiles_n;
   int tile_begin;  // prefix sum of tiles over the task list
-  int node;        // fused leaf-level launch: parent (level L-1) node index; -1 elsewhere
+  int node;        // fused leaf-level / K3f launch: parent (level L-1) node index; -1 elsewhere
+  int aux;         // K3f launch: the leaf's own column r_L of W (selects its output targets)
   double alpha, beta;
+};
+
+// K3f (the output step fused into the leaf GEMM's epilogue): each leaf tile is
+// reduce-added by TMA (cp.reduce.async.bulk.tensor .add.f64) into the level-(L-1) output blocks
+// its W column touches: for leaf column r, target q < count[r] is the parent sub-block at
+// (row_off, col_off) with coefficient sign (+1 / -1) -- C_k += w_kr M_r.
+constexpr int K3F_MAX_TARGETS = 16;
+constexpr int K3F_BN = 64;  // tile width of the K3f leaf GEMM (its staging tiles must fit beside the ring)
+struct K3fTarget {
+  int row_off, col_off, sign, pad;
+};
+struct K3fArgs {
+  const void* maps;          // one CUtensorMap per parent node (its output block), 64-byte aligned
+  const int* count;          // [R]
+  const K3fTarget* targets;  // [R][K3F_MAX_TARGETS]
 };
 
 // Uniform launches (every task has the same tile grid, e.g. all leaves of a level) map a tile to

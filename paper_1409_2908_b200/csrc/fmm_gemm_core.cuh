@@ -52,6 +52,11 @@ static_assert(THREADS == GEMM_THREADS, "host and device agree on the block size"
 constexpr int A_BYTES = BM * BK * 8;                           // 16 KB
 __host__ __device__ constexpr int gemm_smem_bytes(int bn) { return GEMM_STAGES * (A_BYTES + BK * bn * 8) + 1024 /*align*/ + 256 /*barriers*/; }
 __host__ __device__ constexpr int fused_smem_bytes(int bn) { return gemm_smem_bytes(bn) + FUSED_PTR_BYTES; }
+// K3f: a 4-stage ring plus two staging tiles (+alpha acc and -alpha acc) of 128 x bn doubles
+constexpr int K3F_STAGES = 4;
+__host__ __device__ constexpr int k3f_smem_bytes(int bn) {
+  return K3F_STAGES * (A_BYTES + BK * bn * 8) + 1024 /*align*/ + 1024 /*barriers, aligned*/ + 2 * BM * bn * 8;
+}
 constexpr int GROUP_M = 8;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -85,6 +90,21 @@ __device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map
       : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_shared() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// K3f: shared-memory box (16 columns x 128 rows, 128B swizzle) reduce-added into a global tile
+__device__ __forceinline__ void tma_reduce_add_2d(const void* map, int c0, int c1, unsigned src) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+          reinterpret_cast<unsigned long long>(map)),
+      "r"(c0), "r"(c1), "r"(src)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void sts_f64x2(unsigned addr, double a, double b) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(a), "d"(b) : "memory");
+}
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
@@ -204,10 +224,12 @@ __device__ __forceinline__ void run_job(const FusedArgs& fa, int jidx, int lane,
   }
 }
 
-template <int BN, int WGM, int WGN, bool FUSED>
+template <int BN, int WGM, int WGN, bool FUSED, bool K3F = false>
 __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, const CUtensorMap* __restrict__ maps,
-                                          int ntasks, int total_tiles, Uniform uni, const FusedArgs& fa) {
-  constexpr int STAGES = GEMM_STAGES;
+                                          int ntasks, int total_tiles, Uniform uni, const FusedArgs& fa,
+                                          const K3fArgs* ka = nullptr) {
+  static_assert(!(FUSED && K3F), "one epilogue mode");
+  constexpr int STAGES = K3F ? K3F_STAGES : GEMM_STAGES;
   static_assert(WGM * WGN == CONSUMERS, "8 consumer warps");
   constexpr int WTM = BM / WGM, WTN = BN / WGN;
   static_assert(WTM % 16 == 0 && WTN % 16 == 0, "warp tile must be a multiple of 16");
@@ -406,6 +428,45 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
       release();
     }
 
+    if constexpr (K3F) {
+      // ---- K3f epilogue: +alpha acc and -alpha acc staged in shared memory (128B-swizzled boxes of
+      // 16 columns x 128 rows), then one thread reduce-adds the right one into every output block
+      // the leaf's W column touches.  Zero-filled rows / columns of a ragged tile add zeros.
+      const unsigned stg_p = bars + 1024u, stg_n = stg_p + (unsigned)(BM * BN * 8);
+      const bool issuer = cw == 0 && lane == 0;
+      if (issuer) bulk_wait_read_all();  // the previous tile's reduces have read the staging tiles
+      named_bar_sync(1, CONSUMERS * 32);
+      const int cofs_k = (c == 0) ? 0 : (c == 1) ? 8 : (c == 2) ? 2 : 10;
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        const int row = wm + 16 * (i >> 1) + 2 * r + (i & 1);
+#pragma unroll
+        for (int jj = 0; jj < NI; ++jj) {
+          const int col = wn + 16 * (jj >> 1) + 4 * (jj & 1) + cofs_k;  // even: a 16-byte pair
+          const unsigned off = (unsigned)(col >> 4) * (unsigned)(BM * 128) + (unsigned)row * 128u +
+                               ((((unsigned)(col & 15) >> 1) ^ (unsigned)(row & 7)) << 4);
+          const double v0 = alpha * acc[i][jj][0], v1 = alpha * acc[i][jj][1];
+          sts_f64x2(stg_p + off, v0, v1);
+          sts_f64x2(stg_n + off, -v0, -v1);
+        }
+      }
+      fence_proxy_async_shared();
+      named_bar_sync(1, CONSUMERS * 32);
+      if (issuer) {
+        const int col_leaf = __ldg(&t.aux);
+        const void* map = reinterpret_cast<const char*>(ka->maps) + 128 * __ldg(&t.node);
+        const int nt = __ldg(&ka->count[col_leaf]);
+        for (int q = 0; q < nt; ++q) {
+          const K3fTarget tg = ka->targets[col_leaf * K3F_MAX_TARGETS + q];
+          const unsigned src = tg.sign > 0 ? stg_p : stg_n;
+#pragma unroll
+          for (int b = 0; b < BN / 16; ++b)
+            tma_reduce_add_2d(map, tg.col_off + tc.n0 + 16 * b, tg.row_off + tc.m0, src + (unsigned)(b * BM * 128));
+        }
+        bulk_commit();
+      }
+      continue;
+    }
     // ---- epilogue: C = alpha * acc (+ beta * C), from registers ----
     const int cofs = (c == 0) ? 0 : (c == 1) ? 8 : (c == 2) ? 2 : 10;  // map0[2c]
 #pragma unroll
@@ -445,6 +506,9 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
       if (fa.njobs0 + idx >= fa.njobs) break;
       run_job(fa, fa.njobs0 + idx, lane, sp);
     }
+  }
+  if constexpr (K3F) {
+    if (cw == 0 && lane == 0) bulk_wait_all();  // the last reduces complete before the CTA's smem goes
   }
 }
 

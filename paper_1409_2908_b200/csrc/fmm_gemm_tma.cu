@@ -25,6 +25,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   gemm_body<BN, WGM, WGN, false>(tasks, maps, ntasks, total_tiles, uni, FusedArgs{});
 }
 
+// K3f: the leaf GEMM whose epilogue reduce-adds every tile into its W targets (tile 128 x 64)
+__global__ void __launch_bounds__(THREADS, 1)
+    grouped_dgemm_k3f(const GemmTask* __restrict__ tasks, const CUtensorMap* __restrict__ maps, int ntasks,
+                      int total_tiles, Uniform uni, K3fArgs ka) {
+  gemm_body<K3F_BN, 4, 2, false, true>(tasks, maps, ntasks, total_tiles, uni, FusedArgs{}, &ka);
+}
+
 // ---- host side: tensor maps ----
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -43,6 +50,33 @@ EncodeFn encode_fn() {
   return fn;
 }
 
+void make_map(CUtensorMap* m, const double* ptr, long long rows, long long cols, long long ld, int box_cols, int box_rows);
+}  // namespace
+
+void gemm_k3f_target_map(void* out, const double* ptr, long long rows, long long cols, long long ld) {
+  make_map(reinterpret_cast<CUtensorMap*>(out), ptr, rows, cols, ld, 16, BM);  // 16 columns x 128 rows
+}
+
+void gemm_k3f_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int uniform_tm,
+                     int uniform_tn, const K3fArgs& ka, cudaStream_t stream) {
+  if (total_tiles <= 0 || ntasks <= 0) return;
+  static std::atomic<unsigned long long> configured{0};
+  int dev_ = 0;
+  FMM_CUDA(cudaGetDevice(&dev_));
+  const unsigned long long bit = 1ull << (dev_ & 63);
+  const size_t smem = (size_t)k3f_smem_bytes(K3F_BN);
+  if (!(configured.load() & bit)) {
+    FMM_CUDA(cudaFuncSetAttribute(grouped_dgemm_k3f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured.fetch_or(bit);
+  }
+  const Uniform uni{uniform_tm * uniform_tn, uniform_tm, uniform_tn};
+  const int grid = (int)std::min<long long>(total_tiles, gemm_sm_count());
+  grouped_dgemm_k3f<<<grid, THREADS, smem, stream>>>(d_tasks, reinterpret_cast<const CUtensorMap*>(d_maps), ntasks,
+                                                      (int)total_tiles, uni, ka);
+  FMM_CUDA(cudaGetLastError());
+}
+
+namespace {
 void make_map(CUtensorMap* m, const double* ptr, long long rows, long long cols, long long ld, int box_cols, int box_rows) {
   EncodeFn fn = encode_fn();
   if (!fn) throw Error(FMM_E_CUDA, "cuTensorMapEncodeTiled unavailable");

@@ -108,6 +108,11 @@ void gemm_tma_maps(const std::vector<GemmTask>& tasks, void* out);
 // uniform_tm/tn: the common tile grid when every task has the same one (else 0, 0).
 void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn,
                      int uniform_tm, int uniform_tn, cudaStream_t stream);
+// K3f leaf GEMM (128 x K3F_BN tiles; epilogue reduce-adds into the W targets through TMA): the
+// tensor map of one parent output block (box 16 columns x 128 rows, 128B swizzle) and the launch.
+void gemm_k3f_target_map(void* out, const double* ptr, long long rows, long long cols, long long ld);
+void gemm_k3f_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int uniform_tm,
+                     int uniform_tn, const K3fArgs& ka, cudaStream_t stream);
 // TMA kernel configuration: consumer warp grid of a tile width, SM count, dynamic shared memory.
 void gemm_bn_config(int bn, int* wgm, int* wgn);
 int gemm_sm_count();

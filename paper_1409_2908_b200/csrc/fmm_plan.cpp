@@ -47,7 +47,8 @@ struct Dims {
 using PlanDims = Dims;
 
 struct Launch {
-  enum Kind { FORM_A, FORM_B, GEMM, ASSEMBLE, STRIPS, SKINNY, FUSED, REDUCE /* no kernel: reduce_rows only */ } kind;
+  enum Kind { FORM_A, FORM_B, GEMM, ASSEMBLE, STRIPS, SKINNY, FUSED, REDUCE /* no kernel: reduce_rows only */,
+              ZERO /* K3f: zero the level-(L-1) output blocks (cudaMemset2DAsync per block) */ } kind;
   int level = 0;
   size_t table_off = 0;  // byte offset in the device table buffer
   int count = 0;         // nodes / tasks
@@ -65,6 +66,9 @@ struct Launch {
   double flops = 0, gemm_bytes = 0;
   std::vector<int> node_ids;  // FORM / ASSEMBLE: parent node index of every table entry
   int nin = 0, nout = 0;      // ASSEMBLE: inputs / outputs per table entry
+  bool k3f = false;           // GEMM: the K3f leaf GEMM (epilogue reduce-adds into the W targets)
+  size_t k3f_maps_off = 0, k3f_count_off = 0, k3f_targets_off = 0;  // GEMM k3f: its device tables
+  std::vector<std::array<long long, 4>> zero_blocks;  // ZERO: (host pointer bits, ld, rows, cols)
   // NCCL distributed plans with dist_chunks: rows [first, second) of C (plan orientation) to reduce
   // on the communication stream once this launch is done (a chunk of the assembly that writes C)
   std::vector<std::pair<long long, long long>> reduce_rows;
@@ -125,6 +129,7 @@ struct fmm_plan_s {
   bool use_tma = true;  // FMM_NO_TMA=1 forces the cp.async GEMM (diagnostics)
   bool fuse = true;     // fuse_leaf_level option (FMM_NO_FUSE=1 overrides)
   bool collapse = false;  // the last two levels' formation / assembly in one pass each (sec. 6c)
+  bool k3f = false;       // fuse_output: the level-L output step in the leaf GEMM's epilogue (K3f)
   bool tiled_peel = false;  // R7c: the last split's rows were peeled to 128-row-aligned leaves
   unsigned long long* d_ctr = nullptr;  // fused launch counters: claim0, claim1, ready[np], tiles[np]
   size_t ctr_bytes = 0;
@@ -398,6 +403,9 @@ struct fmm_plan_s {
   // NCCL distributed plans: split the assembly launch that writes C into dist_chunks row chunks,
   // each followed by the reduce of its rows of C (run() issues it on s_comm)
   void chunk_final_assembly();
+  // K3f: zero the level-(L-1) outputs, then the leaf GEMM whose epilogue reduce-adds every tile
+  // into its W targets (replaces the level-L assembly)
+  void emit_k3f(std::vector<GemmTask>& tasks, bool lazy_kernels);
 };
 
 View fmm_plan_s::opA(int l, long long z, const View& root) const {
@@ -625,6 +633,7 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
       t.alpha = a.sigma * b.sigma;
       t.beta = 0.0;
       t.node = (int)(z / R);
+      t.aux = (int)(z % R);
       if (t.m > 0 && t.n > 0) tasks.push_back(t);
     }
     if (L == 0 && opt.shard_count > 1) {
@@ -652,7 +661,8 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
       if (r1 <= r0) zero(0, d.P);
       else zero(0, r0), zero(r1, d.P);
     }
-    emit_gemm(Launch::GEMM, L, tasks);
+    if (k3f) emit_k3f(tasks, lazy_kernels);
+    else emit_gemm(Launch::GEMM, L, tasks);
   }
 
   // ---- assembly and peel strips, levels L..1 ----
@@ -660,7 +670,7 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
     const Dims& d = dims[l];
     const Dims& dp = dims[l - 1];
     if (collapse && l == L) emit_two_level_assembly(lazy_kernels);
-    if (!(collapse && l >= L - 1) && d.P > 0 && d.N > 0) {
+    if (!(collapse && l >= L - 1) && !(k3f && l == L) && d.P > 0 && d.N > 0) {
       std::vector<char> tab;
       std::vector<int> node_ids;
       const int nin = R, nout = M * Nb;
@@ -834,6 +844,92 @@ void fmm_plan_s::chunk_final_assembly() {
   if (!tail.reduce_rows.empty()) out.push_back(tail);
   launches.swap(out);
   dist_chunked = true;
+}
+
+// K3f (SURVEY 8(a) a6 option 4 with a fixed-function reduction): the level-L assembly
+// C_k = sum_r w_kr M_r of every level-(L-1) node moves into the leaf GEMM's epilogue.  Each leaf tile
+// is reduce-added (TMA, fp64 add in L2) into the sub-blocks k of its parent's output with w_kr != 0:
+// +acc where w = 1, -acc where w = -1.  The parents' outputs are zeroed first.
+void fmm_plan_s::emit_k3f(std::vector<GemmTask>& tasks, bool lazy_kernels) {
+  const Dims& dp = dims[L - 1];
+  const Dims& d = dims[L];
+  const int Nb = alg->N;
+  auto push = [&](const void* ptr, size_t n) { return push_tab(ptr, n); };
+  // zero the outputs of the needed level-(L-1) nodes (their core and strips; strips rewrite theirs)
+  Launch zl;
+  zl.kind = Launch::ZERO;
+  zl.level = L - 1;
+  for (long long zp = 0; zp < nodes_at[L - 1]; ++zp) {
+    if (!needed[L - 1][zp]) continue;
+    const View o = out_view(L - 1, zp);
+    zl.zero_blocks.push_back({(long long)reinterpret_cast<uintptr_t>(o.ptr), o.ld, dp.P, dp.N});
+    zl.elem_writes += (double)dp.P * dp.N;
+  }
+  zl.count = (int)zl.zero_blocks.size();
+  launches.push_back(zl);
+  if (tasks.empty()) return;
+  if (!lazy_kernels) {
+    bool ok = gemm_tma_eligible(tasks);
+    for (long long zp = 0; zp < nodes_at[L - 1]; ++zp) {
+      if (!needed[L - 1][zp]) continue;
+      const View o = out_view(L - 1, zp);
+      ok &= al16(o.ptr) && o.ld % 2 == 0;
+    }
+    if (!ok)
+      throw Error(FMM_E_UNSUPPORTED, "fuse_output (K3f) needs 16-byte aligned A, B, C with even leading dimensions (TMA)");
+  }
+  Launch ln;
+  ln.kind = Launch::GEMM;
+  ln.level = L;
+  ln.k3f = true;
+  ln.tma = !lazy_kernels;
+  ln.bn = K3F_BN;
+  ln.tiles = gemm_prepare(tasks, 128, ln.bn);
+  gemm_uniform_grid(tasks, &ln.uni_tm, &ln.uni_tn);
+  ln.count = (int)tasks.size();
+  ln.aligned16 = gemm_tasks_aligned16(tasks);
+  for (auto& t : tasks) {
+    ln.flops += 2.0 * t.m * t.n * (double)t.k;
+    ln.gemm_bytes += 8.0 * ((double)t.m * t.k + (double)t.k * t.n);
+  }
+  ln.table_off = push(tasks.data(), tasks.size() * sizeof(GemmTask));
+  {  // operand maps (A, B per task), as every TMA GEMM launch
+    std::vector<char> maps(2 * gemm_tma_map_bytes() * tasks.size());
+    if (!lazy_kernels) gemm_tma_maps(tasks, maps.data());
+    ln.maps_off = push(lazy_kernels ? nullptr : maps.data(), maps.size());
+  }
+  {  // one target map per parent node: its output block, dims[L-1].P x dims[L-1].N
+    const size_t mb = gemm_tma_map_bytes();
+    std::vector<char> tm(mb * (size_t)nodes_at[L - 1], 0);
+    if (!lazy_kernels)
+      for (long long zp = 0; zp < nodes_at[L - 1]; ++zp) {
+        if (!needed[L - 1][zp]) continue;
+        const View o = out_view(L - 1, zp);
+        gemm_k3f_target_map(tm.data() + mb * zp, o.ptr, dp.P, dp.N, o.ld);
+      }
+    ln.k3f_maps_off = push(lazy_kernels ? nullptr : tm.data(), tm.size());
+  }
+  {  // per leaf column r of W: its targets (row / column offset of sub-block k in the parent, sign)
+    std::vector<int> count(R, 0);
+    std::vector<K3fTarget> tg((size_t)R * K3F_MAX_TARGETS);
+    for (int r = 0; r < R; ++r)
+      for (int k = 0; k < alg->M * Nb; ++k) {
+        const double w = alg->Wd[(size_t)k * R + r];
+        if (w == 0.0) continue;
+        K3fTarget& x = tg[(size_t)r * K3F_MAX_TARGETS + count[r]++];
+        x.row_off = (int)((k / Nb) * d.P);
+        x.col_off = (int)((k % Nb) * d.N);
+        x.sign = w > 0 ? 1 : -1;
+        x.pad = 0;
+      }
+    if (const char* e = getenv("FMM_K3F_MAX_TARGETS"))  // timing diagnostics only: drops targets (wrong C)
+      for (int& cnt : count) cnt = std::min(cnt, atoi(e));
+    ln.k3f_count_off = push(count.data(), count.size() * sizeof(int));
+    ln.k3f_targets_off = push(tg.data(), tg.size() * sizeof(K3fTarget));
+    // the reduce-adds, as output traffic: every leaf element once per target
+    for (const auto& t : tasks) ln.elem_writes += (double)t.m * t.n * count[t.aux];
+  }
+  launches.push_back(ln);
 }
 
 // The fused leaf level (fmm_gemm_tma.cu, FUSED kernel).  Jobs: formation (F) of the level-L S / T
@@ -1321,6 +1417,20 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
                   M * K <= 4 && K * Nb <= 4 && M * Nb <= 4 && dl.P1 == dl.P && dl.Q1 == dl.Q && dl.N1 == dl.N;
     if (p->collapse) p->fuse = false;
   }
+  // K3f (fuse_output): W entries 0 / +-1 (the staged tile is added as +acc or -acc), MN <= 16
+  // targets per leaf, one shard (each leaf whole), the plain TMA leaf GEMM.  It replaces the
+  // collapsed levels (whose assembly reads the leaf products) and the fused leaf level.
+  {
+    const char* e = getenv("FMM_K3F");
+    bool want = e ? e[0] == '1' : p->opt.fuse_output != 0;
+    bool unit = true;
+    for (double w : a->Wd) unit &= (w == 0.0 || w == 1.0 || w == -1.0);
+    if (want && L >= 1 && unit && M * Nb <= K3F_MAX_TARGETS && p->opt.shard_count == 1 && p->use_tma) {
+      p->k3f = true;
+      p->collapse = false;
+      p->fuse = false;
+    }
+  }
   p->setup_sharding();
   p->setup_workspace();
   // compile the streaming/write-once kernels for the 16-byte variant now (NVRTC)
@@ -1500,8 +1610,9 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
     dist_reduce_rows(p->dist_comm, p->opt.shard_count, C, crows, ccols, ln.reduce_rows, p->dist_root, p->s_comm);
   };
   // NVTX: one range per launch, named by phase and recursion level (profiling)
-  static const char* const kNvtx[] = {"fmm form A", "fmm form B", "fmm leaf gemm", "fmm assemble", "fmm strips",
-                                      "fmm thin", "fmm fused leaf level", "fmm reduce"};
+  static const char* const kNvtx[] = {"fmm form A", "fmm form B",           "fmm leaf gemm", "fmm assemble", "fmm strips",
+                                      "fmm thin",   "fmm fused leaf level", "fmm reduce",    "fmm zero"};
+  static_assert(sizeof(kNvtx) / sizeof(kNvtx[0]) == Launch::ZERO + 1, "one NVTX name per launch kind");
   char nvtx_name[64];
   nvtxRangePushA(p->dist_comm || p->p2p ? "fmm_execute (distributed)" : "fmm_execute");
   struct NvtxPop {
@@ -1519,7 +1630,7 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
                    : (ln.kind == Launch::GEMM || ln.kind == Launch::FUSED || (ln.kind == Launch::SKINNY && ln.level == p->L))
                        ? 1
                        : 2;
-    const int prof_phase = ph < 2 ? ph : ln.kind == Launch::ASSEMBLE ? 2 : 3;
+    const int prof_phase = ph < 2 ? ph : (ln.kind == Launch::ASSEMBLE || ln.kind == Launch::ZERO) ? 2 : 3;
     if (ln.kind == Launch::SKINNY) {
       const int* ids = reinterpret_cast<const int*>(d_tab + ln.ids_off);
       if (timed && ph != phase) {
@@ -1545,6 +1656,11 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
       case Launch::SKINNY:
       case Launch::REDUCE:
         break;
+      case Launch::ZERO:
+        for (const auto& zb : ln.zero_blocks)
+          FMM_CUDA(cudaMemset2DAsync(reinterpret_cast<void*>((uintptr_t)zb[0]), (size_t)zb[1] * 8, 0, (size_t)zb[3] * 8,
+                                     (size_t)zb[2], ls));
+        break;
       case Launch::FUSED: {
         FusedArgs fa{};
         for (int q = 0; q < ln.nprogs; ++q) {
@@ -1568,7 +1684,14 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
       }
       case Launch::GEMM:
       case Launch::STRIPS:
-        if (ln.tma)
+        if (ln.k3f) {
+          K3fArgs ka;
+          ka.maps = d_tab + ln.k3f_maps_off;
+          ka.count = reinterpret_cast<const int*>(d_tab + ln.k3f_count_off);
+          ka.targets = reinterpret_cast<const K3fTarget*>(d_tab + ln.k3f_targets_off);
+          gemm_k3f_launch(reinterpret_cast<const GemmTask*>(tab), d_tab + ln.maps_off, ln.count, ln.tiles, ln.uni_tm,
+                          ln.uni_tn, ka, ls);
+        } else if (ln.tma)
           gemm_tma_launch(reinterpret_cast<const GemmTask*>(tab), d_tab + ln.maps_off, ln.count, ln.tiles, ln.bn,
                           ln.uni_tm, ln.uni_tn, ls);
         else
@@ -1656,6 +1779,7 @@ void fmm_plan_options_default(fmm_plan_options* o) {
   o->cuda_graphs = 1;
   o->peel_tiles = 0;  // measured: c3 12.60 -> 12.78 ms, c5 258.0 -> 257.3 (R7c)
   o->dist_chunks = 4;
+  o->fuse_output = 0;
 }
 
 fmm_status_t fmm_plan_create(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels,
@@ -1995,6 +2119,17 @@ fmm_status_t fmm_fused_compile_check(const fmm_alg* alg, int layout, int cse, in
   FMM_API_END
 }
 
+fmm_status_t fmm_plan_stats_ex2(const fmm_plan_t* p, double* out, int n) {
+  FMM_API_BEGIN
+  if (!p || !out || n < 0) throw Error(FMM_E_INVALID_ARG, "bad argument");
+  double s[17] = {0};
+  FMM_CHECK_STATUS(fmm_plan_stats_ex(p, s));
+  s[16] = p->k3f ? 1.0 : 0.0;
+  std::memcpy(out, s, sizeof(double) * (size_t)std::min(n, 17));
+  return FMM_OK;
+  FMM_API_END
+}
+
 fmm_status_t fmm_plan_stats_ex(const fmm_plan_t* p, double out[16]) {
   FMM_API_BEGIN
   if (!p || !out) throw Error(FMM_E_INVALID_ARG, "null argument");
@@ -2006,7 +2141,7 @@ fmm_status_t fmm_plan_stats_ex(const fmm_plan_t* p, double out[16]) {
     if (leaf) s[8] += ln.flops;
     if (ln.kind == Launch::FUSED) s[9] += bytes, s[10] += 1;
     if (ln.kind == Launch::FORM_A || ln.kind == Launch::FORM_B) s[11] += bytes;
-    if (ln.kind == Launch::ASSEMBLE) s[12] += bytes;
+    if (ln.kind == Launch::ASSEMBLE || ln.kind == Launch::ZERO || (ln.kind == Launch::GEMM && ln.k3f)) s[12] += bytes;
     if (!leaf && (ln.kind == Launch::STRIPS || ln.kind == Launch::SKINNY)) s[13] += ln.flops;
   }
   s[14] = p->collapse ? 1.0 : 0.0;

@@ -34,7 +34,8 @@ class _Options(ctypes.Structure):
                 ("shard_rank", ctypes.c_int), ("shard_count", ctypes.c_int),
                 ("workspace_limit_bytes", ctypes.c_size_t), ("peel_align", ctypes.c_int),
                 ("fuse_leaf_level", ctypes.c_int), ("shard_mode", ctypes.c_int), ("collapse_levels", ctypes.c_int),
-                ("cuda_graphs", ctypes.c_int), ("peel_tiles", ctypes.c_int), ("dist_chunks", ctypes.c_int)]
+                ("cuda_graphs", ctypes.c_int), ("peel_tiles", ctypes.c_int), ("dist_chunks", ctypes.c_int),
+                ("fuse_output", ctypes.c_int)]
 
 
 # fmm_barrier_fn: int (*)(void* ctx), a host barrier over the ranks of a peer-memory plan
@@ -57,6 +58,7 @@ def _load():
         "fmm_plan_workspace_bytes": [vp, ctypes.POINTER(ctypes.c_size_t)],
         "fmm_plan_stats": [vp, ctypes.POINTER(dp)],
         "fmm_plan_stats_ex": [vp, ctypes.POINTER(dp)],
+        "fmm_plan_stats_ex2": [vp, ctypes.POINTER(dp), i32],
         "fmm_fused_compile_check": [vp, i32, i32, i32],
         "fmm_alg_permute": [vp, i32, ctypes.POINTER(vp)],
         "fmm_nccl_unique_id": [ctypes.c_char_p],
@@ -251,7 +253,8 @@ class Plan:
                  device: Optional[int] = None, workspace_limit_bytes: int = 0, peel_align: bool = True,
                  fuse: bool = False, collapse: bool = True, comm: Optional[Comm] = None, root: int = 0,
                  shard_mode: str = "leaf", cuda_graphs: bool = True, peel_tiles: bool = False,
-                 p2p: Optional["P2P"] = None, barrier=None, dist_chunks: Optional[int] = None):
+                 p2p: Optional["P2P"] = None, barrier=None, dist_chunks: Optional[int] = None,
+                 fuse_output: Optional[bool] = None):
         """comm: an NCCL Comm -> fmm_plan_create_dist (the reduce runs inside execute, in dist_chunks
         overlapped row chunks where it applies).  p2p + barrier: a P2P object and a zero-argument host
         barrier over the same ranks (e.g. torch.distributed.barrier) -> fmm_plan_create_p2p (the
@@ -277,6 +280,8 @@ class Plan:
         o.shard_mode = {"leaf": 0, "top": 1}[shard_mode]
         if dist_chunks is not None:
             o.dist_chunks = int(dist_chunks)
+        if fuse_output is not None:
+            o.fuse_output = int(bool(fuse_output))
         self.device = torch.cuda.current_device() if device is None else device
         h = ctypes.c_void_p()
         self.comm = comm  # a distributed plan keeps its communicator / peer buffers alive
@@ -318,11 +323,11 @@ class Plan:
         return b.value
 
     def stats(self) -> dict:
-        s = (ctypes.c_double * 16)()
-        _check(_lib.fmm_plan_stats_ex(self._h, s))
+        s = (ctypes.c_double * 17)()
+        _check(_lib.fmm_plan_stats_ex2(self._h, s, 17))
         keys = ["gemm_flops", "add_flops", "add_bytes", "gemm_bytes", "launches", "levels", "leaves", "paper_flops",
                 "leaf_flops", "fused_add_bytes", "fused_launches", "formation_bytes", "assembly_bytes", "strip_flops",
-                "collapsed", "tiled_peel"]
+                "collapsed", "tiled_peel", "fused_output"]
         return dict(zip(keys, list(s)))
 
     def new_output(self):
