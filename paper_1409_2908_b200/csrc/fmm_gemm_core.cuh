@@ -43,6 +43,12 @@ typedef CUtensorMap_opaque CUtensorMap;
 #endif
 
 constexpr int BM = 128, BK = 16;
+#ifndef FMM_F1_EMUL_U
+#define FMM_F1_EMUL_U 1
+#endif
+#ifndef FMM_F1_EMUL_V
+#define FMM_F1_EMUL_V 1
+#endif
 #ifndef FMM_GEMM_STAGES
 #define FMM_GEMM_STAGES 6
 #endif
@@ -364,13 +370,29 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
       for (int i = 0; i < MI; ++i) {
         const unsigned x = (i & 1) ? xa1 : xa0;
         const unsigned chunk = ((unsigned)(2 * s) + ca) ^ x;
-        a[i] = lds64(sa + a_row0 + (unsigned)(16 * (i >> 1) + (i & 1)) * 128u + chunk * 16u + ha);
+        const unsigned off = a_row0 + (unsigned)(16 * (i >> 1) + (i & 1)) * 128u + chunk * 16u + ha;
+        a[i] = lds64(sa + off);
+#if FMM_F1_EMUL_U > 1  // timing experiment: a leaf operand formed in registers from
+        // FMM_F1_EMUL_U parent tiles -- extra fragment loads (other rows of the same stage, so the
+        // bank pattern is unchanged) and DADDs on the FP64 pipe the DMMAs use; results are wrong
+#pragma unroll
+        for (int q = 1; q < FMM_F1_EMUL_U; ++q) a[i] = a[i] + lds64(sa + ((off + 2048u * q) & (unsigned)(A_BYTES - 1)));
+#endif
       }
       const unsigned krow = (unsigned)(4 * s + c);
 #pragma unroll
       for (int jj = 0; jj < NI; ++jj) {
         const unsigned chunk = (cb0 + 2u * (jj & 1)) ^ (krow & 7u);
-        b[jj] = lds64(sb + b_box0 + (unsigned)(jj >> 1) * 2048u + krow * 128u + chunk * 16u + hb * 8u);
+        const unsigned off = b_box0 + (unsigned)(jj >> 1) * 2048u + krow * 128u + chunk * 16u + hb * 8u;
+        b[jj] = lds64(sb + off);
+#if FMM_F1_EMUL_V > 1
+#pragma unroll
+        for (int q = 1; q < FMM_F1_EMUL_V; ++q) {
+          unsigned o2 = off + 2048u * q;
+          while (o2 >= (unsigned)B_BYTES_T) o2 -= (unsigned)B_BYTES_T;
+          b[jj] = b[jj] + lds64(sb + o2);
+        }
+#endif
       }
     };
     auto mma = [&](const double (&a)[MI], const double (&b)[NI]) {

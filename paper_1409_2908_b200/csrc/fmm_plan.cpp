@@ -164,6 +164,7 @@ struct fmm_plan_s {
   bool profile_launches = false;
   std::vector<cudaEvent_t> ev_l;
   std::vector<int> ev_l_phase;
+  std::vector<int> ev_l_kind, ev_l_level;  // the launch behind each event (kind, recursion level)
 
   // host-execute staging: two buffer sets, copy-in / copy-out streams, ordering events
   double *sA[2] = {nullptr, nullptr}, *sB[2] = {nullptr, nullptr}, *sC[2] = {nullptr, nullptr};
@@ -1585,15 +1586,19 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
     if (!p->s_comm) FMM_CUDA(cudaStreamCreateWithFlags(&p->s_comm, cudaStreamNonBlocking));
   }
   int nl = 0;  // profile_launches: events recorded so far
-  auto mark = [&](int phase_of_launch) {
+  auto mark = [&](int phase_of_launch, int kind = -1, int level = -1) {
     if (!p->profile_launches) return;
     if ((int)p->ev_l.size() <= nl) {
       cudaEvent_t e;
       FMM_CUDA(cudaEventCreate(&e));
       p->ev_l.push_back(e);
       p->ev_l_phase.push_back(0);
+      p->ev_l_kind.push_back(-1);
+      p->ev_l_level.push_back(-1);
     }
     p->ev_l_phase[nl] = phase_of_launch;
+    p->ev_l_kind[nl] = kind;
+    p->ev_l_level[nl] = level;
     FMM_CUDA(cudaEventRecord(p->ev_l[nl++], ls));
   };
   mark(-1);  // start
@@ -1639,7 +1644,7 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
       }
       skinny_launch(reinterpret_cast<const GemmTask*>(d_tab + ln.table_off), ids, ln.nrow, ln.max_n, ids + ln.nrow,
                     ln.ncol, ln.max_m, ls);
-      mark(prof_phase);
+      mark(prof_phase, (int)ln.kind, ln.level);
       continue;
     }
     if (timed && ph != phase) {
@@ -1698,7 +1703,7 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
           gemm_launch(reinterpret_cast<const GemmTask*>(tab), ln.count, ln.tiles, ln.aligned16, ls);
         break;
     }
-    mark(prof_phase);
+    mark(prof_phase, (int)ln.kind, ln.level);
     reduce_after(ln);
   }
   if (capture) {
@@ -1753,8 +1758,12 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
       FMM_CUDA(cudaEventCreate(&e));
       p->ev_l.push_back(e);
       p->ev_l_phase.push_back(0);
+      p->ev_l_kind.push_back(-1);
+      p->ev_l_level.push_back(-1);
     }
     p->ev_l_phase[nl] = 4;
+    p->ev_l_kind[nl] = Launch::REDUCE;
+    p->ev_l_level[nl] = 0;
     FMM_CUDA(cudaEventRecord(p->ev_l[nl++], stream));
   }
   if (p->profile_launches) p->ev_l_phase.resize(nl);
@@ -2195,6 +2204,30 @@ fmm_status_t fmm_execute_timed(fmm_plan_t* p, const double* A, int64_t lda, cons
   float total = 0;
   if (p->ev_l_phase.size() > 1) FMM_CUDA(cudaEventElapsedTime(&total, p->ev_l[0], p->ev_l[p->ev_l_phase.size() - 1]));
   ms[4] = total;
+  return FMM_OK;
+  FMM_API_END
+}
+
+fmm_status_t fmm_execute_profile(fmm_plan_t* p, const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                                 int64_t ldc, void* stream, int max, int* kind, int* level, float* ms, int* n) {
+  FMM_API_BEGIN
+  if (!p || !n || max < 0 || (max > 0 && (!kind || !level || !ms))) throw Error(FMM_E_INVALID_ARG, "bad argument");
+  p->profile_launches = true;
+  struct Off {
+    fmm_plan_t* p;
+    ~Off() { p->profile_launches = false; }
+  } off{p};
+  run(p, A, lda, B, ldb, C, ldc, (cudaStream_t)stream, p->ev);
+  FMM_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  const int cnt = (int)p->ev_l_phase.size() - 1;
+  *n = std::max(cnt, 0);
+  for (int q = 0; q < std::min(cnt, max); ++q) {
+    float t = 0;
+    FMM_CUDA(cudaEventElapsedTime(&t, p->ev_l[q], p->ev_l[q + 1]));
+    ms[q] = t;
+    kind[q] = p->ev_l_kind[q + 1];
+    level[q] = p->ev_l_level[q + 1];
+  }
   return FMM_OK;
   FMM_API_END
 }

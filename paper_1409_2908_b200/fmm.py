@@ -75,6 +75,8 @@ def _load():
         "fmm_execute_timed": [vp, vp, i64, vp, i64, vp, i64, vp, ctypes.POINTER(ctypes.c_float)],
         "fmm_execute_host": [vp, vp, i64, vp, i64, vp, i64, vp],
         "fmm_execute_events": [vp, vp, i64, vp, i64, vp, i64, vp, ctypes.POINTER(vp)],
+        "fmm_execute_profile": [vp, vp, i64, vp, i64, vp, i64, vp, i32, ctypes.POINTER(i32), ctypes.POINTER(i32),
+                                ctypes.POINTER(ctypes.c_float), ctypes.POINTER(i32)],
         "fmm_execute_host_async": [vp, vp, i64, vp, i64, vp, i64, vp],
         "fmm_probe_fp64_peak": [ctypes.POINTER(dp), ctypes.POINTER(dp)],
         "fmm_sync": [vp],
@@ -359,6 +361,21 @@ class Plan:
         _check(_lib.fmm_execute_timed(self._h, *self._args(A, B, C), _stream_ptr(stream), ms))
         return C, {"formation_ms": ms[0], "gemm_ms": ms[1], "assembly_ms": ms[2], "strips_ms": ms[3],
                    "total_ms": ms[4]}
+
+    KINDS = ["form_A", "form_B", "leaf_gemm", "assembly", "strips", "thin", "fused_leaf_level", "combine", "zero"]
+
+    def execute_profile(self, A, B, C=None, stream=None, max_launches=256):
+        """Blocking diagnostic execute (fmm_execute_profile): [(kind, level, ms)] per launch."""
+        if C is None:
+            C = self.new_output()
+        kind = (ctypes.c_int * max_launches)()
+        level = (ctypes.c_int * max_launches)()
+        ms = (ctypes.c_float * max_launches)()
+        n = ctypes.c_int()
+        _check(_lib.fmm_execute_profile(self._h, *self._args(A, B, C), _stream_ptr(stream), max_launches, kind, level,
+                                        ms, ctypes.byref(n)))
+        return [(self.KINDS[kind[q]] if 0 <= kind[q] < len(self.KINDS) else str(kind[q]), level[q], ms[q])
+                for q in range(min(n.value, max_launches))]
 
     def execute_events(self, A, B, C, events, stream=None):
         """Asynchronous execute that records 4 torch.cuda.Event on the stream: before, after
