@@ -249,6 +249,16 @@ fmm_status_t fmm_plan_create_p2p(const fmm_alg* alg, int64_t P, int64_t Q, int64
    [*first, *last) of C (row-major) or columns [*first, *last) (column-major).  Host only. */
 fmm_status_t fmm_dist_slab(int64_t P, int64_t Nc, int layout, int nranks, int rank, int64_t* first, int64_t* last);
 
+/* Which top-level blocks of A and B this plan reads (host only): a sharded plan (leaf or top-level
+   mode) forms only the level-1 S_r / T_r of the products it owns, so it reads A-block (a, b) only if
+   u_{(a,b) r} != 0 for one of them (likewise B).  needA has M*K entries (row a*K + b of the caller's
+   base case <M,K,N>), needB K*N; core = {P', Q', N'}, the block grid's extent (the blocks are
+   P'/M x Q'/K and Q'/K x N'/N); *need_all = 1 when the plan also reads the peeled edges (it owns the
+   top-level peel strips) or has no recursion, i.e. all of A and B.  Used to send each rank only
+   the input blocks it reads. */
+fmm_status_t fmm_plan_input_blocks(const fmm_plan_t* plan, uint8_t* needA, uint8_t* needB, int64_t core[3],
+                                   int* need_all);
+
 /* Workspace bytes held by the plan. */
 fmm_status_t fmm_plan_workspace_bytes(const fmm_plan_t* plan, size_t* bytes);
 

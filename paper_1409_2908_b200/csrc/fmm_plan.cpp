@@ -1868,6 +1868,41 @@ fmm_status_t fmm_plan(const fmm_alg* alg, int64_t M, int64_t K, int64_t N, int l
   return fmm_plan_create(alg, M, K, N, levels, nullptr, dev, out);
 }
 
+fmm_status_t fmm_plan_input_blocks(const fmm_plan_t* p, uint8_t* needA, uint8_t* needB, int64_t core[3], int* need_all) {
+  FMM_API_BEGIN
+  if (!p || !needA || !needB || !core || !need_all) throw Error(FMM_E_INVALID_ARG, "null argument");
+  const fmm_alg* a = p->alg;  // plan orientation (the Prop. 1 transpose for column-major plans)
+  const int M = a->M, K = a->K, Nb = a->N, R = a->R;
+  std::vector<uint8_t> pa((size_t)M * K, 0), pb((size_t)K * Nb, 0);
+  const Dims& d0 = p->dims[0];
+  const bool strips = d0.P1 < d0.P || d0.Q1 < d0.Q || d0.N1 < d0.N;
+  bool all = p->L < 1 || (strips && p->strip_owner[0][0]);
+  if (!all)
+    for (int r = 0; r < R; ++r) {
+      if (!p->needed[1][r]) continue;
+      for (int i = 0; i < M * K; ++i) pa[i] |= a->Ud[(size_t)i * R + r] != 0.0;
+      for (int j = 0; j < K * Nb; ++j) pb[j] |= a->Vd[(size_t)j * R + r] != 0.0;
+    }
+  if (all) std::fill(pa.begin(), pa.end(), 1), std::fill(pb.begin(), pb.end(), 1);
+  // back to the caller's orientation: column-major plans multiply B^T A^T with <N,K,M>, so the plan's
+  // A block (c, b) is the caller's B block (b, c) and the plan's B block (b, a) the caller's A block (a, b)
+  if (!p->colmajor) {
+    std::copy(pa.begin(), pa.end(), needA);
+    std::copy(pb.begin(), pb.end(), needB);
+    core[0] = d0.P1, core[1] = d0.Q1, core[2] = d0.N1;
+  } else {
+    const int uM = Nb, uN = M;  // the caller's base case is <Nb, K, M> of the plan's <M, K, Nb>
+    for (int b = 0; b < K; ++b)
+      for (int c = 0; c < uN; ++c) needB[b * uN + c] = pa[c * K + b];
+    for (int x = 0; x < uM; ++x)
+      for (int b = 0; b < K; ++b) needA[x * K + b] = pb[b * Nb + x];
+    core[0] = d0.N1, core[1] = d0.Q1, core[2] = d0.P1;
+  }
+  *need_all = all ? 1 : 0;
+  return FMM_OK;
+  FMM_API_END
+}
+
 fmm_status_t fmm_plan_workspace_bytes(const fmm_plan_t* p, size_t* bytes) {
   FMM_API_BEGIN
   if (!p || !bytes) throw Error(FMM_E_INVALID_ARG, "null argument");

@@ -56,6 +56,8 @@ def _load():
         "fmm_plan_create": [vp, i64, i64, i64, i32, ctypes.POINTER(_Options), i32, ctypes.POINTER(vp)],
         "fmm_plan": [vp, i64, i64, i64, i32, ctypes.POINTER(vp)],
         "fmm_plan_workspace_bytes": [vp, ctypes.POINTER(ctypes.c_size_t)],
+        "fmm_plan_input_blocks": [vp, ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(ctypes.c_uint8), p64,
+                                  ctypes.POINTER(i32)],
         "fmm_plan_stats": [vp, ctypes.POINTER(dp)],
         "fmm_plan_stats_ex": [vp, ctypes.POINTER(dp)],
         "fmm_plan_stats_ex2": [vp, ctypes.POINTER(dp), i32],
@@ -323,6 +325,17 @@ class Plan:
         b = ctypes.c_size_t()
         _check(_lib.fmm_plan_workspace_bytes(self._h, ctypes.byref(b)))
         return b.value
+
+    def input_blocks(self):
+        """(needA, needB, (P', Q', N'), need_all): the top-level blocks of A (M*K flags, row-major over
+        the block grid) and B (K*N) this plan reads (fmm_plan_input_blocks)."""
+        a = self.alg
+        na = (ctypes.c_uint8 * (a.M * a.K))()
+        nb = (ctypes.c_uint8 * (a.K * a.N))()
+        core = (ctypes.c_int64 * 3)()
+        allf = ctypes.c_int()
+        _check(_lib.fmm_plan_input_blocks(self._h, na, nb, core, ctypes.byref(allf)))
+        return [bool(x) for x in na], [bool(x) for x in nb], tuple(core), bool(allf.value)
 
     def stats(self) -> dict:
         s = (ctypes.c_double * 17)()

@@ -445,3 +445,42 @@ def test_distributed_plan_chunked_reduce(alg, shape, layout, chunks, root):
         assert np.array_equal(C.cpu().numpy(), A @ B)
     _, t = p.execute_timed(dev(A, layout), dev(B, layout), C)
     assert t["gemm_ms"] > 0 and t["total_ms"] >= t["gemm_ms"]
+
+
+@pytest.mark.parametrize("alg,shape,layout,mode,G", [("alg_424_26", (640, 200, 640), "row", "top", 3),
+                                                     ("hk_class_323_15", (361, 120, 363), "col", "top", 4),
+                                                     ("winograd_class_222_7", (256, 256, 256), "row", "leaf", 4),
+                                                     ("alg_433_29", (480, 96, 96), "row", "leaf", 8)])
+def test_shard_reads_only_its_input_blocks(alg, shape, layout, mode, G):
+    # fmm_plan_input_blocks: a shard reads only the top-level A / B blocks its level-1 products touch
+    # (send a rank only those).  Poison every other block -- and the peeled edges unless
+    # the shard owns the top-level strips -- with NaN: the shard's partial product must not change.
+    P, Q, N = shape
+    A, B = I.problem(P, Q, N, seed=24, kind="integers")
+    a = falg(alg)
+    restricted = 0
+    for g in range(G):
+        p = F.Plan(a, P, Q, N, 2, layout=layout, shard_rank=g, shard_count=G, shard_mode=mode)
+        needA, needB, (P1, Q1, N1), need_all = p.input_blocks()
+        clean = p.execute(dev(A, layout), dev(B, layout)).cpu().numpy()
+        if need_all:
+            continue
+        Ap, Bp = A.copy(), B.copy()
+        pb, qb, nb = P1 // a.M, Q1 // a.K, N1 // a.N
+        keepA = np.zeros_like(A, dtype=bool)
+        keepB = np.zeros_like(B, dtype=bool)
+        for i, need in enumerate(needA):
+            if need:
+                x, y = divmod(i, a.K)
+                keepA[x * pb:(x + 1) * pb, y * qb:(y + 1) * qb] = True
+        for j, need in enumerate(needB):
+            if need:
+                x, y = divmod(j, a.N)
+                keepB[x * qb:(x + 1) * qb, y * nb:(y + 1) * nb] = True
+        Ap[~keepA] = np.nan
+        Bp[~keepB] = np.nan
+        restricted += int(not (keepA.all() and keepB.all()))
+        got = p.execute(dev(Ap, layout), dev(Bp, layout)).cpu().numpy()
+        assert np.array_equal(got, clean), (g, np.isnan(got).sum())
+    print(f"{alg} {mode} G={G}: {restricted} of {G} shards read a strict subset of A and B")
+    assert restricted >= 1  # measured: 2 of 3, 3 of 4, 2 of 4, 8 of 8 for the four cases
