@@ -73,7 +73,10 @@ __global__ void __launch_bounds__(256) skinny_rows(const GemmTask* __restrict__ 
 // through shared memory in k-chunks; lanes split k and read A rows coalesced, 16 bytes at a time
 // when A is 16-byte aligned with an even lda, with up to 16 loads in flight per lane; each lane
 // accumulates all n outputs of its rows, then a warp shuffle reduction.
-constexpr int KC = 256, ROWS_PER_WARP = 2;
+#ifndef FMM_SKINNY_RPW
+#define FMM_SKINNY_RPW 2
+#endif
+constexpr int KC = 256, ROWS_PER_WARP = FMM_SKINNY_RPW;
 __global__ void __launch_bounds__(256) skinny_cols(const GemmTask* __restrict__ tasks, const int* __restrict__ ids,
                                                    int count) {
   __shared__ double bt[THIN][KC];
