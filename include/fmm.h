@@ -100,6 +100,9 @@ typedef struct {
                                one streaming pass each (the level-(L-1) S_r, T_r and M_r are never
                                written to HBM: DESIGN.md sec. 6c), where it applies: streaming,
                                L >= 2, a base case with MK, KN, MN <= 4, no peeling at level L-1.
+                               (With the environment variable FMM_WIDE_ASM=1, also the assembly
+                               alone for base cases up to MN <= 16, no fused leaf level: DESIGN.md
+                               sec. 6g; measured slower than the separate levels, so off.)
                                The chains are the oracle's two levels exactly (CSE is not used
                                there).  0: one level per launch. */
   int cuda_graphs;          /* 1: the second and later fmm_execute calls with the same A/B/C
@@ -285,8 +288,11 @@ fmm_status_t fmm_plan_stats(const fmm_plan_t* plan, double out[8]);
    [15] 1 if the last split's rows were peeled to 128-row-aligned leaves (peel_tiles, R7c) */
 fmm_status_t fmm_plan_stats_ex(const fmm_plan_t* plan, double out[16]);
 
-/* The same, extensible: fills out[0 .. min(n, 17) - 1]; out[0..15] as fmm_plan_stats_ex, then
-   [16] 1 if the output step is fused into the leaf GEMM (fuse_output applied), else 0. */
+/* The same, extensible: fills out[0 .. min(n, 18) - 1]; out[0..15] as fmm_plan_stats_ex, then
+   [16] 1 if the output step is fused into the leaf GEMM (fuse_output applied), else 0;
+   [17] 1 if the last two levels' assembly runs as one pass (collapse_levels: with the formation for
+        the <2,2,2> family, or alone -- the wide warp-per-column kernel, FMM_WIDE_ASM=1 -- for base
+        cases with MN <= 16), else 0. */
 fmm_status_t fmm_plan_stats_ex2(const fmm_plan_t* plan, double* out, int n);
 
 /* Cost model (host only, no allocation): predicted milliseconds of a plan of `alg` for the problem

@@ -97,6 +97,9 @@ struct LincombKernel {
   LincombCost cost{};
   int temps = 0;
   bool row_grid = false;  // 2-D grid (column segments x rows) instead of the flattened map
+  int warp_rows = 0;      // > 0: the wide two-level assembly -- warp_rows warps per block, one per
+                          // output column k2 of W, 32 vector positions per block (x), rows (y)
+  int dyn_smem = 0;       // dynamic shared memory of the launch (the wide assembly's cp.async ring)
 };
 
 namespace {
@@ -313,6 +316,11 @@ void compile(LincombKernel& k) {
   nvrtcDestroyProgram(&prog);
   FMM_CUDA(cudaLibraryLoadData(&k.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
   FMM_CUDA(cudaLibraryGetKernel(&k.kern, k.lib, "lincomb"));
+  if (k.dyn_smem > 48 * 1024) {
+    int dev = 0;
+    FMM_CUDA(cudaGetDevice(&dev));
+    FMM_CUDA(cudaKernelSetAttributeForDevice(k.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, k.dyn_smem, dev));
+  }
 }
 
 std::mutex g_mu;
@@ -348,6 +356,14 @@ void lincomb_launch(const LincombKernel& k, const void* d_nodes, int nnodes, lon
   if (total >= (1ll << 32)) throw Error(FMM_E_UNSUPPORTED, "lincomb: block too large for one launch");
   // one position per thread; the kernel's grid-stride loop form is kept (measured: 2-8 positions
   // per thread were 1-7 % slower, while the loop form alone took c5t's assembly 0.97 -> 0.87 ms)
+  if (k.warp_rows > 0) {
+    const dim3 g((unsigned)((cvec + 31) / 32), (unsigned)std::min<long long>(rows, 65535), (unsigned)nnodes);
+    int r = (int)rows, c = (int)cvec;
+    unsigned long long magic = 0;
+    void* args[] = {(void*)&d_nodes, &r, &c, &magic};
+    FMM_CUDA(cudaLaunchKernel((const void*)k.kern, g, dim3(32 * k.warp_rows), args, (size_t)k.dyn_smem, stream));
+    return;
+  }
   dim3 grid = k.row_grid ? dim3((unsigned)((cvec + k.threads - 1) / k.threads), (unsigned)std::min<long long>(rows, 65535),
                                  (unsigned)zdim)
                          : dim3((unsigned)((total + k.threads - 1) / k.threads), 1, (unsigned)zdim);
@@ -720,6 +736,137 @@ std::string generate_two_level(const TwoLevelSpec& sp, LincombCost& cost) {
   cost.writes_per_elem = writes;
   return asm_row_grid ? o.str() : stage_pointers(o.str(), nin, nout);
 }
+// The two-level assembly for base cases too large to hold the (MN)^2 outputs of a position in one
+// thread's registers (MN > 4): C[k1][k2] = sum_r1 W[k1][r1] M1[r1][k2], M1[r1][k2] =
+// sum_r2 W[k2][r2] M[r1][r2] (P:569-572 applied twice), the oracle's two levels in its order.
+// A block owns 32 vector positions of one row of the level-L blocks and has one warp per output
+// column k2 (warp-uniform chains).  For each r1 in order, the warps stage the R leaf products
+// M[r1][.] of the block's positions in shared memory (each element read from HBM once; the next r1's
+// loads are issued before this r1's arithmetic), then warp k2 forms M1[r1][k2] from shared memory and
+// adds it into its MN accumulators C[k1][k2], k1 with W[k1][r1] != 0.  HBM traffic: R^2 reads and
+// (MN)^2 writes per position, against R^2 + 2 R MN + (MN)^2 for the two separate levels.
+// two positions per thread (double2), one block per SM (the MN accumulators take the registers), a
+// ring of up to 96 KB.  Measured (c4): 2.30 ms, against 2.67 ms for one position per thread with two
+// blocks per SM and 2.05 ms for the two separate assembly levels.
+constexpr int WIDE_VEC = 2, WIDE_BLOCKS_PER_SM = 1;
+int wide_stages(int stage_bytes) { return std::max(3, std::min(8, 96 * 1024 / stage_bytes)); }
+
+std::string generate_two_level_wide(const TwoLevelSpec& sp, LincombCost& cost) {
+  const int rows = sp.rows, R = sp.R, V = sp.vec;
+  const std::string T = V == 2 ? "double2" : "double";
+  std::vector<std::string> comps = V == 2 ? std::vector<std::string>{".x", ".y"} : std::vector<std::string>{""};
+  auto X = [&](int i, int r) { return sp.X[(size_t)i * R + r]; };
+  const int per = (R + rows - 1) / rows;  // leaf products each warp stages per r1
+  // stages of the cp.async ring: as deep as ~96 KB of shared memory allows (one block per SM: the
+  // accumulators take the registers), so enough bytes are in flight to keep HBM busy
+  const int stage_bytes = R * 32 * 8 * V;
+  const int D = wide_stages(stage_bytes);
+  std::ostringstream o;
+  o << "// generated by fmm_codegen.cpp: wide two-level assembly rows=" << rows << " R=" << R << " vec=" << V << " stages=" << D << "\n";
+  o << "struct Node { const double* in[" << R * R << "]; double* out[" << rows * rows << "]; long long ld_in; long long ld_out; };\n";
+  o << "__device__ __forceinline__ void cpa(void* dst, const double* src) {\n";
+  if (V == 2)
+    o << "  asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\" :: \"r\"((unsigned)__cvta_generic_to_shared(dst)), \"l\"(src) : \"memory\");\n";
+  else
+    o << "  asm volatile(\"cp.async.ca.shared.global [%0], [%1], 8;\" :: \"r\"((unsigned)__cvta_generic_to_shared(dst)), \"l\"(src) : \"memory\");\n";
+  o << "}\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(" << 32 * rows << ", " << WIDE_BLOCKS_PER_SM << ") lincomb(const Node* __restrict__ nodes, int nrows, int cvec, unsigned long long magic) {\n";
+  o << "  extern __shared__ " << T << " smd[];  // [" << D << "][" << R << "][32]\n";
+  o << "  const Node& nd = nodes[blockIdx.z];\n";
+  o << "  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;\n";
+  o << "  const int cv = blockIdx.x * 32 + lane;\n";
+  o << "  const bool live = cv < cvec;\n";
+  o << "  for (int row = blockIdx.y; row < nrows; row += gridDim.y) {\n";
+  o << "    const long long pi = (long long)row * nd.ld_in + (long long)cv * " << V << ";\n";
+  o << "    const long long po = (long long)row * nd.ld_out + (long long)cv * " << V << ";\n";
+  // issue the copies of step r (this warp's leaf products r2 = warp + rows q) into its ring slot
+  o << "    auto issue = [&](int r) {\n";
+  o << "      " << T << "* buf = smd + (r % " << D << ") * " << R * 32 << ";\n";
+  for (int q = 0; q < per; ++q)
+    o << "      { const int r2 = warp + " << rows * q << "; if (r2 < " << R << " && live) cpa(buf + r2 * 32 + lane, nd.in[r * " << R
+      << " + r2] + pi); }\n";
+  o << "      asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n";
+  o << "    };\n";
+  for (int d = 0; d < D - 1; ++d) o << "    if (" << d << " < " << R << ") issue(" << d << "); else asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n";
+  o << "    " << T << " acc[" << rows << "];\n";
+  o << "    for (int r1 = 0; r1 < " << R << "; ++r1) {\n";
+  o << "      asm volatile(\"cp.async.wait_group " << D - 2 << ";\" ::: \"memory\");\n";
+  o << "      __syncthreads();  // step r1 staged by every warp; every warp is done with step r1 - 1\n";
+  o << "      if (r1 + " << D - 1 << " < " << R << ") issue(r1 + " << D - 1 << ");  // into the slot of step r1 - 1\n";
+  o << "      else asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n";
+  o << "      const " << T << "* sm = smd + (r1 % " << D << ") * " << R * 32 << ";\n";
+  o << "      " << T << " u;\n";
+  // M1[r1][k2] for k2 = warp: a warp-uniform switch over the generated chains
+  o << "      switch (warp) {\n";
+  for (int k2 = 0; k2 < rows; ++k2) {
+    o << "      case " << k2 << ": {\n";
+    bool first = true;
+    for (int r2 = 0; r2 < R; ++r2) {
+      const double w = X(k2, r2);
+      if (w == 0.0) continue;
+      for (auto& c : comps) {
+        const std::string v = "sm[" + std::to_string(r2 * 32) + " + lane]" + c;
+        if (first) o << "        u" << c << " = " << (w == 1.0 ? v : w == -1.0 ? "-" + v : dlit(w) + " * " + v) << ";\n";
+        else o << "        u" << c << " = u" << c << (w == 1.0 ? " + " + v : w == -1.0 ? " - " + v : " + " + dlit(w) + " * " + v) << ";\n";
+      }
+      first = false;
+    }
+    if (first)
+      for (auto& c : comps) o << "        u" << c << " = 0.0;\n";
+    o << "        break; }\n";
+  }
+  o << "      }\n";
+  // accumulate: a uniform switch over r1 (the first term of each k1 initialises)
+  o << "      switch (r1) {\n";
+  std::vector<int> firstr(rows, -1);
+  for (int k1 = 0; k1 < rows; ++k1)
+    for (int r1 = 0; r1 < R; ++r1)
+      if (X(k1, r1) != 0.0) {
+        firstr[k1] = r1;
+        break;
+      }
+  for (int r1 = 0; r1 < R; ++r1) {
+    o << "      case " << r1 << ":\n";
+    for (int k1 = 0; k1 < rows; ++k1) {
+      const double w = X(k1, r1);
+      if (w == 0.0) continue;
+      for (auto& c : comps) {
+        const std::string d = "acc[" + std::to_string(k1) + "]" + c, v = "u" + c;
+        if (firstr[k1] == r1) o << "        " << d << " = " << (w == 1.0 ? v : w == -1.0 ? "-" + v : dlit(w) + " * " + v) << ";\n";
+        else o << "        " << d << " = " << d << (w == 1.0 ? " + " + v : w == -1.0 ? " - " + v : " + " + dlit(w) + " * " + v) << ";\n";
+      }
+    }
+    o << "        break;\n";
+  }
+  o << "      }\n";
+  o << "    }\n";
+  o << "    if (live) {\n";
+  for (int k1 = 0; k1 < rows; ++k1) {
+    if (firstr[k1] < 0)
+      for (auto& c : comps) o << "      acc[" << k1 << "]" << c << " = 0.0;\n";
+    o << "      __stcs((" << T << "*)(nd.out[" << k1 << " * " << rows << " + warp] + po), acc[" << k1 << "]);\n";
+  }
+  o << "    }\n";
+  o << "    __syncthreads();  // the next row's prologue reuses the ring\n";
+  o << "  }\n}\n";
+  // per element position (all warps together): R^2 reads, (MN)^2 writes; additions of every chain
+  double chain_adds = 0;
+  for (int k2 = 0; k2 < rows; ++k2) {
+    int t = 0;
+    for (int r2 = 0; r2 < R; ++r2) t += X(k2, r2) != 0.0;
+    chain_adds += t > 0 ? t - 1 : 0;
+  }
+  double acc_adds = 0;
+  for (int k1 = 0; k1 < rows; ++k1) {
+    int t = 0;
+    for (int r1 = 0; r1 < R; ++r1) t += X(k1, r1) != 0.0;
+    acc_adds += t > 0 ? t - 1 : 0;
+  }
+  cost.adds_per_elem = R * chain_adds + rows * acc_adds;
+  cost.reads_per_elem = (double)R * R;
+  cost.writes_per_elem = (double)rows * rows;
+  return o.str();
+}
 }  // namespace
 
 std::shared_ptr<LincombKernel> twolevel_get(const TwoLevelSpec& spec) {
@@ -731,8 +878,17 @@ std::shared_ptr<LincombKernel> twolevel_get(const TwoLevelSpec& spec) {
   k->spec.nout = spec.side == 2 ? spec.rows * spec.rows : spec.R * spec.R;
   k->spec.vec = spec.vec;
   k->spec.strategy = FMM_ADD_STREAMING;
-  k->source = generate_two_level(spec, k->cost);
+  const bool wide = spec.side == 2 && spec.rows > 4;
+  TwoLevelSpec sp = spec;
+  if (wide) sp.vec = std::min(WIDE_VEC, spec.vec);  // 16-byte vectors only where the views allow them
+  k->spec.vec = sp.vec;
+  k->source = wide ? generate_two_level_wide(sp, k->cost) : generate_two_level(sp, k->cost);
   k->row_grid = spec.side == 2;
+  k->warp_rows = wide ? spec.rows : 0;
+  if (wide) {
+    const int stage_bytes = sp.R * 32 * 8 * sp.vec;
+    k->dyn_smem = wide_stages(stage_bytes) * stage_bytes;
+  }
   std::lock_guard<std::mutex> lock(g_mu);
   auto it = g_cache.find(k->source);
   if (it != g_cache.end()) return it->second;

@@ -129,6 +129,8 @@ struct fmm_plan_s {
   bool use_tma = true;  // FMM_NO_TMA=1 forces the cp.async GEMM (diagnostics)
   bool fuse = true;     // fuse_leaf_level option (FMM_NO_FUSE=1 overrides)
   bool collapse = false;  // the last two levels' formation / assembly in one pass each (sec. 6c)
+  bool collapse_asm = false;  // the last two levels' assembly in one pass (with collapse, or the wide
+                              // warp-per-column kernel for base cases with MN up to 16, sec. 6g)
   bool k3f = false;       // fuse_output: the level-L output step in the leaf GEMM's epilogue (K3f)
   bool tiled_peel = false;  // R7c: the last split's rows were peeled to 128-row-aligned leaves
   unsigned long long* d_ctr = nullptr;  // fused launch counters: claim0, claim1, ready[np], tiles[np]
@@ -327,6 +329,7 @@ struct fmm_plan_s {
       offM[l].assign(nodes_at[l], -1);
       bool any_unneeded = false;
       if (collapse && l == L - 1) continue;  // never materialised (sec. 6c)
+      const bool noM = collapse_asm && l == L - 1;  // the collapsed assembly never writes M at L-1
       for (long long z = 0; z < nodes_at[l]; ++z) {
         const int r = (int)(z % R);
         if (!needed[l][z]) {
@@ -339,9 +342,9 @@ struct fmm_plan_s {
         const bool formB = collapse && l == L ? (idxV[r] >= 0 || idxV[r1] >= 0) : idxV[r] >= 0;
         if (formA) offS[l][z] = take(d.P * ldS[l]);
         if (formB) offT[l][z] = take(d.Q * ldT[l]);
-        offM[l][z] = take(d.P * ldM[l]);
+        if (!noM) offM[l][z] = take(d.P * ldM[l]);
       }
-      if (any_unneeded) offZero[l] = take(d.P * ldM[l]);
+      if (any_unneeded && !noM) offZero[l] = take(d.P * ldM[l]);
     }
     ws_bytes = (size_t)total * sizeof(double);
     if (opt.workspace_limit_bytes && ws_bytes > opt.workspace_limit_bytes)
@@ -670,8 +673,8 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
   for (int l = L; l >= 1; --l) {
     const Dims& d = dims[l];
     const Dims& dp = dims[l - 1];
-    if (collapse && l == L) emit_two_level_assembly(lazy_kernels);
-    if (!(collapse && l >= L - 1) && !(k3f && l == L) && d.P > 0 && d.N > 0) {
+    if (collapse_asm && l == L) emit_two_level_assembly(lazy_kernels);
+    if (!(collapse_asm && l >= L - 1) && !(k3f && l == L) && d.P > 0 && d.N > 0) {
       std::vector<char> tab;
       std::vector<int> node_ids;
       const int nin = R, nout = M * Nb;
@@ -1417,6 +1420,14 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
     p->collapse = p->opt.collapse_levels && !(e && e[0] == '1') && L >= 2 && p->opt.strategy == FMM_ADD_STREAMING &&
                   M * K <= 4 && K * Nb <= 4 && M * Nb <= 4 && dl.P1 == dl.P && dl.Q1 == dl.Q && dl.N1 == dl.N;
     if (p->collapse) p->fuse = false;
+    p->collapse_asm = p->collapse;
+    // the assembly alone for larger base cases (MN <= 16): the wide warp-per-column kernel (sec. 6g).
+    // It halves the assembly's HBM bytes but runs shared-memory bound at about half the HBM rate, so
+    // it measured slower than the two separate levels on c4 and c5t: only on request (FMM_WIDE_ASM=1)
+    const char* w = getenv("FMM_WIDE_ASM");
+    if (!p->collapse && w && w[0] == '1' && p->opt.collapse_levels && !(e && e[0] == '1') && !p->fuse && L >= 2 &&
+        p->opt.strategy == FMM_ADD_STREAMING && M * Nb <= 16 && dl.P1 == dl.P && dl.Q1 == dl.Q && dl.N1 == dl.N)
+      p->collapse_asm = true;
   }
   // K3f (fuse_output): W entries 0 / +-1 (the staged tile is added as +acc or -acc), MN <= 16
   // targets per leaf, one shard (each leaf whole), the plain TMA leaf GEMM.  It replaces the
@@ -1429,6 +1440,7 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
     if (want && L >= 1 && unit && M * Nb <= K3F_MAX_TARGETS && p->opt.shard_count == 1 && p->use_tma) {
       p->k3f = true;
       p->collapse = false;
+      p->collapse_asm = false;
       p->fuse = false;
     }
   }
@@ -1985,8 +1997,11 @@ double predict_dims(const fmm_alg& a, const std::vector<PlanDims>& dims) {
   const int fu = formed_columns(a.Ud, M * K, R), fv = formed_columns(a.Vd, K * Nb, R);
   using D = PlanDims;
   // collapsed last two levels (collapse_levels, as plan_init decides it)
-  const bool collapse = L >= 2 && M * K <= 4 && K * Nb <= 4 && M * Nb <= 4 && dims[L - 1].P1 == dims[L - 1].P &&
-                        dims[L - 1].Q1 == dims[L - 1].Q && dims[L - 1].N1 == dims[L - 1].N;
+  const bool nopeel = L >= 2 && dims[L - 1].P1 == dims[L - 1].P && dims[L - 1].Q1 == dims[L - 1].Q &&
+                      dims[L - 1].N1 == dims[L - 1].N;
+  const bool collapse = nopeel && M * K <= 4 && K * Nb <= 4 && M * Nb <= 4;
+  const char* wide = getenv("FMM_WIDE_ASM");  // the wide two-level assembly (sec. 6g), on request only
+  const bool collapse_asm = collapse || (nopeel && M * Nb <= 16 && wide && wide[0] == '1');
   auto materialized = [&](const std::vector<double>& X, int rows) {
     std::vector<int> sing(R);
     for (int r = 0; r < R; ++r) {
@@ -2015,6 +2030,13 @@ double predict_dims(const fmm_alg& a, const std::vector<PlanDims>& dims) {
                (double)(R * R + M * Nb * M * Nb) * c2.P * c2.N);
     } else if (collapse && l == L) {
       bytes = 0;
+    } else if (collapse_asm && l == L - 1) {  // its formation as usual; both levels' assembly at once
+      const D& c2 = dims[L];
+      bytes = 8.0 * nodes *
+              ((double)(M * K + fu) * c.P * c.Q * (fu > 0) + (double)(K * Nb + fv) * c.Q * c.N * (fv > 0) +
+               (double)(R * R + M * Nb * M * Nb) * c2.P * c2.N);
+    } else if (collapse_asm && l == L) {  // its formation only
+      bytes = 8.0 * nodes * ((double)(M * K + fu) * c.P * c.Q * (fu > 0) + (double)(K * Nb + fv) * c.Q * c.N * (fv > 0));
     }
     t += bytes / cm.add_bw + (collapse && l == L ? 0.0 : cm.launch * (1 + (fu > 0) + (fv > 0)));
     // peel strips of the level-(l-1) nodes
@@ -2166,10 +2188,11 @@ fmm_status_t fmm_fused_compile_check(const fmm_alg* alg, int layout, int cse, in
 fmm_status_t fmm_plan_stats_ex2(const fmm_plan_t* p, double* out, int n) {
   FMM_API_BEGIN
   if (!p || !out || n < 0) throw Error(FMM_E_INVALID_ARG, "bad argument");
-  double s[17] = {0};
+  double s[18] = {0};
   FMM_CHECK_STATUS(fmm_plan_stats_ex(p, s));
   s[16] = p->k3f ? 1.0 : 0.0;
-  std::memcpy(out, s, sizeof(double) * (size_t)std::min(n, 17));
+  s[17] = p->collapse_asm ? 1.0 : 0.0;
+  std::memcpy(out, s, sizeof(double) * (size_t)std::min(n, 18));
   return FMM_OK;
   FMM_API_END
 }

@@ -338,11 +338,11 @@ class Plan:
         return [bool(x) for x in na], [bool(x) for x in nb], tuple(core), bool(allf.value)
 
     def stats(self) -> dict:
-        s = (ctypes.c_double * 17)()
-        _check(_lib.fmm_plan_stats_ex2(self._h, s, 17))
+        s = (ctypes.c_double * 18)()
+        _check(_lib.fmm_plan_stats_ex2(self._h, s, 18))
         keys = ["gemm_flops", "add_flops", "add_bytes", "gemm_bytes", "launches", "levels", "leaves", "paper_flops",
                 "leaf_flops", "fused_add_bytes", "fused_launches", "formation_bytes", "assembly_bytes", "strip_flops",
-                "collapsed", "tiled_peel", "fused_output"]
+                "collapsed", "tiled_peel", "fused_output", "collapsed_assembly"]
         return dict(zip(keys, list(s)))
 
     def new_output(self):

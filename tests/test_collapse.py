@@ -81,10 +81,11 @@ def test_not_collapsed_where_it_does_not_apply():
     Ca, sa = _run(F, "strassen_222_7", A, B, 2, collapse=True)
     Cb, sb = _run(F, "strassen_222_7", A, B, 2, collapse=False)
     assert sa["launches"] == sb["launches"] and np.array_equal(Ca, A @ B) and np.array_equal(Cb, A @ B)
-    A, B = I.problem(270, 180, 270, seed=5, kind="integers")  # <3,2,3>: base case too large
-    Ca, sa = _run(F, "hk_class_323_15", A, B, 2, collapse=True)
+    A, B = I.problem(540, 360, 540, seed=5, kind="integers")  # <3,2,3>: base case too large (the
+    Ca, sa = _run(F, "hk_class_323_15", A, B, 2, collapse=True)  # wide assembly only on request)
     _, sb = _run(F, "hk_class_323_15", A, B, 2, collapse=False)
-    assert sa["collapsed"] == 0 and sa["launches"] == sb["launches"] and np.array_equal(Ca, A @ B)
+    assert sa["collapsed"] == 0 and sa["collapsed_assembly"] == 0 and sa["launches"] == sb["launches"]
+    assert np.array_equal(Ca, A @ B)
     A, B = I.problem(256, 256, 256, seed=6, kind="integers")  # write-once strategy
     Ca, sa = _run(F, "strassen_222_7", A, B, 2, strategy="write_once")
     assert np.array_equal(Ca, A @ B)
@@ -118,3 +119,52 @@ def test_collapsed_strided_views(layout):
     else:
         rest[:, 2:P + 2] = 5.0
     assert bool((rest == 5.0).all())
+
+
+# The wide two-level assembly: base cases with MN <= 16 collapse the last two
+# levels' assembly only (one warp per output column k2 of W, leaf products staged in shared memory);
+# its chains are the oracle's two levels in the oracle's order, so with CSE off it equals the
+# one-level-per-launch assembly bit for bit.
+WIDE = [("hk_class_323_15", 540, 360, 541, 2, "row"),  # a top-level column strip
+        ("alg_424_26", 1008, 240, 960, 2, "row"), ("alg_433_29", 1152, 216, 234, 2, "col"),
+        ("laderman_class_333_23", 378, 360, 342, 2, "row"), ("alg_424_26", 128, 32, 2080, 2, "col"),
+        ("flip_234_20", 256, 432, 320, 2, "row")]
+
+
+@pytest.fixture
+def wide(monkeypatch):
+    monkeypatch.setenv("FMM_WIDE_ASM", "1")  # measured slower than the separate levels: opt-in
+
+
+@pytest.mark.parametrize("name,P,Q,N,L,layout", WIDE)
+def test_wide_assembly_equals_separate_and_oracle(name, P, Q, N, L, layout, wide):
+    F = _lib()
+    A, B = I.problem(P, Q, N, seed=P + N)
+    Cw, sw = _run(F, name, A, B, L, layout, cse=False, collapse=True)
+    Cs, ss = _run(F, name, A, B, L, layout, cse=False, collapse=False)
+    assert sw["collapsed_assembly"] == 1 and ss["collapsed_assembly"] == 0
+    assert sw["add_bytes"] < ss["add_bytes"] and sw["launches"] == ss["launches"] - 1
+    assert np.array_equal(Cw, Cs)
+    nrm = np.linalg.norm(A) * np.linalg.norm(B)
+    assert np.max(np.abs(Cw - O.fast(A, B, O.load_alg(F.alg_path(name)), L))) <= 1e-12 * nrm
+
+
+@pytest.mark.parametrize("G", [2, 5])
+def test_wide_assembly_shards_sum_to_product(G, wide):
+    F = _lib()
+    A, B = I.problem(640, 160, 640, seed=9, kind="integers")
+    total = np.zeros((640, 640))
+    for g in range(G):
+        C, st = _run(F, "alg_424_26", A, B, 2, shard_rank=g, shard_count=G)
+        assert st["collapsed_assembly"] == 1
+        total += C
+    assert np.array_equal(total, A @ B)
+
+
+def test_wide_assembly_peeled_level_not_collapsed(wide):
+    # level L-1 peeled (90 / 2 = 45 is odd, R7b): its strips need the level-(L-1) M, so no collapse
+    F = _lib()
+    A, B = I.problem(270, 180, 270, seed=5, kind="integers")
+    Ca, sa = _run(F, "hk_class_323_15", A, B, 2, collapse=True)
+    _, sb = _run(F, "hk_class_323_15", A, B, 2, collapse=False)
+    assert sa["collapsed_assembly"] == 0 and sa["launches"] == sb["launches"] and np.array_equal(Ca, A @ B)
