@@ -154,3 +154,25 @@ def test_p2p_plan_combines_inside_execute(world, layout, alg, root):
         pr.join(timeout=300)
     assert all(pr.exitcode == 0 for pr in procs), [pr.exitcode for pr in procs]
     assert q.get(timeout=5), "the combined C differs from A*B"
+
+
+@pytest.mark.parametrize("workload,extra", [("c1", []), ("c3", ["--shard-mode", "top", "--output", "slabs"])])
+def test_bench_two_ranks_on_one_gpu(workload, extra):
+    # `bench.py --gpus 2` with no torchrun wrapper launches the two ranks itself; with gloo they share
+    # this GPU and the peer-memory plan combines inside fmm_execute (a control-flow check: the line
+    # says it is not a measurement)
+    import json
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR",
+                                                             "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dist-backend", "gloo",
+                        "--workload", workload, "--steps", "3", "--warmup", "3", "--no-cpu", "--no-other", *extra],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and "peer-memory combine inside fmm_execute" in line["config"]["parallelism"]
+    assert "NOT a measurement" in line["config"]["dist_backend"]
+    assert line["result_check"]["ok"]
