@@ -476,6 +476,46 @@ class Run:
             best = min(best, e0.elapsed_time(e1))
         return self.flops / (best * 1e-3) / 1e9
 
+    def shard_scaling(self):
+        # N = 1 only: the compute side of the multi-GPU split, measured on this GPU -- for G = 2, 4, 8
+        # every shard plan of the headline workload (leaf-level HYBRID shards, then top-level product
+        # ranges) runs here in turn; max_g t_g against t_1 / G is the load balance a G-GPU run would
+        # see before its combine.  The combine itself (NCCL / peer memory over NVLink) is not
+        # measurable on one GPU: its volume is the partial C per rank, reported beside.
+        args, torch, stream, F = self.args, self.torch, self.stream, self.F
+        if self.world != 1 or args.no_other:
+            return None
+        out = {"what": "per-shard device time of the headline workload's shard plans, run one after another on "
+                       "this GPU (compute only; no combine)", "t1_ms": self.ms_step, "G": {}}
+        try:
+            for mode in ("leaf", "top"):
+                for G in (2, 4, 8):
+                    ts = []
+                    for g in range(G):
+                        p = F.Plan(self.alg, self.P, self.Q, self.N, self.L, layout=self.w["layout"], shard_rank=g,
+                                   shard_count=G, shard_mode=mode)
+                        for _ in range(3):
+                            p.execute(self.A, self.B, self.C, stream=stream)
+                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        torch.cuda.synchronize()
+                        e0.record(stream)
+                        for _ in range(5):
+                            p.execute(self.A, self.B, self.C, stream=stream)
+                        e1.record(stream)
+                        torch.cuda.synchronize()
+                        ts.append(e0.elapsed_time(e1) / 5)
+                        del p
+                    tmax = max(ts)
+                    out["G"][f"{mode}{G}"] = {"shard_ms": ts, "max_ms": tmax, "mean_ms": sum(ts) / G,
+                                             "balance_max_over_mean": tmax / (sum(ts) / G),
+                                             "compute_efficiency": self.ms_step / (G * tmax),
+                                             "partial_C_bytes_per_rank": 8.0 * self.P * self.N}
+            self.plan.execute(self.A, self.B, self.C, stream=stream)  # C holds the headline result again
+            torch.cuda.synchronize()
+        except Exception as ex:  # noqa: BLE001  (a comparison leg only)
+            out["error"] = str(ex)[:200]
+        return out
+
     def own_classical(self):
         # the classical comparison on our own DMMA GEMM (L = 0): at N > 1 each rank multiplies its
         # row slab of A by B with no exchange (SURVEY f1's classical row-slab split), max over ranks
@@ -775,6 +815,7 @@ class Run:
         roofline = self.roofline()
         cub = self.cublas()
         own = self.own_classical()
+        shards = self.shard_scaling()
         e2e = self.e2e()
         try:
             bcast = self.broadcast()
@@ -853,6 +894,7 @@ class Run:
                 "paper_effective_gflops": (2.0 * P * Q * N - P * N) / (ms_step * 1e-3) / 1e9,
                 "plan": {k: st[k] for k in ("gemm_flops", "add_flops", "add_bytes", "launches", "leaves")},
                 "configs": subs,
+                "shard_compute_scaling": shards,
             }
             print(json.dumps(line), flush=True)
         if world > 1:

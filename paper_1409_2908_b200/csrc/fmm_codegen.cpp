@@ -204,7 +204,13 @@ std::string generate(const LincombSpec& s, const Program& p, LincombCost& cost) 
   used.erase(-1);
   double adds = 0, reads = 0, writes = 0;
   if (!wo) {
-    for (int i : used) o << "    const " << T << " x" << i << " = ldnc" << V << "(nd.in[" << i << "] + pi);\n";
+    for (int i : used) {
+      if (s.skip_null)  // a shard's absent leaf product: zeros, without touching memory
+        o << "    const " << T << " x" << i << " = nd.in[" << i << "] ? ldnc" << V << "(nd.in[" << i << "] + pi) : "
+          << (V == 2 ? "make_double2(0.0, 0.0)" : "0.0") << ";\n";
+      else
+        o << "    const " << T << " x" << i << " = ldnc" << V << "(nd.in[" << i << "] + pi);\n";
+    }
     reads = (double)used.size();
     for (size_t t = 0; t < p.temps.size(); ++t) {
       const int a = std::get<0>(p.temps[t]), b = std::get<1>(p.temps[t]);
@@ -687,8 +693,14 @@ std::string generate_two_level(const TwoLevelSpec& sp, LincombCost& cost) {
       if (any) groups.push_back(r1);
     }
     auto loads = [&](int r1) {
-      for (int r2 : r2s)
-        o << "    const " << T << " m" << r1 << "_" << r2 << " = __ldcg((const " << T << "*)(nd.in[" << r1 * R + r2 << "] + pi));\n";
+      for (int r2 : r2s) {
+        const std::string ptr = "nd.in[" + std::to_string(r1 * R + r2) + "]";
+        if (sp.skip_null)
+          o << "    const " << T << " m" << r1 << "_" << r2 << " = " << ptr << " ? __ldcg((const " << T << "*)(" << ptr
+            << " + pi)) : " << (V == 2 ? "make_double2(0.0, 0.0)" : "0.0") << ";\n";
+        else
+          o << "    const " << T << " m" << r1 << "_" << r2 << " = __ldcg((const " << T << "*)(" << ptr << " + pi));\n";
+      }
       reads += (double)r2s.size();
     };
     auto arith = [&](int r1) {
@@ -782,9 +794,11 @@ std::string generate_two_level_wide(const TwoLevelSpec& sp, LincombCost& cost) {
   // issue the copies of step r (this warp's leaf products r2 = warp + rows q) into its ring slot
   o << "    auto issue = [&](int r) {\n";
   o << "      " << T << "* buf = smd + (r % " << D << ") * " << R * 32 << ";\n";
-  for (int q = 0; q < per; ++q)
-    o << "      { const int r2 = warp + " << rows * q << "; if (r2 < " << R << " && live) cpa(buf + r2 * 32 + lane, nd.in[r * " << R
-      << " + r2] + pi); }\n";
+  for (int q = 0; q < per; ++q) {
+    o << "      { const int r2 = warp + " << rows * q << "; if (r2 < " << R << " && live) {\n";
+    o << "        const double* src = nd.in[r * " << R << " + r2];\n";
+    o << "        if (src) cpa(buf + r2 * 32 + lane, src + pi); else buf[r2 * 32 + lane] = " << T << "{};\n      } }\n";
+  }
   o << "      asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n";
   o << "    };\n";
   for (int d = 0; d < D - 1; ++d) o << "    if (" << d << " < " << R << ") issue(" << d << "); else asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n";

@@ -137,6 +137,7 @@ struct LincombSpec {
   int strategy = FMM_ADD_STREAMING;
   int cse = 0;
   int vec = 2;  // doubles per thread access (2 = 16-byte vectors)
+  int skip_null = 0;  // streaming: a null input pointer reads as zeros (a shard's absent leaf products)
 };
 struct LincombKernel;  // compiled function handle
 // Per-node pointer table entry layout used by every generated kernel:
@@ -167,6 +168,7 @@ struct TwoLevelSpec {
   std::vector<double> X;      // rows x R, row-major (U, V or W)
   std::vector<char> materialize;  // formation: R*R flags
   int vec = 2;
+  int skip_null = 0;  // assembly: a null input pointer reads as zeros (a shard's absent leaf products)
 };
 std::shared_ptr<LincombKernel> twolevel_get(const TwoLevelSpec& spec);
 LincombCost lincomb_cost(const LincombKernel& k);

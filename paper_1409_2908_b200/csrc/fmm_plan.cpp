@@ -215,11 +215,15 @@ struct fmm_plan_s {
     slot[vec] = lincomb_get(spec_for(side, vec));
     return slot[vec];
   }
+  // a sharded streaming plan points its assembly tables at null for the leaf products it does not
+  // own (instead of a zero block): the kernels read them as zeros without the HBM traffic
+  bool skip_absent() const { return opt.shard_count > 1 && opt.strategy == FMM_ADD_STREAMING && !fuse; }
   LincombSpec spec_for(int side, int vec) const {
     LincombSpec s;
     s.strategy = opt.strategy;
     s.cse = opt.cse;
     s.vec = vec;
+    s.skip_null = side == 2 && skip_absent();
     const int M = alg->M, K = alg->K, Nb = alg->N;
     if (side == 0 || side == 1) {
       const int rows = side == 0 ? M * K : K * Nb;
@@ -689,7 +693,7 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
         auto** out = reinterpret_cast<double**>(e.data() + sizeof(void*) * nin);
         auto* lds = reinterpret_cast<long long*>(e.data() + sizeof(void*) * (nin + nout));
         for (int r = 0; r < R; ++r) {
-          in[r] = outView(l, zp * R + r).ptr;
+          in[r] = skip_absent() && !needed[l][zp * R + r] ? nullptr : outView(l, zp * R + r).ptr;
           aligned &= al16(in[r]);
         }
         for (int k = 0; k < nout; ++k) {
@@ -1266,7 +1270,7 @@ void fmm_plan_s::emit_two_level_assembly(bool lazy_kernels) {
     auto** out = reinterpret_cast<double**>(e.data() + sizeof(void*) * nin);
     auto* lds = reinterpret_cast<long long*>(e.data() + sizeof(void*) * (nin + nout));
     for (int q = 0; q < nin; ++q) {
-      in[q] = out_view(L, zg * R * R + q).ptr;
+      in[q] = skip_absent() && !needed[L][zg * R * R + q] ? nullptr : out_view(L, zg * R * R + q).ptr;
       aligned &= ((reinterpret_cast<uintptr_t>(in[q]) & 15) == 0);
     }
     for (int k1 = 0; k1 < rows; ++k1)
@@ -1288,6 +1292,7 @@ void fmm_plan_s::emit_two_level_assembly(bool lazy_kernels) {
   sp.R = R;
   sp.X = alg->Wd;
   sp.vec = aligned ? 2 : 1;
+  sp.skip_null = skip_absent();
   Launch ln;
   ln.kind = Launch::ASSEMBLE;
   ln.level = L - 1;
