@@ -189,8 +189,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fuse", type=int, default=0, help="fused leaf level (formation/GEMM/assembly in one launch)")
     ap.add_argument("--collapse", type=int, default=1, help="last two levels' formation / assembly in one pass each")
-    ap.add_argument("--shard-mode", default="leaf", choices=["leaf", "top"],
-                    help="N > 1: leaf-level HYBRID sharding or the top-level products in contiguous ranges")
+    ap.add_argument("--shard-mode", default="leaf", choices=["leaf", "top", "slab"],
+                    help="N > 1: leaf-level HYBRID sharding or the top-level products in contiguous ranges (partial "
+                         "C per rank, combined); or slab: each rank runs the whole method on its slab of C's rows "
+                         "(columns when column-major), nothing to combine")
     ap.add_argument("--combine", default="auto", choices=["auto", "lib", "p2p", "torch"],
                     help="N > 1: the partial-C combine.  lib: NCCL inside fmm_execute (fmm_plan_create_dist, "
                          "row chunks overlapped with the assembly); p2p: the peer-memory pull-reduce inside "
@@ -279,17 +281,32 @@ class Run:
         args, w, F, torch = self.args, self.w, self.F, self.torch
         P, Q, N, L, world, rank, device = self.P, self.Q, self.N, self.L, self.world, self.rank, self.device
         self.A_np, self.B_np = gen_inputs(w)
-        self.A = to_device(self.A_np, w["layout"], device)
-        self.B = to_device(self.B_np, w["layout"], device)
+        self.slab = world > 1 and args.shard_mode == "slab"
+        self.Pp, self.Np = P, N  # this rank's plan dimensions (slab mode: its slab of C)
+        self.Ax_np, self.Bx_np = self.A_np, self.B_np
+        if self.slab:
+            r0, r1 = F.dist_slab(P, N, w["layout"], world, rank)
+            self.slab_range = (r0, r1)
+            if w["layout"] == "row":
+                self.Ax_np, self.Pp = self.A_np[r0:r1], r1 - r0
+            else:
+                self.Bx_np, self.Np = self.B_np[:, r0:r1], r1 - r0
+        self.A = to_device(self.Ax_np, w["layout"], device)
+        self.B = to_device(self.Bx_np, w["layout"], device)
         self.alg = F.load_alg(w["alg"])
         # N > 1: the combine runs inside fmm_execute -- NCCL (lib, fmm_plan_create_dist) or the
         # peer-memory pull-reduce over CUDA IPC (p2p, fmm_plan_create_p2p) -- or after it (torch)
-        self.lib_comm = F.Comm.from_torch_distributed(device=device.index) if (world > 1 and args.combine == "lib") else None
-        self.p2p = F.P2P.from_torch_distributed(8 * P * N, device=device.index) if (world > 1 and args.combine == "p2p") else None
-        self.plan = F.Plan(self.alg, P, Q, N, L, layout=w["layout"], strategy=args.strategy, cse=bool(args.cse),
-                           shard_rank=rank, shard_count=world, fuse=bool(args.fuse), collapse=bool(args.collapse),
-                           comm=self.lib_comm, p2p=self.p2p, barrier=(self.dist.barrier if self.p2p else None),
-                           root="slabs" if args.output == "slabs" else 0, shard_mode=args.shard_mode)
+        combined = world > 1 and not self.slab
+        self.lib_comm = F.Comm.from_torch_distributed(device=device.index) if (combined and args.combine == "lib") else None
+        self.p2p = F.P2P.from_torch_distributed(8 * P * N, device=device.index) if (combined and args.combine == "p2p") else None
+        if self.slab:  # the whole method on this rank's slab: an ordinary single-GPU plan
+            self.plan = F.Plan(self.alg, self.Pp, Q, self.Np, L, layout=w["layout"], strategy=args.strategy,
+                               cse=bool(args.cse), fuse=bool(args.fuse), collapse=bool(args.collapse))
+        else:
+            self.plan = F.Plan(self.alg, P, Q, N, L, layout=w["layout"], strategy=args.strategy, cse=bool(args.cse),
+                               shard_rank=rank, shard_count=world, fuse=bool(args.fuse), collapse=bool(args.collapse),
+                               comm=self.lib_comm, p2p=self.p2p, barrier=(self.dist.barrier if self.p2p else None),
+                               root="slabs" if args.output == "slabs" else 0, shard_mode=args.shard_mode)
         self.outer, self.inner = (P, N) if w["layout"] == "row" else (N, P)
         self.C = self.plan.new_output()
         self.st = self.plan.stats()
@@ -299,7 +316,7 @@ class Run:
 
     def combine(self):
         from paper_1409_2908_b200.dist import combine_partials, scatter_partials
-        if self.world == 1 or self.args.combine != "torch":  # lib / p2p plans combine inside fmm_execute
+        if self.world == 1 or self.slab or self.args.combine != "torch":  # lib / p2p combine inside fmm_execute
             return
         if self.args.output == "slabs":
             scatter_partials(self.C)
@@ -372,7 +389,9 @@ class Run:
         if self.rank != 0:
             return None
         torch, w, F, A, B, C = self.torch, self.w, self.F, self.A, self.B, self.C
-        if self.args.output == "slabs" and self.world > 1:
+        if self.slab:  # rank 0's own slab, against its slab of A (rows) or B (columns)
+            lo, hi = 0, (self.Pp if w["layout"] == "row" else self.Np)
+        elif self.args.output == "slabs" and self.world > 1:
             lo, hi = F.dist_slab(self.P, self.N, w["layout"], self.world, 0)
         else:
             lo, hi = 0, (self.P if w["layout"] == "row" else self.N)
@@ -399,7 +418,7 @@ class Run:
         # kernel, addition CTAs on their own SMs), with --fuse 1 the separate kernels
         import numpy as np
         args, torch, stream = self.args, self.torch, self.stream
-        if args.no_other or self.L < 1:
+        if args.no_other or self.L < 1 or self.slab:
             return None
         try:
             plan_o = self.F.Plan(self.alg, self.P, self.Q, self.N, self.L, layout=self.w["layout"],
@@ -510,6 +529,35 @@ class Run:
                                              "balance_max_over_mean": tmax / (sum(ts) / G),
                                              "compute_efficiency": self.ms_step / (G * tmax),
                                              "partial_C_bytes_per_rank": 8.0 * self.P * self.N}
+            # the other partition, for comparison: each rank runs the whole method on its slab of C
+            # (rows of a row-major C, columns of a column-major one: A's rows or B's columns), so no
+            # partial products exist and nothing is combined; every rank reads all of B (all of A)
+            lay = self.w["layout"]
+            for G in (2, 4, 8):
+                ts = []
+                for g in range(G):
+                    r0, r1 = F.dist_slab(self.P, self.N, lay, G, g)
+                    if lay == "row":
+                        p = F.Plan(self.alg, r1 - r0, self.Q, self.N, self.L, layout=lay)
+                        a_, b_, c_ = self.A[r0:r1], self.B, self.C[r0:r1]
+                    else:
+                        p = F.Plan(self.alg, self.P, self.Q, r1 - r0, self.L, layout=lay)
+                        a_, b_, c_ = self.A, self.B[:, r0:r1], self.C[:, r0:r1]
+                    for _ in range(3):
+                        p.execute(a_, b_, c_, stream=stream)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    torch.cuda.synchronize()
+                    e0.record(stream)
+                    for _ in range(5):
+                        p.execute(a_, b_, c_, stream=stream)
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    ts.append(e0.elapsed_time(e1) / 5)
+                    del p
+                tmax = max(ts)
+                out["G"][f"slab{G}"] = {"shard_ms": ts, "max_ms": tmax, "mean_ms": sum(ts) / G,
+                                       "balance_max_over_mean": tmax / (sum(ts) / G),
+                                       "compute_efficiency": self.ms_step / (G * tmax), "partial_C_bytes_per_rank": 0.0}
             self.plan.execute(self.A, self.B, self.C, stream=stream)  # C holds the headline result again
             torch.cuda.synchronize()
         except Exception as ex:  # noqa: BLE001  (a comparison leg only)
@@ -520,6 +568,8 @@ class Run:
         # the classical comparison on our own DMMA GEMM (L = 0): at N > 1 each rank multiplies its
         # row slab of A by B with no exchange (SURVEY f1's classical row-slab split), max over ranks
         torch, F, w, A, B, stream = self.torch, self.F, self.w, self.A, self.B, self.stream
+        if self.slab:
+            return None  # slab mode already is the row / column-slab split (with the fast method)
         try:
             lay = w["layout"]
             r0, r1 = F.dist_slab(self.P, self.N, lay, self.world, self.rank)
@@ -555,7 +605,7 @@ class Run:
         args, torch, w, world, rank = self.args, self.torch, self.w, self.world, self.rank
         if args.no_e2e:
             return None
-        P, Q, N = self.P, self.Q, self.N
+        P, Q, N = self.Pp, self.Q, self.Np  # this rank's problem (all of it unless slab mode)
 
         def pinned(x, rows, cols):
             if w["layout"] == "row":
@@ -563,9 +613,9 @@ class Run:
                         else torch.empty(rows, cols, dtype=torch.float64)).pin_memory()
             return (torch.from_numpy(np.ascontiguousarray(x.T)) if x is not None
                     else torch.empty(cols, rows, dtype=torch.float64)).pin_memory().t()
-        Ah, Bh, Ch = pinned(self.A_np, P, Q), pinned(self.B_np, Q, N), pinned(None, P, N)
+        Ah, Bh, Ch = pinned(self.Ax_np, P, Q), pinned(self.Bx_np, Q, N), pinned(None, P, N)
         h2d = 8 * (P * Q + Q * N)
-        d2h = 8 * P * N if rank == 0 else 0
+        d2h = 8 * P * N if (rank == 0 or self.slab) else 0
 
         def e2e_step():
             if world == 1:
@@ -576,7 +626,7 @@ class Run:
                 self.B.copy_(Bh, non_blocking=True)
                 self.plan.execute(self.A, self.B, self.C, stream=self.stream)
                 self.combine()
-                if rank == 0:
+                if rank == 0 or self.slab:  # slab mode: every rank downloads its slab of C
                     Ch.copy_(self.C, non_blocking=True)
                 torch.cuda.synchronize()
         e2e_step()
@@ -591,8 +641,9 @@ class Run:
         self.plan.sync()
         torch.cuda.synchronize()
         ms_e = self.max_over_ranks((time.perf_counter() - h0) * 1e3)
-        combine_name = {"p2p": "peer-memory combine inside fmm_execute", "lib": "NCCL reduce inside fmm_execute",
-                        "torch": "torch.distributed reduce"}[self.args.combine]
+        combine_name = ("no combine: every rank multiplies its slab" if self.slab else
+                        {"p2p": "peer-memory combine inside fmm_execute", "lib": "NCCL reduce inside fmm_execute",
+                         "torch": "torch.distributed reduce"}[self.args.combine])
         return {"value": self.flops / (ms_e / n_e2e * 1e-3) / 1e9, "unit": "GFLOPS", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": ms_e / n_e2e, "steps": n_e2e,
                 "timing": "host wall clock over the steps, device synchronised on both sides",
@@ -612,6 +663,8 @@ class Run:
         import numpy as np
         from paper_1409_2908_b200.dist import storage_view
         torch, dist, stream = self.torch, self.dist, self.stream
+        if self.slab:
+            return self.broadcast_slabs()
         needA, needB, core, need_all = self.plan.input_blocks()
         needs = [None] * self.world
         dist.all_gather_object(needs, (needA, needB, need_all))
@@ -687,6 +740,48 @@ class Run:
         return {"ms": bms, "bytes_sent": sent, "bytes_if_every_rank_got_everything": full * (self.world - 1),
                 "restricted_to_blocks_read": restricted,
                 "blocks_read_per_rank": [[int(sum(n[0])), int(sum(n[1])), bool(n[2])] for n in needs],
+                "algbw_gbs": sent / (bms * 1e-3) / 1e9 if bms > 0 else None,
+                "value_with_broadcast": self.flops / ((self.ms_step + bms) * 1e-3) / 1e9}
+
+    def broadcast_slabs(self):
+        # slab mode: the operand every rank needs whole (B for a row-major problem, A for a column-
+        # major one) is broadcast; the other is cut into the ranks' slabs and sent point to point
+        # (NCCL; with gloo the slabs are not sent)
+        from paper_1409_2908_b200.dist import storage_view
+        torch, dist, stream, w = self.torch, self.dist, self.stream, self.w
+        row = w["layout"] == "row"
+        whole = self.B if row else self.A
+        full = to_device(self.A_np if row else self.B_np, w["layout"], self.device) if self.rank == 0 else None
+        send = self.args.dist_backend == "nccl"
+        own = self.A if row else self.B
+        spans = [self.F.dist_slab(self.P, self.N, w["layout"], self.world, g) for g in range(self.world)]
+        reps = 3
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        torch.cuda.synchronize()
+        b0.record(stream)
+        for _ in range(reps):
+            dist.broadcast(storage_view(whole), src=0)
+            if send:
+                ops = []
+                for g in range(1, self.world):
+                    r0, r1 = spans[g]
+                    if self.rank == 0:
+                        part = full[r0:r1] if row else full[:, r0:r1]
+                        ops.append(dist.P2POp(dist.isend, storage_view(part), g))
+                    elif self.rank == g:
+                        ops.append(dist.P2POp(dist.irecv, storage_view(own), 0))
+                if ops:
+                    for wk in dist.batch_isend_irecv(ops):
+                        wk.wait()
+        b1.record(stream)
+        torch.cuda.synchronize()
+        bms = self.max_over_ranks(b0.elapsed_time(b1) / reps)
+        sent = 8.0 * whole.numel() * (self.world - 1) + (
+            8.0 * sum((r1 - r0) for r0, r1 in spans[1:]) * (self.Q) if send else 0.0)
+        return {"ms": bms, "bytes_sent": sent,
+                "what": "broadcast of the operand every rank reads whole" + (" + its slab of the other, point to point"
+                                                                             if send else " (gloo: slabs not sent)"),
                 "algbw_gbs": sent / (bms * 1e-3) / 1e9 if bms > 0 else None,
                 "value_with_broadcast": self.flops / ((self.ms_step + bms) * 1e-3) / 1e9}
 
@@ -848,6 +943,9 @@ class Run:
             where = "reduce to rank 0" if args.output == "root" else "slab-distributed output"
             if world == 1:
                 parallelism = "1 GPU"
+            elif self.slab:
+                parallelism = (f"slabs x{world}: every rank runs the whole method on its slab of C's "
+                               f"{'rows' if w['layout'] == 'row' else 'columns'}; no partial products, no combine")
             elif args.combine == "p2p":
                 parallelism = (f"{args.shard_mode}-level shards x{world} + peer-memory combine inside fmm_execute "
                                f"(fmm_plan_create_p2p: one pull-reduce kernel per rank over CUDA IPC), {where}")

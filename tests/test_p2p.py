@@ -156,7 +156,8 @@ def test_p2p_plan_combines_inside_execute(world, layout, alg, root):
     assert q.get(timeout=5), "the combined C differs from A*B"
 
 
-@pytest.mark.parametrize("workload,extra", [("c1", []), ("c3", ["--shard-mode", "top", "--output", "slabs"])])
+@pytest.mark.parametrize("workload,extra", [("c1", []), ("c3", ["--shard-mode", "top", "--output", "slabs"]),
+                                            ("c1", ["--shard-mode", "slab"])])
 def test_bench_two_ranks_on_one_gpu(workload, extra):
     # `bench.py --gpus 2` with no torchrun wrapper launches the two ranks itself; with gloo they share
     # this GPU and the peer-memory plan combines inside fmm_execute (a control-flow check: the line
@@ -173,6 +174,7 @@ def test_bench_two_ranks_on_one_gpu(workload, extra):
     lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 1
     line = json.loads(lines[0])
-    assert line["n_gpus"] == 2 and "peer-memory combine inside fmm_execute" in line["config"]["parallelism"]
+    want = "no combine" if "slab" in extra else "peer-memory combine inside fmm_execute"
+    assert line["n_gpus"] == 2 and want in line["config"]["parallelism"]
     assert "NOT a measurement" in line["config"]["dist_backend"]
     assert line["result_check"]["ok"]
