@@ -3,7 +3,8 @@
 // A strip is a classical product with one tiny dimension (1 to 2N-1 rows or columns).  On the
 // 128-row DMMA tile it would waste up to 99 % of the tensor work, so thin tasks of a strip launch
 // run here instead, on the FP64 CUDA cores, HBM/L2-bound:
-//   row strips (m <= 8): a block covers 32 output columns x 8 k-slices; each thread keeps all
+//   row strips (m <= 8): a block covers 32 output columns x 8 k-slices (8 B loads in flight per
+//       thread); each thread keeps all
 //       m rows of its column in registers over its k-slice (B read once, coalesced; A[i][k] a
 //       warp-uniform broadcast), and the slices are reduced through shared memory.  (A 64-column
 //       variant with 16-byte loads was measured slower on c3: 0.19 vs 0.16 ms.)
@@ -33,12 +34,16 @@ __global__ void __launch_bounds__(256) skinny_rows(const GemmTask* __restrict__ 
   for (int i = 0; i < THIN; ++i) acc[i] = 0.0;
   if (j < t.n) {
     int k = ks;
-    for (; k + 24 < t.k; k += 32) {  // 4 independent B loads in flight per thread
-      double b[4];
+#ifndef FMM_SKINNY_ROW_UNROLL
+#define FMM_SKINNY_ROW_UNROLL 8  // measured on c3: 4 -> 8 in flight, strips 0.372 -> 0.349 ms
+#endif
+    constexpr int U = FMM_SKINNY_ROW_UNROLL;
+    for (; k + 8 * (U - 1) < t.k; k += 8 * U) {  // U independent B loads in flight per thread
+      double b[U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) b[u] = __ldg(t.B + (long long)(k + 8 * u) * t.ldb + j);
+      for (int u = 0; u < U; ++u) b[u] = __ldg(t.B + (long long)(k + 8 * u) * t.ldb + j);
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int i = 0; i < THIN; ++i)
           if (i < t.m) acc[i] = fma(__ldg(t.A + (long long)i * t.lda + k + 8 * u), b[u], acc[i]);
@@ -76,7 +81,10 @@ __global__ void __launch_bounds__(256) skinny_rows(const GemmTask* __restrict__ 
 #ifndef FMM_SKINNY_RPW
 #define FMM_SKINNY_RPW 2
 #endif
-constexpr int KC = 256, ROWS_PER_WARP = FMM_SKINNY_RPW;
+#ifndef FMM_SKINNY_KC
+#define FMM_SKINNY_KC 256
+#endif
+constexpr int KC = FMM_SKINNY_KC, ROWS_PER_WARP = FMM_SKINNY_RPW;
 __global__ void __launch_bounds__(256) skinny_cols(const GemmTask* __restrict__ tasks, const int* __restrict__ ids,
                                                    int count) {
   __shared__ double bt[THIN][KC];
@@ -98,31 +106,33 @@ __global__ void __launch_bounds__(256) skinny_cols(const GemmTask* __restrict__ 
     }
     __syncthreads();
     if (v2) {
-      // lane covers k pairs kk = 2 lane + 64 s, s = 0..3 (the 256-wide chunk)
-      double2 a[ROWS_PER_WARP][4];
+      // lane covers k pairs kk = 2 lane + 64 s, s = 0..3 of each 256-wide group of the chunk
+      for (int g0 = 0; g0 < kc; g0 += 256) {
+        double2 a[ROWS_PER_WARP][4];
 #pragma unroll
-      for (int q = 0; q < ROWS_PER_WARP; ++q) {
-        const int i = row0 + q;
+        for (int q = 0; q < ROWS_PER_WARP; ++q) {
+          const int i = row0 + q;
+#pragma unroll
+          for (int s4 = 0; s4 < 4; ++s4) {
+            const int kk = g0 + 2 * lane + 64 * s4;
+            const double* ap = t.A + (long long)i * t.lda + k0 + kk;
+            a[q][s4] = (i < t.m && kk + 1 < kc) ? __ldg(reinterpret_cast<const double2*>(ap))
+                       : (i < t.m && kk < kc) ? make_double2(__ldg(ap), 0.0) : make_double2(0.0, 0.0);
+          }
+        }
 #pragma unroll
         for (int s4 = 0; s4 < 4; ++s4) {
-          const int kk = 2 * lane + 64 * s4;
-          const double* ap = t.A + (long long)i * t.lda + k0 + kk;
-          a[q][s4] = (i < t.m && kk + 1 < kc) ? __ldg(reinterpret_cast<const double2*>(ap))
-                     : (i < t.m && kk < kc) ? make_double2(__ldg(ap), 0.0) : make_double2(0.0, 0.0);
+          const int kk = g0 + 2 * lane + 64 * s4;
+          if (kk >= kc) continue;
+          const bool second = kk + 1 < kc;
+#pragma unroll
+          for (int j = 0; j < THIN; ++j)
+            if (j < t.n) {
+              const double b0 = bt[j][kk], b1 = second ? bt[j][kk + 1] : 0.0;
+#pragma unroll
+              for (int q = 0; q < ROWS_PER_WARP; ++q) acc[q][j] = fma(a[q][s4].y, b1, fma(a[q][s4].x, b0, acc[q][j]));
+            }
         }
-      }
-#pragma unroll
-      for (int s4 = 0; s4 < 4; ++s4) {
-        const int kk = 2 * lane + 64 * s4;
-        if (kk >= kc) continue;
-        const bool second = kk + 1 < kc;
-#pragma unroll
-        for (int j = 0; j < THIN; ++j)
-          if (j < t.n) {
-            const double b0 = bt[j][kk], b1 = second ? bt[j][kk + 1] : 0.0;
-#pragma unroll
-            for (int q = 0; q < ROWS_PER_WARP; ++q) acc[q][j] = fma(a[q][s4].y, b1, fma(a[q][s4].x, b0, acc[q][j]));
-          }
       }
     } else {
 #pragma unroll
