@@ -139,9 +139,11 @@ int gemm_choose_bn(const std::vector<GemmTask>& tasks) {
       sms = 148;
     cudaGetLastError();
   }
-  // relative DMMA efficiency of each tile width (narrow tiles read more operand bytes per flop)
+  // relative DMMA efficiency of each tile width per useful flop, measured on c2's 2048^3 leaves
+  // with the padding divided out (profiles/r2_leaf_gemm_study.jsonl, round-2 kernel): nearly flat,
+  // so the padding decides
   static const int menu[] = {128, 112, 96, 80, 64};
-  static const double eff[] = {1.00, 0.985, 0.975, 0.965, 0.94};
+  static const double eff[] = {1.00, 0.998, 0.996, 0.996, 0.993};
   int best = 128;
   double best_t = 1e300;
   for (int q = 0; q < 5; ++q) {

@@ -1973,7 +1973,7 @@ double gemm_time(double count, long long m, long long n, long long k, const Cost
   if (k <= 0) return cm.launch;
   if (std::min(m, n) <= 8) return 2.0 * count * m * n * (double)k / (cm.sms * cm.thin) + cm.launch;
   static const int menu[] = {128, 112, 96, 80, 64};
-  static const double eff[] = {1.00, 0.985, 0.975, 0.965, 0.94};
+  static const double eff[] = {1.00, 0.998, 0.996, 0.996, 0.993};  // as gemm_choose_bn (round-2 kernel)
   double best = 1e300;
   for (int q = 0; q < 5; ++q) {
     const double tiles = count * (double)((m + 127) / 128) * (double)((n + menu[q] - 1) / menu[q]);

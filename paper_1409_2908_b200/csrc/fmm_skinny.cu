@@ -3,9 +3,8 @@
 // A strip is a classical product with one tiny dimension (1 to 2N-1 rows or columns).  On the
 // 128-row DMMA tile it would waste up to 99 % of the tensor work, so thin tasks of a strip launch
 // run here instead, on the FP64 CUDA cores, HBM/L2-bound:
-//   row strips (m <= 8): a block covers 32 output columns x 8 k-slices (8 B loads in flight per
-//       thread); each thread keeps all
-//       m rows of its column in registers over its k-slice (B read once, coalesced; A[i][k] a
+//   row strips (m <= 8): a block covers 32 output columns x 8 k-slices (eight loads of B in
+//       flight per thread); each thread keeps all m rows of its column in registers over its k-slice (B read once, coalesced; A[i][k] a
 //       warp-uniform broadcast), and the slices are reduced through shared memory.  (A 64-column
 //       variant with 16-byte loads was measured slower on c3: 0.19 vs 0.16 ms.)
 //   column strips (n <= 8): four output rows per warp; lanes split k (A rows read coalesced,
