@@ -480,6 +480,8 @@ std::string fused_generate(const std::vector<LincombSpec>& specs, int bn) {
   gemm_bn_config(bn, &wgm, &wgn);
   std::ostringstream o;
   o << "// generated by fmm_codegen.cpp: fused leaf level, BN=" << bn << "\n#define FMM_NVRTC 1\n";
+  // the ring geometry of the nvcc-compiled kernels, so the host's shared-memory sizes match
+  o << "#define FMM_GEMM_BK " << gemm_bk() << "\n#define FMM_GEMM_STAGES " << gemm_stages() << "\n";
   if (const char* e = getenv("FMM_FUSED_LD")) o << "#define FMM_LD_KIND " << atoi(e) << "\n";  // diagnostics
   o << strip_pragma_once(kFmmDeviceSrc) << "\n" << strip_pragma_once(kFmmCoreSrc) << "\nnamespace fmm {\n";
   for (size_t q = 0; q < specs.size(); ++q) {

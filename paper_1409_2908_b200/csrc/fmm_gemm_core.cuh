@@ -42,7 +42,14 @@ struct alignas(64) CUtensorMap_opaque {
 typedef CUtensorMap_opaque CUtensorMap;
 #endif
 
-constexpr int BM = 128, BK = 16;
+// BK: k-depth of a ring stage of the fused leaf level and K3f; the plain kernel is instantiated for
+// k-steps KS = 16 and 32 (eight 4-deep slices per stage: A as two 128 x 16 boxes, B as 32 x 16
+// boxes), half the stage hand-overs per flop; the ring keeps the same bytes in flight (96 KB of k)
+#ifndef FMM_GEMM_BK
+#define FMM_GEMM_BK 16
+#endif
+constexpr int BM = 128, BK = FMM_GEMM_BK;
+static_assert(BK == 16 || BK == 32, "a stage holds one or two 16-column A boxes");
 #ifndef FMM_F1_EMUL_U
 #define FMM_F1_EMUL_U 1
 #endif
@@ -50,16 +57,19 @@ constexpr int BM = 128, BK = 16;
 #define FMM_F1_EMUL_V 1
 #endif
 #ifndef FMM_GEMM_STAGES
-#define FMM_GEMM_STAGES 6
+#define FMM_GEMM_STAGES 6  // of 16-deep stages; 32-deep rings have half as many
 #endif
-constexpr int GEMM_STAGES = FMM_GEMM_STAGES;
+__host__ __device__ constexpr int ring_stages(int ks) { return FMM_GEMM_STAGES * 16 / ks; }
+constexpr int GEMM_STAGES = ring_stages(BK);
 constexpr int CONSUMERS = 8, THREADS = 128 + CONSUMERS * 32;  // warpgroup 0 = producer, 1-2 = consumers
 static_assert(THREADS == GEMM_THREADS, "host and device agree on the block size");
-constexpr int A_BYTES = BM * BK * 8;                           // 16 KB
-__host__ __device__ constexpr int gemm_smem_bytes(int bn) { return GEMM_STAGES * (A_BYTES + BK * bn * 8) + 1024 /*align*/ + 256 /*barriers*/; }
+constexpr int A_BYTES = BM * BK * 8;                           // 16 KB per 16 columns of k
+__host__ __device__ constexpr int gemm_smem_bytes(int bn, int ks = BK) {
+  return ring_stages(ks) * (BM * ks * 8 + ks * bn * 8) + 1024 /*align*/ + 256 /*barriers*/;
+}
 __host__ __device__ constexpr int fused_smem_bytes(int bn) { return gemm_smem_bytes(bn) + FUSED_PTR_BYTES; }
 // K3f: a 4-stage ring plus two staging tiles (+alpha acc and -alpha acc) of 128 x bn doubles
-constexpr int K3F_STAGES = 4;
+constexpr int K3F_STAGES = 64 / BK;
 __host__ __device__ constexpr int k3f_smem_bytes(int bn) {
   return K3F_STAGES * (A_BYTES + BK * bn * 8) + 1024 /*align*/ + 1024 /*barriers, aligned*/ + 2 * BM * bn * 8;
 }
@@ -230,17 +240,22 @@ __device__ __forceinline__ void run_job(const FusedArgs& fa, int jidx, int lane,
   }
 }
 
-template <int BN, int WGM, int WGN, bool FUSED, bool K3F = false>
+template <int BN, int WGM, int WGN, bool FUSED, bool K3F = false, int KS = BK>
 __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, const CUtensorMap* __restrict__ maps,
                                           int ntasks, int total_tiles, Uniform uni, const FusedArgs& fa,
                                           const K3fArgs* ka = nullptr) {
   static_assert(!(FUSED && K3F), "one epilogue mode");
-  constexpr int STAGES = K3F ? K3F_STAGES : GEMM_STAGES;
+  static_assert(KS == 16 || KS == 32, "16- or 32-deep stages");
+  static_assert(KS == BK || !(FUSED || K3F), "the fused and K3f kernels use BK-deep stages");
+  constexpr int STAGES = K3F ? K3F_STAGES : ring_stages(KS);
+  constexpr int A_BYTES = BM * KS * 8;
   static_assert(WGM * WGN == CONSUMERS, "8 consumer warps");
   constexpr int WTM = BM / WGM, WTN = BN / WGN;
   static_assert(WTM % 16 == 0 && WTN % 16 == 0, "warp tile must be a multiple of 16");
   constexpr int MI = WTM / 8, NI = WTN / 8;
-  constexpr int B_BYTES_T = BK * BN * 8;  // BN/16 boxes of 16 x 16
+  constexpr int B_BYTES_T = KS * BN * 8;  // BN/16 boxes of KS x 16
+  constexpr int B_BOX = KS * 128;          // bytes of one B box (KS rows of 16 doubles)
+  constexpr int SL = KS / 4;               // 4-deep slices per stage
   constexpr int STAGE_T = A_BYTES + B_BYTES_T;
   extern __shared__ unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -299,14 +314,15 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
         }
         const CUtensorMap* ma = maps + 2 * tc.task;
         const CUtensorMap* mb = ma + 1;
-        const int KT = (__ldg(&tasks[tc.task].k) + BK - 1) / BK;
+        const int KT = (__ldg(&tasks[tc.task].k) + KS - 1) / KS;
         for (int kt = 0; kt < KT; ++kt) {
           mbar_wait(empty_bar(stage), phase ^ 1u);
           const unsigned sa = base + stage * STAGE_T, sb = sa + A_BYTES;
           mbar_expect_tx(full_bar(stage), STAGE_T);
-          tma_load_2d(sa, ma, kt * BK, tc.m0, full_bar(stage));
 #pragma unroll
-          for (int b = 0; b < BN / 16; ++b) tma_load_2d(sb + b * 2048, mb, tc.n0 + 16 * b, kt * BK, full_bar(stage));
+          for (int h = 0; h < KS / 16; ++h) tma_load_2d(sa + h * 16384, ma, kt * KS + 16 * h, tc.m0, full_bar(stage));
+#pragma unroll
+          for (int b = 0; b < BN / 16; ++b) tma_load_2d(sb + b * B_BOX, mb, tc.n0 + 16 * b, kt * KS, full_bar(stage));
           if (++stage == STAGES) stage = 0, phase ^= 1u;
         }
       }
@@ -335,7 +351,7 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
   //   k row = 4s + c; chunk = (box col >> 1) ^ (k row & 7)
   const unsigned map0 = (r == 0) ? 0u : (r == 1) ? 1u : (r == 2) ? 8u : (r == 3) ? 9u : (r == 4) ? 2u : (r == 5) ? 3u : (r == 6) ? 10u : 11u;
   const unsigned hb = map0 & 1u, cb0 = map0 >> 1;
-  const unsigned b_box0 = (unsigned)(wn / 16) * 2048u;
+  const unsigned b_box0 = (unsigned)(wn / 16) * (unsigned)B_BOX;
 
   int stage = 0;
   unsigned phase = 0;
@@ -343,7 +359,7 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
     const TileCoord tc = locate<BN>(tasks, ntasks, tile, uni);
     const GemmTask& t = tasks[tc.task];
     const int kdim = __ldg(&t.k);
-    const int KT = (kdim + BK - 1) / BK;
+    const int KT = (kdim + KS - 1) / KS;
     // epilogue parameters, fetched now so their latency hides behind the main loop
     const double alpha = __ldg(&t.alpha), beta = __ldg(&t.beta);
     const int m = __ldg(&t.m), n = __ldg(&t.n);
@@ -366,11 +382,12 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
 
     // fragments of one 4-deep k-slice from shared memory, and its MI x NI DMMAs
     auto load = [&](double (&a)[MI], double (&b)[NI], unsigned sa, unsigned sb, int s) {
+      const unsigned sa_h = sa + (unsigned)(s >> 2) * 16384u;  // the A box of this slice's 16 columns
 #pragma unroll
       for (int i = 0; i < MI; ++i) {
         const unsigned x = (i & 1) ? xa1 : xa0;
-        const unsigned chunk = ((unsigned)(2 * s) + ca) ^ x;
-        const unsigned off = a_row0 + (unsigned)(16 * (i >> 1) + (i & 1)) * 128u + chunk * 16u + ha;
+        const unsigned chunk = ((unsigned)(2 * (s & 3)) + ca) ^ x;
+        const unsigned off = a_row0 + (unsigned)(16 * (i >> 1) + (i & 1)) * 128u + chunk * 16u + ha + (sa_h - sa);
         a[i] = lds64(sa + off);
 #if FMM_F1_EMUL_U > 1  // timing experiment: a leaf operand formed in registers from
         // FMM_F1_EMUL_U parent tiles -- extra fragment loads (other rows of the same stage, so the
@@ -383,7 +400,7 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
 #pragma unroll
       for (int jj = 0; jj < NI; ++jj) {
         const unsigned chunk = (cb0 + 2u * (jj & 1)) ^ (krow & 7u);
-        const unsigned off = b_box0 + (unsigned)(jj >> 1) * 2048u + krow * 128u + chunk * 16u + hb * 8u;
+        const unsigned off = b_box0 + (unsigned)(jj >> 1) * (unsigned)B_BOX + krow * 128u + chunk * 16u + hb * 8u;
         b[jj] = lds64(sb + off);
 #if FMM_F1_EMUL_V > 1
 #pragma unroll
@@ -413,19 +430,22 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
     // Then a ragged last k-step runs only the 4-deep slices that hold data (the rest is zero fill),
     // and a warp whose sub-tile lies beyond m or n (ragged edge tiles) issues no DMMA at all but
     // waits for and releases every stage with the others.
-    const int KF = active ? kdim / BK : 0;
+    const int KF = active ? kdim / KS : 0;
     if (KF > 0) {
-      static_assert(BK / 4 == 4, "four slices per stage");
+      static_assert(SL % 2 == 0, "slices come in pairs");
       double a0[MI], b0[NI], a1[MI], b1[NI];
       mbar_wait(full_bar(stage), phase);
       unsigned sa = base + stage * STAGE_T, sb = sa + A_BYTES;
       load(a0, b0, sa, sb, 0);
       for (int kt = 0; kt < KF; ++kt) {
-        load(a1, b1, sa, sb, 1);
-        mma(a0, b0);
-        load(a0, b0, sa, sb, 2);
-        mma(a1, b1);
-        load(a1, b1, sa, sb, 3);
+#pragma unroll
+        for (int s = 0; s + 2 < SL; s += 2) {
+          load(a1, b1, sa, sb, s + 1);
+          mma(a0, b0);
+          load(a0, b0, sa, sb, s + 2);
+          mma(a1, b1);
+        }
+        load(a1, b1, sa, sb, SL - 1);
         mma(a0, b0);
         if (kt + 1 < KF) {
           const int nx = stage + 1 == STAGES ? 0 : stage + 1;
@@ -440,7 +460,7 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
     for (int kt = KF; kt < KT; ++kt) {
       mbar_wait(full_bar(stage), phase);
       const unsigned sa = base + stage * STAGE_T, sb = sa + A_BYTES;
-      const int ks = active ? (kdim - kt * BK + 3) / 4 : 0;
+      const int ks = active ? (kdim - kt * KS + 3) / 4 : 0;
 #pragma unroll 1
       for (int s = 0; s < ks; ++s) {
         double a[MI], b[NI];

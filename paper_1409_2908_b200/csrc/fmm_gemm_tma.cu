@@ -18,11 +18,11 @@ namespace fmm {
 
 namespace {
 
-template <int BN, int WGM, int WGN>
+template <int BN, int WGM, int WGN, int KS>
 __global__ void __launch_bounds__(THREADS, 1)
     grouped_dgemm_tma(const GemmTask* __restrict__ tasks, const CUtensorMap* __restrict__ maps, int ntasks,
                       int total_tiles, Uniform uni) {
-  gemm_body<BN, WGM, WGN, false>(tasks, maps, ntasks, total_tiles, uni, FusedArgs{});
+  gemm_body<BN, WGM, WGN, false, false, KS>(tasks, maps, ntasks, total_tiles, uni, FusedArgs{});
 }
 
 // K3f: the leaf GEMM whose epilogue reduce-adds every tile into its W targets (tile 128 x 64)
@@ -102,24 +102,38 @@ bool gemm_tma_eligible(const std::vector<GemmTask>& tasks) {
   return true;
 }
 
-void gemm_tma_maps(const std::vector<GemmTask>& tasks, void* out) {
+void gemm_tma_maps(const std::vector<GemmTask>& tasks, void* out, int ks) {
   auto* maps = reinterpret_cast<CUtensorMap*>(out);
   for (size_t i = 0; i < tasks.size(); ++i) {
     const GemmTask& t = tasks[i];
-    make_map(&maps[2 * i], t.A, t.m, t.k, t.lda, BK, BM);      // A view: m rows x k cols, box 128 x 16
-    make_map(&maps[2 * i + 1], t.B, t.k, t.n, t.ldb, 16, BK);  // B view: k rows x n cols, box 16 x 16
+    make_map(&maps[2 * i], t.A, t.m, t.k, t.lda, 16, BM);      // A view: m rows x k cols, box 128 x 16
+    make_map(&maps[2 * i + 1], t.B, t.k, t.n, t.ldb, 16, ks);  // B view: k rows x n cols, box ks x 16
   }
 }
 
-template <int BN, int WGM, int WGN>
+// 32-deep stages halve the stage hand-overs; measured on the round-2 kernel: leaf GEMM 0.979 -> 0.987
+// of the DMMA peak at k = 2048 (c2), 0.924 -> 0.930 at k = 600 (c4), but 0.920 -> 0.918 at k = 450
+// (c3) and 0.915 -> 0.912 at k = 400 (c5t), whose short tiles see the 3-stage ring fill more often
+int gemm_choose_bk(const std::vector<GemmTask>& tasks) {
+  if (const char* e = getenv("FMM_GEMM_BK_RUN")) return atoi(e) == 32 ? 32 : 16;
+  double f32 = 0, f = 0;
+  for (const auto& t : tasks) {
+    const double w = (double)t.m * t.n * (double)t.k;
+    f += w;
+    if (t.k >= 512) f32 += w;
+  }
+  return f > 0 && f32 >= 0.5 * f ? 32 : 16;
+}
+
+template <int BN, int WGM, int WGN, int KS>
 static void launch_cfg(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int sms,
                        Uniform uni, cudaStream_t stream) {
   static std::atomic<unsigned long long> configured{0};  // bit d: attribute set on device d
   int dev_ = 0;
   FMM_CUDA(cudaGetDevice(&dev_));
   const unsigned long long bit = 1ull << (dev_ & 63);
-  auto kern = grouped_dgemm_tma<BN, WGM, WGN>;
-  const size_t smem = (size_t)gemm_smem_bytes(BN);
+  auto kern = grouped_dgemm_tma<BN, WGM, WGN, KS>;
+  const size_t smem = (size_t)gemm_smem_bytes(BN, KS);
   if (!(configured.load() & bit)) {
     FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured.fetch_or(bit);
@@ -185,22 +199,33 @@ void gemm_bn_config(int bn, int* wgm, int* wgn) {
 }
 
 int gemm_sm_count() { return sm_count(); }
-int gemm_tma_smem_bytes(int bn) { return gemm_smem_bytes(bn); }
+static_assert(BK_K3F == BK, "the K3f maps and kernel agree on the k-step");
+int gemm_bk() { return BK; }
+int gemm_stages() { return GEMM_STAGES; }
+int gemm_tma_smem_bytes(int bn) { return gemm_smem_bytes(bn, BK); }
 int gemm_fused_smem_bytes(int bn) { return fused_smem_bytes(bn); }
 
-void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn,
+template <int KS>
+static void launch_ks(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn, int sms,
+                      Uniform uni, cudaStream_t stream) {
+  switch (bn) {
+    case 128: launch_cfg<128, 2, 4, KS>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
+    case 112: launch_cfg<112, 8, 1, KS>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
+    case 96: launch_cfg<96, 4, 2, KS>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
+    case 80: launch_cfg<80, 8, 1, KS>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
+    case 64: launch_cfg<64, 4, 2, KS>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
+    default: throw Error(FMM_E_INVALID_ARG, "unsupported GEMM tile width " + std::to_string(bn));
+  }
+}
+
+void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn, int bk,
                      int uniform_tm, int uniform_tn, cudaStream_t stream) {
   const Uniform uni{uniform_tm * uniform_tn, uniform_tm, uniform_tn};
   if (total_tiles <= 0 || ntasks <= 0) return;
   const int sms = sm_count();
-  switch (bn) {
-    case 128: launch_cfg<128, 2, 4>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
-    case 112: launch_cfg<112, 8, 1>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
-    case 96: launch_cfg<96, 4, 2>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
-    case 80: launch_cfg<80, 8, 1>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
-    case 64: launch_cfg<64, 4, 2>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
-    default: throw Error(FMM_E_INVALID_ARG, "unsupported GEMM tile width " + std::to_string(bn));
-  }
+  if (bk == 32) launch_ks<32>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
+  else if (bk == 16) launch_ks<16>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
+  else throw Error(FMM_E_INVALID_ARG, "unsupported GEMM k-step " + std::to_string(bk));
 }
 
 }  // namespace fmm

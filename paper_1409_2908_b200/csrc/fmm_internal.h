@@ -104,9 +104,11 @@ int gemm_tile_n();
 // TMA + warp-specialised variant (fmm_gemm_tma.cu): needs 16-byte aligned views, even lds.
 bool gemm_tma_eligible(const std::vector<GemmTask>& tasks);
 size_t gemm_tma_map_bytes();  // bytes of one tensor map (two per task: A then B)
-void gemm_tma_maps(const std::vector<GemmTask>& tasks, void* out);
+void gemm_tma_maps(const std::vector<GemmTask>& tasks, void* out, int ks);  // ks: the launch's k-step (B box rows)
+int gemm_choose_bk(const std::vector<GemmTask>& tasks);                      // 16 or 32
+constexpr int BK_K3F = 16;  // the K3f leaf GEMM's k-step (its maps and smem; fmm_gemm_core.cuh BK)
 // uniform_tm/tn: the common tile grid when every task has the same one (else 0, 0).
-void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn,
+void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn, int bk,
                      int uniform_tm, int uniform_tn, cudaStream_t stream);
 // K3f leaf GEMM (128 x K3F_BN tiles; epilogue reduce-adds into the W targets through TMA): the
 // tensor map of one parent output block (box 16 columns x 128 rows, 128B swizzle) and the launch.
@@ -116,6 +118,8 @@ void gemm_k3f_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, lo
 // TMA kernel configuration: consumer warp grid of a tile width, SM count, dynamic shared memory.
 void gemm_bn_config(int bn, int* wgm, int* wgn);
 int gemm_sm_count();
+int gemm_bk();      // k-depth of a TMA ring stage (FMM_GEMM_BK of the nvcc build)
+int gemm_stages();  // ring stages (FMM_GEMM_STAGES of the nvcc build)
 int gemm_tma_smem_bytes(int bn);
 int gemm_fused_smem_bytes(int bn);
 // (tiles_m, tiles_n) shared by every task of a prepared list, or (0, 0).

@@ -58,6 +58,7 @@ struct Launch {
   bool aligned16 = true;
   bool tma = false;          // GEMM launches: TMA warp-specialised kernel
   int bn = 128;              // GEMM launches: CTA tile width
+  int bk = 16;               // GEMM launches: k-depth of a TMA ring stage (16 or 32)
   int uni_tm = 0, uni_tn = 0;  // GEMM launches: common tile grid of all tasks (0 = mixed)
   size_t ids_off = 0;        // SKINNY: int ids (row tasks then column tasks)
   int nrow = 0, ncol = 0, max_n = 0, max_m = 0;
@@ -477,6 +478,8 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
   auto choose_tiles = [&](Launch& ln, std::vector<GemmTask>& tasks) {
     ln.tma = !lazy_kernels && use_tma && gemm_tma_eligible(tasks);
     ln.bn = ln.tma ? gemm_choose_bn(tasks) : 128;
+    // the fused leaf level embeds the 16-deep core and reuses this launch's tensor maps
+    ln.bk = ln.tma && !(fuse && ln.kind == Launch::GEMM) ? gemm_choose_bk(tasks) : 16;
     ln.tiles = gemm_prepare(tasks, 128, ln.bn);
     gemm_uniform_grid(tasks, &ln.uni_tm, &ln.uni_tn);
   };
@@ -486,7 +489,7 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
       return;
     }
     std::vector<char> maps(2 * gemm_tma_map_bytes() * tasks.size());
-    if (ln.tma) gemm_tma_maps(tasks, maps.data());
+    if (ln.tma) gemm_tma_maps(tasks, maps.data(), ln.bk);
     ln.maps_off = push(maps.data(), maps.size());
   };
   // one grouped DMMA launch for the regular tasks, one CUDA-core launch for thin ones
@@ -903,7 +906,7 @@ void fmm_plan_s::emit_k3f(std::vector<GemmTask>& tasks, bool lazy_kernels) {
   ln.table_off = push(tasks.data(), tasks.size() * sizeof(GemmTask));
   {  // operand maps (A, B per task), as every TMA GEMM launch
     std::vector<char> maps(2 * gemm_tma_map_bytes() * tasks.size());
-    if (!lazy_kernels) gemm_tma_maps(tasks, maps.data());
+    if (!lazy_kernels) gemm_tma_maps(tasks, maps.data(), BK_K3F);
     ln.maps_off = push(lazy_kernels ? nullptr : maps.data(), maps.size());
   }
   {  // one target map per parent node: its output block, dims[L-1].P x dims[L-1].N
@@ -1715,7 +1718,7 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
                           ln.uni_tn, ka, ls);
         } else if (ln.tma)
           gemm_tma_launch(reinterpret_cast<const GemmTask*>(tab), d_tab + ln.maps_off, ln.count, ln.tiles, ln.bn,
-                          ln.uni_tm, ln.uni_tn, ls);
+                          ln.bk, ln.uni_tm, ln.uni_tn, ls);
         else
           gemm_launch(reinterpret_cast<const GemmTask*>(tab), ln.count, ln.tiles, ln.aligned16, ls);
         break;
@@ -2411,16 +2414,17 @@ fmm_status_t fmm_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const doub
   // the task descriptor (and its tensor maps) go through a stream-ordered upload
   const bool tma = gemm_tma_eligible(t) && !(getenv("FMM_NO_TMA") && getenv("FMM_NO_TMA")[0] == '1');
   const int bn = tma ? gemm_choose_bn(t) : 128;
+  const int bk = tma ? gemm_choose_bk(t) : 16;
   const long long tiles = gemm_prepare(t, 128, bn);
   alignas(128) char buf[1024];
   std::memcpy(buf, t.data(), sizeof(GemmTask));
-  if (tma) gemm_tma_maps(t, buf + 512);
+  if (tma) gemm_tma_maps(t, buf + 512, bk);
   // a stream-ordered descriptor per call: calls on different streams never share one
   GemmTask* d_task = nullptr;
   FMM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_task), sizeof(buf), s));
   FMM_CUDA(cudaMemcpyAsync(d_task, buf, sizeof(buf), cudaMemcpyHostToDevice, s));
   if (tma)
-    gemm_tma_launch(d_task, reinterpret_cast<char*>(d_task) + 512, 1, tiles, bn, t[0].tiles_m, t[0].tiles_n, s);
+    gemm_tma_launch(d_task, reinterpret_cast<char*>(d_task) + 512, 1, tiles, bn, bk, t[0].tiles_m, t[0].tiles_n, s);
   else
     gemm_launch(d_task, 1, tiles, gemm_tasks_aligned16(t), s);
   FMM_CUDA(cudaFreeAsync(d_task, s));
