@@ -842,8 +842,8 @@ class Run:
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / steps
-        ph = np.array([[t["formation_ms"], t["gemm_ms"], t["assembly_ms"], t["strips_ms"], t["total_ms"]]
-                       for t in (plan.execute_timed(A, B, C, stream=stream)[1] for _ in range(2))]).mean(axis=0)
+        ph = np.median(np.array([[t["formation_ms"], t["gemm_ms"], t["assembly_ms"], t["strips_ms"], t["total_ms"]]
+                                 for t in (plan.execute_timed(A, B, C, stream=stream)[1] for _ in range(3))]), axis=0)
         form_ms, gemm_ms, asm_ms, strip_ms, tot_ms = (float(x) for x in ph)
         # sampled rows (columns) of C against cuBLAS on the same rows, then cuBLAS on the whole problem
         g = torch.Generator().manual_seed(7)
@@ -851,16 +851,19 @@ class Run:
         idx = torch.randint(0, outer, (min(32, outer),), generator=g).to(self.device)
         err = ((C[idx] - A[idx] @ B) if w["layout"] == "row" else (C[:, idx] - A @ B[:, idx])).abs().max().item()
         tol = 1e-10 * torch.linalg.norm(A).item() * torch.linalg.norm(B).item()
+        # cuBLAS timed like the plan above: `steps` back-to-back calls between two events (best of 2)
         cub = None
         c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         Cc = torch.matmul(A, B)
         torch.cuda.synchronize()
+        reps = steps if flops < 1e12 else 2
         for _ in range(2):
             c0.record()
-            torch.matmul(A, B, out=Cc)
+            for _ in range(reps):
+                torch.matmul(A, B, out=Cc)
             c1.record()
             c1.synchronize()
-            cub = min(cub or 1e30, c0.elapsed_time(c1))
+            cub = min(cub or 1e30, c0.elapsed_time(c1) / reps)
         del Cc
         add_bytes = st["add_bytes"] - st["fused_add_bytes"]
         leaf_tf = st["leaf_flops"] / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None

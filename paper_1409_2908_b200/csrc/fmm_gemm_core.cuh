@@ -43,8 +43,8 @@ typedef CUtensorMap_opaque CUtensorMap;
 #endif
 
 // BK: k-depth of a ring stage of the fused leaf level and K3f; the plain kernel is instantiated for
-// k-steps KS = 16 and 32 (eight 4-deep slices per stage: A as two 128 x 16 boxes, B as 32 x 16
-// boxes), half the stage hand-overs per flop; the ring keeps the same bytes in flight (96 KB of k)
+// k-steps KS = 16, 32 and 48 (KS/4 4-deep slices per stage: A as KS/16 boxes of 128 x 16, B as
+// boxes of KS x 16): fewer stage hand-overs per flop with about the same bytes in flight
 #ifndef FMM_GEMM_BK
 #define FMM_GEMM_BK 16
 #endif
@@ -59,7 +59,8 @@ static_assert(BK == 16 || BK == 32, "a stage holds one or two 16-column A boxes"
 #ifndef FMM_GEMM_STAGES
 #define FMM_GEMM_STAGES 6  // of 16-deep stages; 32-deep rings have half as many
 #endif
-__host__ __device__ constexpr int ring_stages(int ks) { return FMM_GEMM_STAGES * 16 / ks; }
+// 16-deep: FMM_GEMM_STAGES stages; 32-deep: half as many; 48-deep: two (96 KB of k in flight)
+__host__ __device__ constexpr int ring_stages(int ks) { return ks >= 48 ? 2 : FMM_GEMM_STAGES * 16 / ks; }
 constexpr int GEMM_STAGES = ring_stages(BK);
 constexpr int CONSUMERS = 8, THREADS = 128 + CONSUMERS * 32;  // warpgroup 0 = producer, 1-2 = consumers
 static_assert(THREADS == GEMM_THREADS, "host and device agree on the block size");
@@ -245,7 +246,7 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
                                           int ntasks, int total_tiles, Uniform uni, const FusedArgs& fa,
                                           const K3fArgs* ka = nullptr) {
   static_assert(!(FUSED && K3F), "one epilogue mode");
-  static_assert(KS == 16 || KS == 32, "16- or 32-deep stages");
+  static_assert(KS == 16 || KS == 32 || KS == 48, "16-, 32- or 48-deep stages (whole 16-column A boxes)");
   static_assert(KS == BK || !(FUSED || K3F), "the fused and K3f kernels use BK-deep stages");
   constexpr int STAGES = K3F ? K3F_STAGES : ring_stages(KS);
   constexpr int A_BYTES = BM * KS * 8;

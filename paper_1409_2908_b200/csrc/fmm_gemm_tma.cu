@@ -111,18 +111,22 @@ void gemm_tma_maps(const std::vector<GemmTask>& tasks, void* out, int ks) {
   }
 }
 
-// 32-deep stages halve the stage hand-overs; measured on the round-2 kernel: leaf GEMM 0.979 -> 0.987
-// of the DMMA peak at k = 2048 (c2), 0.924 -> 0.930 at k = 600 (c4), but 0.920 -> 0.918 at k = 450
-// (c3) and 0.915 -> 0.912 at k = 400 (c5t), whose short tiles see the 3-stage ring fill more often
+// Deeper stages mean fewer stage hand-overs per flop.  Measured on the round-2 kernel (leaf GEMM /
+// DMMA peak, 16 / 32 / 48-deep): c2 (k = 2048) 0.980 / 0.987 / 0.987, c4 (k = 600) 0.927 / 0.930 /
+// 0.933, c5 (k = 2000) 0.953 / 0.953 / 0.960, c3 (k = 450) 0.920 / 0.917 / 0.920, c5t (k = 400)
+// 0.915 / 0.912 / 0.918: 48-deep stages (two of them) wherever k is not tiny
 int gemm_choose_bk(const std::vector<GemmTask>& tasks) {
-  if (const char* e = getenv("FMM_GEMM_BK_RUN")) return atoi(e) == 32 ? 32 : 16;
-  double f32 = 0, f = 0;
+  if (const char* e = getenv("FMM_GEMM_BK_RUN")) {
+    const int v = atoi(e);
+    return v == 48 || v == 32 ? v : 16;
+  }
+  double fl = 0, f = 0;
   for (const auto& t : tasks) {
     const double w = (double)t.m * t.n * (double)t.k;
     f += w;
-    if (t.k >= 512) f32 += w;
+    if (t.k >= 96) fl += w;
   }
-  return f > 0 && f32 >= 0.5 * f ? 32 : 16;
+  return f > 0 && fl >= 0.5 * f ? 48 : 16;
 }
 
 template <int BN, int WGM, int WGN, int KS>
@@ -223,7 +227,8 @@ void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, lo
   const Uniform uni{uniform_tm * uniform_tn, uniform_tm, uniform_tn};
   if (total_tiles <= 0 || ntasks <= 0) return;
   const int sms = sm_count();
-  if (bk == 32) launch_ks<32>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
+  if (bk == 48) launch_ks<48>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
+  else if (bk == 32) launch_ks<32>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
   else if (bk == 16) launch_ks<16>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
   else throw Error(FMM_E_INVALID_ARG, "unsupported GEMM k-step " + std::to_string(bk));
 }
