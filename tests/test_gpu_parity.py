@@ -484,3 +484,25 @@ def test_shard_reads_only_its_input_blocks(alg, shape, layout, mode, G):
         assert np.array_equal(got, clean), (g, np.isnan(got).sum())
     print(f"{alg} {mode} G={G}: {restricted} of {G} shards read a strict subset of A and B")
     assert restricted >= 1  # measured: 2 of 3, 3 of 4, 2 of 4, 8 of 8 for the four cases
+
+
+@pytest.mark.parametrize("alg,shape,layout,L", [("winograd_class_222_7", (512, 512, 512), "col", 2),
+                                                ("hk_class_323_15", (301, 200, 299), "row", 2)])
+def test_execute_profile_lists_every_launch(alg, shape, layout, L):
+    # fmm_execute_profile: one entry per launch of the step (kind, recursion level, time); the kinds
+    # follow the plan's structure and the launch count matches fmm_plan_stats
+    P, Q, N = shape
+    A, B = I.problem(P, Q, N, seed=25, kind="integers")
+    p = F.Plan(falg(alg), P, Q, N, L, layout=layout)
+    C = p.new_output()
+    p.execute(dev(A, layout), dev(B, layout), C)  # first use: module loading, kernel attributes
+    prof = p.execute_profile(dev(A, layout), dev(B, layout), C)
+    torch.cuda.synchronize()
+    assert np.array_equal(C.cpu().numpy(), A @ B)
+    kinds = [k for k, _, _ in prof]
+    assert kinds.count("leaf_gemm") == 1 and all(ms >= 0 for _, _, ms in prof)
+    assert kinds.index("form_A") < kinds.index("leaf_gemm") < kinds.index("assembly")
+    st = p.stats()
+    assert len(prof) <= st["launches"]  # a thin-strip entry can hold two kernel launches
+    _, t = p.execute_timed(dev(A, layout), dev(B, layout), C)
+    assert abs(sum(ms for _, _, ms in prof) - t["total_ms"]) < 0.5 * t["total_ms"] + 0.05
