@@ -91,6 +91,12 @@ typedef struct {
                                Streaming strategy only; where collapse_levels applies the collapsed
                                kernels run instead.  Needs TMA-eligible leaf views and no thin
                                leaves, else the plan silently runs the separate kernels.
+                               2: the same launch in background mode: every CTA runs leaf tiles
+                               and the producer warpgroup's three idle warps run the addition
+                               jobs (bitwise equal as well; takes precedence over collapse_levels;
+                               measured slower than the separate kernels on every config,
+                               DESIGN.md sec. 6b).  Needs 256 bytes of shared memory per job
+                               input and producer warp beside the GEMM ring, else separate kernels.
                                0: separate formation / GEMM / assembly launches. */
   int shard_mode;           /* with shard_count > 1: 0 = leaf-level HYBRID sharding (the default:
                                balanced to one leaf row); 1 = the top-level products r1 in contiguous
@@ -313,6 +319,9 @@ fmm_status_t fmm_select(const fmm_alg* const* algs, int nalgs, int64_t P, int64_
    leaf-level kernel of `alg` (fuse_leaf_level = 1) for the given layout, CSE setting and GEMM tile
    width (128, 112, 96, 80 or 64).  FMM_E_CUDA with the compiler log on failure. */
 fmm_status_t fmm_fused_compile_check(const fmm_alg* alg, int layout, int cse, int bn);
+/* The same for ring depth ks (16, 32 or 48) and fuse_leaf_level mode (1 = addition CTAs,
+   2 = background jobs in the GEMM CTAs' spare warps).  fmm_fused_compile_check is (ks 16, mode 1). */
+fmm_status_t fmm_fused_compile_check_ex(const fmm_alg* alg, int layout, int cse, int bn, int ks, int mode);
 
 /* Execute C <- A*B (beta = 0: C is overwritten).  A, B, C are device pointers on the plan's
    device laid out per opt->layout; C must not alias A or B.  Leading dimensions in elements:

@@ -395,7 +395,9 @@ struct FusedKernel {
   std::string source;
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern = nullptr;
-  int bn = 128;
+  int bn = 128, ks = 16;
+  bool bg = false;
+  int stage_w = 0;  // background mode: input staging bytes per producer warp
   int smem_set = -1;  // device on which the dynamic shared-memory limit was raised
 };
 
@@ -406,7 +408,8 @@ namespace {
 // (L2-coherent: assembly inputs are written by other SMs during the launch), the chains (with the
 // program's CSE temporaries) run in registers, every output is stored once -- the streaming K1/K3
 // kernel body, so the fused and the separate paths give bit-identical results.
-void emit_job_fn(std::ostringstream& o, const std::string& name, const LincombSpec& spec, const Program& p, int V) {
+void emit_job_fn(std::ostringstream& o, const std::string& name, const LincombSpec& spec, const Program& p, int V,
+                 int data_regs) {
   const int nin = spec.nin, nout = spec.nout;
   const std::string T = V == 2 ? "double2" : "double";
   std::vector<std::string> comps = V == 2 ? std::vector<std::string>{".x", ".y"} : std::vector<std::string>{""};
@@ -427,8 +430,8 @@ void emit_job_fn(std::ostringstream& o, const std::string& name, const LincombSp
   o << "  const int cvec = cols / " << V << ";\n";
   o << "  for (int row = row0; row < row0 + nrows; ++row) {\n";
   o << "    const long long bi = (long long)row * ldi, bo = (long long)row * ldo;\n";
-  // U element groups per lane per iteration: more loads in flight, within ~96 data registers
-  const int U = std::max(1, std::min(4, 96 / (2 * V * std::max<int>(1, (int)used.size()))));
+  // U element groups per lane per iteration: more loads in flight, within data_regs registers
+  const int U = std::max(1, std::min(4, data_regs / (2 * V * std::max<int>(1, (int)used.size()))));
   o << "    for (int cv = lane; cv < cvec; cv += " << 32 * U << ") {\n";
   for (int u = 0; u < U; ++u) {
     o << "    const bool ok" << u << " = cv + " << 32 * u << " < cvec;\n";
@@ -462,6 +465,78 @@ void emit_job_fn(std::ostringstream& o, const std::string& name, const LincombSp
   o << "    }\n  }\n  __syncwarp();  // every lane is done with the slot before the next job rewrites it\n}\n";
 }
 
+// The inputs a program's chains and temporaries read (ascending).
+std::vector<int> program_inputs(const LincombSpec& spec, const Program& p) {
+  std::set<int> used;
+  for (const auto& e : p.outs)
+    for (const auto& kv : e)
+      if (kv.first < spec.nin) used.insert(kv.first);
+  for (const auto& t : p.temps) {
+    if (std::get<0>(t) < spec.nin) used.insert(std::get<0>(t));
+    if (std::get<1>(t) < spec.nin) used.insert(std::get<1>(t));
+  }
+  return std::vector<int>(used.begin(), used.end());
+}
+
+// Background-mode variant of emit_job_fn for the producer warps (56 registers): per element (8
+// bytes per lane) every input is staged in the warp's shared-memory area st by cp.async -- all of
+// them in flight at once, none held in registers -- then the chains read them back with ld.shared
+// where they use them.  Same chains, same order of operations: bitwise equal to emit_job_fn.
+void emit_job_fn_staged(std::ostringstream& o, const std::string& name, const LincombSpec& spec, const Program& p) {
+  const int nin = spec.nin, nout = spec.nout;
+  const std::vector<int> used = program_inputs(spec, p);
+  std::map<int, int> slot;
+  for (size_t s = 0; s < used.size(); ++s) slot[used[s]] = (int)s;
+  auto var = [&](int v) {
+    if (v < nin) return "lds64(xs + " + std::to_string(256 * slot.at(v)) + "u)";
+    return "t" + std::to_string(v - nin);
+  };
+  o << "__device__ __forceinline__ void " << name
+    << "(const char* nd, int row0, int nrows, int cols, int lane, unsigned sp, unsigned st) {\n";
+  o << "  for (int w = lane; w < " << nin + nout + 2 << "; w += 32) sts_u64(sp + 8u * w, reinterpret_cast<const unsigned long long*>(nd)[w]);\n";
+  o << "  __syncwarp();\n";
+  o << "  const long long ldi = (long long)lds_u64(sp + " << 8 * (nin + nout) << "u), ldo = (long long)lds_u64(sp + " << 8 * (nin + nout + 1) << "u);\n";
+  o << "  const unsigned xs = st + 8u * (unsigned)lane;\n";
+  o << "  for (int row = row0; row < row0 + nrows; ++row) {\n";
+  o << "    const long long bi = (long long)row * ldi, bo = (long long)row * ldo;\n";
+  o << "    for (int cv = lane; cv < cols; cv += 32) {\n";
+  o << "    const long long pi = bi + cv, po = bo + cv;\n";
+  for (int i : used)
+    o << "    cp_async8(xs + " << 256 * slot.at(i) << "u, reinterpret_cast<const double*>(lds_u64(sp + " << 8 * i << "u)) + pi);\n";
+  o << "    cp_async_wait_all();\n";
+  // FMM_FUSED_DIAG (timing diagnostics only, wrong results): 1 = integer XOR in place of every
+  // floating-point operation, 2 = each output a copy of its first input (no arithmetic)
+  const int diag = getenv("FMM_FUSED_DIAG") ? atoi(getenv("FMM_FUSED_DIAG")) : 0;
+  auto bop = [&](const std::string& x, const std::string& y, const char* op) {
+    if (diag == 1) return "__longlong_as_double(__double_as_longlong(" + x + ") ^ __double_as_longlong(" + y + "))";
+    if (diag == 2) return x;
+    return x + " " + op + " " + y;
+  };
+  for (size_t t = 0; t < p.temps.size(); ++t) {
+    const int a = std::get<0>(p.temps[t]), b = std::get<1>(p.temps[t]);
+    const double r = std::get<2>(p.temps[t]);
+    o << "    const double t" << t << " = ";
+    if (r == 1.0) o << bop(var(a), var(b), "+") << ";\n";
+    else if (r == -1.0) o << bop(var(a), var(b), "-") << ";\n";
+    else o << bop(var(a), diag ? var(b) : dlit(r) + " * " + var(b), "+") << ";\n";
+  }
+  for (int q = 0; q < nout; ++q) {
+    o << "    if (double* oq = reinterpret_cast<double*>(lds_u64(sp + " << 8 * (nin + q) << "u))) {\n    double y;\n";
+    if (diag) {
+      bool first = true;
+      for (const auto& kv : p.outs[q]) {
+        if (first) o << "    y = " << var(kv.first) << ";\n", first = false;
+        else if (diag == 1) o << "    y = " << bop("y", var(kv.first), "+") << ";\n";
+      }
+      if (first) o << "    y = 0.0;\n";
+    } else {
+      emit_chain(o, "y", p.outs[q], "", var);
+    }
+    o << "    oq[po] = y;\n    }\n";
+  }
+  o << "    }\n  }\n  __syncwarp();\n}\n";
+}
+
 std::string strip_pragma_once(const char* src) {
   std::string s(src);
   const std::string key = "#pragma once";
@@ -474,21 +549,41 @@ std::map<std::string, std::shared_ptr<FusedKernel>> g_fcache;
 
 }  // namespace
 
-std::string fused_generate(const std::vector<LincombSpec>& specs, int bn) {
+int fused_bg_stage_bytes(const std::vector<LincombSpec>& specs) {
+  int nin = 1;
+  for (const auto& s : specs) nin = std::max(nin, s.nin);
+  return 256 * nin;  // 8 bytes x 32 lanes per input
+}
+
+std::string fused_generate(const std::vector<LincombSpec>& specs, int bn, int ks, bool bg) {
+  if (ks != 16 && ks != 32 && ks != 48) throw Error(FMM_E_INVALID_ARG, "fused: ring depth must be 16, 32 or 48");
   if (specs.empty() || (int)specs.size() > FUSED_MAX_PROGS) throw Error(FMM_E_INVALID_ARG, "fused: bad program count");
   int wgm = 0, wgn = 0;
   gemm_bn_config(bn, &wgm, &wgn);
   std::ostringstream o;
-  o << "// generated by fmm_codegen.cpp: fused leaf level, BN=" << bn << "\n#define FMM_NVRTC 1\n";
+  o << "// generated by fmm_codegen.cpp: fused leaf level, BN=" << bn << ", KS=" << ks << (bg ? ", background jobs" : "")
+    << "\n#define FMM_NVRTC 1\n";
+  // background mode: the producer warpgroup keeps 56 registers per thread and the consumers get 224
+  // (of the CTA's 384 x 168), enough for a job's inputs at U = 1 (the 8-byte variant where 16-byte
+  // ones would spill) and the 64 x 32 warp tile
+  if (bg) {
+    o << "#define FMM_BG_STAGE_W " << fused_bg_stage_bytes(specs) << "\n";
+    int pr = 56, cr = 224;
+    if (const char* e = getenv("FMM_FUSED_REGS")) sscanf(e, "%d,%d", &pr, &cr);  // experiments: "producer,consumer"
+    o << "#define FMM_FUSED_BG 1\n#define FMM_PRODUCER_REGS " << pr << "\n#define FMM_CONSUMER_REGS " << cr << "\n";
+  }
   // the ring geometry of the nvcc-compiled kernels, so the host's shared-memory sizes match
   o << "#define FMM_GEMM_BK " << gemm_bk() << "\n#define FMM_GEMM_STAGES " << gemm_stages() << "\n";
   if (const char* e = getenv("FMM_FUSED_LD")) o << "#define FMM_LD_KIND " << atoi(e) << "\n";  // diagnostics
+  if (getenv("FMM_FUSED_STATS")) o << "#define FMM_FUSED_STATS 1\n";                              // diagnostics
+  if (const char* e = getenv("FMM_FUSED_DIAG")) o << "// diag " << e << "\n";                   // (new cache key)
   o << strip_pragma_once(kFmmDeviceSrc) << "\n" << strip_pragma_once(kFmmCoreSrc) << "\nnamespace fmm {\n";
   for (size_t q = 0; q < specs.size(); ++q) {
     if (specs[q].strategy != FMM_ADD_STREAMING) throw Error(FMM_E_INVALID_ARG, "fused: streaming programs only");
     const Program prog = build_program(specs[q]);
-    emit_job_fn(o, "prog" + std::to_string(q) + "_v2", specs[q], prog, 2);
-    emit_job_fn(o, "prog" + std::to_string(q) + "_v1", specs[q], prog, 1);
+    emit_job_fn(o, "prog" + std::to_string(q) + "_v2", specs[q], prog, 2, 96);
+    emit_job_fn(o, "prog" + std::to_string(q) + "_v1", specs[q], prog, 1, 96);
+    if (bg) emit_job_fn_staged(o, "prog" + std::to_string(q) + "_s", specs[q], prog);
   }
   o << "__device__ void fmm_add_job(const FusedArgs& fa, const FusedJob& j, int lane, unsigned sp) {\n";
   o << "  const char* nd = fa.node_tab[j.prog] + (long long)j.node * fa.node_bytes[j.prog];\n";
@@ -496,11 +591,21 @@ std::string fused_generate(const std::vector<LincombSpec>& specs, int bn) {
   for (size_t q = 0; q < specs.size(); ++q)
     o << "    case " << q << ": if (fa.vec2[" << q << "]) prog" << q << "_v2(nd, j.row0, j.nrows, fa.cols[" << q
       << "], lane, sp); else prog" << q << "_v1(nd, j.row0, j.nrows, fa.cols[" << q << "], lane, sp); break;\n";
-  o << "  }\n}\n}  // namespace fmm\n";
+  o << "  }\n}\n";
+  if (bg) {
+    o << "__device__ void fmm_add_job_bg(const FusedArgs& fa, const FusedJob& j, int lane, unsigned sp, unsigned st) {\n";
+    o << "  const char* nd = fa.node_tab[j.prog] + (long long)j.node * fa.node_bytes[j.prog];\n";
+    o << "  switch (j.prog) {\n";
+    for (size_t q = 0; q < specs.size(); ++q)
+      o << "    case " << q << ": prog" << q << "_s(nd, j.row0, j.nrows, fa.cols[" << q << "], lane, sp, st); break;\n";
+    o << "  }\n}\n";
+  }
+  o << "}  // namespace fmm\n";
   o << "extern \"C\" __global__ void __launch_bounds__(fmm::THREADS, 1)\n"
        "fmm_fused(const fmm::GemmTask* __restrict__ tasks, const fmm::CUtensorMap* __restrict__ maps, int ntasks,\n"
        "          int total_tiles, fmm::Uniform uni, fmm::FusedArgs fa) {\n"
-    << "  fmm::gemm_body<" << bn << ", " << wgm << ", " << wgn << ", true>(tasks, maps, ntasks, total_tiles, uni, fa);\n}\n";
+    << "  fmm::gemm_body<" << bn << ", " << wgm << ", " << wgn << ", true, false, " << ks
+    << ">(tasks, maps, ntasks, total_tiles, uni, fa);\n}\n";
   return o.str();
 }
 
@@ -510,8 +615,16 @@ std::vector<char> fused_compile(const std::string& source) {
   }
   nvrtcProgram prog;
   NVRTC_CHECK(nvrtcCreateProgram(&prog, source.c_str(), "fmm_fused.cu", 0, nullptr, nullptr));
-  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "--fmad=false", "-lineinfo"};
-  nvrtcResult r = nvrtcCompileProgram(prog, 4, opts);
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "--fmad=false", "-lineinfo", "--ptxas-options=-v"};
+  const bool verbose = getenv("FMM_FUSED_PTXAS_V") != nullptr;  // diagnostics: registers / spills to stderr
+  nvrtcResult r = nvrtcCompileProgram(prog, verbose ? 5 : 4, opts);
+  if (verbose && r == NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    nvrtcGetProgramLog(prog, &log[0]);
+    fputs(log.c_str(), stderr);
+  }
   if (r != NVRTC_SUCCESS) {
     size_t n = 0;
     nvrtcGetProgramLogSize(prog, &n);
@@ -525,13 +638,19 @@ std::vector<char> fused_compile(const std::string& source) {
   std::vector<char> cubin(n);
   NVRTC_CHECK(nvrtcGetCUBIN(prog, cubin.data()));
   nvrtcDestroyProgram(&prog);
+  if (const char* path = getenv("FMM_FUSED_CUBIN_DUMP")) {  // diagnostics: keep the cubin (cuobjdump -sass)
+    if (FILE* f = fopen(path, "wb")) fwrite(cubin.data(), 1, cubin.size(), f), fclose(f);
+  }
   return cubin;
 }
 
-std::shared_ptr<FusedKernel> fused_get(const std::vector<LincombSpec>& specs, int bn) {
+std::shared_ptr<FusedKernel> fused_get(const std::vector<LincombSpec>& specs, int bn, int ks, bool bg) {
   auto k = std::make_shared<FusedKernel>();
-  k->source = fused_generate(specs, bn);
+  k->source = fused_generate(specs, bn, ks, bg);
   k->bn = bn;
+  k->ks = ks;
+  k->bg = bg;
+  k->stage_w = bg ? fused_bg_stage_bytes(specs) : 0;
   std::lock_guard<std::mutex> lock(g_fmu);
   auto it = g_fcache.find(k->source);
   if (it != g_fcache.end()) return it->second;
@@ -544,7 +663,7 @@ std::shared_ptr<FusedKernel> fused_get(const std::vector<LincombSpec>& specs, in
 
 void fused_launch(const FusedKernel& k, const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles,
                   int uniform_tm, int uniform_tn, const FusedArgs& fa, cudaStream_t stream) {
-  const int smem = gemm_fused_smem_bytes(k.bn);
+  const int smem = gemm_fused_smem_bytes(k.bn, k.ks, k.stage_w);
   int dev = 0;
   FMM_CUDA(cudaGetDevice(&dev));
   if (k.smem_set != dev) {

@@ -30,7 +30,9 @@
 // first parent: nothing can start before it); the TMA thread waits for ready[parent] before the
 // first load of a tile; consumers count each stored tile into tiles_done[parent] and, out of
 // tiles, join the phase-1 queue.  All CTAs must be co-resident (cooperative launch, grid = #SMs):
-// jobs wait on tiles and tiles on jobs.
+// jobs wait on tiles and tiles on jobs.  FMM_FUSED_BG (background mode): no addition CTAs; warps
+// 1-3 of every CTA's producer warpgroup run the jobs (staged through shared memory, 56 registers)
+// beside the CTA's own leaf tiles -- correct, but the DADDs starve beside DMMA.
 #pragma once
 
 namespace fmm {
@@ -68,13 +70,35 @@ constexpr int A_BYTES = BM * BK * 8;                           // 16 KB per 16 c
 __host__ __device__ constexpr int gemm_smem_bytes(int bn, int ks = BK) {
   return ring_stages(ks) * (BM * ks * 8 + ks * bn * 8) + 1024 /*align*/ + 256 /*barriers*/;
 }
-__host__ __device__ constexpr int fused_smem_bytes(int bn) { return gemm_smem_bytes(bn) + FUSED_PTR_BYTES; }
+// bg_stage: per producer warp, the background jobs' input staging (3 warps)
+__host__ __device__ constexpr int fused_smem_bytes(int bn, int ks = BK, int bg_stage = 0) {
+  return gemm_smem_bytes(bn, ks) + FUSED_PTR_BYTES + 3 * bg_stage;
+}
+#ifndef FMM_BG_STAGE_W
+#define FMM_BG_STAGE_W 0
+#endif
 // K3f: a 4-stage ring plus two staging tiles (+alpha acc and -alpha acc) of 128 x bn doubles
 constexpr int K3F_STAGES = 64 / BK;
 __host__ __device__ constexpr int k3f_smem_bytes(int bn) {
   return K3F_STAGES * (A_BYTES + BK * bn * 8) + 1024 /*align*/ + 1024 /*barriers, aligned*/ + 2 * BM * bn * 8;
 }
 constexpr int GROUP_M = 8;
+// FMM_FUSED_BG (fused kernel only): every CTA runs leaf tiles and the producer warpgroup's warps
+// 1-3 run the addition jobs beside them (no addition CTAs)
+#ifndef FMM_FUSED_BG
+#define FMM_FUSED_BG 0
+#endif
+// register split of the warp-specialised CTA (setmaxnreg).  The CTA is launched with 168 registers
+// per thread (__launch_bounds__(384, 1)); setmaxnreg.inc blocks until the producer's .dec has
+// returned enough of them, so the split must fit what the CTA holds: 128 P + 256 C <= 384 x 168
+#ifndef FMM_PRODUCER_REGS
+#define FMM_PRODUCER_REGS 40
+#endif
+#ifndef FMM_CONSUMER_REGS
+#define FMM_CONSUMER_REGS 232
+#endif
+static_assert(128 * FMM_PRODUCER_REGS + 256 * FMM_CONSUMER_REGS <= 384 * 168,
+              "register split exceeds the CTA's allocation (setmaxnreg.inc would wait forever)");
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -144,6 +168,14 @@ __device__ __forceinline__ unsigned long long lds_u64(unsigned addr) {
   unsigned long long v;
   asm volatile("ld.shared.u64 %0, [%1];\n" : "=l"(v) : "r"(addr));
   return v;
+}
+// background jobs: each lane stages its element's inputs in shared memory (no registers held while
+// the copies are in flight), 8 bytes per lane per input
+__device__ __forceinline__ void cp_async8(unsigned dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 __device__ __forceinline__ void sts_u64(unsigned addr, unsigned long long v) {
   asm volatile("st.shared.u64 [%0], %1;\n" ::"r"(addr), "l"(v) : "memory");
@@ -219,35 +251,58 @@ __device__ __forceinline__ int claim(unsigned long long* ctr, int lane) {
 // Generated per algorithm (fmm_codegen.cpp) in the NVRTC source of the fused kernel.
 // sp: shared address of the warp's FUSED_PTR_SLOT.
 __device__ void fmm_add_job(const FusedArgs& fa, const FusedJob& j, int lane, unsigned sp);
+// background mode: the same chains with the inputs staged at st (FMM_BG_STAGE_W bytes of shared memory)
+__device__ void fmm_add_job_bg(const FusedArgs& fa, const FusedJob& j, int lane, unsigned sp, unsigned st);
 
 // One job with a whole warp: assembly jobs first wait until every leaf tile of their parent is
 // stored; formation jobs publish (release) to the TMA readers of the leaf products.
-__device__ __forceinline__ void run_job(const FusedArgs& fa, int jidx, int lane, unsigned sp) {
+// FMM_FUSED_STATS (diagnostics): clock64 totals in ctr[2 + 2 np + i]: 0 the TMA threads' waits for
+// formation, 1 the assembly jobs' waits for tiles, 2 / 3 job time in producer / consumer warps
+#ifndef FMM_FUSED_STATS
+#define FMM_FUSED_STATS 0
+#endif
+template <bool STAGED = false>
+__device__ __forceinline__ void run_job(const FusedArgs& fa, int jidx, int lane, unsigned sp, unsigned st = 0) {
   const FusedJob j = fa.jobs[jidx];
+#if FMM_FUSED_STATS
+  const long long t0 = clock64();
+#endif
   if (j.kind == 1) {
     if (lane == 0) {
       const unsigned long long target = (unsigned long long)__ldg(&fa.tiles_target[j.dep]);
       while (ld_acquire(&fa.ctr[2 + fa.np + j.dep]) < target) __nanosleep(256);
       fence_proxy_async_global();  // the tiles were stored by generic proxies; TMA reads them
+#if FMM_FUSED_STATS
+      atomicAdd(&fa.ctr[2 + 2 * fa.np + 1], (unsigned long long)(clock64() - t0));
+#endif
     }
     __syncwarp();
   }
-  fmm_add_job(fa, j, lane, sp);
+  if constexpr (STAGED) fmm_add_job_bg(fa, j, lane, sp, st);
+  else fmm_add_job(fa, j, lane, sp);
   if (j.kind == 0) {
     fence_proxy_async_global();
     __threadfence();
     __syncwarp();
     if (lane == 0) atomicAdd(&fa.ctr[2 + j.dep], 1ull);
   }
+#if FMM_FUSED_STATS
+  if (lane == 0) atomicAdd(&fa.ctr[2 + 2 * fa.np + (STAGED ? 2 : 3)], (unsigned long long)(clock64() - t0));
+#endif
 }
 
+#ifdef FMM_BG_PROBE
+__device__ const double* fmm_bg_src;
+__device__ double* fmm_bg_dst;
+__device__ long long fmm_bg_n;
+#endif
 template <int BN, int WGM, int WGN, bool FUSED, bool K3F = false, int KS = BK>
 __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, const CUtensorMap* __restrict__ maps,
                                           int ntasks, int total_tiles, Uniform uni, const FusedArgs& fa,
                                           const K3fArgs* ka = nullptr) {
   static_assert(!(FUSED && K3F), "one epilogue mode");
   static_assert(KS == 16 || KS == 32 || KS == 48, "16-, 32- or 48-deep stages (whole 16-column A boxes)");
-  static_assert(KS == BK || !(FUSED || K3F), "the fused and K3f kernels use BK-deep stages");
+  static_assert(KS == BK || !K3F, "the K3f kernel uses BK-deep stages");
   constexpr int STAGES = K3F ? K3F_STAGES : ring_stages(KS);
   constexpr int A_BYTES = BM * KS * 8;
   static_assert(WGM * WGN == CONSUMERS, "8 consumer warps");
@@ -265,6 +320,7 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
   const unsigned bars = base + STAGES * STAGE_T;
   const unsigned sp = bars + 256u + (unsigned)warp * FUSED_PTR_SLOT;  // fused: this warp's pointer slot
   int gemm_ctas = (int)gridDim.x;
+#if !FMM_FUSED_BG
   if constexpr (FUSED) {
     gemm_ctas = fa.gemm_ctas;
     if ((int)blockIdx.x >= gemm_ctas) {
@@ -282,6 +338,7 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
       return;
     }
   }
+#endif
   auto full_bar = [&](int s) { return bars + 8u * s; };
   auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
 
@@ -296,7 +353,7 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
 
   if (warp < 4) {
     // ------------------------------ producer warpgroup ------------------------------
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(FMM_PRODUCER_REGS) : "memory");
     if (warp == 0 && lane == 0) {
       int stage = 0;
       unsigned phase = 0;
@@ -308,7 +365,13 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
           if (node != ready_node) {
             // (a watchdog __trap() in these waits was measured to slow the whole launch by ~13 %)
             const unsigned long long target = (unsigned long long)__ldg(&fa.ready_target[node]);
+#if FMM_FUSED_STATS
+            const long long t0 = clock64();
+#endif
             while (ld_acquire(&fa.ctr[2 + node]) < target) __nanosleep(128);
+#if FMM_FUSED_STATS
+            atomicAdd(&fa.ctr[2 + 2 * fa.np], (unsigned long long)(clock64() - t0));
+#endif
             fence_proxy_async_global();
             ready_node = node;
           }
@@ -328,9 +391,49 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
         }
       }
     }
+#if FMM_FUSED_BG
+    // background mode: the producer warpgroup's idle warps 1-3 run the addition jobs while the
+    // consumers run the leaf tiles of the same SM (the first parent's formation with every warp)
+    if constexpr (FUSED) {
+      if (warp >= 1) {
+        const unsigned st = bars + 256u + FUSED_PTR_BYTES + (unsigned)(warp - 1) * FMM_BG_STAGE_W;
+        for (;;) {
+          const int idx = claim(&fa.ctr[0], lane);
+          if (idx >= fa.njobs0) break;
+          run_job<true>(fa, idx, lane, sp, st);
+        }
+        for (;;) {
+          const int idx = claim(&fa.ctr[1], lane);
+          if (fa.njobs0 + idx >= fa.njobs) break;
+          run_job<true>(fa, fa.njobs0 + idx, lane, sp, st);
+        }
+      }
+    }
+#endif
+#ifdef FMM_BG_PROBE  // timing experiment: the producer warpgroup's idle warps 1-3 stream-copy a buffer
+    // (read + write, 16-byte accesses, 4 in flight per lane) while the consumers run the GEMM: the
+    // cost of background bandwidth work inside GEMM CTAs (results of the copy are not used)
+    if constexpr (!FUSED && !K3F) {
+      if (warp >= 1 && fmm_bg_n > 0) {
+        const long long n2 = fmm_bg_n / 2;
+        const long long tid = (long long)blockIdx.x * 96 + (warp - 1) * 32 + lane, nth = (long long)gridDim.x * 96;
+        const double2* src = reinterpret_cast<const double2*>(fmm_bg_src);
+        double2* dst = reinterpret_cast<double2*>(fmm_bg_dst);
+        long long e = tid;
+        for (; e + 3 * nth < n2; e += 4 * nth) {
+          double2 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] = __ldcs(src + e + u * nth);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) __stcs(dst + e + u * nth, v[u]);
+        }
+        for (; e < n2; e += nth) __stcs(dst + e, __ldcs(src + e));
+      }
+    }
+#endif
     return;
   }
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(FMM_CONSUMER_REGS) : "memory");
 
   // ------------------------------ consumers ------------------------------
   if constexpr (FUSED) {

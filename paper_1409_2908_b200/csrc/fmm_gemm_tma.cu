@@ -207,7 +207,15 @@ static_assert(BK_K3F == BK, "the K3f maps and kernel agree on the k-step");
 int gemm_bk() { return BK; }
 int gemm_stages() { return GEMM_STAGES; }
 int gemm_tma_smem_bytes(int bn) { return gemm_smem_bytes(bn, BK); }
-int gemm_fused_smem_bytes(int bn) { return fused_smem_bytes(bn); }
+int gemm_fused_smem_bytes(int bn, int ks, int bg_stage) { return fused_smem_bytes(bn, ks, bg_stage); }
+int gemm_max_smem_bytes() {
+  int dev = 0, v = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 232448;  // sm_100
+  }
+  return v;
+}
 
 template <int KS>
 static void launch_ks(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn, int sms,
@@ -226,6 +234,26 @@ void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, lo
                      int uniform_tm, int uniform_tn, cudaStream_t stream) {
   const Uniform uni{uniform_tm * uniform_tn, uniform_tm, uniform_tn};
   if (total_tiles <= 0 || ntasks <= 0) return;
+#ifdef FMM_BG_PROBE
+  {  // FMM_BG_BYTES: bytes the idle producer warps copy in the background (timing experiment)
+    static double* buf = nullptr;
+    static long long n = 0;
+    const char* e = getenv("FMM_BG_BYTES");
+    const long long want = e ? atoll(e) / 16 : 0;  // elements per src / dst half
+    if (want > 0 && want != n) {
+      if (buf) FMM_CUDA(cudaFree(buf));
+      FMM_CUDA(cudaMalloc(&buf, (size_t)want * 16));
+      FMM_CUDA(cudaMemset(buf, 0, (size_t)want * 16));
+      n = want;
+    }
+    const double* src = buf;
+    double* dst = buf ? buf + n : nullptr;
+    const long long nn = want > 0 && total_tiles > 1000 ? n : 0;  // the leaf GEMM only, not tiny strips
+    FMM_CUDA(cudaMemcpyToSymbolAsync(fmm_bg_src, &src, sizeof(src), 0, cudaMemcpyHostToDevice, stream));
+    FMM_CUDA(cudaMemcpyToSymbolAsync(fmm_bg_dst, &dst, sizeof(dst), 0, cudaMemcpyHostToDevice, stream));
+    FMM_CUDA(cudaMemcpyToSymbolAsync(fmm_bg_n, &nn, sizeof(nn), 0, cudaMemcpyHostToDevice, stream));
+  }
+#endif
   const int sms = sm_count();
   if (bk == 48) launch_ks<48>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
   else if (bk == 32) launch_ks<32>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);

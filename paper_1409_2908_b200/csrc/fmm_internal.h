@@ -121,7 +121,8 @@ int gemm_sm_count();
 int gemm_bk();      // k-depth of a TMA ring stage (FMM_GEMM_BK of the nvcc build)
 int gemm_stages();  // ring stages (FMM_GEMM_STAGES of the nvcc build)
 int gemm_tma_smem_bytes(int bn);
-int gemm_fused_smem_bytes(int bn);
+int gemm_fused_smem_bytes(int bn, int ks, int bg_stage = 0);
+int gemm_max_smem_bytes();  // the device's opt-in dynamic shared memory per block
 // (tiles_m, tiles_n) shared by every task of a prepared list, or (0, 0).
 void gemm_uniform_grid(const std::vector<GemmTask>& tasks, int* tm, int* tn);
 // Thin products (one dimension <= skinny_limit()) on the CUDA cores (fmm_skinny.cu): ids index
@@ -185,10 +186,12 @@ std::string lincomb_source(const LincombKernel& k);
 
 // The fused leaf-level kernel: the GEMM core (fmm_gemm_core.cuh) plus the plan's addition programs
 // as straight-line device code (the same chains as the K1/K3 kernels of `progs`), compiled with
-// NVRTC for one tile width; cached by source.
+// NVRTC for one tile width and ring depth ks (16, 32, 48); cached by source.  bg: background mode
+// (FMM_FUSED_BG: the producer warpgroup's spare warps run the jobs, every CTA runs leaf tiles).
 struct FusedKernel;
-std::shared_ptr<FusedKernel> fused_get(const std::vector<LincombSpec>& specs, int bn);
-std::string fused_generate(const std::vector<LincombSpec>& specs, int bn);  // host only
+std::shared_ptr<FusedKernel> fused_get(const std::vector<LincombSpec>& specs, int bn, int ks, bool bg);
+std::string fused_generate(const std::vector<LincombSpec>& specs, int bn, int ks, bool bg);  // host only
+int fused_bg_stage_bytes(const std::vector<LincombSpec>& specs);  // per producer warp (background mode)
 std::vector<char> fused_compile(const std::string& source);                  // host only (NVRTC -> cubin)
 const LincombSpec& lincomb_spec(const LincombKernel& k);
 void fused_launch(const FusedKernel& k, const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles,

@@ -129,6 +129,7 @@ struct fmm_plan_s {
 
   bool use_tma = true;  // FMM_NO_TMA=1 forces the cp.async GEMM (diagnostics)
   bool fuse = true;     // fuse_leaf_level option (FMM_NO_FUSE=1 overrides)
+  bool fuse_bg = false;  // fuse_leaf_level = 2: the jobs run in the GEMM CTAs' spare warps (FMM_FUSE_BG=1)
   bool collapse = false;  // the last two levels' formation / assembly in one pass each (sec. 6c)
   bool collapse_asm = false;  // the last two levels' assembly in one pass (with collapse, or the wide
                               // warp-per-column kernel for base cases with MN up to 16, sec. 6g)
@@ -478,8 +479,8 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
   auto choose_tiles = [&](Launch& ln, std::vector<GemmTask>& tasks) {
     ln.tma = !lazy_kernels && use_tma && gemm_tma_eligible(tasks);
     ln.bn = ln.tma ? gemm_choose_bn(tasks) : 128;
-    // the fused leaf level embeds the 16-deep core and reuses this launch's tensor maps
-    ln.bk = ln.tma && !(fuse && ln.kind == Launch::GEMM) ? gemm_choose_bk(tasks) : 16;
+    // (the fused leaf level reuses this launch's tensor maps and ring depth)
+    ln.bk = ln.tma ? gemm_choose_bk(tasks) : 16;
     ln.tiles = gemm_prepare(tasks, 128, ln.bn);
     gemm_uniform_grid(tasks, &ln.uni_tm, &ln.uni_tn);
   };
@@ -964,6 +965,10 @@ void fmm_plan_s::fuse_leaf_level(bool lazy_kernels) {
   }
   if (ig < 0 || ias < 0) return;
   if (!lazy_kernels && !launches[ig].tma) return;
+  if (fuse_bg) {  // the producer warps' input staging (256 bytes per input, fused_bg_stage_bytes) must fit
+    const int nin = std::max(std::max(alg->M * alg->K, alg->K * alg->N), R);
+    if (gemm_fused_smem_bytes(launches[ig].bn, launches[ig].bk, 256 * nin) > gemm_max_smem_bytes()) return;
+  }
   const long long np = nodes_at[L - 1];
   Launch fz = launches[ig];
   fz.kind = Launch::FUSED;
@@ -1043,7 +1048,7 @@ void fmm_plan_s::fuse_leaf_level(bool lazy_kernels) {
       if (t < best_t) best_t = t, best_k = k;
     }
     if (const char* e = getenv("FMM_FUSE_ADD_CTAS")) best_k = std::max(1, std::min(sms - 1, atoi(e)));
-    fz.gemm_ctas = sms - best_k;
+    fz.gemm_ctas = fuse_bg ? sms : sms - best_k;  // background mode: every SM runs leaf tiles
   }
   auto push = [&](const void* p, size_t n) {
     size_t off = h_tab.size();
@@ -1058,7 +1063,7 @@ void fmm_plan_s::fuse_leaf_level(bool lazy_kernels) {
   if (!lazy_kernels) {
     std::vector<LincombSpec> specs;
     for (int q = 0; q < fz.nprogs; ++q) specs.push_back(lincomb_spec(*kernel(sides[q], 2)));
-    fz.fk = fused_get(specs, fz.bn);
+    fz.fk = fused_get(specs, fz.bn, fz.bk, fuse_bg);
   }
   // replace: GEMM -> FUSED; drop the absorbed formation / assembly launches
   launches[ig] = fz;
@@ -1362,7 +1367,13 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
   p->device = device;
   FMM_CUDA(cudaSetDevice(device));
   if (const char* e = getenv("FMM_NO_TMA")) p->use_tma = !(e[0] == '1');
+  if (p->opt.fuse_leaf_level < 0 || p->opt.fuse_leaf_level > 2) throw Error(FMM_E_INVALID_ARG, "bad fuse_leaf_level");
   p->fuse = p->opt.fuse_leaf_level != 0;
+  p->fuse_bg = p->opt.fuse_leaf_level == 2;
+  if (const char* e = getenv("FMM_FUSE_BG")) {  // experiments: force the background mode on (1) or off (0)
+    p->fuse_bg = e[0] == '1';
+    p->fuse = p->fuse || p->fuse_bg;
+  }
   if (const char* e = getenv("FMM_NO_FUSE")) p->fuse = p->fuse && !(e[0] == '1');
   p->userP = P;
   p->userQ = Q;
@@ -1427,6 +1438,7 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
     // than one level per launch on c4, c5, c5t: the pass is only worth it with every input in registers)
     p->collapse = p->opt.collapse_levels && !(e && e[0] == '1') && L >= 2 && p->opt.strategy == FMM_ADD_STREAMING &&
                   M * K <= 4 && K * Nb <= 4 && M * Nb <= 4 && dl.P1 == dl.P && dl.Q1 == dl.Q && dl.N1 == dl.N;
+    if (p->collapse && p->fuse_bg && p->fuse) p->collapse = false;  // the background mode hides the level
     if (p->collapse) p->fuse = false;
     p->collapse_asm = p->collapse;
     // the assembly alone for larger base cases (MN <= 16): the wide warp-per-column kernel (sec. 6g).
@@ -1482,7 +1494,7 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
   FMM_CUDA(cudaEventCreateWithFlags(&p->upload_done, cudaEventDisableTiming));
   for (auto& e : p->ev) FMM_CUDA(cudaEventCreate(&e));
   if (p->fuse && p->L >= 1) {
-    p->ctr_bytes = sizeof(unsigned long long) * (size_t)(2 + 2 * p->nodes_at[p->L - 1]);
+    p->ctr_bytes = sizeof(unsigned long long) * (size_t)(2 + 2 * p->nodes_at[p->L - 1] + 4);  // + 4 diagnostics
     FMM_CUDA(cudaMalloc(&p->d_ctr, p->ctr_bytes));
   }
 }
@@ -1705,6 +1717,13 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
         FMM_CUDA(cudaMemsetAsync(p->d_ctr, 0, p->ctr_bytes, stream));
         fused_launch(*ln.fk, reinterpret_cast<const GemmTask*>(tab), d_tab + ln.maps_off, ln.count, ln.tiles, ln.uni_tm,
                      ln.uni_tn, fa, stream);
+        if (getenv("FMM_FUSED_STATS")) {  // diagnostics (blocking): the kernel's wait / job clock totals
+          unsigned long long v[4];
+          FMM_CUDA(cudaMemcpyAsync(v, p->d_ctr + 2 + 2 * ln.np, sizeof(v), cudaMemcpyDeviceToHost, stream));
+          FMM_CUDA(cudaStreamSynchronize(stream));
+          fprintf(stderr, "fused stats (Mcycles summed over threads/warps): ready_wait %.3f tile_wait %.3f jobs_bg %.3f jobs_consumer %.3f\n",
+                  v[0] * 1e-6, v[1] * 1e-6, v[2] * 1e-6, v[3] * 1e-6);
+        }
         break;
       }
       case Launch::GEMM:
@@ -2152,8 +2171,13 @@ fmm_status_t fmm_select(const fmm_alg* const* algs, int nalgs, int64_t P, int64_
 }
 
 fmm_status_t fmm_fused_compile_check(const fmm_alg* alg, int layout, int cse, int bn) {
+  return fmm_fused_compile_check_ex(alg, layout, cse, bn, 16, 1);
+}
+
+fmm_status_t fmm_fused_compile_check_ex(const fmm_alg* alg, int layout, int cse, int bn, int ks, int mode) {
   FMM_API_BEGIN
   if (!alg) throw Error(FMM_E_INVALID_ARG, "null algorithm");
+  if (mode != 1 && mode != 2) throw Error(FMM_E_INVALID_ARG, "mode must be 1 (addition CTAs) or 2 (background)");
   std::unique_ptr<fmm_alg> t;
   const fmm_alg* a = alg;
   if (layout == FMM_COL_MAJOR) t.reset(alg_transpose_prop1(*alg)), a = t.get();
@@ -2188,7 +2212,7 @@ fmm_status_t fmm_fused_compile_check(const fmm_alg* alg, int layout, int cse, in
     }
     specs.push_back(sp);
   }
-  fused_compile(fused_generate(specs, bn));
+  fused_compile(fused_generate(specs, bn, ks, mode == 2));
   return FMM_OK;
   FMM_API_END
 }

@@ -62,6 +62,7 @@ def _load():
         "fmm_plan_stats_ex": [vp, ctypes.POINTER(dp)],
         "fmm_plan_stats_ex2": [vp, ctypes.POINTER(dp), i32],
         "fmm_fused_compile_check": [vp, i32, i32, i32],
+        "fmm_fused_compile_check_ex": [vp, i32, i32, i32, i32, i32],
         "fmm_alg_permute": [vp, i32, ctypes.POINTER(vp)],
         "fmm_nccl_unique_id": [ctypes.c_char_p],
         "fmm_comm_create": [ctypes.c_char_p, i32, i32, i32, ctypes.POINTER(vp)],
@@ -255,7 +256,7 @@ class Plan:
     def __init__(self, alg: Algorithm, P: int, Q: int, N: int, levels: int, layout: str = "row",
                  strategy: str = "streaming", cse: bool = True, shard_rank: int = 0, shard_count: int = 1,
                  device: Optional[int] = None, workspace_limit_bytes: int = 0, peel_align: bool = True,
-                 fuse: bool = False, collapse: bool = True, comm: Optional[Comm] = None, root: int = 0,
+                 fuse=False, collapse: bool = True, comm: Optional[Comm] = None, root: int = 0,
                  shard_mode: str = "leaf", cuda_graphs: bool = True, peel_tiles: bool = False,
                  p2p: Optional["P2P"] = None, barrier=None, dist_chunks: Optional[int] = None,
                  fuse_output: Optional[bool] = None):
@@ -263,7 +264,9 @@ class Plan:
         overlapped row chunks where it applies).  p2p + barrier: a P2P object and a zero-argument host
         barrier over the same ranks (e.g. torch.distributed.barrier) -> fmm_plan_create_p2p (the
         peer-memory combine runs inside execute, which then blocks).  root: the rank that receives C,
-        or "slabs" for slab-distributed output."""
+        or "slabs" for slab-distributed output.  fuse: False / 0 separate leaf-level launches, True / 1
+        the fused leaf level with addition CTAs, 2 or "bg" the fused leaf level with the jobs in the
+        GEMM CTAs' spare warps (fuse_leaf_level, fmm.h)."""
         import torch
         self.alg, self.P, self.Q, self.N, self.levels = alg, P, Q, N, levels
         self.layout = ROW_MAJOR if layout == "row" else COL_MAJOR
@@ -279,7 +282,7 @@ class Plan:
         o.shard_rank, o.shard_count = shard_rank, shard_count
         o.workspace_limit_bytes = workspace_limit_bytes
         o.peel_align = int(bool(peel_align))
-        o.fuse_leaf_level = int(bool(fuse))
+        o.fuse_leaf_level = 2 if fuse in (2, "bg") else int(bool(fuse))
         o.collapse_levels = int(bool(collapse))
         o.shard_mode = {"leaf": 0, "top": 1}[shard_mode]
         if dist_chunks is not None:
@@ -465,9 +468,12 @@ def dgemm(A, B, C=None, alpha: float = 1.0, beta: float = 0.0, stream=None):
     return C
 
 
-def fused_compile_check(alg: "Algorithm", layout: str = "row", cse: bool = True, bn: int = 128) -> None:
-    """NVRTC-compile the fused leaf-level kernel of `alg` (host only; raises FmmError on failure)."""
-    _check(_lib.fmm_fused_compile_check(alg._h, ROW_MAJOR if layout == "row" else COL_MAJOR, int(bool(cse)), bn))
+def fused_compile_check(alg: "Algorithm", layout: str = "row", cse: bool = True, bn: int = 128, ks: int = 16,
+                        mode: int = 1) -> None:
+    """NVRTC-compile the fused leaf-level kernel of `alg` (host only; raises FmmError on failure) for
+    ring depth `ks` and fuse_leaf_level `mode` (1 addition CTAs, 2 background jobs)."""
+    _check(_lib.fmm_fused_compile_check_ex(alg._h, ROW_MAJOR if layout == "row" else COL_MAJOR, int(bool(cse)), bn, ks,
+                                           mode))
 
 
 def probe_fp64_peak():

@@ -1,5 +1,6 @@
-"""The fused leaf-level launch (fuse_leaf_level = 1): level-L formation, the leaf DMMA GEMM and the
-level-L assembly in one cooperative kernel, addition CTAs on their own SMs.
+"""The fused leaf-level launch: level-L formation, the leaf DMMA GEMM and the level-L assembly in
+one cooperative kernel -- fuse_leaf_level = 1 with addition CTAs on their own SMs, 2 with the jobs in
+the GEMM CTAs' spare producer warps (background mode).
 
 CPU: the NVRTC-generated fused kernel compiles for every algorithm, layout and tile width.
 GPU: it evaluates the same generated chains as the separate K1/K3 kernels, so fused == separate
@@ -35,6 +36,15 @@ def test_fused_kernel_compiles(name, layout, cse, bn):
     F.fmm.fused_compile_check(F.load_alg(name), layout=layout, cse=cse, bn=bn)
 
 
+@pytest.mark.parametrize("name,layout,bn,ks", [("winograd_class_222_7", "col", 128, 48), ("alg_424_26", "row", 112, 32),
+                                               ("alg_433_29", "row", 128, 16)])
+def test_fused_background_kernel_compiles(name, layout, bn, ks):
+    F = _lib()
+    F.fmm.fused_compile_check(F.load_alg(name), layout=layout, cse=True, bn=bn, ks=ks, mode=2)
+    with pytest.raises(F.FmmError):
+        F.fmm.fused_compile_check(F.load_alg(name), layout=layout, cse=True, bn=bn, ks=24, mode=2)
+
+
 # ---- GPU ----------------------------------------------------------------------------------------
 CASES = [
     ("strassen_222_7", 1, 256, 256, 256, "row"),
@@ -68,10 +78,11 @@ def _run(F, name, A, B, L, layout="row", **kw):
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,L,P,Q,N,layout", CASES)
 @pytest.mark.parametrize("cse", [False, True])
-def test_fused_equals_separate_and_oracle(name, L, P, Q, N, layout, cse):
+@pytest.mark.parametrize("mode", [1, 2])
+def test_fused_equals_separate_and_oracle(name, L, P, Q, N, layout, cse, mode):
     F = _lib()
     A, B = I.problem(P, Q, N, seed=3 + P)
-    Cf, sf = _run(F, name, A, B, L, layout, cse=cse, fuse=True)
+    Cf, sf = _run(F, name, A, B, L, layout, cse=cse, fuse=mode)
     Cs, ss = _run(F, name, A, B, L, layout, cse=cse, fuse=False)
     assert ss["fused_launches"] == 0
     if sf["fused_launches"]:
@@ -83,32 +94,46 @@ def test_fused_equals_separate_and_oracle(name, L, P, Q, N, layout, cse):
 
 
 @pytest.mark.gpu
-def test_fused_is_used_where_eligible():
+@pytest.mark.parametrize("mode", [1, 2])
+def test_fused_is_used_where_eligible(mode):
     F = _lib()
     A, B = I.problem(1024, 1024, 1024, seed=1)
-    _, st = _run(F, "winograd_class_222_7", A, B, 2, fuse=True)
+    _, st = _run(F, "winograd_class_222_7", A, B, 2, fuse=mode)
     assert st["fused_launches"] == 1 and st["fused_add_bytes"] > 0
 
 
 @pytest.mark.gpu
+def test_fused_background_wins_over_collapse():
+    # fuse_leaf_level = 2 takes precedence over collapse_levels (mode 1 yields to it)
+    F = _lib()
+    A, B = I.problem(1024, 1024, 1024, seed=1)
+    _, s1 = _run(F, "winograd_class_222_7", A, B, 2, fuse=1, collapse=True)
+    _, s2 = _run(F, "winograd_class_222_7", A, B, 2, fuse=2, collapse=True)
+    assert s1["fused_launches"] == 0 and s1["collapsed"] == 1
+    assert s2["fused_launches"] == 1 and s2["collapsed"] == 0
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("name", NAMES)
-def test_fused_integer_bit_exact(name):
+@pytest.mark.parametrize("mode", [1, 2])
+def test_fused_integer_bit_exact(name, mode):
     F = _lib()
     a = O.load_alg(F.alg_path(name))
     P, Q, N = 3 * a.M ** 2 + 1, 2 * a.K ** 2 + 1, 2 * a.N ** 2 + 2
     A, B = I.problem(P, Q, N, seed=2, kind="integers")
-    C, _ = _run(F, name, A, B, 2, fuse=True)
+    C, _ = _run(F, name, A, B, 2, fuse=mode)
     assert np.array_equal(C, A @ B)
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("G", [2, 3])
-def test_fused_shards_sum_to_product(G):
+@pytest.mark.parametrize("mode", [1, 2])
+def test_fused_shards_sum_to_product(G, mode):
     F = _lib()
     A, B = I.problem(300, 200, 250, seed=8, kind="integers")
     total = np.zeros((300, 250))
     for g in range(G):
-        C, _ = _run(F, "winograd_class_222_7", A, B, 2, fuse=True, shard_rank=g, shard_count=G)
+        C, _ = _run(F, "winograd_class_222_7", A, B, 2, fuse=mode, shard_rank=g, shard_count=G)
         total += C
     assert np.array_equal(total, A @ B)
 
