@@ -360,12 +360,13 @@ class Run:
         self.ms_step = self.max_over_ranks(t0.elapsed_time(t1)) / args.steps
         self.value = self.flops / (self.ms_step * 1e-3) / 1e9
 
-    def phase_split(self, reps=3):
+    def phase_split(self, reps=5):
         # per-phase device times from a separate pass (fmm_execute_timed: plain launches with an
-        # event after each; formation / leaf products / assembly / peel strips / exposed combine)
+        # event after each; formation / leaf products / assembly / peel strips / exposed combine),
+        # median of `reps` passes after an untimed one
         import numpy as np
         ph = []
-        for _ in range(reps):
+        for it in range(reps + 1):
             if self.world > 1 and self.args.combine == "torch":
                 _, t = self.plan.execute_timed(self.A, self.B, self.C, stream=self.stream)
                 e0 = self.torch.cuda.Event(enable_timing=True)
@@ -377,8 +378,9 @@ class Run:
                 t["total_ms"] += e0.elapsed_time(e1)
             else:
                 _, t = self.plan.execute_timed(self.A, self.B, self.C, stream=self.stream)
-            ph.append([t["formation_ms"], t["gemm_ms"], t["assembly_ms"], t["strips_ms"], t["total_ms"]])
-        m = np.array(ph).mean(axis=0)
+            if it:
+                ph.append([t["formation_ms"], t["gemm_ms"], t["assembly_ms"], t["strips_ms"], t["total_ms"]])
+        m = np.median(np.array(ph), axis=0)
         self.form_ms, self.gemm_ms, self.asm_ms, self.strip_ms, tot = [float(x) for x in m]
         self.comm_ms = max(0.0, tot - self.form_ms - self.gemm_ms - self.asm_ms - self.strip_ms) if self.world > 1 else 0.0
 
@@ -842,8 +844,9 @@ class Run:
         e1.record(stream)
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / steps
+        plan.execute_timed(A, B, C, stream=stream)  # untimed: the first per-launch-event pass
         ph = np.median(np.array([[t["formation_ms"], t["gemm_ms"], t["assembly_ms"], t["strips_ms"], t["total_ms"]]
-                                 for t in (plan.execute_timed(A, B, C, stream=stream)[1] for _ in range(3))]), axis=0)
+                                 for t in (plan.execute_timed(A, B, C, stream=stream)[1] for _ in range(5))]), axis=0)
         form_ms, gemm_ms, asm_ms, strip_ms, tot_ms = (float(x) for x in ph)
         # sampled rows (columns) of C against cuBLAS on the same rows, then cuBLAS on the whole problem
         g = torch.Generator().manual_seed(7)
