@@ -981,7 +981,7 @@ class Run:
                               "assembly": self.asm_ms, "peel_strips": self.strip_ms,
                               "combine_exposed": self.comm_ms if world > 1 else 0.0,
                               "how": "fmm_execute_timed after the timed steps: plain launches, an event after each, "
-                                     "mean of 3"},
+                                     "median of 5 after an untimed pass"},
                 "input_broadcast": bcast,
                 "combine_algbw_gbs": (8.0 * P * N / (self.comm_ms * 1e-3) / 1e9) if world > 1 and self.comm_ms else None,
                 "additions": {"algorithmic_bytes_per_step": st["add_bytes"],
