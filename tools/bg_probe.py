@@ -1,3 +1,11 @@
+"""Background-bandwidth probe (development tool, timing only): with the library built with
+-DFMM_BG_PROBE (FMM_BUILD_VARIANT=bg FMM_EXTRA_FLAGS=-DFMM_BG_PROBE python paper_1409_2908_b200/build.py,
+then FMM_LIB_PATH=.../libfmm_bg.so), the plain leaf GEMM's idle producer warps 1-3 stream-copy
+FMM_BG_BYTES bytes (read + write) of a separate buffer during each leaf GEMM launch; this prints the
+median leaf-GEMM time per volume (profiles/r2_bg_probe.jsonl).
+
+  BG_CFGS=c2,c4 BG_LIST=0,8,16,32,64 python tools/bg_probe.py
+"""
 import json, os, sys
 import torch
 sys.path.insert(0, "/root/repo")
