@@ -63,15 +63,15 @@ def _max_err_on_gpu(C, ref_np, layout):
 
 # Full element-wise parity at BASELINE's full sizes: every entry of C against oracle_fast of the
 # same algorithm and L, for the default plan the bench times and for the other
-# schedules whose numbers DESIGN/README quote: the fused leaf level, and c2's shape-matched
+# schedules whose numbers DESIGN/README quote: the fused leaf level (both modes), and c2's shape-matched
 # Winograd-class L = 3 (collapsed levels 2-3).  c5 (18000^3, ~140 s of oracle time on 16 cores)
 # stays sampled (above and below).
 @pytest.mark.parametrize("cfg,L,variants", [
-    ("c2", None, [dict(), dict(fuse=True, collapse=False)]),
+    ("c2", None, [dict(), dict(fuse=True, collapse=False), dict(fuse=2)]),
     ("c2", 3, [dict()]),
-    ("c3", None, [dict(), dict(fuse=True)]),
-    ("c4", None, [dict(), dict(fuse=True)]),
-    ("c5t", None, [dict(), dict(fuse=True)])])
+    ("c3", None, [dict(), dict(fuse=True), dict(fuse=2)]),
+    ("c4", None, [dict(), dict(fuse=True), dict(fuse=2)]),
+    ("c5t", None, [dict(), dict(fuse=True), dict(fuse=2)])])
 def test_fullsize_elementwise_parity(cfg, L, variants):
     import paper_1409_2908_b200 as F
     w = bench.WORKLOADS[cfg]
