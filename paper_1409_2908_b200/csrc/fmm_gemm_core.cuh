@@ -70,6 +70,21 @@ constexpr int A_BYTES = BM * BK * 8;                           // 16 KB per 16 c
 __host__ __device__ constexpr int gemm_smem_bytes(int bn, int ks = BK) {
   return ring_stages(ks) * (BM * ks * 8 + ks * bn * 8) + 1024 /*align*/ + 256 /*barriers*/;
 }
+// Staged epilogue (EPI = 1): four staging slots, one per SM sub-partition, each shared by the two
+// consumer warps of that sub-partition in turn; a slot holds one warp tile (row stride padded by
+// 16 bytes: conflict-free 16-byte fragment stores).  The ring keeps as many stages as fit beside it.
+constexpr int SMEM_OPTIN = 232448;
+__host__ __device__ constexpr int epi_stride(int bn, int wgn) { return (bn / wgn) * 8 + 16; }
+__host__ __device__ constexpr int epi_slot_bytes(int bn, int wgm, int wgn) { return (BM / wgm) * epi_stride(bn, wgn); }
+__host__ __device__ constexpr int epi_ring_stages(int ks, int bn, int wgm, int wgn, int slots = 4) {
+  return (SMEM_OPTIN - 1024 - 256 - slots * epi_slot_bytes(bn, wgm, wgn)) / (BM * ks * 8 + ks * bn * 8) < ring_stages(ks)
+             ? (SMEM_OPTIN - 1024 - 256 - slots * epi_slot_bytes(bn, wgm, wgn)) / (BM * ks * 8 + ks * bn * 8)
+             : ring_stages(ks);
+}
+__host__ __device__ constexpr int gemm_epi_smem_bytes(int bn, int ks, int wgm, int wgn, int slots = 4) {
+  return epi_ring_stages(ks, bn, wgm, wgn, slots) * (BM * ks * 8 + ks * bn * 8) + 1024 + 256 +
+         slots * epi_slot_bytes(bn, wgm, wgn);
+}
 // bg_stage: per producer warp, the background jobs' input staging (3 warps)
 __host__ __device__ constexpr int fused_smem_bytes(int bn, int ks = BK, int bg_stage = 0) {
   return gemm_smem_bytes(bn, ks) + FUSED_PTR_BYTES + 3 * bg_stage;
@@ -139,6 +154,14 @@ __device__ __forceinline__ void tma_reduce_add_2d(const void* map, int c0, int c
           reinterpret_cast<unsigned long long>(map)),
       "r"(c0), "r"(c1), "r"(src)
       : "memory");
+}
+// staged epilogue: one row of a warp tile, shared memory -> global, by the bulk-copy engine
+__device__ __forceinline__ void bulk_store(double* dst, unsigned src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
@@ -296,14 +319,16 @@ __device__ const double* fmm_bg_src;
 __device__ double* fmm_bg_dst;
 __device__ long long fmm_bg_n;
 #endif
-template <int BN, int WGM, int WGN, bool FUSED, bool K3F = false, int KS = BK>
+template <int BN, int WGM, int WGN, bool FUSED, bool K3F = false, int KS = BK, int EPI = 0>
 __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, const CUtensorMap* __restrict__ maps,
                                           int ntasks, int total_tiles, Uniform uni, const FusedArgs& fa,
                                           const K3fArgs* ka = nullptr) {
   static_assert(!(FUSED && K3F), "one epilogue mode");
   static_assert(KS == 16 || KS == 32 || KS == 48, "16-, 32- or 48-deep stages (whole 16-column A boxes)");
   static_assert(KS == BK || !K3F, "the K3f kernel uses BK-deep stages");
-  constexpr int STAGES = K3F ? K3F_STAGES : ring_stages(KS);
+  static_assert(!EPI || (!FUSED && !K3F), "the staged epilogue is the plain kernel's");
+  constexpr int STAGES = K3F ? K3F_STAGES : EPI ? epi_ring_stages(KS, BN, WGM, WGN, EPI == 2 ? 8 : 4) : ring_stages(KS);
+  static_assert(STAGES >= 2, "at least two ring stages");
   constexpr int A_BYTES = BM * KS * 8;
   static_assert(WGM * WGN == CONSUMERS, "8 consumer warps");
   constexpr int WTM = BM / WGM, WTN = BN / WGN;
@@ -613,8 +638,67 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
       }
       continue;
     }
-    // ---- epilogue: C = alpha * acc (+ beta * C), from registers ----
     const int cofs = (c == 0) ? 0 : (c == 1) ? 8 : (c == 2) ? 2 : 10;  // map0[2c]
+    if constexpr (EPI) {
+      // ---- staged epilogue: the warp writes alpha * acc into its sub-partition's staging slot and
+      // its lanes hand the rows to the bulk-copy engine (cp.async.bulk shared -> global), so the
+      // warp returns to the DMMAs of its next tile while the engine writes C.  The two warps of a
+      // sub-partition (cw, cw + 4) take the slot in turn: named barrier 2 + q "slot staged and
+      // read by the engine" (first -> second), 6 + q "second's copies have read it" (second ->
+      // first, from the second tile on).  Tiles with beta != 0 keep the register epilogue below.
+      // EPI = 2: one slot per warp (no hand-over; the warp only waits for its own previous copies)
+      constexpr int STRIDE = epi_stride(BN, WGN);
+      const int q = cw & 3;
+      const bool second = EPI == 1 && cw >= CONSUMERS / 2;
+      const unsigned slot = bars + 256u + (unsigned)(EPI == 2 ? cw : q) * (unsigned)epi_slot_bytes(BN, WGM, WGN);
+      if (EPI == 2) {
+        bulk_wait_read_all();
+        __syncwarp();
+      } else if (!second) {
+        if (tile != (int)blockIdx.x) named_bar_sync(6 + q, 64);
+      } else {
+        if (tile != (int)blockIdx.x) {
+          bulk_wait_read_all();
+          __syncwarp();
+          named_bar_arrive(6 + q, 64);
+        }
+        named_bar_sync(2 + q, 64);
+      }
+      const bool staged = beta == 0.0;
+      if (staged) {
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          const int lr = 16 * (i >> 1) + 2 * r + (i & 1);
+#pragma unroll
+          for (int jj = 0; jj < NI; ++jj) {
+            const int lc = 16 * (jj >> 1) + 4 * (jj & 1) + cofs;
+            sts_f64x2(slot + (unsigned)(lr * STRIDE + lc * 8), alpha * acc[i][jj][0], alpha * acc[i][jj][1]);
+          }
+        }
+        fence_proxy_async_shared();
+        __syncwarp();
+        const int gcol = tc.n0 + wn;
+        const int nc = min(WTN, n - gcol);
+        if (nc > 0) {
+          for (int lr = lane; lr < WTM; lr += 32) {
+            const int grow = tc.m0 + wm + lr;
+            if (grow >= m) break;
+            double* dst = C + (long long)grow * ldc + gcol;
+            const unsigned src = slot + (unsigned)(lr * STRIDE);
+            if (nc >= 2) bulk_store(dst, src, (unsigned)(nc & ~1) * 8u);
+            if (nc & 1) dst[nc - 1] = lds64(src + (unsigned)(nc - 1) * 8u);
+          }
+        }
+        bulk_commit();
+      }
+      if (EPI == 1 && !second) {
+        if (staged) bulk_wait_read_all();
+        __syncwarp();
+        named_bar_arrive(2 + q, 64);
+      }
+      if (staged) continue;
+    }
+    // ---- epilogue: C = alpha * acc (+ beta * C), from registers ----
 #pragma unroll
     for (int i = 0; i < MI; ++i) {
       const int row = tc.m0 + wm + 16 * (i >> 1) + 2 * r + (i & 1);
@@ -656,6 +740,7 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
   if constexpr (K3F) {
     if (cw == 0 && lane == 0) bulk_wait_all();  // the last reduces complete before the CTA's smem goes
   }
+  if constexpr (EPI) bulk_wait_all();  // the last tile's row copies, before the CTA's smem goes
 }
 
 }  // namespace fmm

@@ -18,11 +18,11 @@ namespace fmm {
 
 namespace {
 
-template <int BN, int WGM, int WGN, int KS>
+template <int BN, int WGM, int WGN, int KS, int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
     grouped_dgemm_tma(const GemmTask* __restrict__ tasks, const CUtensorMap* __restrict__ maps, int ntasks,
                       int total_tiles, Uniform uni) {
-  gemm_body<BN, WGM, WGN, false, false, KS>(tasks, maps, ntasks, total_tiles, uni, FusedArgs{});
+  gemm_body<BN, WGM, WGN, false, false, KS, EPI>(tasks, maps, ntasks, total_tiles, uni, FusedArgs{});
 }
 
 // K3f: the leaf GEMM whose epilogue reduce-adds every tile into its W targets (tile 128 x 64)
@@ -129,23 +129,27 @@ int gemm_choose_bk(const std::vector<GemmTask>& tasks) {
   return f > 0 && fl >= 0.5 * f ? 48 : 16;
 }
 
-template <int BN, int WGM, int WGN, int KS>
+template <int BN, int WGM, int WGN, int KS, int EPI>
 static void launch_cfg(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int sms,
                        Uniform uni, cudaStream_t stream) {
-  static std::atomic<unsigned long long> configured{0};  // bit d: attribute set on device d
-  int dev_ = 0;
-  FMM_CUDA(cudaGetDevice(&dev_));
-  const unsigned long long bit = 1ull << (dev_ & 63);
-  auto kern = grouped_dgemm_tma<BN, WGM, WGN, KS>;
-  const size_t smem = (size_t)gemm_smem_bytes(BN, KS);
-  if (!(configured.load() & bit)) {
-    FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured.fetch_or(bit);
+  if constexpr (EPI && epi_ring_stages(KS, BN, WGM, WGN, EPI == 2 ? 8 : 4) < 2) {
+    throw Error(FMM_E_INVALID_ARG, "staged epilogue: the ring does not fit beside the staging slots");
+  } else {
+    static std::atomic<unsigned long long> configured{0};  // bit d: attribute set on device d
+    int dev_ = 0;
+    FMM_CUDA(cudaGetDevice(&dev_));
+    const unsigned long long bit = 1ull << (dev_ & 63);
+    auto kern = grouped_dgemm_tma<BN, WGM, WGN, KS, EPI>;
+    const size_t smem = (size_t)(EPI ? gemm_epi_smem_bytes(BN, KS, WGM, WGN, EPI == 2 ? 8 : 4) : gemm_smem_bytes(BN, KS));
+    if (!(configured.load() & bit)) {
+      FMM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      configured.fetch_or(bit);
+    }
+    const int grid = (int)std::min<long long>(total_tiles, sms);
+    kern<<<grid, THREADS, smem, stream>>>(d_tasks, reinterpret_cast<const CUtensorMap*>(d_maps), ntasks,
+                                          (int)total_tiles, uni);
+    FMM_CUDA(cudaGetLastError());
   }
-  const int grid = (int)std::min<long long>(total_tiles, sms);
-  kern<<<grid, THREADS, smem, stream>>>(d_tasks, reinterpret_cast<const CUtensorMap*>(d_maps), ntasks, (int)total_tiles,
-                                        uni);
-  FMM_CUDA(cudaGetLastError());
 }
 
 int gemm_choose_bn(const std::vector<GemmTask>& tasks) {
@@ -217,21 +221,50 @@ int gemm_max_smem_bytes() {
   return v;
 }
 
-template <int KS>
+template <int KS, int EPI>
 static void launch_ks(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn, int sms,
                       Uniform uni, cudaStream_t stream) {
   switch (bn) {
-    case 128: launch_cfg<128, 2, 4, KS>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
-    case 112: launch_cfg<112, 8, 1, KS>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
-    case 96: launch_cfg<96, 4, 2, KS>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
-    case 80: launch_cfg<80, 8, 1, KS>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
-    case 64: launch_cfg<64, 4, 2, KS>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
+    case 128: launch_cfg<128, 2, 4, KS, EPI>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
+    case 112: launch_cfg<112, 8, 1, KS, EPI>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
+    case 96: launch_cfg<96, 4, 2, KS, EPI>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
+    case 80: launch_cfg<80, 8, 1, KS, EPI>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
+    case 64: launch_cfg<64, 4, 2, KS, EPI>(d_tasks, d_maps, ntasks, total_tiles, sms, uni, stream); break;
     default: throw Error(FMM_E_INVALID_ARG, "unsupported GEMM tile width " + std::to_string(bn));
   }
 }
 
+// Staged epilogue (gemm_body EPI = 1): whether a launch uses it, and the ring depth that leaves
+// room for its staging slots (48-deep stages where two of them still fit, else 32, else 16).
+// FMM_GEMM_EPI = 0 / 1 overrides the choice.
+// a launch whose ring does not fit beside eight slots falls back to the four shared ones
+static int gemm_choose_epi_fallback(int bn, int* bk);
+static constexpr bool epi_fits(int bn, int ks, int slots) {
+  return bn == 128 ? epi_ring_stages(ks, 128, 2, 4, slots) >= 2
+         : bn == 112 ? epi_ring_stages(ks, 112, 8, 1, slots) >= 2
+         : bn == 96  ? epi_ring_stages(ks, 96, 4, 2, slots) >= 2
+         : bn == 80  ? epi_ring_stages(ks, 80, 8, 1, slots) >= 2
+                     : epi_ring_stages(ks, 64, 4, 2, slots) >= 2;
+}
+int gemm_choose_epi(const std::vector<GemmTask>& tasks, int bn, int* bk) {
+  int epi = 0;
+  if (const char* e = getenv("FMM_GEMM_EPI")) epi = atoi(e);
+  (void)tasks;
+  if (epi != 1 && epi != 2) return 0;
+  const int slots = epi == 2 ? 8 : 4;
+  while (*bk > 16 && !epi_fits(bn, *bk, slots)) *bk = *bk == 48 ? 32 : 16;
+  if (epi_fits(bn, *bk, slots)) return epi;
+  if (epi == 2) return gemm_choose_epi_fallback(bn, bk);
+  return 0;
+}
+
+static int gemm_choose_epi_fallback(int bn, int* bk) {
+  while (*bk > 16 && !epi_fits(bn, *bk, 4)) *bk = *bk == 48 ? 32 : 16;
+  return epi_fits(bn, *bk, 4) ? 1 : 0;
+}
+
 void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn, int bk,
-                     int uniform_tm, int uniform_tn, cudaStream_t stream) {
+                     int uniform_tm, int uniform_tn, cudaStream_t stream, int epi) {
   const Uniform uni{uniform_tm * uniform_tn, uniform_tm, uniform_tn};
   if (total_tiles <= 0 || ntasks <= 0) return;
 #ifdef FMM_BG_PROBE
@@ -255,9 +288,23 @@ void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, lo
   }
 #endif
   const int sms = sm_count();
-  if (bk == 48) launch_ks<48>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
-  else if (bk == 32) launch_ks<32>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
-  else if (bk == 16) launch_ks<16>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
+  if (epi == 1) {
+    if (bk == 48) launch_ks<48, 1>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
+    else if (bk == 32) launch_ks<32, 1>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
+    else if (bk == 16) launch_ks<16, 1>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
+    else throw Error(FMM_E_INVALID_ARG, "unsupported GEMM k-step " + std::to_string(bk));
+    return;
+  }
+  if (epi == 2) {
+    if (bk == 48) launch_ks<48, 2>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
+    else if (bk == 32) launch_ks<32, 2>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
+    else if (bk == 16) launch_ks<16, 2>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
+    else throw Error(FMM_E_INVALID_ARG, "unsupported GEMM k-step " + std::to_string(bk));
+    return;
+  }
+  if (bk == 48) launch_ks<48, 0>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
+  else if (bk == 32) launch_ks<32, 0>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
+  else if (bk == 16) launch_ks<16, 0>(d_tasks, d_maps, ntasks, total_tiles, bn, sms, uni, stream);
   else throw Error(FMM_E_INVALID_ARG, "unsupported GEMM k-step " + std::to_string(bk));
 }
 

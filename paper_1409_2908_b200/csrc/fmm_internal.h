@@ -105,11 +105,14 @@ int gemm_tile_n();
 bool gemm_tma_eligible(const std::vector<GemmTask>& tasks);
 size_t gemm_tma_map_bytes();  // bytes of one tensor map (two per task: A then B)
 void gemm_tma_maps(const std::vector<GemmTask>& tasks, void* out, int ks);  // ks: the launch's k-step (B box rows)
-int gemm_choose_bk(const std::vector<GemmTask>& tasks);                      // 16 or 32
+int gemm_choose_bk(const std::vector<GemmTask>& tasks);                      // 16, 32 or 48
+// staged epilogue (bulk-copy stores) for a launch of tile width bn: 1 / 0; may lower *bk so the
+// ring fits beside the staging slots
+int gemm_choose_epi(const std::vector<GemmTask>& tasks, int bn, int* bk);
 constexpr int BK_K3F = 16;  // the K3f leaf GEMM's k-step (its maps and smem; fmm_gemm_core.cuh BK)
 // uniform_tm/tn: the common tile grid when every task has the same one (else 0, 0).
 void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn, int bk,
-                     int uniform_tm, int uniform_tn, cudaStream_t stream);
+                     int uniform_tm, int uniform_tn, cudaStream_t stream, int epi = 0);
 // K3f leaf GEMM (128 x K3F_BN tiles; epilogue reduce-adds into the W targets through TMA): the
 // tensor map of one parent output block (box 16 columns x 128 rows, 128B swizzle) and the launch.
 void gemm_k3f_target_map(void* out, const double* ptr, long long rows, long long cols, long long ld);

@@ -58,7 +58,8 @@ struct Launch {
   bool aligned16 = true;
   bool tma = false;          // GEMM launches: TMA warp-specialised kernel
   int bn = 128;              // GEMM launches: CTA tile width
-  int bk = 16;               // GEMM launches: k-depth of a TMA ring stage (16 or 32)
+  int bk = 16;               // GEMM launches: k-depth of a TMA ring stage (16, 32 or 48)
+  int epi = 0;               // GEMM launches: staged epilogue (bulk-copy stores of C)
   int uni_tm = 0, uni_tn = 0;  // GEMM launches: common tile grid of all tasks (0 = mixed)
   size_t ids_off = 0;        // SKINNY: int ids (row tasks then column tasks)
   int nrow = 0, ncol = 0, max_n = 0, max_m = 0;
@@ -481,6 +482,7 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
     ln.bn = ln.tma ? gemm_choose_bn(tasks) : 128;
     // (the fused leaf level reuses this launch's tensor maps and ring depth)
     ln.bk = ln.tma ? gemm_choose_bk(tasks) : 16;
+    ln.epi = ln.tma ? gemm_choose_epi(tasks, ln.bn, &ln.bk) : 0;
     ln.tiles = gemm_prepare(tasks, 128, ln.bn);
     gemm_uniform_grid(tasks, &ln.uni_tm, &ln.uni_tn);
   };
@@ -1737,7 +1739,7 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
                           ln.uni_tn, ka, ls);
         } else if (ln.tma)
           gemm_tma_launch(reinterpret_cast<const GemmTask*>(tab), d_tab + ln.maps_off, ln.count, ln.tiles, ln.bn,
-                          ln.bk, ln.uni_tm, ln.uni_tn, ls);
+                          ln.bk, ln.uni_tm, ln.uni_tn, ls, ln.epi);
         else
           gemm_launch(reinterpret_cast<const GemmTask*>(tab), ln.count, ln.tiles, ln.aligned16, ls);
         break;
@@ -2438,7 +2440,8 @@ fmm_status_t fmm_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const doub
   // the task descriptor (and its tensor maps) go through a stream-ordered upload
   const bool tma = gemm_tma_eligible(t) && !(getenv("FMM_NO_TMA") && getenv("FMM_NO_TMA")[0] == '1');
   const int bn = tma ? gemm_choose_bn(t) : 128;
-  const int bk = tma ? gemm_choose_bk(t) : 16;
+  int bk = tma ? gemm_choose_bk(t) : 16;
+  const int epi = tma ? gemm_choose_epi(t, bn, &bk) : 0;
   const long long tiles = gemm_prepare(t, 128, bn);
   alignas(128) char buf[1024];
   std::memcpy(buf, t.data(), sizeof(GemmTask));
@@ -2448,7 +2451,7 @@ fmm_status_t fmm_dgemm(int64_t m, int64_t n, int64_t k, double alpha, const doub
   FMM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_task), sizeof(buf), s));
   FMM_CUDA(cudaMemcpyAsync(d_task, buf, sizeof(buf), cudaMemcpyHostToDevice, s));
   if (tma)
-    gemm_tma_launch(d_task, reinterpret_cast<char*>(d_task) + 512, 1, tiles, bn, bk, t[0].tiles_m, t[0].tiles_n, s);
+    gemm_tma_launch(d_task, reinterpret_cast<char*>(d_task) + 512, 1, tiles, bn, bk, t[0].tiles_m, t[0].tiles_n, s, epi);
   else
     gemm_launch(d_task, 1, tiles, gemm_tasks_aligned16(t), s);
   FMM_CUDA(cudaFreeAsync(d_task, s));
