@@ -141,11 +141,21 @@ typedef struct {
                                on integer inputs).  Applies when W has only 0 / +-1 entries and
                                MN <= 16, one shard, no fused leaf level; it replaces the collapsed
                                last two levels.  0 (default): separate assembly kernels. */
+  int small_fused;          /* 1 (default): a one-level streaming plan (after the cutoff, levels = 1)
+                               with no peeling at the top level, one shard, base case MK, KN, MN <= 64 and
+                               R <= 128, whose leaf products would give the leaf GEMM fewer 128-row
+                               tiles than the GPU has SMs, runs the whole step as ONE launch: a
+                               CTA per (32 x 32 leaf tile, product r) forms its S_r rows and T_r
+                               columns from A and B in shared memory, multiplies them on the FP64
+                               tensor pipe, and the last CTA of each tile forms C_k = sum_r w_kr M_r
+                               in ascending r.  Below the paper's cutoff
+                               (Sec. 3.4) the separate launches cost more than the
+                               arithmetic.  0: the separate launches. */
 } fmm_plan_options;
 
 /* Fill *opt with the defaults: row-major, streaming, cse = 1, shard 0 of 1, no limit,
    peel_align = 1, fuse_leaf_level = 0, collapse_levels = 1, cuda_graphs = 1, peel_tiles = 0,
-   dist_chunks = 4, fuse_output = 0. */
+   dist_chunks = 4, fuse_output = 0, small_fused = 1. */
 void fmm_plan_options_default(fmm_plan_options* opt);
 
 /* ---- algorithms ------------------------------------------------------------------------- */
@@ -294,11 +304,12 @@ fmm_status_t fmm_plan_stats(const fmm_plan_t* plan, double out[8]);
    [15] 1 if the last split's rows were peeled to 128-row-aligned leaves (peel_tiles, R7c) */
 fmm_status_t fmm_plan_stats_ex(const fmm_plan_t* plan, double out[16]);
 
-/* The same, extensible: fills out[0 .. min(n, 18) - 1]; out[0..15] as fmm_plan_stats_ex, then
+/* The same, extensible: fills out[0 .. min(n, 19) - 1]; out[0..15] as fmm_plan_stats_ex, then
    [16] 1 if the output step is fused into the leaf GEMM (fuse_output applied), else 0;
    [17] 1 if the last two levels' assembly runs as one pass (collapse_levels: with the formation for
         the <2,2,2> family, or alone -- the wide warp-per-column kernel, FMM_WIDE_ASM=1 -- for base
-        cases with MN <= 16), else 0. */
+        cases with MN <= 16), else 0;
+   [18] 1 if the plan runs the whole step as one launch (small_fused applied), else 0. */
 fmm_status_t fmm_plan_stats_ex2(const fmm_plan_t* plan, double* out, int n);
 
 /* Cost model (host only, no allocation): predicted milliseconds of a plan of `alg` for the problem

@@ -118,6 +118,44 @@ void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, lo
 void gemm_k3f_target_map(void* out, const double* ptr, long long rows, long long cols, long long ld);
 void gemm_k3f_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int uniform_tm,
                      int uniform_tn, const K3fArgs& ka, cudaStream_t stream);
+// One-launch path for small one-level plans (fmm_small.cu, option small_fused): a term of an
+// operand / output combination -- block index in the base case's grid (A: M x K, B: K x N) or the
+// product index r (W), and its coefficient; per r (per output block k) the terms [off[r], off[r+1]).
+struct SmallTerm {
+  long long off;  // A / B terms: element offset of the block in the operand (rebuilt per execute's lds)
+  double coef;
+  int blk;
+  int pad_;
+};
+struct SmallArgs {
+  const double* A;
+  const double* B;
+  double* C;
+  long long lda, ldb, ldc;
+  int pm, pk, pn;  // leaf dimensions (P / M, Q / K, N / N_base: the plan requires exact division)
+  int M, K, N, R;  // base case
+  int tiles_m, tiles_n;
+  const int* u_off;
+  const SmallTerm* u_terms;
+  const int* v_off;
+  const SmallTerm* v_terms;
+  const int* w_off;
+  const SmallTerm* w_terms;
+  double* Mbuf;    // R x tiles x 32 x 32 doubles
+  unsigned* cnt;   // per tile position, zero between launches
+  int kc, g;       // k-chunk depth (a power of two) and assembly group (small_config)
+  int kc_log2;
+  int stage_max;   // doubles of one raw chunk buffer (the largest term counts)
+  int nw;          // W terms (<= 256)
+  int vec2;        // 1: every A / B view is 16-byte aligned (16-byte copies)
+  int cluster;     // 1: the R CTAs of a tile are a cluster (C_k from the peers' shared memory)
+  int smem;        // dynamic shared memory bytes of the launch
+};
+int small_tile();  // the tile edge (32)
+// chunk depth / assembly group for the largest per-product term counts; false: does not fit
+bool small_config(int max_nu, int max_nv, int pk, int R, int* kc, int* g);
+void small_launch(const SmallArgs& a, cudaStream_t stream);
+bool small_cluster_ok(int R, int smem);  // the cluster variant fits (R <= 16, co-resident)
 // TMA kernel configuration: consumer warp grid of a tile width, SM count, dynamic shared memory.
 void gemm_bn_config(int bn, int* wgm, int* wgn);
 int gemm_sm_count();

@@ -48,7 +48,8 @@ using PlanDims = Dims;
 
 struct Launch {
   enum Kind { FORM_A, FORM_B, GEMM, ASSEMBLE, STRIPS, SKINNY, FUSED, REDUCE /* no kernel: reduce_rows only */,
-              ZERO /* K3f: zero the level-(L-1) output blocks (cudaMemset2DAsync per block) */ } kind;
+              ZERO /* K3f: zero the level-(L-1) output blocks (cudaMemset2DAsync per block) */,
+              SMALL /* small_fused: the whole one-level step as one launch (fmm_small.cu) */ } kind;
   int level = 0;
   size_t table_off = 0;  // byte offset in the device table buffer
   int count = 0;         // nodes / tasks
@@ -69,6 +70,8 @@ struct Launch {
   std::vector<int> node_ids;  // FORM / ASSEMBLE: parent node index of every table entry
   int nin = 0, nout = 0;      // ASSEMBLE: inputs / outputs per table entry
   bool k3f = false;           // GEMM: the K3f leaf GEMM (epilogue reduce-adds into the W targets)
+  SmallArgs small{};          // SMALL: the launch's arguments (device table pointers filled at run time)
+  size_t small_off[6] = {};   // SMALL: byte offsets of u_off, u_terms, v_off, v_terms, w_off, w_terms
   size_t k3f_maps_off = 0, k3f_count_off = 0, k3f_targets_off = 0;  // GEMM k3f: its device tables
   std::vector<std::array<long long, 4>> zero_blocks;  // ZERO: (host pointer bits, ld, rows, cols)
   // NCCL distributed plans with dist_chunks: rows [first, second) of C (plan orientation) to reduce
@@ -136,6 +139,9 @@ struct fmm_plan_s {
                               // warp-per-column kernel for base cases with MN up to 16, sec. 6g)
   bool k3f = false;       // fuse_output: the level-L output step in the leaf GEMM's epilogue (K3f)
   bool tiled_peel = false;  // R7c: the last split's rows were peeled to 128-row-aligned leaves
+  bool small = false;       // small_fused: one launch for the whole one-level step (sec. 6h)
+  double* small_M = nullptr;     // its leaf-product tiles (R x tiles x 32 x 32)
+  unsigned* small_cnt = nullptr;  // its per-tile completion counters
   unsigned long long* d_ctr = nullptr;  // fused launch counters: claim0, claim1, ready[np], tiles[np]
   size_t ctr_bytes = 0;
   // kernels (vec 2 / vec 1 variants created lazily)
@@ -186,6 +192,8 @@ struct fmm_plan_s {
     if (ws) cudaFree(ws);
     if (scratch) cudaFree(scratch);
     if (d_ctr) cudaFree(d_ctr);
+    if (small_M) cudaFree(small_M);
+    if (small_cnt) cudaFree(small_cnt);
     for (auto& sl : slot) {
       if (sl.d_tab) cudaFree(sl.d_tab);
       if (sl.gexec) cudaGraphExecDestroy(sl.gexec);
@@ -417,6 +425,8 @@ struct fmm_plan_s {
   // K3f: zero the level-(L-1) outputs, then the leaf GEMM whose epilogue reduce-adds every tile
   // into its W targets (replaces the level-L assembly)
   void emit_k3f(std::vector<GemmTask>& tasks, bool lazy_kernels);
+  // small_fused: the one launch of a small one-level plan and its term tables
+  void emit_small();
 };
 
 View fmm_plan_s::opA(int l, long long z, const View& root) const {
@@ -461,6 +471,77 @@ View fmm_plan_s::opB(int l, long long z, const View& root) const {
               par.sigma * coefV[r]};
 }
 
+static bool al16(const void* p);
+// small_fused (sec. 6h): one SMALL launch; its term tables list, per product r, the nonzero
+// u_ir (v_jr) with their block index in A's M x K (B's K x N) grid, and per output block k the
+// nonzero w_kr in ascending r -- the orders of the separate kernels' chains without CSE
+void fmm_plan_s::emit_small() {
+  const fmm_alg* a = alg;
+  const int M = a->M, K = a->K, Nb = a->N;
+  auto terms = [&](const std::vector<double>& X, int rows, bool by_r, std::vector<int>& off, std::vector<SmallTerm>& t) {
+    const int outer = by_r ? R : rows, inner = by_r ? rows : R;
+    off.assign(outer + 1, 0);
+    for (int o = 0; o < outer; ++o) {
+      for (int i = 0; i < inner; ++i) {
+        const double c = by_r ? X[(size_t)i * R + o] : X[(size_t)o * R + i];
+        if (c != 0.0) t.push_back(SmallTerm{0, c, i, 0});
+      }
+      off[o + 1] = (int)t.size();
+    }
+  };
+  std::vector<int> uo, vo, wo;
+  std::vector<SmallTerm> ut, vt, wt;
+  terms(a->Ud, M * K, true, uo, ut);
+  terms(a->Vd, K * Nb, true, vo, vt);
+  terms(a->Wd, M * Nb, false, wo, wt);
+  Launch ln;
+  ln.kind = Launch::SMALL;
+  ln.level = 1;
+  const Dims& d = dims[1];
+  for (auto& tm : ut) tm.off = (tm.blk / K) * d.P * cur_lda + (tm.blk % K) * d.Q;
+  for (auto& tm : vt) tm.off = (tm.blk / Nb) * d.Q * cur_ldb + (tm.blk % Nb) * d.N;
+  ln.small_off[0] = push_tab(uo.data(), uo.size() * sizeof(int));
+  ln.small_off[1] = push_tab(ut.data(), ut.size() * sizeof(SmallTerm));
+  ln.small_off[2] = push_tab(vo.data(), vo.size() * sizeof(int));
+  ln.small_off[3] = push_tab(vt.data(), vt.size() * sizeof(SmallTerm));
+  ln.small_off[4] = push_tab(wo.data(), wo.size() * sizeof(int));
+  ln.small_off[5] = push_tab(wt.data(), wt.size() * sizeof(SmallTerm));
+  const int T = small_tile();
+  SmallArgs& sa = ln.small;
+  sa.A = cur_A, sa.B = cur_B, sa.C = cur_C;
+  sa.lda = cur_lda, sa.ldb = cur_ldb, sa.ldc = cur_ldc;
+  sa.pm = (int)d.P, sa.pk = (int)d.Q, sa.pn = (int)d.N;
+  sa.M = M, sa.K = K, sa.N = Nb, sa.R = R;
+  sa.tiles_m = (int)((d.P + T - 1) / T), sa.tiles_n = (int)((d.N + T - 1) / T);
+  sa.Mbuf = small_M, sa.cnt = small_cnt;
+  int max_nu = 0, max_nv = 0;
+  for (int r = 0; r < R; ++r) max_nu = std::max(max_nu, uo[r + 1] - uo[r]), max_nv = std::max(max_nv, vo[r + 1] - vo[r]);
+  if (!small_config(max_nu, max_nv, sa.pk, R, &sa.kc, &sa.g)) throw Error(FMM_E_UNSUPPORTED, "internal: small_fused config");
+  sa.kc_log2 = 0;
+  while ((1 << sa.kc_log2) < sa.kc) ++sa.kc_log2;
+  sa.stage_max = max_nu * T * (sa.kc + 4) + max_nv * sa.kc * (T + 8);
+  sa.smem = std::max({8 * (2 * sa.stage_max + T * (sa.kc + 4) + sa.kc * (T + 8)), 8 * R * sa.g, 3 * T * T * 8});
+  sa.nw = (int)wt.size();
+  bool v2 = al16(cur_A) && al16(cur_B) && cur_lda % 2 == 0 && cur_ldb % 2 == 0;
+  for (const auto& tm : ut) v2 = v2 && tm.off % 2 == 0;
+  for (const auto& tm : vt) v2 = v2 && tm.off % 2 == 0;
+  sa.vec2 = v2 ? 1 : 0;
+  // the cluster variant (C_k over distributed shared memory) measured slower on c1 (26.7 against
+  // 18.5 us per step): only on request (FMM_SMALL_CLUSTER=1)
+  const char* cl = getenv("FMM_SMALL_CLUSTER");
+  sa.cluster = cl && cl[0] == '1' && R >= M * Nb && small_cluster_ok(R, sa.smem);
+  ln.count = R;
+  ln.tiles = (long long)sa.tiles_m * sa.tiles_n * R;
+  // work: the leaf products, the formation reads / adds and the assembly (as the separate kernels)
+  ln.flops = 2.0 * R * d.P * (double)d.Q * d.N;
+  ln.gemm_bytes = 8.0 * R * (d.P * d.Q + d.Q * d.N + d.P * d.N);
+  ln.elem_reads = (double)ut.size() * d.P * d.Q + (double)vt.size() * d.Q * d.N + (double)wt.size() * d.P * d.N;
+  ln.elem_writes = (double)M * Nb * d.P * d.N;
+  ln.elem_adds = (double)(ut.size() - uo.size() + 1) * d.P * d.Q + (double)(vt.size() - vo.size() + 1) * d.Q * d.N +
+                 (double)(wt.size() - M * Nb) * d.P * d.N;
+  launches.push_back(ln);
+}
+
 static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 void fmm_plan_s::build(const double* A, long long lda, const double* B, long long ldb, double* C, long long ldc,
@@ -469,6 +550,10 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
   h_tab.clear();
   scratch_used = 0;
   cur_A = A, cur_B = B, cur_C = C, cur_lda = lda, cur_ldb = ldb, cur_ldc = ldc;
+  if (small) {  // the whole step as one launch (sec. 6h)
+    emit_small();
+    return;
+  }
   const View rootA{const_cast<double*>(A), lda, 1.0}, rootB{const_cast<double*>(B), ldb, 1.0};
   const int M = alg->M, K = alg->K, Nb = alg->N;
   auto push = [&](const void* p, size_t n) {
@@ -1466,6 +1551,43 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
       p->fuse = false;
     }
   }
+  // small_fused (sec. 6h): one launch for a one-level plan whose leaf products would leave most
+  // SMs idle.  The leaf GEMM tiles are 128 x 128 at most; below one per SM the step is launch bound.
+  {
+    const char* e = getenv("FMM_NO_SMALL");
+    // the one launch reads A and B with 8-byte copies, so R7b's alignment peel is not needed: the
+    // paper's minimal peeling decides whether the top level divides exactly
+    std::vector<Dims> dd = p->dims;
+    if (L == 1 && p->opt.peel_align) {
+      bool tp = false;
+      dd = plan_dims(*a, p->P, p->Q, p->N, levels, false, false, &tp);
+    }
+    const Dims& d0 = dd[0];
+    int max_nu = 0, max_nv = 0;
+    for (int r = 0; r < R; ++r) {
+      int nu = 0, nv = 0;
+      for (int i = 0; i < M * K; ++i) nu += a->Ud[(size_t)i * R + r] != 0.0;
+      for (int j = 0; j < K * Nb; ++j) nv += a->Vd[(size_t)j * R + r] != 0.0;
+      max_nu = std::max(max_nu, nu), max_nv = std::max(max_nv, nv);
+    }
+    int kc = 0, g = 0, nw = 0;
+    for (double w : a->Wd) nw += w != 0.0;
+    if (nw <= 256 && p->opt.small_fused && !(e && e[0] == '1') && L == 1 && (int)dd.size() == 2 && d0.P1 == d0.P && d0.Q1 == d0.Q &&
+        d0.N1 == d0.N && p->opt.strategy == FMM_ADD_STREAMING && p->opt.shard_count == 1 && !p->dist_comm && !p->p2p && !p->k3f && !p->fuse && M * K <= 64 &&
+        K * Nb <= 64 && M * Nb <= 64 && R <= 128 && small_config(max_nu, max_nv, (int)std::min<long long>(dd[1].Q, 1 << 30), R, &kc, &g)) {
+      const Dims& d = dd[1];
+      const long long gemm_tiles = (long long)R * ((d.P + 127) / 128) * ((d.N + 127) / 128);
+      const int T = small_tile();
+      const long long tiles = ((d.P + T - 1) / T) * ((d.N + T - 1) / T);
+      if (d.P >= 1 && d.Q >= 1 && d.N >= 1 && d.Q < (1LL << 30) && gemm_tiles < gemm_sm_count() && tiles * R < (1LL << 31)) {
+        p->small = true;
+        p->dims = dd;
+        FMM_CUDA(cudaMalloc(&p->small_M, (size_t)tiles * R * T * T * sizeof(double)));
+        FMM_CUDA(cudaMalloc(&p->small_cnt, (size_t)tiles * sizeof(unsigned)));
+        FMM_CUDA(cudaMemset(p->small_cnt, 0, (size_t)tiles * sizeof(unsigned)));
+      }
+    }
+  }
   p->setup_sharding();
   p->setup_workspace();
   // compile the streaming/write-once kernels for the 16-byte variant now (NVRTC)
@@ -1650,8 +1772,9 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
   };
   // NVTX: one range per launch, named by phase and recursion level (profiling)
   static const char* const kNvtx[] = {"fmm form A", "fmm form B",           "fmm leaf gemm", "fmm assemble", "fmm strips",
-                                      "fmm thin",   "fmm fused leaf level", "fmm reduce",    "fmm zero"};
-  static_assert(sizeof(kNvtx) / sizeof(kNvtx[0]) == Launch::ZERO + 1, "one NVTX name per launch kind");
+                                      "fmm thin",   "fmm fused leaf level", "fmm reduce",    "fmm zero",
+                                      "fmm small fused step"};
+  static_assert(sizeof(kNvtx) / sizeof(kNvtx[0]) == Launch::SMALL + 1, "one NVTX name per launch kind");
   char nvtx_name[64];
   nvtxRangePushA(p->dist_comm || p->p2p ? "fmm_execute (distributed)" : "fmm_execute");
   struct NvtxPop {
@@ -1666,7 +1789,8 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
       continue;
     }
     const int ph = (ln.kind == Launch::FORM_A || ln.kind == Launch::FORM_B) ? 0
-                   : (ln.kind == Launch::GEMM || ln.kind == Launch::FUSED || (ln.kind == Launch::SKINNY && ln.level == p->L))
+                   : (ln.kind == Launch::GEMM || ln.kind == Launch::FUSED || ln.kind == Launch::SMALL ||
+                      (ln.kind == Launch::SKINNY && ln.level == p->L))
                        ? 1
                        : 2;
     const int prof_phase = ph < 2 ? ph : (ln.kind == Launch::ASSEMBLE || ln.kind == Launch::ZERO) ? 2 : 3;
@@ -1695,6 +1819,17 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
       case Launch::SKINNY:
       case Launch::REDUCE:
         break;
+      case Launch::SMALL: {
+        SmallArgs sa = ln.small;
+        sa.u_off = reinterpret_cast<const int*>(d_tab + ln.small_off[0]);
+        sa.u_terms = reinterpret_cast<const SmallTerm*>(d_tab + ln.small_off[1]);
+        sa.v_off = reinterpret_cast<const int*>(d_tab + ln.small_off[2]);
+        sa.v_terms = reinterpret_cast<const SmallTerm*>(d_tab + ln.small_off[3]);
+        sa.w_off = reinterpret_cast<const int*>(d_tab + ln.small_off[4]);
+        sa.w_terms = reinterpret_cast<const SmallTerm*>(d_tab + ln.small_off[5]);
+        small_launch(sa, ls);
+        break;
+      }
       case Launch::ZERO:
         for (const auto& zb : ln.zero_blocks)
           FMM_CUDA(cudaMemset2DAsync(reinterpret_cast<void*>((uintptr_t)zb[0]), (size_t)zb[1] * 8, 0, (size_t)zb[3] * 8,
@@ -1830,6 +1965,7 @@ void fmm_plan_options_default(fmm_plan_options* o) {
   o->peel_tiles = 0;  // measured: c3 12.60 -> 12.78 ms, c5 258.0 -> 257.3 (R7c)
   o->dist_chunks = 4;
   o->fuse_output = 0;
+  o->small_fused = 1;
 }
 
 fmm_status_t fmm_plan_create(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels,
@@ -1965,7 +2101,8 @@ fmm_status_t fmm_plan_stats(const fmm_plan_t* p, double out[8]) {
             : (ln.kind == Launch::FORM_A || ln.kind == Launch::FORM_B || ln.kind == Launch::ASSEMBLE) && ln.kern
                 ? lincomb_steps(*ln.kern)  // pairwise: one launch per chain position
                 : 1;
-    if (ln.kind == Launch::GEMM || ln.kind == Launch::FUSED || (ln.kind == Launch::SKINNY && ln.level == p->L))
+    if (ln.kind == Launch::GEMM || ln.kind == Launch::FUSED || ln.kind == Launch::SMALL ||
+        (ln.kind == Launch::SKINNY && ln.level == p->L))
       s[6] += ln.count;
     if (ln.kind == Launch::SKINNY) s[4] += (ln.nrow > 0) + (ln.ncol > 0) - 1;
   }
@@ -2222,11 +2359,12 @@ fmm_status_t fmm_fused_compile_check_ex(const fmm_alg* alg, int layout, int cse,
 fmm_status_t fmm_plan_stats_ex2(const fmm_plan_t* p, double* out, int n) {
   FMM_API_BEGIN
   if (!p || !out || n < 0) throw Error(FMM_E_INVALID_ARG, "bad argument");
-  double s[18] = {0};
+  double s[19] = {0};
   FMM_CHECK_STATUS(fmm_plan_stats_ex(p, s));
   s[16] = p->k3f ? 1.0 : 0.0;
   s[17] = p->collapse_asm ? 1.0 : 0.0;
-  std::memcpy(out, s, sizeof(double) * (size_t)std::min(n, 18));
+  s[18] = p->small ? 1.0 : 0.0;
+  std::memcpy(out, s, sizeof(double) * (size_t)std::min(n, 19));
   return FMM_OK;
   FMM_API_END
 }
@@ -2238,7 +2376,8 @@ fmm_status_t fmm_plan_stats_ex(const fmm_plan_t* p, double out[16]) {
   FMM_CHECK_STATUS(fmm_plan_stats(p, s));
   for (const Launch& ln : p->launches) {
     const double bytes = 8.0 * (ln.elem_reads + ln.elem_writes);
-    const bool leaf = ln.kind == Launch::GEMM || ln.kind == Launch::FUSED || (ln.kind == Launch::SKINNY && ln.level == p->L);
+    const bool leaf = ln.kind == Launch::GEMM || ln.kind == Launch::FUSED || ln.kind == Launch::SMALL ||
+                      (ln.kind == Launch::SKINNY && ln.level == p->L);
     if (leaf) s[8] += ln.flops;
     if (ln.kind == Launch::FUSED) s[9] += bytes, s[10] += 1;
     if (ln.kind == Launch::FORM_A || ln.kind == Launch::FORM_B) s[11] += bytes;

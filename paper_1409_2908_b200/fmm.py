@@ -35,7 +35,7 @@ class _Options(ctypes.Structure):
                 ("workspace_limit_bytes", ctypes.c_size_t), ("peel_align", ctypes.c_int),
                 ("fuse_leaf_level", ctypes.c_int), ("shard_mode", ctypes.c_int), ("collapse_levels", ctypes.c_int),
                 ("cuda_graphs", ctypes.c_int), ("peel_tiles", ctypes.c_int), ("dist_chunks", ctypes.c_int),
-                ("fuse_output", ctypes.c_int)]
+                ("fuse_output", ctypes.c_int), ("small_fused", ctypes.c_int)]
 
 
 # fmm_barrier_fn: int (*)(void* ctx), a host barrier over the ranks of a peer-memory plan
@@ -259,7 +259,7 @@ class Plan:
                  fuse=False, collapse: bool = True, comm: Optional[Comm] = None, root: int = 0,
                  shard_mode: str = "leaf", cuda_graphs: bool = True, peel_tiles: bool = False,
                  p2p: Optional["P2P"] = None, barrier=None, dist_chunks: Optional[int] = None,
-                 fuse_output: Optional[bool] = None):
+                 fuse_output: Optional[bool] = None, small: Optional[bool] = None):
         """comm: an NCCL Comm -> fmm_plan_create_dist (the reduce runs inside execute, in dist_chunks
         overlapped row chunks where it applies).  p2p + barrier: a P2P object and a zero-argument host
         barrier over the same ranks (e.g. torch.distributed.barrier) -> fmm_plan_create_p2p (the
@@ -289,6 +289,8 @@ class Plan:
             o.dist_chunks = int(dist_chunks)
         if fuse_output is not None:
             o.fuse_output = int(bool(fuse_output))
+        if small is not None:
+            o.small_fused = int(bool(small))
         self.device = torch.cuda.current_device() if device is None else device
         h = ctypes.c_void_p()
         self.comm = comm  # a distributed plan keeps its communicator / peer buffers alive
@@ -341,11 +343,11 @@ class Plan:
         return [bool(x) for x in na], [bool(x) for x in nb], tuple(core), bool(allf.value)
 
     def stats(self) -> dict:
-        s = (ctypes.c_double * 18)()
-        _check(_lib.fmm_plan_stats_ex2(self._h, s, 18))
+        s = (ctypes.c_double * 19)()
+        _check(_lib.fmm_plan_stats_ex2(self._h, s, 19))
         keys = ["gemm_flops", "add_flops", "add_bytes", "gemm_bytes", "launches", "levels", "leaves", "paper_flops",
                 "leaf_flops", "fused_add_bytes", "fused_launches", "formation_bytes", "assembly_bytes", "strip_flops",
-                "collapsed", "tiled_peel", "fused_output", "collapsed_assembly"]
+                "collapsed", "tiled_peel", "fused_output", "collapsed_assembly", "small_fused"]
         return dict(zip(keys, list(s)))
 
     def new_output(self):
@@ -378,7 +380,8 @@ class Plan:
         return C, {"formation_ms": ms[0], "gemm_ms": ms[1], "assembly_ms": ms[2], "strips_ms": ms[3],
                    "total_ms": ms[4]}
 
-    KINDS = ["form_A", "form_B", "leaf_gemm", "assembly", "strips", "thin", "fused_leaf_level", "combine", "zero"]
+    KINDS = ["form_A", "form_B", "leaf_gemm", "assembly", "strips", "thin", "fused_leaf_level", "combine", "zero",
+             "small_fused"]
 
     def execute_profile(self, A, B, C=None, stream=None, max_launches=256):
         """Blocking diagnostic execute (fmm_execute_profile): [(kind, level, ms)] per launch."""

@@ -69,6 +69,7 @@ def _run(F, name, A, B, L, layout="row", **kw):
             return torch.from_numpy(np.ascontiguousarray(x)).cuda()
         return torch.from_numpy(np.ascontiguousarray(x.T)).cuda().t()
     kw.setdefault("collapse", False)  # collapsed levels take precedence over the fused leaf level
+    kw.setdefault("small", False)  # compare against the separate launches, not the one-launch small path
     p = F.Plan(F.load_alg(name), P, Q, N, L, layout=layout, **kw)
     C = p.execute(dev(A), dev(B))
     torch.cuda.synchronize()

@@ -145,7 +145,9 @@ def test_strategies_and_cse(strategy, cse):
 def test_three_strategies_round_identically(name, L, P, Q, N):
     # without CSE every strategy sums each chain in ascending index order: bitwise equal
     A, B = I.problem(P, Q, N, seed=12)
-    Cs, _ = run(name, A, B, L, strategy="streaming", cse=False)
+    # (the separate streaming kernels: the one-launch small path sums the leaf products' k in
+    # another order)
+    Cs, _ = run(name, A, B, L, strategy="streaming", cse=False, small=False)
     for strategy in ("write_once", "pairwise"):
         C, _ = run(name, A, B, L, strategy=strategy, cse=False)
         assert np.array_equal(C, Cs), strategy
@@ -175,7 +177,7 @@ def test_addition_bytes_equal_the_oracles_chain_count(name, strategy):
     b = 64
     P, Q, N = a.M * b, a.K * b, a.N * b
     A, B = I.problem(P, Q, N, seed=14, kind="integers")
-    C, p = run(name, A, B, 1, strategy=strategy, cse=False)
+    C, p = run(name, A, B, 1, strategy=strategy, cse=False, small=False)  # the separate kernels' bytes
     reads, writes = O.addition_traffic(oalg(name), strategy, alias_singletons=True)
     assert p.stats()["add_bytes"] == 8 * b * b * (reads + writes)
     assert np.array_equal(C, A @ B)
@@ -346,6 +348,24 @@ def test_every_tma_tile_width(bn, monkeypatch):
     Ai, Bi = I.problem(260, 72, 410, seed=15, kind="integers")
     C, _ = run("alg_433_29", Ai, Bi, 1)
     assert np.array_equal(C, Ai @ Bi)
+
+
+@pytest.mark.parametrize("epi", ["1", "2"])
+@pytest.mark.parametrize("bn", ["128", "112", "80", "64"])
+def test_staged_epilogue(epi, bn, monkeypatch):
+    # the leaf GEMM's staged bulk-copy epilogue (FMM_GEMM_EPI, DESIGN 6d): ragged rows, an odd
+    # column count (the last column stored directly), several tiles per CTA (slot hand-over)
+    monkeypatch.setenv("FMM_GEMM_EPI", epi)
+    monkeypatch.setenv("FMM_GEMM_BN", bn)
+    A, B = I.problem(300, 200, 333, seed=16)
+    C = F.dgemm(dev(A), dev(B)).cpu().numpy()
+    assert np.max(np.abs(C - O.classical(A, B))) <= bound(A, B, 1e-13)
+    Ai, Bi = I.problem(1037, 96, 1201, seed=17, kind="integers")
+    C, _ = run("alg_433_29", Ai, Bi, 1)
+    assert np.array_equal(C, Ai @ Bi)
+    A, B = I.problem(2050, 300, 1999, seed=18)
+    C, _ = run("winograd_class_222_7", A, B, 2)
+    assert np.max(np.abs(C - O.fast(A, B, oalg("winograd_class_222_7"), 2))) <= bound(A, B, 1e-12)
 
 
 def test_execute_host_async_pipeline():
