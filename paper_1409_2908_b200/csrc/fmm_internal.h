@@ -127,6 +127,7 @@ struct SmallTerm {
   int blk;
   int pad_;
 };
+constexpr int SMALL_MAX_R = 64, SMALL_MAX_UV = 160, SMALL_MAX_W = 256;  // R, MN <= 64; nnz(U), nnz(V), nnz(W)
 struct SmallArgs {
   const double* A;
   const double* B;
@@ -135,20 +136,18 @@ struct SmallArgs {
   int pm, pk, pn;  // leaf dimensions (P / M, Q / K, N / N_base: the plan requires exact division)
   int M, K, N, R;  // base case
   int tiles_m, tiles_n;
-  const int* u_off;
-  const SmallTerm* u_terms;
-  const int* v_off;
-  const SmallTerm* v_terms;
-  const int* w_off;
-  const SmallTerm* w_terms;
+  // the term tables travel in the kernel parameters (constant bank: no global loads in the prologue)
+  int u_off[SMALL_MAX_R + 1], v_off[SMALL_MAX_R + 1], w_off[SMALL_MAX_R + 1];
+  SmallTerm u_terms[SMALL_MAX_UV], v_terms[SMALL_MAX_UV], w_terms[SMALL_MAX_W];
   double* Mbuf;    // R x tiles x 32 x 32 doubles
-  unsigned* cnt;   // per tile position, zero between launches
-  int kc, g;       // k-chunk depth (a power of two) and assembly group (small_config)
-  int kc_log2;
+  unsigned* cnt;   // 2 per tile position (arrive, depart), zero between launches
+  int kc, g;       // k-chunk depth (16, 32 or 64) and assembly group (small_config)
   int stage_max;   // doubles of one raw chunk buffer (the largest term counts)
   int nw;          // W terms (<= 256)
   int vec2;        // 1: every A / B view is 16-byte aligned (16-byte copies)
   int cluster;     // 1: the R CTAs of a tile are a cluster (C_k from the peers' shared memory)
+  int prefetch;    // 1: the next chunk's copies are issued before the current chunk is used
+  int coop;        // 1: the whole grid is resident; the R CTAs of a tile assemble it together
   int smem;        // dynamic shared memory bytes of the launch
 };
 int small_tile();  // the tile edge (32)
@@ -156,6 +155,7 @@ int small_tile();  // the tile edge (32)
 bool small_config(int max_nu, int max_nv, int pk, int R, int* kc, int* g);
 void small_launch(const SmallArgs& a, cudaStream_t stream);
 bool small_cluster_ok(int R, int smem);  // the cluster variant fits (R <= 16, co-resident)
+bool small_coop_ok(long long grid, int smem);  // every CTA of the launch is co-resident
 // TMA kernel configuration: consumer warp grid of a tile width, SM count, dynamic shared memory.
 void gemm_bn_config(int bn, int* wgm, int* wgn);
 int gemm_sm_count();

@@ -70,8 +70,7 @@ struct Launch {
   std::vector<int> node_ids;  // FORM / ASSEMBLE: parent node index of every table entry
   int nin = 0, nout = 0;      // ASSEMBLE: inputs / outputs per table entry
   bool k3f = false;           // GEMM: the K3f leaf GEMM (epilogue reduce-adds into the W targets)
-  SmallArgs small{};          // SMALL: the launch's arguments (device table pointers filled at run time)
-  size_t small_off[6] = {};   // SMALL: byte offsets of u_off, u_terms, v_off, v_terms, w_off, w_terms
+  SmallArgs small{};          // SMALL: the launch's arguments (term tables included)
   size_t k3f_maps_off = 0, k3f_count_off = 0, k3f_targets_off = 0;  // GEMM k3f: its device tables
   std::vector<std::array<long long, 4>> zero_blocks;  // ZERO: (host pointer bits, ld, rows, cols)
   // NCCL distributed plans with dist_chunks: rows [first, second) of C (plan orientation) to reduce
@@ -500,14 +499,14 @@ void fmm_plan_s::emit_small() {
   const Dims& d = dims[1];
   for (auto& tm : ut) tm.off = (tm.blk / K) * d.P * cur_lda + (tm.blk % K) * d.Q;
   for (auto& tm : vt) tm.off = (tm.blk / Nb) * d.Q * cur_ldb + (tm.blk % Nb) * d.N;
-  ln.small_off[0] = push_tab(uo.data(), uo.size() * sizeof(int));
-  ln.small_off[1] = push_tab(ut.data(), ut.size() * sizeof(SmallTerm));
-  ln.small_off[2] = push_tab(vo.data(), vo.size() * sizeof(int));
-  ln.small_off[3] = push_tab(vt.data(), vt.size() * sizeof(SmallTerm));
-  ln.small_off[4] = push_tab(wo.data(), wo.size() * sizeof(int));
-  ln.small_off[5] = push_tab(wt.data(), wt.size() * sizeof(SmallTerm));
   const int T = small_tile();
   SmallArgs& sa = ln.small;
+  std::copy(uo.begin(), uo.end(), sa.u_off);
+  std::copy(vo.begin(), vo.end(), sa.v_off);
+  std::copy(wo.begin(), wo.end(), sa.w_off);
+  std::copy(ut.begin(), ut.end(), sa.u_terms);
+  std::copy(vt.begin(), vt.end(), sa.v_terms);
+  std::copy(wt.begin(), wt.end(), sa.w_terms);
   sa.A = cur_A, sa.B = cur_B, sa.C = cur_C;
   sa.lda = cur_lda, sa.ldb = cur_ldb, sa.ldc = cur_ldc;
   sa.pm = (int)d.P, sa.pk = (int)d.Q, sa.pn = (int)d.N;
@@ -517,8 +516,6 @@ void fmm_plan_s::emit_small() {
   int max_nu = 0, max_nv = 0;
   for (int r = 0; r < R; ++r) max_nu = std::max(max_nu, uo[r + 1] - uo[r]), max_nv = std::max(max_nv, vo[r + 1] - vo[r]);
   if (!small_config(max_nu, max_nv, sa.pk, R, &sa.kc, &sa.g)) throw Error(FMM_E_UNSUPPORTED, "internal: small_fused config");
-  sa.kc_log2 = 0;
-  while ((1 << sa.kc_log2) < sa.kc) ++sa.kc_log2;
   sa.stage_max = max_nu * T * (sa.kc + 4) + max_nv * sa.kc * (T + 8);
   sa.smem = std::max({8 * (2 * sa.stage_max + T * (sa.kc + 4) + sa.kc * (T + 8)), 8 * R * sa.g, 3 * T * T * 8});
   sa.nw = (int)wt.size();
@@ -530,6 +527,9 @@ void fmm_plan_s::emit_small() {
   // 18.5 us per step): only on request (FMM_SMALL_CLUSTER=1)
   const char* cl = getenv("FMM_SMALL_CLUSTER");
   sa.cluster = cl && cl[0] == '1' && R >= M * Nb && small_cluster_ok(R, sa.smem);
+  sa.prefetch = !(getenv("FMM_SMALL_PREFETCH") && getenv("FMM_SMALL_PREFETCH")[0] == '0');
+  // the R CTAs of a tile assemble it together when the whole grid is resident (else the last one)
+  sa.coop = !sa.cluster && small_coop_ok((long long)sa.tiles_m * sa.tiles_n * R, sa.smem) && !(getenv("FMM_SMALL_COOP") && getenv("FMM_SMALL_COOP")[0] == '0');
   ln.count = R;
   ln.tiles = (long long)sa.tiles_m * sa.tiles_n * R;
   // work: the leaf products, the formation reads / adds and the assembly (as the separate kernels)
@@ -1570,9 +1570,12 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
       for (int j = 0; j < K * Nb; ++j) nv += a->Vd[(size_t)j * R + r] != 0.0;
       max_nu = std::max(max_nu, nu), max_nv = std::max(max_nv, nv);
     }
-    int kc = 0, g = 0, nw = 0;
+    int kc = 0, g = 0, nw = 0, nuv = 0, nvv = 0;
     for (double w : a->Wd) nw += w != 0.0;
-    if (nw <= 256 && p->opt.small_fused && !(e && e[0] == '1') && L == 1 && (int)dd.size() == 2 && d0.P1 == d0.P && d0.Q1 == d0.Q &&
+    for (double u : a->Ud) nuv += u != 0.0;
+    for (double v : a->Vd) nvv += v != 0.0;
+    if (nw <= SMALL_MAX_W && nuv <= SMALL_MAX_UV && nvv <= SMALL_MAX_UV && R <= SMALL_MAX_R && M * Nb <= SMALL_MAX_R &&
+        p->opt.small_fused && !(e && e[0] == '1') && L == 1 && (int)dd.size() == 2 && d0.P1 == d0.P && d0.Q1 == d0.Q &&
         d0.N1 == d0.N && p->opt.strategy == FMM_ADD_STREAMING && p->opt.shard_count == 1 && !p->dist_comm && !p->p2p && !p->k3f && !p->fuse && M * K <= 64 &&
         K * Nb <= 64 && M * Nb <= 64 && R <= 128 && small_config(max_nu, max_nv, (int)std::min<long long>(dd[1].Q, 1 << 30), R, &kc, &g)) {
       const Dims& d = dd[1];
@@ -1583,8 +1586,8 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
         p->small = true;
         p->dims = dd;
         FMM_CUDA(cudaMalloc(&p->small_M, (size_t)tiles * R * T * T * sizeof(double)));
-        FMM_CUDA(cudaMalloc(&p->small_cnt, (size_t)tiles * sizeof(unsigned)));
-        FMM_CUDA(cudaMemset(p->small_cnt, 0, (size_t)tiles * sizeof(unsigned)));
+        FMM_CUDA(cudaMalloc(&p->small_cnt, 2 * (size_t)tiles * sizeof(unsigned)));
+        FMM_CUDA(cudaMemset(p->small_cnt, 0, 2 * (size_t)tiles * sizeof(unsigned)));
       }
     }
   }
@@ -1819,17 +1822,9 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
       case Launch::SKINNY:
       case Launch::REDUCE:
         break;
-      case Launch::SMALL: {
-        SmallArgs sa = ln.small;
-        sa.u_off = reinterpret_cast<const int*>(d_tab + ln.small_off[0]);
-        sa.u_terms = reinterpret_cast<const SmallTerm*>(d_tab + ln.small_off[1]);
-        sa.v_off = reinterpret_cast<const int*>(d_tab + ln.small_off[2]);
-        sa.v_terms = reinterpret_cast<const SmallTerm*>(d_tab + ln.small_off[3]);
-        sa.w_off = reinterpret_cast<const int*>(d_tab + ln.small_off[4]);
-        sa.w_terms = reinterpret_cast<const SmallTerm*>(d_tab + ln.small_off[5]);
-        small_launch(sa, ls);
+      case Launch::SMALL:
+        small_launch(ln.small, ls);
         break;
-      }
       case Launch::ZERO:
         for (const auto& zb : ln.zero_blocks)
           FMM_CUDA(cudaMemset2DAsync(reinterpret_cast<void*>((uintptr_t)zb[0]), (size_t)zb[1] * 8, 0, (size_t)zb[3] * 8,

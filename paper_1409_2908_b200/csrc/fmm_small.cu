@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 #include "fmm_internal.h"
 
@@ -60,101 +61,138 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // CL: the R CTAs of a tile form a thread-block cluster (R <= 16); each keeps its M_r tile in
 // shared memory and CTA k < MN forms C_k's tile from its peers' tiles over distributed shared
 // memory (no scratch round trip, no counter).  Otherwise the last CTA of the tile does it.
-template <bool CL>
+#ifdef FMM_SMALL_TIMING  // diagnostics build: phase timestamps (globaltimer, ns) of CTA 0 and of the
+                         // last CTA of tile 0, printed by thread 0
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  return v;
+}
+#define TSTAMP(i) (tst[i] = gtime())
+#else
+#define TSTAMP(i) ((void)0)
+#endif
+template <bool CL, int KC, int V>
 __global__ void __launch_bounds__(THREADS) small_fmm_kernel(SmallArgs a) {
+#ifdef FMM_SMALL_TIMING
+  unsigned long long tst[10] = {};
+#endif
+  TSTAMP(0);
   extern __shared__ double smem[];
   __shared__ SmallTerm tu[64], tv[64], tw[256];
   __shared__ int wo[65];
   __shared__ int is_last;
   __shared__ __align__(16) double mts[CL ? TM * TN : 2];
+  constexpr int LDA = KC + 4, LDB = TN + 8;        // raw / formed chunk row strides (doubles)
+  constexpr int ACP = KC / V, BCP = TN / V;        // copies per A / B chunk row
+  constexpr int ACT = (TM * ACP + THREADS - 1) / THREADS, BCT = (KC * BCP + THREADS - 1) / THREADS;
+  constexpr int SPT = (TM * KC + THREADS - 1) / THREADS, TPT = (KC * TN + THREADS - 1) / THREADS;
   const int npos = a.tiles_m * a.tiles_n;
   const int pos = CL ? blockIdx.x / a.R : blockIdx.x % npos, r = CL ? blockIdx.x % a.R : blockIdx.x / npos;
   const int i0 = (pos / a.tiles_n) * TM, j0 = (pos % a.tiles_n) * TN;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int grp = warp >> 2, sub = warp & 3;  // group grp takes the k-steps ks = grp mod 4
   const int wm = (sub >> 1) * 16, wn = (sub & 1) * 16;
-  const int u0 = __ldg(&a.u_off[r]), nu = __ldg(&a.u_off[r + 1]) - u0;
-  const int v0 = __ldg(&a.v_off[r]), nv = __ldg(&a.v_off[r + 1]) - v0;
+  const int u0 = a.u_off[r], nu = a.u_off[r + 1] - u0;
+  const int v0 = a.v_off[r], nv = a.v_off[r + 1] - v0;
   if (t < nu) tu[t] = a.u_terms[u0 + t];
   if (t < nv) tv[t] = a.v_terms[v0 + t];
+  const int MN = a.M * a.N;
   __syncthreads();
-  const int KC = a.kc, LDA = KC + 4, LDB = TN + 8;
-  const int stage = nu * TM * LDA + nv * KC * LDB;  // doubles per raw chunk buffer
-  double* sS = smem + 2 * a.stage_max;              // formed S_r chunk: TM x LDA
-  double* sT = sS + TM * LDA;                       // formed T_r chunk: KC x LDB
-  // stage chunk k0 of every term's sub-tile into raw buffer b.  KC is a power of two and each
-  // thread keeps one column (pair) of the chunk, stepping down the rows: no division in the loop.
-  // 16-byte copies (two columns) where every view is 16-byte aligned (a.vec2), else 8-byte copies;
-  // the source size of a copy clips it at the operand's edge (zero fill).
-  const int lkc = a.kc_log2;
-  const int vw = a.vec2 ? 2 : 1;                           // doubles per copy
-  const int lcp = lkc - (a.vec2 ? 1 : 0);                  // log2 of copies per A chunk row
-  const int a_col = (t & ((1 << lcp) - 1)) * vw, a_row0 = t >> lcp, a_step = THREADS >> lcp;
-  const int b_col = (t & (TN / vw - 1)) * vw, b_row0 = t / (TN / vw), b_step = THREADS / (TN / vw);
+  TSTAMP(1);
+  const int stage = a.stage_max;            // doubles per raw chunk buffer
+  double* sS = smem + 2 * stage;            // formed S_r chunk: TM x LDA
+  double* sT = sS + TM * LDA;               // formed T_r chunk: KC x LDB
+  // stage chunk k0 of every term's sub-tile into raw buffer b: every index below is a compile-time
+  // shift of the thread id; the source size of a copy clips it at the operand's edge (zero fill)
   auto load = [&](int k0, int b) {
-    const unsigned base = smem_u32(smem + b * a.stage_max);
-    const int ka = k0 + a_col;
-    const unsigned a_bytes = (unsigned)max(0, min(vw, a.pk - ka)) * 8u;
-    for (int q = 0; q < nu; ++q) {
-      const double* src = a.A + tu[q].off + (long long)i0 * a.lda + ka;
-      const unsigned dst = base + 8u * (unsigned)(q * TM * LDA + a_col);
-      for (int i = a_row0; i < TM; i += a_step) {
-        const unsigned nb = i0 + i < a.pm ? a_bytes : 0u;
-        cpn(dst + 8u * (unsigned)(i * LDA), src + (long long)i * a.lda, nb, a.vec2);
+    const unsigned base = smem_u32(smem + b * stage);
+#pragma unroll
+    for (int it = 0; it < ACT; ++it) {
+      const int e = t + it * THREADS, i = e / ACP, col = (e % ACP) * V;
+      if (e < TM * ACP) {
+        const unsigned nb = i0 + i < a.pm ? (unsigned)max(0, min(V, a.pk - k0 - col)) * 8u : 0u;
+        const long long go = (long long)(i0 + i) * a.lda + k0 + col;
+        const unsigned so = 8u * (unsigned)(i * LDA + col);
+        for (int q = 0; q < nu; ++q) cpn(base + 8u * (unsigned)(q * TM * LDA) + so, a.A + tu[q].off + go, nb, V == 2);
       }
     }
-    const int jb = j0 + b_col;
-    const unsigned b_bytes = (unsigned)max(0, min(vw, a.pn - jb)) * 8u;
-    for (int q = 0; q < nv; ++q) {
-      const double* src = a.B + tv[q].off + (long long)k0 * a.ldb + jb;
-      const unsigned dst = base + 8u * (unsigned)(nu * TM * LDA + q * KC * LDB + b_col);
-      for (int kk = b_row0; kk < KC; kk += b_step) {
-        const unsigned nb = k0 + kk < a.pk ? b_bytes : 0u;
-        cpn(dst + 8u * (unsigned)(kk * LDB), src + (long long)kk * a.ldb, nb, a.vec2);
+    const unsigned bb = base + 8u * (unsigned)(nu * TM * LDA);
+#pragma unroll
+    for (int it = 0; it < BCT; ++it) {
+      const int e = t + it * THREADS, kk = e / BCP, col = (e % BCP) * V;
+      if (e < KC * BCP) {
+        const unsigned nb = k0 + kk < a.pk ? (unsigned)max(0, min(V, a.pn - j0 - col)) * 8u : 0u;
+        const long long go = (long long)(k0 + kk) * a.ldb + j0 + col;
+        const unsigned so = 8u * (unsigned)(kk * LDB + col);
+        for (int q = 0; q < nv; ++q) cpn(bb + 8u * (unsigned)(q * KC * LDB) + so, a.B + tv[q].off + go, nb, V == 2);
       }
     }
     cp_commit();
   };
-  (void)stage;
   double acc[2][2][2] = {};
   const int nchunks = (a.pk + KC - 1) / KC;
   load(0, 0);
   for (int c = 0; c < nchunks; ++c) {
-    if (c + 1 < nchunks) {
+    if (c + 1 < nchunks && a.prefetch) {
       load((c + 1) * KC, (c + 1) & 1);
       cp_wait<1>();
     } else {
       cp_wait<0>();
     }
     __syncthreads();
-    // form the chunk of S_r and T_r from the staged sub-tiles (independent elements: the loads of
-    // several elements are in flight at once)
-    const double* ra = smem + (c & 1) * a.stage_max;
+    if (c == 0) TSTAMP(2);
+    // form the chunk of S_r and T_r from the staged sub-tiles: terms outside, the thread's
+    // elements (independent) inside, so their shared-memory loads are in flight together
+    const double* ra = smem + (c & 1) * stage;
     const double* rb = ra + nu * TM * LDA;
     {
-      const int col = t & (KC - 1);
-      for (int i = t >> lkc; i < TM; i += THREADS >> lkc) {
-        const int off = i * LDA + col;
-        double v = nu ? __dmul_rn(tu[0].coef, ra[off]) : 0.0;
-        for (int q = 1; q < nu; ++q) v = __dadd_rn(v, __dmul_rn(tu[q].coef, ra[q * TM * LDA + off]));
-        sS[off] = v;
+      double vs[SPT], vt[TPT];
+#pragma unroll
+      for (int it = 0; it < SPT; ++it) vs[it] = 0.0;
+#pragma unroll
+      for (int it = 0; it < TPT; ++it) vt[it] = 0.0;
+      for (int q = 0; q < nu; ++q) {
+        const double cf = tu[q].coef;
+#pragma unroll
+        for (int it = 0; it < SPT; ++it) {
+          const int e = t + it * THREADS;
+          const double x = __dmul_rn(cf, ra[q * TM * LDA + (e / KC) * LDA + e % KC]);
+          vs[it] = q == 0 ? x : __dadd_rn(vs[it], x);
+        }
       }
-      const int j = t & (TN - 1);
-      for (int kk = t / TN; kk < KC; kk += THREADS / TN) {
-        const int off = kk * LDB + j;
-        double v = nv ? __dmul_rn(tv[0].coef, rb[off]) : 0.0;
-        for (int q = 1; q < nv; ++q) v = __dadd_rn(v, __dmul_rn(tv[q].coef, rb[q * KC * LDB + off]));
-        sT[off] = v;
+      for (int q = 0; q < nv; ++q) {
+        const double cf = tv[q].coef;
+#pragma unroll
+        for (int it = 0; it < TPT; ++it) {
+          const int e = t + it * THREADS;
+          const double x = __dmul_rn(cf, rb[q * KC * LDB + (e / TN) * LDB + e % TN]);
+          vt[it] = q == 0 ? x : __dadd_rn(vt[it], x);
+        }
+      }
+#pragma unroll
+      for (int it = 0; it < SPT; ++it) {
+        const int e = t + it * THREADS;
+        if (e < TM * KC) sS[(e / KC) * LDA + e % KC] = vs[it];
+      }
+#pragma unroll
+      for (int it = 0; it < TPT; ++it) {
+        const int e = t + it * THREADS;
+        if (e < KC * TN) sT[(e / TN) * LDB + e % TN] = vt[it];
       }
     }
     __syncthreads();
-    const int ksteps = (min(KC, a.pk - c * KC) + 3) / 4;
-#pragma unroll 2
-    for (int ks = grp; ks < ksteps; ks += 4) {
+#pragma unroll
+    for (int ks = grp; ks < KC / 4; ks += 4) {  // zero-filled k beyond the leaf depth adds zeros
       double fa[2], fb[2];
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi) fa[mi] = sS[(wm + mi * 8 + (lane >> 2)) * LDA + ks * 4 + (lane & 3)];
@@ -166,7 +204,13 @@ __global__ void __launch_bounds__(THREADS) small_fmm_kernel(SmallArgs a) {
         for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni], fa[mi], fb[ni]);
     }
     __syncthreads();  // the raw buffer (c & 1) and the formed chunk are overwritten next
+    if (c == 0) TSTAMP(3);
+    if (!a.prefetch && c + 1 < nchunks) load((c + 1) * KC, (c + 1) & 1);
   }
+  TSTAMP(4);
+  // the W terms (any CTA may assemble), read while the product tile is stored
+  for (int q = t; q <= MN; q += THREADS) wo[q] = a.w_off[q];
+  for (int q = t; q < a.nw; q += THREADS) tw[q] = a.w_terms[q];
   // the four groups' partial sums, added in group order (deterministic), then M_r's tile ->
   // scratch (tile-major: [r][pos][TM][TN])
   double* red = smem;  // 3 x TM x TN doubles (the raw buffers are free now)
@@ -199,11 +243,6 @@ __global__ void __launch_bounds__(THREADS) small_fmm_kernel(SmallArgs a) {
   if constexpr (CL) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
-    const int MN = a.M * a.N;
-    if (r < MN) {
-      for (int q = t; q <= MN; q += THREADS) wo[q] = __ldg(&a.w_off[q]);
-      for (int q = t; q < a.nw; q += THREADS) tw[q] = a.w_terms[q];
-    }
     cluster.sync();  // every M_r tile of this position is in its CTA's shared memory
     if (r < MN) {
       const int w0 = wo[r], w1 = wo[r + 1];
@@ -225,15 +264,69 @@ __global__ void __launch_bounds__(THREADS) small_fmm_kernel(SmallArgs a) {
   }
   __threadfence();
   __syncthreads();
+  if (a.coop) {
+    // every CTA of the grid is resident (checked by the host): the R CTAs of this tile wait for
+    // each other (counter `arrive`), then each forms C_k for its own slice of the tile's rows from
+    // all R product tiles (staged in shared memory), and the last to leave (`depart`) resets both
+    // counters for the next launch
+    unsigned* arrive = a.cnt + pos;
+    unsigned* depart = a.cnt + npos + pos;
+    if (t == 0) {
+      atomicAdd(arrive, 1u);
+      while (ld_acquire_u32(arrive) < (unsigned)a.R) __nanosleep(32);
+    }
+    __syncthreads();
+    TSTAMP(5);
+    const int rlo = r * TM / a.R, rhi = (r + 1) * TM / a.R, P = (rhi - rlo) * TN;
+    if (P > 0) {
+      const unsigned sbase = smem_u32(smem);
+      for (int e = t; e < a.R * (P / 2); e += THREADS) {
+        const int q = e / (P / 2), h = e % (P / 2);
+        cp16(sbase + 8u * (unsigned)(q * P + 2 * h), a.Mbuf + ((long long)q * npos + pos) * (TM * TN) + rlo * TN + 2 * h);
+      }
+      cp_commit();
+      cp_wait<0>();
+      __syncthreads();
+      TSTAMP(6);
+      for (int x = t; x < P * MN; x += THREADS) {  // one (output block, position) per thread
+        const int k = x / P, e = x % P;
+        const int i = rlo + e / TN, j = e % TN;
+        if (i0 + i >= a.pm || j0 + j >= a.pn) continue;
+        const int w0 = wo[k], w1 = wo[k + 1];
+        double s = 0.0;
+        for (int q = w0; q < w1; ++q) {
+          const double v = __dmul_rn(tw[q].coef, smem[tw[q].blk * P + e]);
+          s = q == w0 ? v : __dadd_rn(s, v);
+        }
+        a.C[(long long)((k / a.N) * a.pm + i0 + i) * a.ldc + (long long)(k % a.N) * a.pn + j0 + j] = s;
+      }
+    }
+    __syncthreads();
+    if (t == 0 && atomicAdd(depart, 1u) == (unsigned)(a.R - 1)) {
+      *arrive = 0u;
+      *depart = 0u;
+    }
+#ifdef FMM_SMALL_TIMING
+    if (pos == 0 && r == 0 && t == 0)
+      printf("small coop cta0: start %llu prologue %llu chunk0-ready %llu loop-done %llu arrived %llu staged %llu end %llu\n",
+             tst[0] % 1000000000ull, tst[1] - tst[0], tst[2] - tst[0], tst[4] - tst[0], tst[5] - tst[0], tst[6] - tst[0],
+             gtime() - tst[0]);
+#endif
+    return;
+  }
   if (t == 0) is_last = atomicAdd(&a.cnt[pos], 1u) == (unsigned)(a.R - 1);
   __syncthreads();
+  TSTAMP(5);
+#ifdef FMM_SMALL_TIMING
+  if (blockIdx.x == 0 && t == 0)
+    printf("small cta0: start %llu prologue %llu chunk0-ready %llu chunk0-done %llu loop-done %llu counted %llu\n",
+           tst[0] % 1000000000ull, tst[1] - tst[0], tst[2] - tst[0], tst[3] - tst[0], tst[4] - tst[0], tst[5] - tst[0]);
+#endif
   if (!is_last) return;
   __threadfence();
   // the last CTA of this tile: stage the R product tiles (G positions at a time, every copy in
   // flight at once) and the W terms, then C_k tile = sum_r w_kr M_r tile for every output block k
-  const int MN = a.M * a.N, G = a.g;
-  for (int k = t; k <= MN; k += THREADS) wo[k] = __ldg(&a.w_off[k]);
-  for (int q = t; q < a.nw; q += THREADS) tw[q] = a.w_terms[q];
+  const int G = a.g;
   const unsigned sbase = smem_u32(smem);
   for (int p0 = 0; p0 < TM * TN; p0 += G) {
     for (int e = t; e < a.R * (G / 2); e += THREADS) {
@@ -243,37 +336,58 @@ __global__ void __launch_bounds__(THREADS) small_fmm_kernel(SmallArgs a) {
     cp_commit();
     cp_wait<0>();
     __syncthreads();
+    if (p0 == 0) TSTAMP(6);
+    // each thread's positions of the group side by side (independent chains), terms in r order
+    constexpr int PPT = TM * TN / THREADS;
     for (int k = 0; k < MN; ++k) {
       const int w0 = wo[k], w1 = wo[k + 1];
       const int kr = k / a.N, kc = k % a.N;
       double* crow = a.C + (long long)(kr * a.pm + i0) * a.ldc + (long long)kc * a.pn + j0;
-      for (int e = t; e < G; e += THREADS) {
-        const int i = (p0 + e) >> 5, j = (p0 + e) & 31;
-        double s = 0.0;
-        for (int q = w0; q < w1; ++q) {
-          const double x = __dmul_rn(tw[q].coef, smem[tw[q].blk * G + e]);
-          s = q == w0 ? x : __dadd_rn(s, x);
+      double sacc[PPT];
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) sacc[p] = 0.0;
+      for (int q = w0; q < w1; ++q) {
+        const double cf = tw[q].coef;
+        const double* mq = smem + tw[q].blk * G;
+#pragma unroll
+        for (int p = 0; p < PPT; ++p) {
+          const int e = t + p * THREADS;
+          if (e < G) {
+            const double x = __dmul_rn(cf, mq[e]);
+            sacc[p] = q == w0 ? x : __dadd_rn(sacc[p], x);
+          }
         }
-        if (i0 + i < a.pm && j0 + j < a.pn) crow[(long long)i * a.ldc + j] = s;
+      }
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        const int e = t + p * THREADS;
+        const int i = (p0 + e) >> 5, j = (p0 + e) & 31;
+        if (e < G && i0 + i < a.pm && j0 + j < a.pn) crow[(long long)i * a.ldc + j] = sacc[p];
       }
     }
     __syncthreads();
   }
   if (t == 0) a.cnt[pos] = 0u;  // ready for the next launch (stream ordered)
+#ifdef FMM_SMALL_TIMING
+  if (pos == 0 && t == 0)
+    printf("small last of tile 0 (r %d): start %llu prologue %llu chunk0-ready %llu loop-done %llu counted %llu "
+           "staged %llu end %llu\n", r, tst[0] % 1000000000ull, tst[1] - tst[0], tst[2] - tst[0], tst[4] - tst[0],
+           tst[5] - tst[0], tst[6] - tst[0], gtime() - tst[0]);
+#endif
 }
 }  // namespace
 
 int small_tile() { return TM; }
 
-// chunk depth and assembly group of a launch: the largest k-chunk (a power of two from 4, at most
-// the leaf depth rounded up) whose two staging buffers fit the budget; the largest group of positions
+// chunk depth and assembly group of a launch: the k-chunk (16, 32 or 64: the leaf depth rounded
+// up, at most 64) whose two staging buffers fit the budget; the largest group of positions
 // (a power of two, 256 .. 1024) whose R product values fit
 bool small_config(int max_nu, int max_nv, int pk, int R, int* kc, int* g) {
-  int k = 4;
-  while (k < pk && k < 256) k *= 2;
   // two raw buffers and the formed chunk of S_r and T_r
   auto bytes = [&](int kk) { return 8 * ((2 * max_nu + 1) * TM * (kk + 4) + (2 * max_nv + 1) * kk * (TN + 8)); };
-  while (k > 4 && bytes(k) > SMEM_BUDGET) k /= 2;
+  int k = pk <= 16 ? 16 : pk <= 32 ? 32 : 64;
+  if (const char* e = getenv("FMM_SMALL_KC")) k = std::min(k, std::max(16, atoi(e)));  // diagnostics
+  while (k > 16 && bytes(k) > SMEM_BUDGET) k /= 2;
   if (bytes(k) > SMEM_BUDGET || max_nu > 64 || max_nv > 64) return false;
   int gg = 1024;
   while (gg > 256 && 8 * R * gg > SMEM_BUDGET) gg /= 2;
@@ -283,19 +397,35 @@ bool small_config(int max_nu, int max_nv, int pk, int R, int* kc, int* g) {
   return true;
 }
 
+template <bool CL, int KC, int V>
+static void set_attrs() {
+  FMM_CUDA(cudaFuncSetAttribute(small_fmm_kernel<CL, KC, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BUDGET));
+  if (CL) FMM_CUDA(cudaFuncSetAttribute(small_fmm_kernel<CL, KC, V>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+}
+static void configure_all() {
+  static std::atomic<unsigned long long> configured{0};
+  int dev = 0;
+  FMM_CUDA(cudaGetDevice(&dev));
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (configured.load() & bit) return;
+  set_attrs<false, 16, 1>(), set_attrs<false, 16, 2>(), set_attrs<false, 32, 1>(), set_attrs<false, 32, 2>();
+  set_attrs<false, 64, 1>(), set_attrs<false, 64, 2>();
+  set_attrs<true, 16, 1>(), set_attrs<true, 16, 2>(), set_attrs<true, 32, 1>(), set_attrs<true, 32, 2>();
+  set_attrs<true, 64, 1>(), set_attrs<true, 64, 2>();
+  configured.fetch_or(bit);
+}
+template <bool CL>
+static auto kernel_for(int kc, int v) -> void (*)(SmallArgs) {
+  if (kc == 16) return v == 2 ? small_fmm_kernel<CL, 16, 2> : small_fmm_kernel<CL, 16, 1>;
+  if (kc == 32) return v == 2 ? small_fmm_kernel<CL, 32, 2> : small_fmm_kernel<CL, 32, 1>;
+  return v == 2 ? small_fmm_kernel<CL, 64, 2> : small_fmm_kernel<CL, 64, 1>;
+}
+
 // whether the cluster variant can run a launch of R-CTA clusters (R <= 16, at least one cluster
 // co-resident with this dynamic shared memory)
 bool small_cluster_ok(int R, int smem) {
   if (R > 16 || R < 1) return false;
-  static std::atomic<unsigned long long> configured{0};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return false;
-  const unsigned long long bit = 1ull << (dev & 63);
-  if (!(configured.load() & bit)) {
-    FMM_CUDA(cudaFuncSetAttribute(small_fmm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BUDGET));
-    FMM_CUDA(cudaFuncSetAttribute(small_fmm_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    configured.fetch_or(bit);
-  }
+  configure_all();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)R);
   cfg.blockDim = dim3(THREADS);
@@ -308,42 +438,46 @@ bool small_cluster_ok(int R, int smem) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, small_fmm_kernel<true>, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, small_fmm_kernel<true, 64, 1>, &cfg) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
   return n > 0;
 }
 
+// whether every CTA of a launch of `grid` CTAs with this dynamic shared memory is co-resident
+// (the cooperative assembly waits for the other CTAs of a tile)
+bool small_coop_ok(long long grid, int smem) {
+  configure_all();
+  int per_sm = 0, sms = 0, dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_fmm_kernel<false, 64, 2>, THREADS, (size_t)smem) !=
+          cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return grid <= (long long)per_sm * sms;
+}
+
 void small_launch(const SmallArgs& a, cudaStream_t stream) {
   const long long grid = (long long)a.tiles_m * a.tiles_n * a.R;
   if (grid <= 0) return;
-  if (a.cluster) {  // attributes were set by small_cluster_ok at plan time
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = (size_t)a.smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)a.R;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    FMM_CUDA(cudaLaunchKernelEx(&cfg, small_fmm_kernel<true>, a));
-    return;
-  }
-  static std::atomic<unsigned long long> configured{0};
-  int dev = 0;
-  FMM_CUDA(cudaGetDevice(&dev));
-  const unsigned long long bit = 1ull << (dev & 63);
-  if (!(configured.load() & bit)) {
-    FMM_CUDA(cudaFuncSetAttribute(small_fmm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BUDGET));
-    configured.fetch_or(bit);
-  }
-  small_fmm_kernel<false><<<(unsigned)grid, THREADS, (size_t)a.smem, stream>>>(a);
-  FMM_CUDA(cudaGetLastError());
+  configure_all();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = (size_t)a.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)a.R;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = a.cluster ? 1 : 0;
+  const int v = a.vec2 ? 2 : 1;
+  FMM_CUDA(cudaLaunchKernelEx(&cfg, a.cluster ? kernel_for<true>(a.kc, v) : kernel_for<false>(a.kc, v), a));
 }
 
 }  // namespace fmm

@@ -27,12 +27,13 @@ def dev(x):
     return torch.from_numpy(np.ascontiguousarray(x)).cuda()
 
 
-@pytest.mark.parametrize("cluster", ["1", "0"])
+@pytest.mark.parametrize("variant", ["coop", "last", "cluster"])
 @pytest.mark.parametrize("name", NAMES)
-def test_every_algorithm_exact(name, cluster, monkeypatch):
-    # cluster "1": the cluster variant where R <= 16 (C_k over distributed shared memory), "0" and
-    # R > 16: the last CTA of each tile assembles from the scratch tiles
-    monkeypatch.setenv("FMM_SMALL_CLUSTER", cluster)
+def test_every_algorithm_exact(name, variant, monkeypatch):
+    # the three assemblies: the R CTAs of a tile together (the grid is resident), the last CTA of
+    # each tile, and the cluster variant where R <= 16 (C_k over distributed shared memory)
+    monkeypatch.setenv("FMM_SMALL_CLUSTER", "1" if variant == "cluster" else "0")
+    monkeypatch.setenv("FMM_SMALL_COOP", "1" if variant == "coop" else "0")
     alg = O.load_alg(os.path.join(ALGS, name + ".txt"))
     M, K, N = alg.M, alg.K, alg.N
     # leaves of 37 x 70 x 46: ragged 32 x 32 tiles, two k chunks of 64 (the second ragged)
@@ -48,10 +49,12 @@ def test_every_algorithm_exact(name, cluster, monkeypatch):
     assert np.array_equal(C2.cpu().numpy(), A @ B)
 
 
-@pytest.mark.parametrize("cluster", ["1", "0"])
-@pytest.mark.parametrize("shape", [(256, 256, 256), (2, 2, 2), (66, 130, 98), (500, 8, 300), (64, 2000, 64)])
-def test_uniform_against_oracle(shape, cluster, monkeypatch):
-    monkeypatch.setenv("FMM_SMALL_CLUSTER", cluster)
+@pytest.mark.parametrize("variant", ["coop", "last", "cluster"])
+@pytest.mark.parametrize("shape", [(256, 256, 256), (2, 2, 2), (66, 130, 98), (500, 8, 300), (64, 2000, 64),
+                                   (1024, 64, 1024)])
+def test_uniform_against_oracle(shape, variant, monkeypatch):
+    monkeypatch.setenv("FMM_SMALL_CLUSTER", "1" if variant == "cluster" else "0")
+    monkeypatch.setenv("FMM_SMALL_COOP", "1" if variant == "coop" else "0")
     P, Q, N = shape
     A, B = I.problem(P, Q, N, seed=P + Q + N)
     name = "strassen_222_7"
