@@ -470,12 +470,18 @@ void small_launch(const SmallArgs& a, cudaStream_t stream) {
   cfg.dynamicSmemBytes = (size_t)a.smem;
   cfg.stream = stream;
   cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = (unsigned)a.R;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
+  if (a.cluster) {
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)a.R;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+  } else {  // the cooperative assembly's CTAs wait for each other: a cooperative launch guarantees
+            // that they are all resident (it fails instead of hanging if they cannot be)
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = a.cluster ? 1 : 0;
+  cfg.numAttrs = (a.cluster || a.coop) ? 1 : 0;
   const int v = a.vec2 ? 2 : 1;
   FMM_CUDA(cudaLaunchKernelEx(&cfg, a.cluster ? kernel_for<true>(a.kc, v) : kernel_for<false>(a.kc, v), a));
 }
