@@ -342,8 +342,11 @@ struct fmm_plan_s {
       offT[l].assign(nodes_at[l], -1);
       offM[l].assign(nodes_at[l], -1);
       bool any_unneeded = false;
-      if (collapse && l == L - 1) continue;  // never materialised (sec. 6c)
+      // collapsed formation: S_r, T_r of level L-1 never materialised (sec. 6c); M_r of level L-1
+      // only if its assembly is not collapsed too
+      if (collapse && collapse_asm && l == L - 1) continue;
       const bool noM = collapse_asm && l == L - 1;  // the collapsed assembly never writes M at L-1
+      const bool noST = collapse && l == L - 1;
       for (long long z = 0; z < nodes_at[l]; ++z) {
         const int r = (int)(z % R);
         if (!needed[l][z]) {
@@ -354,8 +357,8 @@ struct fmm_plan_s {
         // collapsed leaves: materialised unless both levels' columns are singletons (then an alias)
         const bool formA = collapse && l == L ? (idxU[r] >= 0 || idxU[r1] >= 0) : idxU[r] >= 0;
         const bool formB = collapse && l == L ? (idxV[r] >= 0 || idxV[r1] >= 0) : idxV[r] >= 0;
-        if (formA) offS[l][z] = take(d.P * ldS[l]);
-        if (formB) offT[l][z] = take(d.Q * ldT[l]);
+        if (formA && !noST) offS[l][z] = take(d.P * ldS[l]);
+        if (formB && !noST) offT[l][z] = take(d.Q * ldT[l]);
         if (!noM) offM[l][z] = take(d.P * ldM[l]);
       }
       if (any_unneeded && !noM) offZero[l] = take(d.P * ldM[l]);
@@ -1326,7 +1329,7 @@ void fmm_plan_s::emit_two_level_formation(bool lazy_kernels) {
     sp.R = R;
     sp.X = side == 0 ? alg->Ud : alg->Vd;
     sp.materialize = mat;
-    sp.vec = aligned ? 2 : 1;
+    sp.vec = aligned && rows <= 4 ? 2 : 1;  // (MK)^2 > 16 inputs: one element per thread (registers)
     Launch ln;
     ln.kind = side == 0 ? Launch::FORM_A : Launch::FORM_B;
     ln.level = L - 1;
@@ -1523,16 +1526,24 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
     const Dims& dl = p->dims[L >= 1 ? L - 1 : 0];
     // (a variant reloading the inputs of larger base cases from L1/L2 was measured 2-40 % slower
     // than one level per launch on c4, c5, c5t: the pass is only worth it with every input in registers)
-    p->collapse = p->opt.collapse_levels && !(e && e[0] == '1') && L >= 2 && p->opt.strategy == FMM_ADD_STREAMING &&
-                  M * K <= 4 && K * Nb <= 4 && M * Nb <= 4 && dl.P1 == dl.P && dl.Q1 == dl.Q && dl.N1 == dl.N;
+    const bool can = p->opt.collapse_levels && !(e && e[0] == '1') && L >= 2 && p->opt.strategy == FMM_ADD_STREAMING &&
+                     dl.P1 == dl.P && dl.Q1 == dl.Q && dl.N1 == dl.N;
+    p->collapse = can && M * K <= 4 && K * Nb <= 4 && M * Nb <= 4;
     if (p->collapse && p->fuse_bg && p->fuse) p->collapse = false;  // the background mode hides the level
     if (p->collapse) p->fuse = false;
     p->collapse_asm = p->collapse;
+    // the formation alone for base cases with up to 9 x 9 inputs per position (MK, KN <= 9: c4, c5):
+    // one thread keeps the (MK)^2 inputs of a position in registers (one element, not two); the
+    // (MN)^2 outputs of the assembly do not fit, so it stays one level per launch.  Measured
+    // (sec. 6c): c5 -0.4 %, but c4's B side runs at 2.4 TB/s (A side 5.3), so c4 loses 2 %: only on
+    // request (FMM_COLLAPSE_FORM=1)
+    const char* cf = getenv("FMM_COLLAPSE_FORM");
+    if (!p->collapse && can && !p->fuse && M * K <= 9 && K * Nb <= 9 && cf && cf[0] == '1') p->collapse = true;
     // the assembly alone for larger base cases (MN <= 16): the wide warp-per-column kernel (sec. 6g).
     // It halves the assembly's HBM bytes but runs shared-memory bound at about half the HBM rate, so
     // it measured slower than the two separate levels on c4 and c5t: only on request (FMM_WIDE_ASM=1)
     const char* w = getenv("FMM_WIDE_ASM");
-    if (!p->collapse && w && w[0] == '1' && p->opt.collapse_levels && !(e && e[0] == '1') && !p->fuse && L >= 2 &&
+    if (!p->collapse_asm && w && w[0] == '1' && p->opt.collapse_levels && !(e && e[0] == '1') && !p->fuse && L >= 2 &&
         p->opt.strategy == FMM_ADD_STREAMING && M * Nb <= 16 && dl.P1 == dl.P && dl.Q1 == dl.Q && dl.N1 == dl.N)
       p->collapse_asm = true;
   }
@@ -2160,9 +2171,11 @@ double predict_dims(const fmm_alg& a, const std::vector<PlanDims>& dims) {
   // collapsed last two levels (collapse_levels, as plan_init decides it)
   const bool nopeel = L >= 2 && dims[L - 1].P1 == dims[L - 1].P && dims[L - 1].Q1 == dims[L - 1].Q &&
                       dims[L - 1].N1 == dims[L - 1].N;
-  const bool collapse = nopeel && M * K <= 4 && K * Nb <= 4 && M * Nb <= 4;
+  const bool small_case = nopeel && M * K <= 4 && K * Nb <= 4 && M * Nb <= 4;
+  const char* cf = getenv("FMM_COLLAPSE_FORM");
+  const bool collapse = small_case || (nopeel && M * K <= 9 && K * Nb <= 9 && cf && cf[0] == '1');
   const char* wide = getenv("FMM_WIDE_ASM");  // the wide two-level assembly (sec. 6g), on request only
-  const bool collapse_asm = collapse || (nopeel && M * Nb <= 16 && wide && wide[0] == '1');
+  const bool collapse_asm = small_case || (nopeel && M * Nb <= 16 && wide && wide[0] == '1');
   auto materialized = [&](const std::vector<double>& X, int rows) {
     std::vector<int> sing(R);
     for (int r = 0; r < R; ++r) {
@@ -2188,9 +2201,9 @@ double predict_dims(const fmm_alg& a, const std::vector<PlanDims>& dims) {
       bytes = 8.0 * nodes *
               ((double)(M * K * M * K + materialized(a.Ud, M * K)) * c2.P * c2.Q +
                (double)(K * Nb * K * Nb + materialized(a.Vd, K * Nb)) * c2.Q * c2.N +
-               (double)(R * R + M * Nb * M * Nb) * c2.P * c2.N);
+               (collapse_asm ? (double)(R * R + M * Nb * M * Nb) * c2.P * c2.N : (double)(R + M * Nb) * c.P * c.N));
     } else if (collapse && l == L) {
-      bytes = 0;
+      bytes = collapse_asm ? 0 : 8.0 * nodes * (double)(R + M * Nb) * c.P * c.N;  // its assembly only
     } else if (collapse_asm && l == L - 1) {  // its formation as usual; both levels' assembly at once
       const D& c2 = dims[L];
       bytes = 8.0 * nodes *
@@ -2199,7 +2212,7 @@ double predict_dims(const fmm_alg& a, const std::vector<PlanDims>& dims) {
     } else if (collapse_asm && l == L) {  // its formation only
       bytes = 8.0 * nodes * ((double)(M * K + fu) * c.P * c.Q * (fu > 0) + (double)(K * Nb + fv) * c.Q * c.N * (fv > 0));
     }
-    t += bytes / cm.add_bw + (collapse && l == L ? 0.0 : cm.launch * (1 + (fu > 0) + (fv > 0)));
+    t += bytes / cm.add_bw + (collapse && l == L ? (collapse_asm ? 0.0 : cm.launch) : cm.launch * (1 + (fu > 0) + (fv > 0)));
     // peel strips of the level-(l-1) nodes
     t += gemm_time(nodes, pd.P1, pd.N1, pd.Q - pd.Q1, cm);
     t += gemm_time(nodes, pd.P - pd.P1, pd.N, pd.Q, cm);

@@ -81,14 +81,53 @@ def test_not_collapsed_where_it_does_not_apply():
     Ca, sa = _run(F, "strassen_222_7", A, B, 2, collapse=True)
     Cb, sb = _run(F, "strassen_222_7", A, B, 2, collapse=False)
     assert sa["launches"] == sb["launches"] and np.array_equal(Ca, A @ B) and np.array_equal(Cb, A @ B)
-    A, B = I.problem(540, 360, 540, seed=5, kind="integers")  # <3,2,3>: base case too large (the
-    Ca, sa = _run(F, "hk_class_323_15", A, B, 2, collapse=True)  # wide assembly only on request)
-    _, sb = _run(F, "hk_class_323_15", A, B, 2, collapse=False)
+    A, B = I.problem(540, 360, 540, seed=5, kind="integers")  # <3,2,3>: base case too large (the wide
+    Ca, sa = _run(F, "hk_class_323_15", A, B, 2, collapse=True)  # assembly and the formation alone only on
+    _, sb = _run(F, "hk_class_323_15", A, B, 2, collapse=False)  # request)
     assert sa["collapsed"] == 0 and sa["collapsed_assembly"] == 0 and sa["launches"] == sb["launches"]
     assert np.array_equal(Ca, A @ B)
+    A, B = I.problem(720, 360, 540, seed=5, kind="integers")  # <4,3,3>: MK = 12 inputs per row: no collapse
+    Ca, sa = _run(F, "alg_433_29", A, B, 2, collapse=True)  # even on request
+    assert sa["collapsed"] == 0 and np.array_equal(Ca, A @ B)
     A, B = I.problem(256, 256, 256, seed=6, kind="integers")  # write-once strategy
     Ca, sa = _run(F, "strassen_222_7", A, B, 2, strategy="write_once")
     assert np.array_equal(Ca, A @ B)
+
+
+# The formation alone for base cases with MK, KN <= 9 (the assembly stays one level per launch):
+# (MK)^2 inputs of a position held in one thread's registers
+FORM_CASES = [("alg_424_26", 320, 64, 320, "row"), ("hk_class_323_15", 540, 360, 540, "col"),
+              ("laderman_class_333_23", 450, 252, 360, "row"), ("direct_223_11", 200, 120, 180, "row")]
+
+
+@pytest.mark.parametrize("name,P,Q,N,layout", FORM_CASES)
+def test_collapsed_formation_equals_separate_and_oracle(name, P, Q, N, layout, monkeypatch):
+    monkeypatch.setenv("FMM_COLLAPSE_FORM", "1")  # on request only
+    F = _lib()
+    A, B = I.problem(P, Q, N, seed=P + Q)
+    Cc, sc = _run(F, name, A, B, 2, layout, cse=False, collapse=True)
+    Cs, ss = _run(F, name, A, B, 2, layout, cse=False, collapse=False)
+    assert sc["collapsed"] == 1 and sc["collapsed_assembly"] == 0
+    assert sc["formation_bytes"] < ss["formation_bytes"] and sc["assembly_bytes"] == ss["assembly_bytes"]
+    assert np.array_equal(Cc, Cs)  # the oracle's two levels in its order
+    nrm = np.linalg.norm(A) * np.linalg.norm(B)
+    assert np.max(np.abs(Cc - O.fast(A, B, O.load_alg(F.alg_path(name)), 2))) <= 1e-12 * nrm
+    Ai, Bi = I.problem(P, Q, N, seed=3, kind="integers")
+    Ci, _ = _run(F, name, Ai, Bi, 2, layout)
+    assert np.array_equal(Ci, Ai @ Bi)
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_collapsed_formation_shards_sum_to_product(G, monkeypatch):
+    monkeypatch.setenv("FMM_COLLAPSE_FORM", "1")
+    F = _lib()
+    A, B = I.problem(320, 64, 320, seed=8, kind="integers")
+    total = np.zeros((320, 320))
+    for g in range(G):
+        C, st = _run(F, "alg_424_26", A, B, 2, shard_rank=g, shard_count=G)
+        assert st["collapsed"] == 1
+        total += C
+    assert np.array_equal(total, A @ B)
 
 
 @pytest.mark.parametrize("layout", ["row", "col"])
