@@ -155,7 +155,7 @@ int small_tile();  // the tile edge (32)
 bool small_config(int max_nu, int max_nv, int pk, int R, int* kc, int* g);
 void small_launch(const SmallArgs& a, cudaStream_t stream);
 bool small_cluster_ok(int R, int smem);  // the cluster variant fits (R <= 16, co-resident)
-bool small_coop_ok(long long grid, int smem);  // every CTA of the launch is co-resident
+bool small_coop_ok(long long grid, int smem, int kc, int vec2);  // every CTA of the launch is co-resident
 // TMA kernel configuration: consumer warp grid of a tile width, SM count, dynamic shared memory.
 void gemm_bn_config(int bn, int* wgm, int* wgn);
 int gemm_sm_count();

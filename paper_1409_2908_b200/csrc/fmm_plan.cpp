@@ -532,7 +532,7 @@ void fmm_plan_s::emit_small() {
   sa.cluster = cl && cl[0] == '1' && R >= M * Nb && small_cluster_ok(R, sa.smem);
   sa.prefetch = !(getenv("FMM_SMALL_PREFETCH") && getenv("FMM_SMALL_PREFETCH")[0] == '0');
   // the R CTAs of a tile assemble it together when the whole grid is resident (else the last one)
-  sa.coop = !sa.cluster && small_coop_ok((long long)sa.tiles_m * sa.tiles_n * R, sa.smem) && !(getenv("FMM_SMALL_COOP") && getenv("FMM_SMALL_COOP")[0] == '0');
+  sa.coop = !sa.cluster && small_coop_ok((long long)sa.tiles_m * sa.tiles_n * R, sa.smem, sa.kc, sa.vec2) && !(getenv("FMM_SMALL_COOP") && getenv("FMM_SMALL_COOP")[0] == '0');
   ln.count = R;
   ln.tiles = (long long)sa.tiles_m * sa.tiles_n * R;
   // work: the leaf products, the formation reads / adds and the assembly (as the separate kernels)

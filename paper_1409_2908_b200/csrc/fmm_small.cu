@@ -447,11 +447,11 @@ bool small_cluster_ok(int R, int smem) {
 
 // whether every CTA of a launch of `grid` CTAs with this dynamic shared memory is co-resident
 // (the cooperative assembly waits for the other CTAs of a tile)
-bool small_coop_ok(long long grid, int smem) {
+bool small_coop_ok(long long grid, int smem, int kc, int vec2) {
   configure_all();
   int per_sm = 0, sms = 0, dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_fmm_kernel<false, 64, 2>, THREADS, (size_t)smem) !=
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel_for<false>(kc, vec2 ? 2 : 1), THREADS, (size_t)smem) !=
           cudaSuccess ||
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
     cudaGetLastError();
