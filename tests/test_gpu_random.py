@@ -1,5 +1,6 @@
-"""Randomised GPU parity: random algorithm, shape (ragged at any level), levels, layout and plan
-options (strategy, CSE, collapsed levels, fused leaf level, shards) on integer inputs, where every
+"""Randomised GPU parity: random algorithm, shape (ragged at any level, or exact multiples of the
+base case), levels, layout and plan options (strategy, CSE, collapsed levels, fused leaf level, the
+one-launch small path, shards) on integer inputs, where every
 schedule must reproduce A*B exactly (three executes per plan: plain, graph capture, graph replay);
 and on uniform inputs against the oracle's tolerance.
 Seeded (derandomized) so failures reproduce."""
@@ -44,7 +45,18 @@ cases = st.fixed_dictionaries({
     "cse": st.booleans(), "collapse": st.booleans(), "fuse": st.booleans(), "peel_align": st.booleans(),
     "G": st.sampled_from([1, 1, 2, 3]), "mode": st.sampled_from(["leaf", "top"]),
     "seed": st.integers(0, 2 ** 16),
+    # exact: P, Q, N rounded to multiples of the base case (where the one-launch small path applies
+    # at L = 1); small: the small_fused option
+    "exact": st.booleans(), "small": st.booleans(),
 })
+
+
+def _shape(F, c):
+    P, Q, N = c["P"], c["Q"], c["N"]
+    if c["exact"]:
+        a = F.load_alg(c["name"])
+        P, Q, N = max(a.M, P // a.M * a.M), max(a.K, Q // a.K * a.K), max(a.N, N // a.N * a.N)
+    return P, Q, N
 
 
 N_INT = int(os.environ.get("FMM_RANDOM_EXAMPLES", "60"))
@@ -56,12 +68,13 @@ DERAND = os.environ.get("FMM_RANDOM_SEED") is None
 def test_random_plans_integer_exact(c):
     import torch
     F = _lib()
-    A, B = I.problem(c["P"], c["Q"], c["N"], seed=c["seed"], kind="integers")
-    total = np.zeros((c["P"], c["N"]))
+    P, Q, N = _shape(F, c)
+    A, B = I.problem(P, Q, N, seed=c["seed"], kind="integers")
+    total = np.zeros((P, N))
     for g in range(c["G"]):
-        p = F.Plan(F.load_alg(c["name"]), c["P"], c["Q"], c["N"], c["L"], layout=c["layout"], strategy=c["strategy"],
+        p = F.Plan(F.load_alg(c["name"]), P, Q, N, c["L"], layout=c["layout"], strategy=c["strategy"],
                    cse=c["cse"], collapse=c["collapse"], fuse=c["fuse"], peel_align=c["peel_align"], shard_rank=g,
-                   shard_count=c["G"], shard_mode=c["mode"])
+                   shard_count=c["G"], shard_mode=c["mode"], small=c["small"])
         Ad, Bd = _dev(A, c["layout"]), _dev(B, c["layout"])
         C = p.new_output()
         for _ in range(3):  # plain launches, then the CUDA-graph capture, then a replay
@@ -77,9 +90,10 @@ def test_random_plans_integer_exact(c):
 def test_random_plans_float_parity(c):
     import torch
     F = _lib()
-    A, B = I.problem(c["P"], c["Q"], c["N"], seed=c["seed"])
-    p = F.Plan(F.load_alg(c["name"]), c["P"], c["Q"], c["N"], c["L"], layout=c["layout"], strategy=c["strategy"],
-               cse=c["cse"], collapse=c["collapse"], fuse=c["fuse"], peel_align=c["peel_align"])
+    P, Q, N = _shape(F, c)
+    A, B = I.problem(P, Q, N, seed=c["seed"])
+    p = F.Plan(F.load_alg(c["name"]), P, Q, N, c["L"], layout=c["layout"], strategy=c["strategy"],
+               cse=c["cse"], collapse=c["collapse"], fuse=c["fuse"], peel_align=c["peel_align"], small=c["small"])
     C = p.execute(_dev(A, c["layout"]), _dev(B, c["layout"])).cpu().numpy()
     torch.cuda.synchronize()
     nrm = np.linalg.norm(A) * np.linalg.norm(B)
