@@ -170,7 +170,8 @@ void gemm_uniform_grid(const std::vector<GemmTask>& tasks, int* tm, int* tn);
 // the task table; row tasks have m <= limit, column tasks n <= limit.
 int skinny_limit();
 void skinny_launch(const GemmTask* d_tasks, const int* d_row_ids, int nrow, int max_n, const int* d_col_ids, int ncol,
-                   int max_m, cudaStream_t stream);
+                   int max_m, cudaStream_t stream, int thin_r = 8, int thin_c = 8);  // thin_r / thin_c: the
+                   // largest row-strip height / column-strip width of the launch
 // Pick the TMA kernel's tile width (128 rows x bn columns) for a task list from a cost model of
 // padded work, measured per-width efficiency and wave quantisation; FMM_GEMM_BN overrides.
 int gemm_choose_bn(const std::vector<GemmTask>& tasks);

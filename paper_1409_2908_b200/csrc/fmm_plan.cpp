@@ -64,6 +64,7 @@ struct Launch {
   int uni_tm = 0, uni_tn = 0;  // GEMM launches: common tile grid of all tasks (0 = mixed)
   size_t ids_off = 0;        // SKINNY: int ids (row tasks then column tasks)
   int nrow = 0, ncol = 0, max_n = 0, max_m = 0;
+  int thin_r = 0, thin_c = 0;  // SKINNY: largest row-strip height / column-strip width
   size_t maps_off = 0;       // byte offset of the tensor maps (2 per task)
   double elem_reads = 0, elem_writes = 0, elem_adds = 0;  // totals over the launch (elements)
   double flops = 0, gemm_bytes = 0;
@@ -613,8 +614,8 @@ void fmm_plan_s::build(const double* A, long long lda, const double* B, long lon
       std::vector<int> rows, cols;
       for (int q = 0; q < (int)thin.size(); ++q) {
         const auto& t = thin[q];
-        if (t.m <= skinny_limit()) rows.push_back(q), ln.max_n = std::max(ln.max_n, t.n);
-        else cols.push_back(q), ln.max_m = std::max(ln.max_m, t.m);
+        if (t.m <= skinny_limit()) rows.push_back(q), ln.max_n = std::max(ln.max_n, t.n), ln.thin_r = std::max(ln.thin_r, t.m);
+        else cols.push_back(q), ln.max_m = std::max(ln.max_m, t.m), ln.thin_c = std::max(ln.thin_c, t.n);
         ln.flops += 2.0 * t.m * t.n * (double)t.k;
         ln.gemm_bytes += 8.0 * ((double)t.m * t.k + (double)t.k * t.n + (1.0 + (t.beta != 0.0)) * t.m * t.n);
       }
@@ -1815,7 +1816,7 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
         phase = ph;
       }
       skinny_launch(reinterpret_cast<const GemmTask*>(d_tab + ln.table_off), ids, ln.nrow, ln.max_n, ids + ln.nrow,
-                    ln.ncol, ln.max_m, ls);
+                    ln.ncol, ln.max_m, ls, ln.thin_r, ln.thin_c);
       mark(prof_phase, (int)ln.kind, ln.level);
       continue;
     }

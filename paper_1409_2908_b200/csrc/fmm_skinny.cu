@@ -22,21 +22,25 @@ constexpr int THIN = 8;  // strips are < 2 x (base-case dim) wide
 
 // 32 columns x 8 k-slices per block: each thread sums k = ks, ks+8, ... for its column and all
 // m rows (independent loads in flight across slices), then the slices are reduced in smem.
+// TH: the launch's largest strip height rounded up to a power of two (1, 2, 4 or 8): the
+// accumulators of rows that cannot occur take no registers, so thin strips run at a higher
+// occupancy with more loads in flight
+template <int TH>
 __global__ void __launch_bounds__(256) skinny_rows(const GemmTask* __restrict__ tasks, const int* __restrict__ ids,
                                                    int count) {
-  __shared__ double red[8][THIN][33];
+  __shared__ double red[8][TH][33];
   const GemmTask t = tasks[ids[blockIdx.y]];
   const int tx = threadIdx.x & 31, ks = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + tx;
-  double acc[THIN];
+  double acc[TH];
 #pragma unroll
-  for (int i = 0; i < THIN; ++i) acc[i] = 0.0;
+  for (int i = 0; i < TH; ++i) acc[i] = 0.0;
   if (j < t.n) {
     int k = ks;
 #ifndef FMM_SKINNY_ROW_UNROLL
 #define FMM_SKINNY_ROW_UNROLL 8  // measured on c3: 4 -> 8 in flight, strips 0.372 -> 0.349 ms
 #endif
-    constexpr int U = FMM_SKINNY_ROW_UNROLL;
+    constexpr int U = TH <= 2 ? 2 * FMM_SKINNY_ROW_UNROLL : FMM_SKINNY_ROW_UNROLL;
     for (; k + 8 * (U - 1) < t.k; k += 8 * U) {  // U independent B loads in flight per thread
       double b[U];
 #pragma unroll
@@ -44,25 +48,25 @@ __global__ void __launch_bounds__(256) skinny_rows(const GemmTask* __restrict__ 
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int i = 0; i < THIN; ++i)
+        for (int i = 0; i < TH; ++i)
           if (i < t.m) acc[i] = fma(__ldg(t.A + (long long)i * t.lda + k + 8 * u), b[u], acc[i]);
     }
     for (; k < t.k; k += 8) {
       const double b = __ldg(t.B + (long long)k * t.ldb + j);
 #pragma unroll
-      for (int i = 0; i < THIN; ++i)
+      for (int i = 0; i < TH; ++i)
         if (i < t.m) acc[i] = fma(__ldg(t.A + (long long)i * t.lda + k), b, acc[i]);
     }
   }
 #pragma unroll
-  for (int i = 0; i < THIN; ++i) red[ks][i][tx] = acc[i];
+  for (int i = 0; i < TH; ++i) red[ks][i][tx] = acc[i];
   __syncthreads();
   // thread (ks, tx) finalises row i = ks of column j
   if (j < t.n) {
 #pragma unroll
     for (int h = 0; h < 1; ++h) {
       const int i = ks + 8 * h;
-      if (i < t.m) {
+      if (i < t.m && i < TH) {
         double v = 0.0;
 #pragma unroll
         for (int q = 0; q < 8; ++q) v += red[q][i][tx];
@@ -83,19 +87,23 @@ __global__ void __launch_bounds__(256) skinny_rows(const GemmTask* __restrict__ 
 #ifndef FMM_SKINNY_KC
 #define FMM_SKINNY_KC 256
 #endif
-constexpr int KC = FMM_SKINNY_KC, ROWS_PER_WARP = FMM_SKINNY_RPW;
+constexpr int ROWS_PER_WARP = FMM_SKINNY_RPW;
+template <int TH>
 __global__ void __launch_bounds__(256) skinny_cols(const GemmTask* __restrict__ tasks, const int* __restrict__ ids,
                                                    int count) {
-  __shared__ double bt[THIN][KC];
+  // k-chunk of the staged B strip: 16 KB of shared memory whatever the strip width (narrow strips
+  // take their whole k in one chunk: one round trip for the strip instead of one per 256 k)
+  constexpr int KC = (FMM_SKINNY_KC * 8) / TH;
+  __shared__ double bt[TH][KC];
   const GemmTask t = tasks[ids[blockIdx.y]];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int row0 = (blockIdx.x * 8 + warp) * ROWS_PER_WARP;
   const bool v2 = ((reinterpret_cast<uintptr_t>(t.A) & 15) == 0) && ((t.lda & 1) == 0);
-  double acc[ROWS_PER_WARP][THIN];
+  double acc[ROWS_PER_WARP][TH];
 #pragma unroll
   for (int q = 0; q < ROWS_PER_WARP; ++q)
 #pragma unroll
-    for (int j = 0; j < THIN; ++j) acc[q][j] = 0.0;
+    for (int j = 0; j < TH; ++j) acc[q][j] = 0.0;
   for (int k0 = 0; k0 < t.k; k0 += KC) {
     const int kc = min(KC, t.k - k0);
     __syncthreads();
@@ -125,7 +133,7 @@ __global__ void __launch_bounds__(256) skinny_cols(const GemmTask* __restrict__ 
           if (kk >= kc) continue;
           const bool second = kk + 1 < kc;
 #pragma unroll
-          for (int j = 0; j < THIN; ++j)
+          for (int j = 0; j < TH; ++j)
             if (j < t.n) {
               const double b0 = bt[j][kk], b1 = second ? bt[j][kk + 1] : 0.0;
 #pragma unroll
@@ -147,7 +155,7 @@ __global__ void __launch_bounds__(256) skinny_cols(const GemmTask* __restrict__ 
           for (int u = 0; u < 4; ++u)
             if (kk + 32 * u < kc)
 #pragma unroll
-              for (int j = 0; j < THIN; ++j)
+              for (int j = 0; j < TH; ++j)
                 if (j < t.n) acc[q][j] = fma(a[u], bt[j][kk + 32 * u], acc[q][j]);
         }
       }
@@ -157,16 +165,16 @@ __global__ void __launch_bounds__(256) skinny_cols(const GemmTask* __restrict__ 
   for (int q = 0; q < ROWS_PER_WARP; ++q) {
     const int i = row0 + q;
 #pragma unroll
-    for (int j = 0; j < THIN; ++j) {
+    for (int j = 0; j < TH; ++j) {
       double v = acc[q][j];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       acc[q][j] = v;
     }
-    if (i < t.m && lane < t.n) {
+    if (i < t.m && lane < t.n && lane < TH) {
       double v = 0.0;
 #pragma unroll
-      for (int j = 0; j < THIN; ++j)
+      for (int j = 0; j < TH; ++j)
         if (j == lane) v = acc[q][j];
       double* c = t.C + (long long)i * t.ldc + lane;
       *c = t.beta != 0.0 ? fma(t.beta, *c, t.alpha * v) : t.alpha * v;
@@ -177,16 +185,28 @@ __global__ void __launch_bounds__(256) skinny_cols(const GemmTask* __restrict__ 
 
 int skinny_limit() { return THIN; }
 
+static int pow2_at_least(int x) { return x <= 1 ? 1 : x <= 2 ? 2 : x <= 4 ? 4 : 8; }
+
 void skinny_launch(const GemmTask* d_tasks, const int* d_row_ids, int nrow, int max_n, const int* d_col_ids, int ncol,
-                   int max_m, cudaStream_t stream) {
+                   int max_m, cudaStream_t stream, int thin_r, int thin_c) {
   if (nrow > 0 && max_n > 0) {
     dim3 grid((unsigned)((max_n + 31) / 32), (unsigned)nrow);
-    skinny_rows<<<grid, 256, 0, stream>>>(d_tasks, d_row_ids, nrow);
+    switch (pow2_at_least(thin_r)) {
+      case 1: skinny_rows<1><<<grid, 256, 0, stream>>>(d_tasks, d_row_ids, nrow); break;
+      case 2: skinny_rows<2><<<grid, 256, 0, stream>>>(d_tasks, d_row_ids, nrow); break;
+      case 4: skinny_rows<4><<<grid, 256, 0, stream>>>(d_tasks, d_row_ids, nrow); break;
+      default: skinny_rows<8><<<grid, 256, 0, stream>>>(d_tasks, d_row_ids, nrow); break;
+    }
     FMM_CUDA(cudaGetLastError());
   }
   if (ncol > 0 && max_m > 0) {
     dim3 grid((unsigned)((max_m + 8 * ROWS_PER_WARP - 1) / (8 * ROWS_PER_WARP)), (unsigned)ncol);
-    skinny_cols<<<grid, 256, 0, stream>>>(d_tasks, d_col_ids, ncol);
+    switch (pow2_at_least(thin_c)) {
+      case 1: skinny_cols<1><<<grid, 256, 0, stream>>>(d_tasks, d_col_ids, ncol); break;
+      case 2: skinny_cols<2><<<grid, 256, 0, stream>>>(d_tasks, d_col_ids, ncol); break;
+      case 4: skinny_cols<4><<<grid, 256, 0, stream>>>(d_tasks, d_col_ids, ncol); break;
+      default: skinny_cols<8><<<grid, 256, 0, stream>>>(d_tasks, d_col_ids, ncol); break;
+    }
     FMM_CUDA(cudaGetLastError());
   }
 }
