@@ -97,7 +97,10 @@ constexpr int K3F_STAGES = 64 / BK;
 __host__ __device__ constexpr int k3f_smem_bytes(int bn) {
   return K3F_STAGES * (A_BYTES + BK * bn * 8) + 1024 /*align*/ + 1024 /*barriers, aligned*/ + 2 * BM * bn * 8;
 }
-constexpr int GROUP_M = 8;
+#ifndef FMM_GROUP_M
+#define FMM_GROUP_M 8  // row tiles per raster group (tiles of a group run column by column)
+#endif
+constexpr int GROUP_M = FMM_GROUP_M;
 // FMM_FUSED_BG (fused kernel only): every CTA runs leaf tiles and the producer warpgroup's warps
 // 1-3 run the addition jobs beside them (no addition CTAs)
 #ifndef FMM_FUSED_BG
