@@ -193,10 +193,12 @@ def main():
                     help="N > 1: leaf-level HYBRID sharding or the top-level products in contiguous ranges (partial "
                          "C per rank, combined); or slab: each rank runs the whole method on its slab of C's rows "
                          "(columns when column-major), nothing to combine")
-    ap.add_argument("--combine", default="auto", choices=["auto", "lib", "p2p", "torch"],
+    ap.add_argument("--combine", default="auto", choices=["auto", "lib", "p2p", "p2p_push", "torch"],
                     help="N > 1: the partial-C combine.  lib: NCCL inside fmm_execute (fmm_plan_create_dist, "
                          "row chunks overlapped with the assembly); p2p: the peer-memory pull-reduce inside "
-                         "fmm_execute (fmm_plan_create_p2p); torch: torch.distributed.reduce after fmm_execute.  "
+                         "fmm_execute (fmm_plan_create_p2p); p2p_push: the kernels that write C store each "
+                         "rank's partial into the root's buffer over peer memory, the root sums (root output); "
+                         "torch: torch.distributed.reduce after fmm_execute.  "
                          "auto = lib with --dist-backend nccl, p2p with gloo")
     ap.add_argument("--output", default="root", choices=["root", "slabs"],
                     help="N > 1: C summed onto rank 0, or slab-distributed (slab g of C summed onto rank g)")
@@ -298,7 +300,10 @@ class Run:
         # peer-memory pull-reduce over CUDA IPC (p2p, fmm_plan_create_p2p) -- or after it (torch)
         combined = world > 1 and not self.slab
         self.lib_comm = F.Comm.from_torch_distributed(device=device.index) if (combined and args.combine == "lib") else None
-        self.p2p = F.P2P.from_torch_distributed(8 * P * N, device=device.index) if (combined and args.combine == "p2p") else None
+        push = args.combine == "p2p_push" and args.output != "slabs"
+        p2p_bytes = 8 * ((P * N + 1) // 2 * 2) * (world if push else 1)  # push: G partial slots on the root
+        self.p2p = (F.P2P.from_torch_distributed(p2p_bytes, device=device.index)
+                    if (combined and args.combine in ("p2p", "p2p_push")) else None)
         if self.slab:  # the whole method on this rank's slab: an ordinary single-GPU plan
             self.plan = F.Plan(self.alg, self.Pp, Q, self.Np, L, layout=w["layout"], strategy=args.strategy,
                                cse=bool(args.cse), fuse=bool(args.fuse), collapse=bool(args.collapse))
@@ -306,7 +311,8 @@ class Run:
             self.plan = F.Plan(self.alg, P, Q, N, L, layout=w["layout"], strategy=args.strategy, cse=bool(args.cse),
                                shard_rank=rank, shard_count=world, fuse=bool(args.fuse), collapse=bool(args.collapse),
                                comm=self.lib_comm, p2p=self.p2p, barrier=(self.dist.barrier if self.p2p else None),
-                               root="slabs" if args.output == "slabs" else 0, shard_mode=args.shard_mode)
+                               root="slabs" if args.output == "slabs" else 0, shard_mode=args.shard_mode,
+                               p2p_push=push if self.p2p else None)
         self.outer, self.inner = (P, N) if w["layout"] == "row" else (N, P)
         self.C = self.plan.new_output()
         self.st = self.plan.stats()
@@ -645,6 +651,7 @@ class Run:
         ms_e = self.max_over_ranks((time.perf_counter() - h0) * 1e3)
         combine_name = ("no combine: every rank multiplies its slab" if self.slab else
                         {"p2p": "peer-memory combine inside fmm_execute", "lib": "NCCL reduce inside fmm_execute",
+                         "p2p_push": "peer-memory combine inside fmm_execute (partials pushed by the kernels)",
                          "torch": "torch.distributed reduce"}[self.args.combine])
         return {"value": self.flops / (ms_e / n_e2e * 1e-3) / 1e9, "unit": "GFLOPS", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": ms_e / n_e2e, "steps": n_e2e,
@@ -959,9 +966,13 @@ class Run:
             elif self.slab:
                 parallelism = (f"slabs x{world}: every rank runs the whole method on its slab of C's "
                                f"{'rows' if w['layout'] == 'row' else 'columns'}; no partial products, no combine")
-            elif args.combine == "p2p":
+            elif args.combine == "p2p" or (args.combine == "p2p_push" and args.output == "slabs"):
                 parallelism = (f"{args.shard_mode}-level shards x{world} + peer-memory combine inside fmm_execute "
                                f"(fmm_plan_create_p2p: one pull-reduce kernel per rank over CUDA IPC), {where}")
+            elif args.combine == "p2p_push":
+                parallelism = (f"{args.shard_mode}-level shards x{world} + peer-memory combine inside fmm_execute "
+                               "(fmm_plan_create_p2p, p2p_push: the kernels that write C store each rank's partial "
+                               "into rank 0's slots over CUDA IPC; rank 0 sums them), reduce to rank 0")
             elif args.combine == "lib":
                 parallelism = (f"{args.shard_mode}-level shards x{world} + NCCL {where} inside fmm_execute "
                                "(fmm_plan_create_dist; C reduced in row chunks that overlap the assembly where the plan allows)")
@@ -981,7 +992,8 @@ class Run:
                 "roofline": roofline,
                 "clocks": self.clk,
                 "e2e": e2e,
-                "gpu_launches": (int(st["launches"]) + (1 if args.combine == "p2p" and world > 1 else 0)) * args.steps,
+                "gpu_launches": (int(st["launches"]) + (1 if args.combine in ("p2p", "p2p_push") and world > 1 else 0))
+                * args.steps,
                 "cpu_baseline": cpu,
                 "phases_ms": {"formation_levels_below_L" if self.fused else "formation": self.form_ms,
                               "fused_leaf_level" if self.fused else "leaf_gemm": self.gemm_ms,

@@ -151,11 +151,21 @@ typedef struct {
                                in ascending r.  Below the paper's cutoff
                                (Sec. 3.4) the separate launches cost more than the
                                arithmetic.  0: the separate launches. */
+  int p2p_push;             /* peer-memory plans (fmm_plan_create_p2p) with a root rank: 1 = the
+                               launches that write C (the top-level assembly, the top-level peel
+                               strips) store this rank's partial straight into slot `rank` of the
+                               root's fmm_p2p buffer over peer memory (NVLink stores), so the
+                               transfer overlaps the assembly tile by tile; after a host barrier
+                               the root sums its G slots in rank order into C.  Every rank's
+                               buffer must then hold G partials (G x C, each slot rounded up to
+                               16 bytes).  0 (default): each rank writes its partial locally and the
+                               root pulls them (the fmm_p2p_reduce kernel).  Slab output always
+                               pulls. */
 } fmm_plan_options;
 
 /* Fill *opt with the defaults: row-major, streaming, cse = 1, shard 0 of 1, no limit,
    peel_align = 1, fuse_leaf_level = 0, collapse_levels = 1, cuda_graphs = 1, peel_tiles = 0,
-   dist_chunks = 4, fuse_output = 0, small_fused = 1. */
+   dist_chunks = 4, fuse_output = 0, small_fused = 1, p2p_push = 0. */
 void fmm_plan_options_default(fmm_plan_options* opt);
 
 /* ---- algorithms ------------------------------------------------------------------------- */

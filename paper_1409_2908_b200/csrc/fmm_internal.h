@@ -81,7 +81,12 @@ int p2p_nranks(const fmm_p2p* p);
 int p2p_rank(const fmm_p2p* p);
 int p2p_device(const fmm_p2p* p);
 double* p2p_local(const fmm_p2p* p);
+double* p2p_peer(const fmm_p2p* p, int g);  // rank g's buffer as mapped in this process
 size_t p2p_bytes(const fmm_p2p* p);
+// push mode: out = sum over g ascending of slot g (slot_elems apart) of this rank's buffer, rows x
+// inner with leading dimension ld in each slot
+void p2p_reduce_slots(const fmm_p2p* p, long long slot_elems, long long rows, long long inner, long long ld,
+                      double* out, long long ldo, cudaStream_t s);
 void* comm_handle(const fmm_comm* c);
 int comm_nranks(const fmm_comm* c);
 int comm_rank(const fmm_comm* c);

@@ -9,6 +9,7 @@
 // result is deterministic and identical on every run.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -88,6 +89,29 @@ void p2p_reduce_rows(const fmm_p2p* p, long long outer, long long r0, long long 
   else
     p2p_reduce<false><<<grid, 256, 0, s>>>(src, p->nranks, r0, rows, inner, ld, out, ldo);
   FMM_CUDA(cudaGetLastError());
+}
+void p2p_reduce_slots(const fmm_p2p* p, long long slot_elems, long long rows, long long inner, long long ld,
+                      double* out, long long ldo, cudaStream_t s) {
+  if (rows <= 0 || inner <= 0) return;
+  if ((size_t)slot_elems * p->nranks * 8 > p->bytes) throw Error(FMM_E_SHAPE, "the p2p buffer holds fewer than G slots");
+  FMM_CUDA(cudaSetDevice(p->device));
+  PeerPtrs src{};
+  for (int g = 0; g < p->nranks; ++g) src.p[g] = p->local + (size_t)g * slot_elems;
+  const bool vec2 = inner % 2 == 0 && ld % 2 == 0 && ldo % 2 == 0 && slot_elems % 2 == 0 &&
+                    (reinterpret_cast<uintptr_t>(out) & 15) == 0 && (reinterpret_cast<uintptr_t>(p->local) & 15) == 0;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+  const long long work = rows * (vec2 ? inner / 2 : inner);
+  const int grid = (int)std::min<long long>((work + 255) / 256, (long long)sms * 8);
+  if (vec2)
+    p2p_reduce<true><<<grid, 256, 0, s>>>(src, p->nranks, 0, rows, inner, ld, out, ldo);
+  else
+    p2p_reduce<false><<<grid, 256, 0, s>>>(src, p->nranks, 0, rows, inner, ld, out, ldo);
+  FMM_CUDA(cudaGetLastError());
+}
+double* p2p_peer(const fmm_p2p* p, int g) {
+  if (g < 0 || g >= p->nranks || !p->peer[g]) throw Error(FMM_E_INVALID_ARG, "fmm_p2p_open has not mapped every rank");
+  return p->peer[g];
 }
 int p2p_nranks(const fmm_p2p* p) { return p->nranks; }
 int p2p_rank(const fmm_p2p* p) { return p->rank; }

@@ -1683,9 +1683,15 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
   double* const userC = C;
   const long long user_ldc = ldc;
   const long long crows = p->colmajor ? p->userN : p->userP, ccols = p->colmajor ? p->userP : p->userN;
+  // push mode (p2p_push, root output): this rank's partial goes straight into its slot of the
+  // root's buffer -- the kernels that write C store over peer memory, tile by tile
+  const bool push = p->p2p && p->opt.p2p_push && p->dist_root != FMM_DIST_SLABS;
+  const long long slot_elems = (crows * ccols + 1) / 2 * 2;  // slots 16-byte aligned
   if (p->p2p) {
-    if ((size_t)(crows * ccols) * 8 > p2p_bytes(p->p2p)) throw Error(FMM_E_SHAPE, "the p2p partial buffer is smaller than C");
-    C = p2p_local(p->p2p);
+    const size_t need = (size_t)(push ? slot_elems * p2p_nranks(p->p2p) : crows * ccols) * 8;
+    if (need > p2p_bytes(p->p2p))
+      throw Error(FMM_E_SHAPE, push ? "the p2p buffer holds fewer than G partials (p2p_push)" : "the p2p partial buffer is smaller than C");
+    C = push ? p2p_peer(p->p2p, p->dist_root) + (size_t)p2p_rank(p->p2p) * slot_elems : p2p_local(p->p2p);
     ldc = std::max<long long>(ccols, 1);
   }
   // row-major orientation: for column-major, C^T = B^T A^T (Prop. 1)
@@ -1930,8 +1936,12 @@ void run(fmm_plan_t* p, const double* A, long long lda, const double* B, long lo
     long long r0 = 0, r1 = 0;
     if (p->dist_root == FMM_DIST_SLABS) dist_slab_range(crows, G, g, &r0, &r1);
     else if (p->dist_root == g) r0 = 0, r1 = crows;
-    if (r1 > r0 && ccols > 0)
+    if (push) {  // every partial is in the root's slots: the root sums them locally
+      if (p->dist_root == g && crows > 0 && ccols > 0)
+        p2p_reduce_slots(p->p2p, slot_elems, crows, ccols, ldc, userC, user_ldc, stream);
+    } else if (r1 > r0 && ccols > 0) {
       p2p_reduce_rows(p->p2p, crows, r0, r1, ccols, ldc, userC + r0 * user_ldc, user_ldc, stream);
+    }
     FMM_CUDA(cudaStreamSynchronize(stream));
     bar();
   }
@@ -1973,6 +1983,7 @@ void fmm_plan_options_default(fmm_plan_options* o) {
   o->dist_chunks = 4;
   o->fuse_output = 0;
   o->small_fused = 1;
+  o->p2p_push = 0;
 }
 
 fmm_status_t fmm_plan_create(const fmm_alg* alg, int64_t P, int64_t Q, int64_t Nc, int levels,

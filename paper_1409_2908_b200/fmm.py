@@ -35,7 +35,7 @@ class _Options(ctypes.Structure):
                 ("workspace_limit_bytes", ctypes.c_size_t), ("peel_align", ctypes.c_int),
                 ("fuse_leaf_level", ctypes.c_int), ("shard_mode", ctypes.c_int), ("collapse_levels", ctypes.c_int),
                 ("cuda_graphs", ctypes.c_int), ("peel_tiles", ctypes.c_int), ("dist_chunks", ctypes.c_int),
-                ("fuse_output", ctypes.c_int), ("small_fused", ctypes.c_int)]
+                ("fuse_output", ctypes.c_int), ("small_fused", ctypes.c_int), ("p2p_push", ctypes.c_int)]
 
 
 # fmm_barrier_fn: int (*)(void* ctx), a host barrier over the ranks of a peer-memory plan
@@ -259,7 +259,8 @@ class Plan:
                  fuse=False, collapse: bool = True, comm: Optional[Comm] = None, root: int = 0,
                  shard_mode: str = "leaf", cuda_graphs: bool = True, peel_tiles: bool = False,
                  p2p: Optional["P2P"] = None, barrier=None, dist_chunks: Optional[int] = None,
-                 fuse_output: Optional[bool] = None, small: Optional[bool] = None):
+                 fuse_output: Optional[bool] = None, small: Optional[bool] = None,
+                 p2p_push: Optional[bool] = None):
         """comm: an NCCL Comm -> fmm_plan_create_dist (the reduce runs inside execute, in dist_chunks
         overlapped row chunks where it applies).  p2p + barrier: a P2P object and a zero-argument host
         barrier over the same ranks (e.g. torch.distributed.barrier) -> fmm_plan_create_p2p (the
@@ -291,6 +292,8 @@ class Plan:
             o.fuse_output = int(bool(fuse_output))
         if small is not None:
             o.small_fused = int(bool(small))
+        if p2p_push is not None:
+            o.p2p_push = int(bool(p2p_push))
         self.device = torch.cuda.current_device() if device is None else device
         h = ctypes.c_void_p()
         self.comm = comm  # a distributed plan keeps its communicator / peer buffers alive

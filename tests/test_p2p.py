@@ -2,7 +2,8 @@
 with its HYBRID leaf shard written into its IPC-exported partial buffer, then ONE
 reduce kernel per rank pulling its slab from every rank's partial -- called by hand
 (fmm_p2p_reduce_slab) and inside fmm_execute of the library's peer-memory plan
-(fmm_plan_create_p2p, root and slab output).  The ranks share the one GPU of
+(fmm_plan_create_p2p, root and slab output; and the push mode, p2p_push, where the kernels that
+write C store each rank's partial straight into the root's buffer).  The ranks share the one GPU of
 this box (CUDA IPC works between processes on one device), gloo carries only the handle exchange
 and the two barriers; no kernel waits on another rank's kernel.  Integer inputs: the slabs must
 equal the exact product bit for bit, in both layouts."""
@@ -90,7 +91,7 @@ def test_p2p_slab_combine(world, layout, alg):
     assert q.get(timeout=5), "reduced slabs differ from A*B"
 
 
-def _plan_worker(rank, world, port, layout, alg_name, root, q):
+def _plan_worker(rank, world, port, layout, alg_name, root, q, push=False):
     # the library's own combine: fmm_plan_create_p2p, the reduce inside fmm_execute, the host
     # barrier supplied as a callback (gloo's torch.distributed.barrier)
     import sys
@@ -108,8 +109,10 @@ def _plan_worker(rank, world, port, layout, alg_name, root, q):
             if layout == "row":
                 return torch.from_numpy(np.ascontiguousarray(x)).cuda()
             return torch.from_numpy(np.ascontiguousarray(x.T)).cuda().t()
-        p2p = F.P2P.from_torch_distributed(8 * P * N)
-        plan = F.Plan(F.load_alg(alg_name), P, Q, N, 2, layout=layout, p2p=p2p, barrier=dist.barrier, root=root)
+        # push mode: every rank's buffer holds G partial slots (16-byte aligned), the root's receives them
+        p2p = F.P2P.from_torch_distributed(8 * ((P * N + 1) // 2 * 2) * (world if push else 1))
+        plan = F.Plan(F.load_alg(alg_name), P, Q, N, 2, layout=layout, p2p=p2p, barrier=dist.barrier, root=root,
+                      p2p_push=push)
         want = A @ B
         ok = True
         for it in range(3):  # the partial buffers are reused across executes
@@ -137,17 +140,22 @@ def _plan_worker(rank, world, port, layout, alg_name, root, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,layout,alg,root", [(2, "row", "winograd_class_222_7", 0),
-                                                   (2, "col", "hk_class_323_15", 1),
-                                                   (3, "row", "alg_424_26", "slabs"),
-                                                   (2, "col", "strassen_222_7", "slabs")])
-def test_p2p_plan_combines_inside_execute(world, layout, alg, root):
+@pytest.mark.parametrize("world,layout,alg,root,push", [(2, "row", "winograd_class_222_7", 0, False),
+                                                        (2, "col", "hk_class_323_15", 1, False),
+                                                        (3, "row", "alg_424_26", "slabs", False),
+                                                        (2, "col", "strassen_222_7", "slabs", False),
+                                                        # push mode (p2p_push): the partials are stored into
+                                                        # the root's slots by the kernels that write C
+                                                        (2, "row", "winograd_class_222_7", 0, True),
+                                                        (3, "col", "alg_424_26", 2, True),
+                                                        (3, "row", "hk_class_323_15", 1, True)])
+def test_p2p_plan_combines_inside_execute(world, layout, alg, root, push):
     import __graft_entry__
     __graft_entry__.build()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_plan_worker, args=(r, world, port, layout, alg, root, q)) for r in range(world)]
+    procs = [ctx.Process(target=_plan_worker, args=(r, world, port, layout, alg, root, q, push)) for r in range(world)]
     for pr in procs:
         pr.start()
     for pr in procs:
@@ -157,7 +165,7 @@ def test_p2p_plan_combines_inside_execute(world, layout, alg, root):
 
 
 @pytest.mark.parametrize("workload,extra", [("c1", []), ("c3", ["--shard-mode", "top", "--output", "slabs"]),
-                                            ("c1", ["--shard-mode", "slab"])])
+                                            ("c1", ["--shard-mode", "slab"]), ("c3", ["--combine", "p2p_push"])])
 def test_bench_two_ranks_on_one_gpu(workload, extra):
     # `bench.py --gpus 2` with no torchrun wrapper launches the two ranks itself; with gloo they share
     # this GPU and the peer-memory plan combines inside fmm_execute (a control-flow check: the line
