@@ -20,7 +20,12 @@ def time_plan(alg, w, L, A, B, reps=3):
         p = F.Plan(alg, w["P"], w["Q"], w["N"], L, layout=w["layout"])
     except F.FmmError as e:
         return None, str(e)[:80]
-    C = p.new_output()
+    try:
+        C = p.new_output()
+    except torch.OutOfMemoryError as e:  # the plan's workspace left no room for C (c5 at L = 3)
+        del p
+        torch.cuda.empty_cache()
+        return None, "out of memory: " + str(e)[:60]
     p.execute(A, B, C)  # builds the launch tables
     p.execute(A, B, C)  # captures the CUDA graph; the timed calls replay it
     torch.cuda.synchronize()
