@@ -153,6 +153,7 @@ struct SmallArgs {
   int cluster;     // 1: the R CTAs of a tile are a cluster (C_k from the peers' shared memory)
   int prefetch;    // 1: the next chunk's copies are issued before the current chunk is used
   int coop;        // 1: the whole grid is resident; the R CTAs of a tile assemble it together
+  int direct;      // 1: the classical product (<1,1,1;1>, L = 0): each CTA writes its tile to C
   int smem;        // dynamic shared memory bytes of the launch
 };
 int small_tile();  // the tile edge (32)

@@ -480,7 +480,11 @@ static bool al16(const void* p);
 // nonzero w_kr in ascending r -- the orders of the separate kernels' chains without CSE
 void fmm_plan_s::emit_small() {
   const fmm_alg* a = alg;
-  const int M = a->M, K = a->K, Nb = a->N;
+  // L = 0 (the classical product below the cutoff): the same kernel with the trivial base case
+  // <1,1,1;1>, each CTA writing its tile of C directly
+  const bool direct = L == 0;
+  const int M = direct ? 1 : a->M, K = direct ? 1 : a->K, Nb = direct ? 1 : a->N, R = direct ? 1 : this->R;
+  const std::vector<double> one{1.0};
   auto terms = [&](const std::vector<double>& X, int rows, bool by_r, std::vector<int>& off, std::vector<SmallTerm>& t) {
     const int outer = by_r ? R : rows, inner = by_r ? rows : R;
     off.assign(outer + 1, 0);
@@ -494,13 +498,13 @@ void fmm_plan_s::emit_small() {
   };
   std::vector<int> uo, vo, wo;
   std::vector<SmallTerm> ut, vt, wt;
-  terms(a->Ud, M * K, true, uo, ut);
-  terms(a->Vd, K * Nb, true, vo, vt);
-  terms(a->Wd, M * Nb, false, wo, wt);
+  terms(direct ? one : a->Ud, M * K, true, uo, ut);
+  terms(direct ? one : a->Vd, K * Nb, true, vo, vt);
+  terms(direct ? one : a->Wd, M * Nb, false, wo, wt);
   Launch ln;
   ln.kind = Launch::SMALL;
-  ln.level = 1;
-  const Dims& d = dims[1];
+  ln.level = direct ? 0 : 1;
+  const Dims& d = dims[direct ? 0 : 1];
   for (auto& tm : ut) tm.off = (tm.blk / K) * d.P * cur_lda + (tm.blk % K) * d.Q;
   for (auto& tm : vt) tm.off = (tm.blk / Nb) * d.Q * cur_ldb + (tm.blk % Nb) * d.N;
   const int T = small_tile();
@@ -523,6 +527,7 @@ void fmm_plan_s::emit_small() {
   sa.stage_max = max_nu * T * (sa.kc + 4) + max_nv * sa.kc * (T + 8);
   sa.smem = std::max({8 * (2 * sa.stage_max + T * (sa.kc + 4) + sa.kc * (T + 8)), 8 * R * sa.g, 3 * T * T * 8});
   sa.nw = (int)wt.size();
+  sa.direct = direct ? 1 : 0;
   bool v2 = al16(cur_A) && al16(cur_B) && cur_lda % 2 == 0 && cur_ldb % 2 == 0;
   for (const auto& tm : ut) v2 = v2 && tm.off % 2 == 0;
   for (const auto& tm : vt) v2 = v2 && tm.off % 2 == 0;
@@ -530,19 +535,20 @@ void fmm_plan_s::emit_small() {
   // the cluster variant (C_k over distributed shared memory) measured slower on c1 (26.7 against
   // 18.5 us per step): only on request (FMM_SMALL_CLUSTER=1)
   const char* cl = getenv("FMM_SMALL_CLUSTER");
-  sa.cluster = cl && cl[0] == '1' && R >= M * Nb && small_cluster_ok(R, sa.smem);
+  sa.cluster = !direct && cl && cl[0] == '1' && R >= M * Nb && small_cluster_ok(R, sa.smem);
   sa.prefetch = !(getenv("FMM_SMALL_PREFETCH") && getenv("FMM_SMALL_PREFETCH")[0] == '0');
   // the R CTAs of a tile assemble it together when the whole grid is resident (else the last one)
-  sa.coop = !sa.cluster && small_coop_ok((long long)sa.tiles_m * sa.tiles_n * R, sa.smem, sa.kc, sa.vec2) && !(getenv("FMM_SMALL_COOP") && getenv("FMM_SMALL_COOP")[0] == '0');
+  sa.coop = !direct && !sa.cluster && small_coop_ok((long long)sa.tiles_m * sa.tiles_n * R, sa.smem, sa.kc, sa.vec2) && !(getenv("FMM_SMALL_COOP") && getenv("FMM_SMALL_COOP")[0] == '0');
   ln.count = R;
   ln.tiles = (long long)sa.tiles_m * sa.tiles_n * R;
   // work: the leaf products, the formation reads / adds and the assembly (as the separate kernels)
   ln.flops = 2.0 * R * d.P * (double)d.Q * d.N;
   ln.gemm_bytes = 8.0 * R * (d.P * d.Q + d.Q * d.N + d.P * d.N);
-  ln.elem_reads = (double)ut.size() * d.P * d.Q + (double)vt.size() * d.Q * d.N + (double)wt.size() * d.P * d.N;
-  ln.elem_writes = (double)M * Nb * d.P * d.N;
-  ln.elem_adds = (double)(ut.size() - uo.size() + 1) * d.P * d.Q + (double)(vt.size() - vo.size() + 1) * d.Q * d.N +
-                 (double)(wt.size() - M * Nb) * d.P * d.N;
+  ln.elem_reads = direct ? 0.0 : (double)ut.size() * d.P * d.Q + (double)vt.size() * d.Q * d.N + (double)wt.size() * d.P * d.N;
+  ln.elem_writes = direct ? 0.0 : (double)M * Nb * d.P * d.N;
+  ln.elem_adds = direct ? 0.0
+                        : (double)(ut.size() - uo.size() + 1) * d.P * d.Q + (double)(vt.size() - vo.size() + 1) * d.Q * d.N +
+                              (double)(wt.size() - M * Nb) * d.P * d.N;
   launches.push_back(ln);
 }
 
@@ -1601,6 +1607,17 @@ void plan_init(fmm_plan_t* p, const fmm_alg* alg, long long P, long long Q, long
         FMM_CUDA(cudaMalloc(&p->small_cnt, 2 * (size_t)tiles * sizeof(unsigned)));
         FMM_CUDA(cudaMemset(p->small_cnt, 0, 2 * (size_t)tiles * sizeof(unsigned)));
       }
+    }
+    // L = 0 below the cutoff: the classical product through the same one launch (base case
+    // <1,1,1;1>, each CTA writes its 32 x 32 tile of C) when the GEMM's 128-row tiles would leave
+    // most SMs idle (256^3: 4 tiles)
+    const Dims& z = p->dims[0];
+    if (!p->small && L == 0 && p->opt.small_fused && !(e && e[0] == '1') && p->opt.shard_count == 1 && !p->dist_comm &&
+        !p->p2p && z.P >= 1 && z.Q >= 1 && z.N >= 1 && z.Q < (1LL << 30) &&
+        ((z.P + 127) / 128) * ((z.N + 127) / 128) < gemm_sm_count() && small_config(1, 1, (int)z.Q, 1, &kc, &g)) {
+      p->small = true;
+      FMM_CUDA(cudaMalloc(&p->small_M, 16));  // unused: the tiles go straight to C
+      FMM_CUDA(cudaMalloc(&p->small_cnt, 16));
     }
   }
   p->setup_sharding();

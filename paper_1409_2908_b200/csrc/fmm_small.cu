@@ -223,6 +223,25 @@ __global__ void __launch_bounds__(THREADS) small_fmm_kernel(SmallArgs a) {
                                     2 * (lane & 3)) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
   }
   __syncthreads();
+  if (a.direct) {  // L = 0: the tile is C's (w = 1); no assembly
+    if (grp == 0) {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 2; ++ni) {
+          const int row = wm + mi * 8 + (lane >> 2), col = wn + ni * 8 + 2 * (lane & 3);
+          const int o = row * TN + col;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            double v = acc[mi][ni][h];
+#pragma unroll
+            for (int g = 0; g < 3; ++g) v = __dadd_rn(v, red[g * TM * TN + o + h]);
+            if (i0 + row < a.pm && j0 + col + h < a.pn) a.C[(long long)(i0 + row) * a.ldc + j0 + col + h] = v;
+          }
+        }
+    }
+    return;
+  }
   if (grp == 0) {
     double* mt = CL ? mts : a.Mbuf + ((long long)r * npos + pos) * (TM * TN);
 #pragma unroll

@@ -106,3 +106,19 @@ def test_not_applied_where_it_does_not_fit():
     assert plan("strassen_222_7", 257, 256, 256).stats()["small_fused"] == 0.0
     assert plan("strassen_222_7", 4096, 512, 4096).stats()["small_fused"] == 0.0
     assert plan("strassen_222_7", 256, 256, 256, fuse_output=True).stats()["small_fused"] == 0.0
+
+
+@pytest.mark.parametrize("shape", [(256, 256, 256), (1, 1, 1), (100, 37, 250), (512, 1024, 300)])
+def test_classical_below_the_cutoff(shape):
+    # L = 0 below the cutoff: the classical product through the same one launch (base case
+    # <1,1,1;1>, each CTA writes its tile of C directly)
+    P, Q, N = shape
+    p = plan("strassen_222_7", P, Q, N, L=0)
+    assert p.stats()["small_fused"] == 1.0 and p.stats()["launches"] == 1.0
+    A, B = I.problem(P, Q, N, seed=P + 2 * Q + 3 * N)
+    C = p.execute(dev(A), dev(B)).cpu().numpy()
+    assert np.max(np.abs(C - O.classical(A, B))) <= 1e-13 * np.linalg.norm(A) * np.linalg.norm(B)
+    Ai, Bi = I.problem(P, Q, N, seed=5, kind="integers")
+    assert np.array_equal(p.execute(dev(Ai), dev(Bi)).cpu().numpy(), Ai @ Bi)
+    # large products keep the grouped GEMM
+    assert plan("strassen_222_7", 4096, 256, 4096, L=0).stats()["small_fused"] == 0.0

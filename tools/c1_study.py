@@ -45,3 +45,18 @@ t_cub = timeit(lambda: torch.matmul(A, B))
 err = (C - A @ B).abs().max().item()
 print(json.dumps({"cfg": c, "step_ms": t_fmm, "cublas_ms": t_cub, "vs_cublas": t_cub / t_fmm, "max_err": err,
                   "stats": p.stats()}))
+
+# the classical product below the cutoff (L = 0) through the same one launch
+p0 = F.Plan(F.load_alg(w["alg"]), P, Q, N, 0, layout="row")
+C0 = p0.new_output()
+t0 = timeit(lambda: p0.execute(A, B, C0))
+g = torch.cuda.CUDAGraph()
+Cg = torch.empty_like(C)
+with torch.cuda.graph(g):
+    for _ in range(20):
+        torch.matmul(A, B, out=Cg)
+torch.cuda.synchronize()
+t_cub_graph = timeit(lambda: g.replay(), reps=50) / 20
+print(json.dumps({"cfg": c, "L0_step_ms": t0, "L0_stats_small": p0.stats()["small_fused"], "cublas_graph_ms": t_cub_graph,
+                  "cublas_plain_out_ms": timeit(lambda: torch.matmul(A, B, out=Cg)),
+                  "max_err_L0": (C0 - A @ B).abs().max().item()}))
