@@ -365,7 +365,8 @@ fmm_status_t fmm_execute_timed(fmm_plan_t* plan, const double* A, int64_t lda, c
 /* Diagnostics: fmm_execute with an event after every launch (plain launches, blocking); for the
    first min(*n, max) launches: kind[q] (0 A formation, 1 B formation, 2 leaf GEMM, 3 assembly,
    4 peel strips, 5 thin products on CUDA cores, 6 fused leaf level, 7 combine, 8 zeroing for
-   fuse_output), level[q] (recursion level) and ms[q]; *n = the number of launches. */
+   fuse_output, 9 the one-launch small_fused step), level[q] (recursion level) and ms[q]; *n = the
+   number of launches. */
 fmm_status_t fmm_execute_profile(fmm_plan_t* plan, const double* A, int64_t lda, const double* B, int64_t ldb,
                                  double* C, int64_t ldc, void* stream, int max, int* kind, int* level, float* ms,
                                  int* n);
