@@ -148,7 +148,9 @@ def _plan_worker(rank, world, port, layout, alg_name, root, q, push=False):
                                                         # the root's slots by the kernels that write C
                                                         (2, "row", "winograd_class_222_7", 0, True),
                                                         (3, "col", "alg_424_26", 2, True),
-                                                        (3, "row", "hk_class_323_15", 1, True)])
+                                                        (3, "row", "hk_class_323_15", 1, True),
+                                                        # slab output with p2p_push: the pull path
+                                                        (2, "row", "strassen_222_7", "slabs", True)])
 def test_p2p_plan_combines_inside_execute(world, layout, alg, root, push):
     import __graft_entry__
     __graft_entry__.build()
