@@ -148,6 +148,32 @@ __device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map
       "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(bar)
       : "memory");
 }
+// Experiments (off by default): FMM_L2_HINT=1 loads the operand tiles with an L2
+// evict_last policy, so the streaming output does not push operand panels that other SMs still read
+// out of L2 (DRAM re-reads on c2 / c5); FMM_GEMM_STG=1 stores the epilogue through st.global
+// (STG) instead of the generic ST the compiler emits for C, =2 through st.global.cs (evict-first)
+#ifndef FMM_L2_HINT
+#define FMM_L2_HINT 0
+#endif
+#ifndef FMM_GEMM_STG
+#define FMM_GEMM_STG 0
+#endif
+__device__ __forceinline__ void st_global_v2(double2* p, double a, double b) {
+  asm volatile("st.global.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_hint(unsigned dst, const CUtensorMap* map, int c0, int c1, unsigned bar,
+                                                 unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3}], [%4], %5;\n" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ unsigned long long l2_policy_evict_last() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_shared() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 // K3f: shared-memory box (16 columns x 128 rows, 128B swizzle) reduce-added into a global tile
@@ -411,10 +437,20 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
           mbar_wait(empty_bar(stage), phase ^ 1u);
           const unsigned sa = base + stage * STAGE_T, sb = sa + A_BYTES;
           mbar_expect_tx(full_bar(stage), STAGE_T);
+#if FMM_L2_HINT
+          const unsigned long long pol = l2_policy_evict_last();
+#pragma unroll
+          for (int h = 0; h < KS / 16; ++h)
+            tma_load_2d_hint(sa + h * 16384, ma, kt * KS + 16 * h, tc.m0, full_bar(stage), pol);
+#pragma unroll
+          for (int b = 0; b < BN / 16; ++b)
+            tma_load_2d_hint(sb + b * B_BOX, mb, tc.n0 + 16 * b, kt * KS, full_bar(stage), pol);
+#else
 #pragma unroll
           for (int h = 0; h < KS / 16; ++h) tma_load_2d(sa + h * 16384, ma, kt * KS + 16 * h, tc.m0, full_bar(stage));
 #pragma unroll
           for (int b = 0; b < BN / 16; ++b) tma_load_2d(sb + b * B_BOX, mb, tc.n0 + 16 * b, kt * KS, full_bar(stage));
+#endif
           if (++stage == STAGES) stage = 0, phase ^= 1u;
         }
       }
@@ -721,7 +757,13 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
             v0 = fma(beta, o.x, v0);
             v1 = fma(beta, o.y, v1);
           }
+#if FMM_GEMM_STG == 2
+          __stcs(p, make_double2(v0, v1));
+#elif FMM_GEMM_STG == 1
+          st_global_v2(p, v0, v1);
+#else
           *p = make_double2(v0, v1);
+#endif
         } else if (col < n) {
           crow[col] = beta != 0.0 ? fma(beta, crow[col], v0) : v0;
         }
