@@ -526,3 +526,40 @@ def test_execute_profile_lists_every_launch(alg, shape, layout, L):
     assert len(prof) <= st["launches"]  # a thin-strip entry can hold two kernel launches
     _, t = p.execute_timed(dev(A, layout), dev(B, layout), C)
     assert abs(sum(ms for _, _, ms in prof) - t["total_ms"]) < 0.5 * t["total_ms"] + 0.05
+
+
+# ---- thin peel strips: both row-strip forms (fmm_skinny.cu) --------------------
+# Strip heights 1-7 (TH 1, 2, 4, 8), k below / at / above the pipelined batch (4 slices x 4 rows,
+# two batches in flight), ragged and odd column counts (the 128-column block's tail, a lone last
+# column), row- and column-major; integer inputs, so every case is bit-exact against int64 matmul.
+_STRIP_CASES = [("alg_433_29", 1, 4 * 37 + 3, 3 * 5 + 2, 3 * 43 + 2),
+                ("alg_433_29", 1, 4 * 40 + 1, 3 * 11, 3 * 90 + 1),
+                ("hk_class_323_15", 2, 9 * 31 + 5, 4 * 9 + 3, 9 * 29 + 7),
+                ("hk_class_323_15", 1, 3 * 70 + 2, 2 * 1 + 1, 3 * 45 + 1),
+                ("strassen_222_7", 2, 4 * 50 + 3, 4 * 40 + 1, 4 * 64 + 3),
+                ("alg_424_26", 1, 4 * 30 + 3, 2 * 17 + 1, 4 * 33 + 3)]
+
+
+def _strip_cases_check():
+    for name, L, P, Q, N in _STRIP_CASES:
+        for layout in ("row", "col"):
+            Ai, Bi = I.problem(P, Q, N, seed=P + Q + N, kind="integers")
+            C, p = run(name, Ai, Bi, L, layout=layout, peel_align=False)
+            assert np.array_equal(C, Ai @ Bi), (name, L, P, Q, N, layout)
+
+
+def test_thin_strips_row_forms():
+    assert "alg_424_26" in NAMES
+    _strip_cases_check()  # the default (wide) row-strip form
+
+
+def test_thin_strips_row_forms_narrow():
+    # the 32-column row-strip form, selected once per process by FMM_SKINNY_ROWS=narrow
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = ("import sys; sys.path[:0] = [%r, %r]; import test_gpu_parity as T; T._strip_cases_check(); print('ok')"
+            % (here, os.path.dirname(here)))
+    env = dict(os.environ, FMM_SKINNY_ROWS="narrow")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
