@@ -203,9 +203,21 @@ __global__ void __launch_bounds__(256, TH <= 4 ? FMM_SKINNY_COLS_MINB : 3) skinn
     __syncthreads();
     // the n values of a k-row by n consecutive lanes (one L1 wavefront per 32 / n rows; a thread
     // per row would touch 32 lines per load), stored conflict-free through the padded stride
-    for (int e = threadIdx.x; e < kc * t.n; e += blockDim.x) {
-      const int kk = e / t.n, j = e - kk * t.n;
-      bt[j * KSTR + kk] = __ldg(t.B + (long long)(k0 + kk) * t.ldb + j);
+    // (eight loads issued before their stores: one L2 round trip per eight elements per thread,
+    // not one each -- the staging was the block's critical path)
+    const int ne = kc * t.n;
+    for (int e0 = threadIdx.x; e0 < ne; e0 += 8 * 256) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + 256 * u, kk = e / t.n, j = e - kk * t.n;
+        v[u] = e < ne ? __ldg(t.B + (long long)(k0 + kk) * t.ldb + j) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + 256 * u, kk = e / t.n, j = e - kk * t.n;
+        if (e < ne) bt[j * KSTR + kk] = v[u];
+      }
     }
     __syncthreads();
     if (v2) {
