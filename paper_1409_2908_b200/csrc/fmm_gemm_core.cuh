@@ -738,6 +738,32 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
       if (staged) continue;
     }
     // ---- epilogue: C = alpha * acc (+ beta * C), from registers ----
+    // Interior warp tiles with beta = 0 (all but the ragged edge of a leaf) take a straight-line
+    // form: one base pointer, compile-time offsets, no per-element range or beta branches.  ncu's
+    // source page put 3.5 % of c5t's samples on the general form's ~700 instructions (BSSY / BRA
+    // around every store), i.e. the tile boundary was issue-bound, not store-bound (DESIGN 6d).
+#if !defined(FMM_GEMM_NOSTORE) && !defined(FMM_GEMM_NO_FAST_EPI)
+    if (beta == 0.0 && tc.m0 + wm + WTM <= m && tc.n0 + wn + WTN <= n) {
+      double* c0 = C + (long long)(tc.m0 + wm + 2 * r) * ldc + (tc.n0 + wn + cofs);
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        double* crow = c0 + (long long)(16 * (i >> 1) + (i & 1)) * ldc;
+#pragma unroll
+        for (int jj = 0; jj < NI; ++jj) {
+          double2* p = reinterpret_cast<double2*>(crow + 16 * (jj >> 1) + 4 * (jj & 1));
+          const double v0 = alpha * acc[i][jj][0], v1 = alpha * acc[i][jj][1];
+#if FMM_GEMM_STG == 2
+          __stcs(p, make_double2(v0, v1));
+#elif FMM_GEMM_STG == 1
+          st_global_v2(p, v0, v1);
+#else
+          *p = make_double2(v0, v1);
+#endif
+        }
+      }
+    } else
+#endif
+    {
 #pragma unroll
     for (int i = 0; i < MI; ++i) {
       const int row = tc.m0 + wm + 16 * (i >> 1) + 2 * r + (i & 1);
@@ -768,6 +794,7 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
           crow[col] = beta != 0.0 ? fma(beta, crow[col], v0) : v0;
         }
       }
+    }
     }
     if constexpr (FUSED) {  // publish the stored tile (release) to the assembly jobs of its parent
       __threadfence();
