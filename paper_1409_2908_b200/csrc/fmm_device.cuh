@@ -37,6 +37,10 @@ struct K3fArgs {
 // its task by division; others binary-search the tile prefix sums in the task table.
 struct Uniform {
   int tiles, tiles_m, tiles_n;  // tiles == 0: not uniform
+  // floor((2^32 - 1) / d) for d = tiles and d = (raster group height) * tiles_n: the tile map divides
+  // by multiply-high plus one correction instead of the ~25-instruction emulated division (the
+  // tile boundary of the leaf GEMM is issue-bound, DESIGN 6d).  0: divide.
+  unsigned magic_tiles = 0, magic_span = 0;
 };
 
 // ---- fused leaf level (K1 level L + K2 + K3 level L in one persistent launch) ----------------

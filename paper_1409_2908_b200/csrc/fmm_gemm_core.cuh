@@ -265,12 +265,26 @@ __device__ __forceinline__ double ldcg1(const double* p) {
 struct TileCoord {
   int task, m0, n0;
 };
+// x / d for 0 <= x < 2^31 with magic = floor((2^32 - 1) / d): the multiply-high estimate is the
+// quotient or one below it, so one correction makes it exact
+__device__ __forceinline__ int magic_div(int x, int d, unsigned magic, int& rem) {
+  unsigned q = __umulhi((unsigned)x, magic);
+  unsigned r = (unsigned)x - q * (unsigned)d;
+  if (r >= (unsigned)d) ++q, r -= (unsigned)d;
+  rem = (int)r;
+  return (int)q;
+}
+
 template <int BN>
 __device__ __forceinline__ TileCoord locate(const GemmTask* __restrict__ tasks, int ntasks, int tile, Uniform u) {
   int lo, tiles_m, tiles_n, local;
   if (u.tiles) {
-    lo = tile / u.tiles;
-    local = tile - lo * u.tiles;
+    if (u.magic_tiles) {
+      lo = magic_div(tile, u.tiles, u.magic_tiles, local);
+    } else {
+      lo = tile / u.tiles;
+      local = tile - lo * u.tiles;
+    }
     tiles_m = u.tiles_m;
     tiles_n = u.tiles_n;
   } else {
@@ -285,12 +299,24 @@ __device__ __forceinline__ TileCoord locate(const GemmTask* __restrict__ tasks, 
     local = tile - __ldg(&tasks[lo].tile_begin);
   }
   const int span = GROUP_M * tiles_n;
-  const int group = local / span;
+  int group, in_span;
+  if (u.tiles && u.magic_span) {
+    group = magic_div(local, span, u.magic_span, in_span);
+  } else {
+    group = local / span;
+    in_span = local - group * span;
+  }
   const int first_m = group * GROUP_M;
   const int gsize = min(tiles_m - first_m, GROUP_M);
-  const int tm = first_m + (local % span) % gsize;
-  const int tn = (local % span) / gsize;
-  return {lo, tm * BM, tn * BN};
+  int tn, tm_in;
+  if (gsize == GROUP_M) {  // every group but a ragged last one: a compile-time divisor
+    tn = in_span / GROUP_M;
+    tm_in = in_span % GROUP_M;
+  } else {
+    tn = in_span / gsize;
+    tm_in = in_span - tn * gsize;
+  }
+  return {lo, (first_m + tm_in) * BM, tn * BN};
 }
 
 
@@ -523,8 +549,18 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
 
   int stage = 0;
   unsigned phase = 0;
+  // The tile -> (task, m0, n0) map (three integer divisions, or a binary search) of the NEXT tile
+  // is computed inside the current tile's main loop, where issue slots are idle behind the DMMAs;
+  // the two warps of a sub-partition do it in different k-steps so one of them keeps the pipe fed.
+  // Measured (profiles/r2_fast_epilogue_study.jsonl): 112-wide tiles gain (c3 0.930 -> 0.933, c4 0.937 ->
+  // 0.945 of the DMMA peak); 80-wide tiles lose (ptxas spills two registers into the main loop: c5t
+  // 0.935 -> 0.924, c5 0.966 -> 0.958) and 128-wide tiles are unchanged, so only BN = 112 does it.
+  constexpr bool NEXT_IN_LOOP = BN == 112;
+  TileCoord tc_next = locate<BN>(tasks, ntasks, (int)blockIdx.x < total_tiles ? (int)blockIdx.x : 0, uni);
   for (int tile = blockIdx.x; tile < total_tiles; tile += gemm_ctas) {
-    const TileCoord tc = locate<BN>(tasks, ntasks, tile, uni);
+    const TileCoord tc = tc_next;
+    const int tile_next = tile + gemm_ctas;
+    bool have_next = false;
     const GemmTask& t = tasks[tc.task];
     const int kdim = __ldg(&t.k);
     const int KT = (kdim + KS - 1) / KS;
@@ -605,7 +641,12 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
       mbar_wait(full_bar(stage), phase);
       unsigned sa = base + stage * STAGE_T, sb = sa + A_BYTES;
       load(a0, b0, sa, sb, 0);
+      const int pfk = min(cw >= CONSUMERS / 2 ? 1 : 0, KF - 1);
       for (int kt = 0; kt < KF; ++kt) {
+        if (NEXT_IN_LOOP && kt == pfk) {
+          if (tile_next < total_tiles) tc_next = locate<BN>(tasks, ntasks, tile_next, uni);
+          have_next = true;
+        }
 #pragma unroll
         for (int s = 0; s + 2 < SL; s += 2) {
           load(a1, b1, sa, sb, s + 1);
@@ -637,6 +678,7 @@ __device__ __forceinline__ void gemm_body(const GemmTask* __restrict__ tasks, co
       }
       release();
     }
+    if (!have_next && tile_next < total_tiles) tc_next = locate<BN>(tasks, ntasks, tile_next, uni);
 
     if constexpr (K3F) {
       // ---- K3f epilogue: +alpha acc and -alpha acc staged in shared memory (128B-swizzled boxes of

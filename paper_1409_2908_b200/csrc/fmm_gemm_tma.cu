@@ -57,6 +57,17 @@ void gemm_k3f_target_map(void* out, const double* ptr, long long rows, long long
   make_map(reinterpret_cast<CUtensorMap*>(out), ptr, rows, cols, ld, 16, BM);  // 16 columns x 128 rows
 }
 
+// the uniform tile grid of a launch and the magic numbers its tile map divides with
+static Uniform make_uniform(int tm, int tn) {
+  Uniform u{tm * tn, tm, tn};
+  if (u.tiles > 0) {
+    u.magic_tiles = 0xFFFFFFFFu / (unsigned)u.tiles;
+    u.magic_span = 0xFFFFFFFFu / (unsigned)(GROUP_M * tn);
+  }
+  return u;
+}
+
+
 void gemm_k3f_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int uniform_tm,
                      int uniform_tn, const K3fArgs& ka, cudaStream_t stream) {
   if (total_tiles <= 0 || ntasks <= 0) return;
@@ -69,7 +80,7 @@ void gemm_k3f_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, lo
     FMM_CUDA(cudaFuncSetAttribute(grouped_dgemm_k3f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured.fetch_or(bit);
   }
-  const Uniform uni{uniform_tm * uniform_tn, uniform_tm, uniform_tn};
+  const Uniform uni = make_uniform(uniform_tm, uniform_tn);
   const int grid = (int)std::min<long long>(total_tiles, gemm_sm_count());
   grouped_dgemm_k3f<<<grid, THREADS, smem, stream>>>(d_tasks, reinterpret_cast<const CUtensorMap*>(d_maps), ntasks,
                                                       (int)total_tiles, uni, ka);
@@ -265,7 +276,7 @@ static int gemm_choose_epi_fallback(int bn, int* bk) {
 
 void gemm_tma_launch(const GemmTask* d_tasks, const void* d_maps, int ntasks, long long total_tiles, int bn, int bk,
                      int uniform_tm, int uniform_tn, cudaStream_t stream, int epi) {
-  const Uniform uni{uniform_tm * uniform_tn, uniform_tm, uniform_tn};
+  const Uniform uni = make_uniform(uniform_tm, uniform_tn);
   if (total_tiles <= 0 || ntasks <= 0) return;
 #ifdef FMM_BG_PROBE
   {  // FMM_BG_BYTES: bytes the idle producer warps copy in the background (timing experiment)
