@@ -121,3 +121,32 @@ def test_dist_slabs_partition_the_outer_dimension(F, outer, G):
         assert max(sizes) - min(sizes) <= 1
     with pytest.raises(F.FmmError):
         F.dist_slab(4, 4, "row", 2, 2)
+
+
+def test_tile_map_magic_division_is_exact():
+    # the leaf GEMM's tile -> task map (csrc/fmm_gemm_core.cuh, magic_div; host side make_uniform in
+    # fmm_gemm_tma.cu) divides by q = umulhi(x, floor((2^32 - 1) / d)) plus ONE correction step.
+    # The estimate is the quotient or one below it for every 0 <= x < 2^31: checked here on the
+    # divisors' edge cases (1, powers of two, 2^k +- 1, large d) and on random pairs.
+    import random
+    rng = random.Random(7)
+
+    def magic_div(x, d):
+        magic = 0xFFFFFFFF // d
+        q = (x * magic) >> 32
+        r = x - q * d
+        assert 0 <= r < 2 * d, (x, d)      # at most one correction is ever needed
+        if r >= d:
+            q, r = q + 1, r - d
+        return q, r
+
+    ds = [1, 2, 3, 5, 7, 8, 9, 45, 72, 80, 112, 400, 841 * 45, 2 ** 16 - 1, 2 ** 16, 2 ** 16 + 1,
+          2 ** 30, 2 ** 31 - 1] + [rng.randrange(1, 2 ** 31) for _ in range(200)]
+    for d in ds:
+        xs = [0, 1, d - 1, d, d + 1, 2 * d - 1, 2 * d, 2 ** 31 - 1, 2 ** 31 - d] + \
+             [rng.randrange(0, 2 ** 31) for _ in range(200)]
+        for k in range(1, 40):                       # multiples of d and their neighbours
+            xs += [k * d - 1, k * d, k * d + 1]
+        for x in xs:
+            if 0 <= x < 2 ** 31:
+                assert magic_div(x, d) == divmod(x, d), (x, d)
